@@ -1,0 +1,413 @@
+"""DS-Sync sync-iteration benchmark (BASELINE.json metric) on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c1]
+                    [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step is one DS-Sync iteration of the hot path over the config's worker
+buffers: every worker's fused optimizer step + ordered group average
+(block groups on even t, comb groups on odd t), device-resident in HBM.
+Default workload = BASELINE config C2 (W=8 workers, groups of 2 and 4,
+25M-float buffers, vanilla SGD), all W workers packed over the N GPUs
+(W/N per GPU, so N=1 holds all 8; scaling is strong: total work fixed).
+BSP (ordered gradient fold + step) is measured on the same buffers.
+
+Prints ONE JSON line (rank 0).  --impl reference times the reference's own
+CPU implementation (oracle/_ref = the unmodified reference sources) on the
+box's host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DS-Sync sync iters/s & effective GB/s vs BSP at 1/2/4/8 B200 (% of roofline)"
+
+# BASELINE configs.  bytes/elem: algorithmic HBM bytes per
+# worker-element per iteration (fp32): sgd 12, momentum 20, adam(w) 28.
+CONFIGS = {
+    "c1": dict(W=4, N=2, rect=False, d=20, opt=0, alpha=0.05, wd=0.0,
+               desc="C1: W=4, 2 groups of 2 shuffled every iteration, d=20 (logistic size), vanilla SGD"),
+    "c2": dict(W=8, N=2, rect=True, d=25_000_000, opt=0, alpha=0.05, wd=0.0,
+               desc="C2: W=8 workers, DS-Sync groups of 2 (even t) / 4 (odd t), d=25,000,000 fp32 "
+                    "(ResNet-50 size), vanilla SGD alpha=0.05"),
+    "c3": dict(W=32, N=4, rect=True, d=36_500_000, opt=1, alpha=0.1, wd=1e-4,
+               desc="C3: W=32 virtual workers, groups of 4 (even) / 8 (odd), d=36,500,000 fp32 "
+                    "(WideResNet-28-10 size), SGD-momentum 0.9 wd=1e-4"),
+    "c4": dict(W=64, N=8, rect=False, d=340_000_000, opt=3, alpha=3e-5, wd=0.01,
+               desc="C4: W=64 virtual workers, groups of 8, d=340,000,000 fp32 (BERT-large size), AdamW"),
+}
+BYTES_PER_ELEM = {0: 12, 1: 20, 2: 28, 3: 28}
+OPT_NAMES = ["vanilla-sgd", "sgd-momentum", "adam", "adamw"]
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(1.0)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        return time.time()
+
+    def stop(self, t0, t1):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        samples = [ln for (ts, ln) in self.lines if t0 - 0.06 <= ts <= t1 + 0.06] or [ln for _, ln in self.lines[-3:]]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in samples:
+            parts = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                for n, v in zip(names, parts[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def reference_arm(args, cfg):
+    """The reference's own CPU path: apply_step for every worker + each
+    group's ring_allreduce_avg (oracle/_ref = /root/reference/proj/src
+    compiled unmodified), all host threads, on a d-sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.oracle import REF_SO, Reference
+    import ctypes as C
+    from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
+
+    if not os.path.exists(REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdssync_ref.so not built"}))
+        return
+    R = Reference()
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    threads = os.cpu_count() or 1
+    d_sample = min(d, args.ref_sample)
+    hp = R.hp_array(weight_decay=cfg["wd"])
+    h = R.lib.ref_bench_create(W, d_sample, cfg["opt"], hp.ctypes.data, 1)
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
+    tables = []
+    for p in (0, 1):
+        groups = make_partition(s, p).groups
+        members = np.array([x for g in groups for x in g], np.int32)
+        offsets = np.cumsum([0] + [len(g) for g in groups]).astype(np.int32)
+        tables.append((members, offsets, len(groups)))
+    err = C.create_string_buffer(512)
+
+    def ds(t):
+        m, o, n = tables[t & 1]
+        rc = R.lib.ref_bench_ds_step(h, t, cfg["alpha"], m.ctypes.data, o.ctypes.data, n, threads, err, 512)
+        assert rc == 0, err.value
+
+    for t in range(args.warmup):
+        ds(t)
+    t0 = time.perf_counter()
+    for t in range(args.warmup, args.warmup + args.steps):
+        ds(t)
+    dt = (time.perf_counter() - t0) / args.steps
+    # BSP on the same sample
+    tb0 = time.perf_counter()
+    nb = max(1, min(args.steps, 20))
+    for t in range(nb):
+        rc = R.lib.ref_bench_bsp_step(h, t, cfg["alpha"], threads, err, 512)
+        assert rc == 0, err.value
+    dtb = (time.perf_counter() - tb0) / nb
+    R.lib.ref_bench_destroy(h)
+    scale = d_sample / d  # per-element work: iters/s at full d = sample iters/s * d_sample / d
+    value = (1.0 / dt) * scale
+    sample = (f"W={W} workers x d={d_sample:,} fp64 (reference is fp64-only) of the d={d:,} workload, "
+              f"{args.steps} timed DS iterations; iters/s scaled by {d_sample}/{d}")
+    out = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "W": W, "N": N, "d": d, "optimizer": OPT_NAMES[cfg["opt"]],
+                   "rectangular": cfg["rect"]},
+        "effective_gbs": W * d * 4 / (1000.0 / value / 1e3) / 1e9,
+        "bsp": {"iters_s": (1.0 / dtb) * scale},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def cpu_baseline(cfg, seconds=12.0, sample_d=1 << 20):
+    """cpu_baseline leg of our arm: the same reference CPU path, bounded."""
+    from oracle.oracle import REF_SO, Reference
+    import ctypes as C
+    from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
+    if not os.path.exists(REF_SO):
+        return {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": "oracle/_ref missing"}
+    R = Reference()
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    threads = os.cpu_count() or 1
+    ds_ = min(d, sample_d)
+    hp = R.hp_array(weight_decay=cfg["wd"])
+    h = R.lib.ref_bench_create(W, ds_, cfg["opt"], hp.ctypes.data, 1)
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
+    tabs = []
+    for p in (0, 1):
+        groups = make_partition(s, p).groups
+        tabs.append((np.array([x for g in groups for x in g], np.int32),
+                     np.cumsum([0] + [len(g) for g in groups]).astype(np.int32), len(groups)))
+    err = C.create_string_buffer(512)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        m, o, ng = tabs[n & 1]
+        R.lib.ref_bench_ds_step(h, n, cfg["alpha"], m.ctypes.data, o.ctypes.data, ng, threads, err, 512)
+        n += 1
+        el = time.perf_counter() - t0
+        if el > seconds and n >= 2:
+            break
+    R.lib.ref_bench_destroy(h)
+    return {"value": n / el * ds_ / d, "unit": "iters/s", "cores": threads, "kind": "reference",
+            "sample": f"{n} DS iterations of W={W} x d={ds_:,} fp64 in {el:.1f} s on {threads} threads "
+                      f"(reference apply_step + ring_allreduce_avg), scaled by {ds_}/{d}"}
+
+
+# ---------------------------------------------------------------------------
+def our_arm(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2007_03298_b200 import (BUF_GRADS, BUF_PARAMS, DsSyncEngine, OptimizerHyperparams, OptimizerKind,
+                                       StrategyKind, SyncStrategy, Topology, WorldConfig)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    G = args.gpus
+    if world != G:
+        raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    if W % G:
+        raise SystemExit(f"W={W} not divisible by {G} GPUs")
+    P = W // G
+    peak, peak_kind = load_peaks()
+    hp = OptimizerHyperparams(weight_decay=cfg["wd"])
+    stream = torch.cuda.current_stream()
+
+    def make(kind):
+        s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W), 1,
+                         cfg["rect"] and kind == StrategyKind.DS_SYNC)
+        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, "f32", local, rank, G)
+        e.set_stream(stream.cuda_stream)
+        if G > 1:
+            hs = [None] * G
+            dist.all_gather_object(hs, e.ipc_export())
+            e.ipc_attach(hs)
+        e.quadratic_init(7, 4.0)
+        e.quadratic_gradients(0, 1, 1.0, 0.5)
+        torch.cuda.synchronize()
+        return e
+
+    def timed(e, k0, K, per_launch=False):
+        e.enable_timing(per_launch)
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for t in range(k0, k0 + K):
+            e.step(t, cfg["alpha"])
+        b.record(stream)
+        torch.cuda.synchronize()
+        if G > 1:
+            dist.barrier()
+        ms = a.elapsed_time(b)
+        kt = e.kernel_times() if per_launch else (0.0, 0, 0.0)
+        e.enable_timing(False)
+        return ms, kt
+
+    def max_over_ranks(x):
+        if G == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    res = {}
+    clocks = ClockSampler(local)
+    for kind, name in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
+        e = make(kind)
+        l0 = e.launch_count
+        for t in range(args.warmup):
+            e.step(t, cfg["alpha"])
+        e.check()
+        if name == "ds":
+            clocks.start()
+            tc0 = time.time()
+        ms, _ = timed(e, args.warmup, args.steps)
+        if name == "ds":
+            tc1 = time.time()
+            res["clocks"] = clocks.stop(tc0, tc1)
+        launches = e.launch_count - l0
+        ms = max_over_ranks(ms)
+        # per-launch event timing of the hot kernels (second pass)
+        ms2, (ktot, kn, kmax) = timed(e, args.warmup + args.steps, args.steps, per_launch=True)
+        e.check()
+        res[name] = dict(ms=ms / args.steps, kernel_ms=ktot, kernel_launches=kn, kernel_max_ms=kmax,
+                         launches_per_step=launches / (args.warmup + args.steps))
+        if name == "ds":
+            # e2e through the C-ABI with host buffers: pinned H2D of every
+            # local worker's gradient, the step, D2H of every worker's params.
+            K2 = max(3, min(args.steps, args.e2e_steps))
+            hg = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
+            hw = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
+            e.download_all(BUF_GRADS, hg)
+            if G > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for t in range(K2):
+                e.upload_all(BUF_GRADS, hg)
+                e.step(args.warmup + 2 * args.steps + t, cfg["alpha"])
+                e.download_all(BUF_PARAMS, hw)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms = max_over_ranks(a.elapsed_time(b)) / K2
+            res["e2e"] = dict(ms=e2e_ms, h2d=P * d * 4 * G, d2h=P * d * 4 * G, wall=time.perf_counter() - t0)
+            e.check()
+        e.close()
+        del e
+        torch.cuda.synchronize()
+
+    if G > 1:
+        dist.barrier()
+    if rank != 0:
+        if G > 1:
+            dist.destroy_process_group()
+        return
+
+    ds, bsp = res["ds"], res["bsp"]
+    ipsec = 1000.0 / ds["ms"]
+    bpe = BYTES_PER_ELEM[cfg["opt"]]
+    alg_bytes_step = W * d * bpe  # whole job, all ranks
+    # dominant kernel: fused DS group kernel (1 GPU) — algorithmic bytes per
+    # launch = (bytes of the step on this GPU) / launches per step
+    k_ms_avg = ds["kernel_ms"] / max(ds["kernel_launches"], 1)
+    per_gpu_bytes = P * d * bpe
+    achieved = per_gpu_bytes * args.steps / (ds["kernel_ms"] / 1e3) / 1e9 if ds["kernel_ms"] else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{args.config}_g{G}")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC,
+        "value": ipsec,
+        "unit": "iters/s",
+        "n_gpus": G,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ds["ms"],
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: isotropic-quadratic gradients (SplitMix64/Box-Muller, seeds 7/1), device-resident",
+        "config": {"workload": cfg["desc"], "W": W, "N": N, "d": d, "optimizer": OPT_NAMES[cfg["opt"]],
+                   "rectangular": cfg["rect"], "workers_per_gpu": P, "parallelism": f"dp{G} (W/G workers per GPU)",
+                   "l2": f"inputs larger than L2: {P * d * 4 / 1e6:.0f} MB per array per GPU"
+                         if P * d * 4 > 126e6 else "inputs smaller than L2 (latency-bound config)"},
+        "effective_gbs": W * d * 4 / (ds["ms"] / 1e3) / 1e9,
+        "hbm_gbs_algorithmic": alg_bytes_step / (ds["ms"] / 1e3) / 1e9,
+        "bsp": {"iters_s": 1000.0 / bsp["ms"], "ms_per_step": bsp["ms"],
+                "effective_gbs": W * d * 4 / (bsp["ms"] / 1e3) / 1e9,
+                "ds_over_bsp": bsp["ms"] / ds["ms"]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_kind": peak_kind, "kernel": "ds_group_kernel (fused apply_step + ordered fold + broadcast)"
+                     if G == 1 else "DS step kernels (local step + two-shot NVLink fold)",
+                     "avg_launch_ms": k_ms_avg, "launches_per_step": ds["launches_per_step"],
+                     "alg_bytes_per_launch": per_gpu_bytes * args.steps / max(ds["kernel_launches"], 1)},
+        "gpu_launches": int(round(ds["launches_per_step"] * args.steps)),
+        "clocks": res.get("clocks"),
+        "e2e": {"value": 1000.0 / res["e2e"]["ms"], "unit": "iters/s", "h2d_bytes_per_step": res["e2e"]["h2d"],
+                "d2h_bytes_per_step": res["e2e"]["d2h"],
+                "path": "C-ABI dss_upload_all(grads, pinned) + dss_step + dss_download_all(params, pinned)"},
+    }
+    if G == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(out))
+    if G > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=1 << 19)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+    else:
+        our_arm(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

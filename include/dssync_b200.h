@@ -1,0 +1,253 @@
+/*
+ * dssync_b200.h — C-ABI of the B200-native DS-Sync (divide-and-shuffle
+ * synchronization, arXiv 2007.03298) step.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * exposes it as free C++ functions in namespace dssync (static lib, no FFI):
+ *
+ *   make_partition  /root/reference/proj/include/dssync/schedule.hpp:37  (src/schedule.cpp:31-54)
+ *   group_of        /root/reference/proj/include/dssync/schedule.hpp:40  (src/schedule.cpp:56-65)
+ *   check_mixing    /root/reference/proj/include/dssync/schedule.hpp:45  (src/schedule.cpp:67-90)
+ *   validate(World) /root/reference/proj/include/dssync/schedule.hpp:23  (src/schedule.cpp:8-24)
+ *   validate(Strat) /root/reference/proj/include/dssync/sync.hpp:43      (src/sync.cpp:47-66)
+ *   apply_step      /root/reference/proj/include/dssync/optim.hpp:51-52  (src/optim.cpp:46-98)
+ *   sync_round      /root/reference/proj/include/dssync/sync.hpp:128-129 (src/sync.cpp:268-282)
+ *   run_training DS branch  src/sync.cpp:347-374, BSP branch src/sync.cpp:375-428
+ *   mean_of / ring|tree|ps_allreduce_avg  src/param.cpp:42-53, src/comm.cpp:78-289
+ *   QuadraticProblem::stochastic_gradient (A = mu*I)  src/problems.cpp:134-136,173-193
+ *
+ * Everything here is plain C: opaque handle, C scalars, host pointers and
+ * sizes.  No torch types.  Every entry point returns a dss_status; the text
+ * of the last failure (same wording as the reference's exceptions) and, for
+ * divergence, the (rank, iteration) pair the reference's DivergenceError
+ * carries (errors.hpp:16-25) are available through dss_last_error().
+ *
+ * Product path only: there is no CPU fallback.  Device entry points fail
+ * with DSS_ECUDA when no B200 is present.
+ */
+#ifndef DSSYNC_B200_H_
+#define DSSYNC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (sync.cpp/schedule.cpp exceptions -> ints) ------------ */
+typedef enum {
+  DSS_OK = 0,
+  DSS_EINVAL = 1,     /* std::invalid_argument (schedule.cpp:8-24, sync.cpp:47-66, comm.cpp:56-72) */
+  DSS_EDIVERGED = 2,  /* dssync::DivergenceError(rank, iteration) (errors.hpp:16-25) */
+  DSS_ECUDA = 3,      /* CUDA runtime failure / no device */
+  DSS_ENCCL = 4,      /* peer/IPC failure on the multi-GPU path */
+  DSS_ERUNTIME = 5    /* std::runtime_error outside the training loop (param.cpp:28-32) */
+} dss_status;
+
+/* ---- enums mirror the reference's enum classes, same ordinal order ------ */
+typedef enum { DSS_VANILLA_SGD = 0, DSS_SGD_MOMENTUM = 1, DSS_ADAM = 2, DSS_ADAMW = 3 } dss_optimizer_kind; /* optim.hpp:11 */
+typedef enum { DSS_BSP = 0, DSS_DS_SYNC = 1 } dss_strategy_kind;  /* sync.hpp:14 */
+typedef enum { DSS_RING = 0, DSS_TREE = 1, DSS_PS = 2 } dss_topology; /* sync.hpp:15 */
+typedef enum { DSS_F32 = 0, DSS_F64 = 1 } dss_dtype;
+
+/* Worker-major device buffers, [local_workers][d_pad]. */
+typedef enum {
+  DSS_BUF_PARAMS = 0,   /* WorkerState::params            (sync.hpp:57) */
+  DSS_BUF_GRADS = 1,    /* GradSample::grad                (problems.hpp:31) */
+  DSS_BUF_MOMENT1 = 2,  /* OptimizerState::first_moment    (optim.hpp:31) */
+  DSS_BUF_MOMENT2 = 3   /* OptimizerState::second_moment   (optim.hpp:32) */
+} dss_buffer;
+
+/* OptimizerHyperparams (optim.hpp:16-23); alpha is passed per step. */
+typedef struct {
+  double momentum;
+  double beta1;
+  double beta2;
+  double epsilon;
+  double weight_decay;
+} dss_hparams;
+
+/* SyncStrategy (sync.hpp:34-39) + WorldConfig (schedule.hpp:17-20). */
+typedef struct {
+  int kind;         /* dss_strategy_kind */
+  int topology;     /* dss_topology; the arithmetic is topology-independent (comm.hpp:71-74) */
+  int world_size;   /* W */
+  int group_size;   /* N */
+  int num_servers;  /* ps only */
+  int rectangular;  /* 0 = reference rules (W == N*N or W == N).  1 = builder extension
+                       W = N*K: even t -> K blocks of N, odd t -> N combs of K.
+                       Not part of the reference: parity there is pinned only by the oracle. */
+} dss_strategy;
+
+/* SyncRoundOutcome (sync.hpp:119-122). */
+typedef struct {
+  long critical_path_steps;
+  long total_messages;
+} dss_outcome;
+
+/* Context configuration.  One context per process/GPU. */
+typedef struct {
+  dss_strategy strategy;
+  int optimizer;        /* dss_optimizer_kind */
+  dss_hparams hp;
+  int dtype;            /* dss_dtype */
+  long dim;             /* d, parameters per worker */
+  int device;           /* CUDA ordinal */
+  int rank;             /* this GPU's index among n_gpus (process rank) */
+  int n_gpus;           /* G; world_size must be a multiple of G.  Workers are packed
+                           contiguously: gpu(k) = k / (W/G) */
+  int path;             /* 0 = auto.  1 = route every multi-member group through the
+                           cross-GPU two-shot path (step in place, then ordered slice
+                           fold) even on one GPU: exercises the multi-GPU kernels on a
+                           single device for parity tests.  Results are bit-identical. */
+} dss_config;
+
+typedef struct dss_ctx dss_ctx;
+
+/* ======================= host-only schedule (no GPU) ===================== */
+
+/* validate(WorldConfig) (schedule.cpp:8-24); rectangular=1 accepts W % N == 0. */
+int dss_validate_world(int world_size, int group_size, int rectangular);
+
+/* validate(SyncStrategy) (sync.cpp:47-66). */
+int dss_validate_strategy(const dss_strategy* s);
+
+/* is_square_mode (schedule.cpp:26-29). Returns 1/0, or -1 on invalid input. */
+int dss_is_square_mode(int world_size, int group_size);
+
+/* make_partition (schedule.cpp:31-54) / partition_for (sync.cpp:131-141 when
+ * kind == BSP).  Writes the groups as CSR: members[0..W) grouped, ascending
+ * inside each group; offsets[0..n_groups]; *n_groups.  members must hold W
+ * ints and offsets W+1 ints. */
+int dss_partition(const dss_strategy* s, long t, int* members, int* offsets, int* n_groups);
+
+/* group_of (schedule.cpp:56-65): members of rank's group, *count of them. */
+int dss_group_of(const dss_strategy* s, long t, int rank, int* members, int* count);
+
+/* check_mixing (schedule.cpp:67-90): 1 true, 0 false, <0 error status negated. */
+int dss_check_mixing(const dss_strategy* s, long t);
+
+/* Closed-form SyncRoundOutcome of one round at iteration t: max over groups
+ * of the collective's serial steps, sum of its messages (comm.cpp:78-289:
+ * ring 2m-1 / 2m-1, tree 3log2m / m*log2m + 2(m-1), ps 2m / 2*m*min(P, dim)). */
+int dss_round_outcome(const dss_strategy* s, long t, long payload_dim, dss_outcome* out);
+
+/* Multi-GPU plan for (strategy, t, n_gpus, rank): how many groups this GPU
+ * folds locally, how many span GPUs, and the [lo, hi) element slice this GPU
+ * owns in each spanning group (two-shot ownership).  Host-only, for tests. */
+typedef struct {
+  int local_groups;      /* groups whose members all live on this GPU */
+  int spanning_groups;   /* groups with members on this GPU and on others */
+  int owned_slices;      /* spanning groups in which this GPU owns a non-empty slice */
+  long owned_elems;      /* sum of owned slice lengths */
+} dss_plan_summary;
+int dss_plan(const dss_strategy* s, long t, long dim, int n_gpus, int rank,
+             dss_plan_summary* out, long* slice_lo, long* slice_hi, int* slice_group, int max_slices);
+
+/* ============================ device context ============================= */
+
+int dss_create(const dss_config* cfg, dss_ctx** out);
+int dss_destroy(dss_ctx* ctx);
+
+/* Run all device work on this stream (e.g. the caller's current stream).
+ * NULL restores the context's own stream. */
+int dss_set_stream(dss_ctx* ctx, void* cuda_stream);
+
+/* First global rank hosted here and how many (P = W / n_gpus). */
+int dss_local_workers(const dss_ctx* ctx, int* first_rank, int* count);
+
+/* Padded row length in elements (multiple of 64) and element size in bytes. */
+long dss_row_stride(const dss_ctx* ctx);
+int dss_elem_size(const dss_ctx* ctx);
+
+/* Device address of a worker row (global rank hosted here), for zero-copy
+ * interop (e.g. wrapping into a framework tensor for the NCCL baseline). */
+int dss_device_ptr(dss_ctx* ctx, int buffer, int rank, void** out);
+
+/* Host <-> device copies of one worker's row: n elements of the context's
+ * dtype (n <= dim).  Stream-ordered; dss_download synchronizes. */
+int dss_upload(dss_ctx* ctx, int buffer, int rank, const void* host, long n);
+int dss_download(dss_ctx* ctx, int buffer, int rank, void* host, long n);
+
+/* Whole-buffer copies for every local worker: host is [P][dim] contiguous.
+ * Async w.r.t. the host when the host memory is pinned. */
+int dss_upload_all(dss_ctx* ctx, int buffer, const void* host);
+int dss_download_all(dss_ctx* ctx, int buffer, void* host);
+
+/* Fill a buffer of every local worker with a copy of one host row. */
+int dss_broadcast_row(dss_ctx* ctx, int buffer, const void* host_row);
+
+/* OptimizerState::step_count per worker (optim.hpp:33).  Bias corrections
+ * use 1 - pow(beta, step_count + 1) in double on the host (optim.cpp:76-78). */
+int dss_set_step_count(dss_ctx* ctx, int rank, long step_count);
+long dss_get_step_count(const dss_ctx* ctx, int rank);
+
+/* ---- the hot path ---- */
+
+/* One full iteration at t with learning rate alpha:
+ *   DS-Sync: every worker apply_step(own w, own g) then every group averages
+ *            its stepped params in ascending-rank order (sync.cpp:347-374),
+ *            fused: each element is read once and written once.
+ *   BSP:     the world averages gradients in ascending-rank order, then every
+ *            worker apply_step(own w, mean g) (sync.cpp:375-428).
+ * Non-finite results are latched on the device; they surface as
+ * DSS_EDIVERGED from dss_check() (or from this call when check != 0). */
+int dss_step(dss_ctx* ctx, long t, double alpha, int check, dss_outcome* out);
+
+/* sync_round (sync.cpp:268-282): group averaging only, no optimizer step.
+ * Optimizer state untouched. */
+int dss_sync_round(dss_ctx* ctx, long t, int check, dss_outcome* out);
+
+/* apply_step (optim.cpp:46-98) for every local worker with its own gradient,
+ * no averaging. */
+int dss_apply_step(dss_ctx* ctx, double alpha, int check);
+
+/* Synthetic gradients of the isotropic quadratic (problems.cpp:134-136,173-193):
+ *   g_k = mu * (w_k - w*) + (sigma / sqrt(d)) * gaussian_i(seed, kGradientNoise, k, t)
+ * with the reference's SplitMix64 stream (rng.cpp:20-51), counter-addressed. */
+int dss_quadratic_gradients(dss_ctx* ctx, long t, uint64_t seed, double mu, double sigma);
+
+/* w* = gaussians of stream (problem_seed, kDataGen, 1, 0) (problems.cpp:157-159)
+ * and every worker's params = w* + sqrt(delta0) * u, u the normalised
+ * gaussian vector of stream (problem_seed, kInitParams, 0, 0) (problems.cpp:161-165). */
+int dss_quadratic_init(dss_ctx* ctx, uint64_t problem_seed, double delta0);
+/* Upload an explicit optimum w* (dim elements of the context dtype). */
+int dss_set_optimum(dss_ctx* ctx, const void* host, long n);
+
+/* Latched divergence check (synchronizes).  DSS_OK or DSS_EDIVERGED. */
+int dss_check(dss_ctx* ctx);
+/* Clear latched divergence flags. */
+int dss_clear_error(dss_ctx* ctx);
+
+/* Text of the last failure; *rank / *iteration are set for DSS_EDIVERGED
+ * (else -1).  Returns the status of the last failure. */
+int dss_last_error(const dss_ctx* ctx, char* buf, size_t len, int* rank, long* iteration);
+/* Text of the last failure of a context-free call (schedule functions). */
+int dss_last_global_error(char* buf, size_t len);
+
+/* ---- per-kernel timing (CUDA events on the launching stream) ---- */
+/* When enabled, every hot-path kernel launch is bracketed by events; the
+ * totals over the launches since the last reset are returned. */
+int dss_enable_timing(dss_ctx* ctx, int on);
+int dss_kernel_times(dss_ctx* ctx, double* total_ms, long* launches, double* max_launch_ms);
+/* gpu_launches: hot-path kernels launched since creation (all kinds). */
+long dss_launch_count(const dss_ctx* ctx);
+
+/* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
+/* CUDA IPC handles of this GPU's params, grads and flag buffers:
+ * DSS_IPC_BYTES bytes written to out. */
+#define DSS_IPC_BYTES 256
+int dss_ipc_export(dss_ctx* ctx, void* out);
+/* Map every GPU's exported handles (n_gpus * DSS_IPC_BYTES bytes, rank
+ * order, own entry ignored).  Must be called on every rank before the first
+ * multi-GPU dss_step.  Requires peer access between all GPUs. */
+int dss_ipc_attach(dss_ctx* ctx, const void* all_handles);
+/* Cross-GPU barrier over the flag buffers (also used by tests). */
+int dss_barrier(dss_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DSSYNC_B200_H_ */

@@ -1,0 +1,31 @@
+"""B200-native DS-Sync (divide-and-shuffle synchronization, arXiv 2007.03298).
+
+The hot path — fused apply_step + ordered group average (+ cross-GPU
+two-shot over NVLink) — lives in the CUDA C-ABI library
+``libdssync_b200.so`` (include/dssync_b200.h).  This package is its ctypes
+binding plus a reference-shaped API (see api.py).
+"""
+from .api import (  # noqa: F401
+    DivergenceError,
+    DsSyncEngine,
+    GroupPartition,
+    OptimizerHyperparams,
+    OptimizerKind,
+    OptimizerState,
+    StepResult,
+    StrategyKind,
+    SyncRoundOutcome,
+    SyncStrategy,
+    Topology,
+    WorkerState,
+    WorldConfig,
+    apply_step,
+    check_mixing,
+    group_of,
+    is_square_mode,
+    make_partition,
+    round_outcome,
+    sync_round,
+    validate,
+)
+from ._lib import BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_PARAMS  # noqa: F401

@@ -1,0 +1,466 @@
+"""Reference-shaped interface over the C-ABI.
+
+Mirrors the reference's operator API for the DS-Sync path — same names,
+argument meaning and error behaviour — so callers and parity tests read like
+the reference's own (proj/include/dssync/*.hpp):
+
+  WorldConfig, validate, is_square_mode, make_partition, group_of,
+  check_mixing                                   schedule.hpp:17-45
+  OptimizerKind/Hyperparams/State, StepResult,
+  apply_step                                     optim.hpp:11-52
+  StrategyKind, Topology, SyncStrategy, validate,
+  WorkerState, SyncRoundOutcome, sync_round      sync.hpp:14-129
+  DivergenceError                                errors.hpp:16-25
+
+``apply_step`` and ``sync_round`` take host-resident workers like the
+reference (upload -> CUDA kernel -> download).  ``DsSyncEngine`` keeps the
+workers resident in HBM across iterations — the performance path.
+
+Errors: std::invalid_argument -> ValueError, DivergenceError ->
+DivergenceError(rank, iteration), CUDA failures -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+class OptimizerKind(enum.IntEnum):  # optim.hpp:11
+    VANILLA_SGD = 0
+    SGD_MOMENTUM = 1
+    ADAM = 2
+    ADAMW = 3
+
+    @staticmethod
+    def from_string(name: str) -> "OptimizerKind":  # optim.cpp:9-15
+        table = {"vanilla-sgd": 0, "sgd-momentum": 1, "adam": 2, "adamw": 3}
+        if name not in table:
+            raise ValueError("unknown optimizer kind: " + name)
+        return OptimizerKind(table[name])
+
+    def __str__(self) -> str:
+        return ["vanilla-sgd", "sgd-momentum", "adam", "adamw"][int(self)]
+
+
+class StrategyKind(enum.IntEnum):  # sync.hpp:14
+    BSP = 0
+    DS_SYNC = 1
+
+    @staticmethod
+    def from_string(name: str) -> "StrategyKind":  # sync.cpp:15-19
+        if name == "bsp":
+            return StrategyKind.BSP
+        if name == "ds-sync":
+            return StrategyKind.DS_SYNC
+        raise ValueError("unknown strategy: " + name)
+
+    def __str__(self) -> str:
+        return "bsp" if self == StrategyKind.BSP else "ds-sync"
+
+
+class Topology(enum.IntEnum):  # sync.hpp:15
+    RING = 0
+    TREE = 1
+    PS = 2
+
+    @staticmethod
+    def from_string(name: str) -> "Topology":  # sync.cpp:21-26
+        table = {"ring": 0, "tree": 1, "ps": 2}
+        if name not in table:
+            raise ValueError("unknown topology: " + name)
+        return Topology(table[name])
+
+    def __str__(self) -> str:
+        return ["ring", "tree", "ps"][int(self)]
+
+
+class DivergenceError(RuntimeError):
+    """errors.hpp:16-25: a worker produced a non-finite value at iteration t."""
+
+    def __init__(self, rank: int, iteration: int, what: str):
+        super().__init__(what)
+        self.rank = rank
+        self.iteration = iteration
+
+
+@dataclass
+class WorldConfig:  # schedule.hpp:17-20
+    world_size: int = 1
+    group_size: int = 1
+
+
+@dataclass
+class GroupPartition:  # schedule.hpp:28-31
+    iteration: int
+    groups: List[List[int]]
+
+
+@dataclass
+class OptimizerHyperparams:  # optim.hpp:16-23
+    alpha: float = 0.1
+    momentum: float = 0.9
+    beta1: float = 0.9
+    beta2: float = 0.999
+    epsilon: float = 1e-8
+    weight_decay: float = 0.0
+
+
+@dataclass
+class OptimizerState:  # optim.hpp:25-34
+    kind: OptimizerKind = OptimizerKind.VANILLA_SGD
+    hp: OptimizerHyperparams = field(default_factory=OptimizerHyperparams)
+    first_moment: Optional[np.ndarray] = None
+    second_moment: Optional[np.ndarray] = None
+    step_count: int = 0
+
+
+@dataclass
+class StepResult:  # optim.hpp:36-39
+    params: np.ndarray
+    state: OptimizerState
+
+
+@dataclass
+class SyncStrategy:  # sync.hpp:34-39
+    kind: StrategyKind = StrategyKind.BSP
+    topology: Topology = Topology.RING
+    world: WorldConfig = field(default_factory=WorldConfig)
+    num_servers: int = 1
+    rectangular: bool = False  # builder extension W = N*K (not in the reference)
+
+
+@dataclass
+class WorkerState:  # sync.hpp:55-61 (running_stats unused by the quadratic path)
+    rank: int = 0
+    params: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    opt: OptimizerState = field(default_factory=OptimizerState)
+
+
+@dataclass
+class SyncRoundOutcome:  # sync.hpp:119-122
+    critical_path_steps: int = 0
+    total_messages: int = 0
+
+
+# ---------------------------------------------------------------------------
+def _raise(status: int, msg: str, rank: int = -1, iteration: int = -1):
+    if status == L.DSS_OK:
+        return
+    if status == L.DSS_EINVAL:
+        raise ValueError(msg)
+    if status == L.DSS_EDIVERGED:
+        raise DivergenceError(rank, iteration, msg)
+    raise RuntimeError(msg)
+
+
+def _check_global(status: int):
+    if status != L.DSS_OK:
+        _raise(status, L.global_error())
+
+
+def _c_strategy(s: SyncStrategy) -> L.dss_strategy:
+    return L.dss_strategy(int(s.kind), int(s.topology), int(s.world.world_size),
+                          int(s.world.group_size), int(s.num_servers), 1 if s.rectangular else 0)
+
+
+def _as_strategy(x) -> SyncStrategy:
+    if isinstance(x, SyncStrategy):
+        return x
+    if isinstance(x, WorldConfig):  # make_partition(WorldConfig, t): the DS schedule
+        return SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, x)
+    raise TypeError("expected WorldConfig or SyncStrategy")
+
+
+def validate(x) -> None:
+    """validate(WorldConfig) (schedule.cpp:8-24) or validate(SyncStrategy) (sync.cpp:47-66)."""
+    lib = L.load()
+    if isinstance(x, WorldConfig):
+        _check_global(lib.dss_validate_world(x.world_size, x.group_size, 0))
+    else:
+        s = _c_strategy(x)
+        _check_global(lib.dss_validate_strategy(C.byref(s)))
+
+
+def is_square_mode(cfg: WorldConfig) -> bool:  # schedule.cpp:26-29
+    return L.load().dss_is_square_mode(cfg.world_size, cfg.group_size) == 1
+
+
+def make_partition(cfg, t: int) -> GroupPartition:
+    """make_partition (schedule.cpp:31-54); a SyncStrategy gives partition_for (sync.cpp:131-141)."""
+    s = _c_strategy(_as_strategy(cfg))
+    W = max(s.world_size, 1)
+    members = np.zeros(W, dtype=np.int32)
+    offsets = np.zeros(W + 1, dtype=np.int32)
+    n = C.c_int(0)
+    _check_global(L.load().dss_partition(C.byref(s), t, members.ctypes.data, offsets.ctypes.data, C.byref(n)))
+    groups = [members[offsets[g]:offsets[g + 1]].tolist() for g in range(n.value)]
+    return GroupPartition(t, groups)
+
+
+def group_of(cfg, t: int, rank: int) -> List[int]:  # schedule.cpp:56-65
+    s = _c_strategy(_as_strategy(cfg))
+    members = np.zeros(max(s.world_size, 1), dtype=np.int32)
+    n = C.c_int(0)
+    _check_global(L.load().dss_group_of(C.byref(s), t, rank, members.ctypes.data, C.byref(n)))
+    return members[:n.value].tolist()
+
+
+def check_mixing(cfg, t: int) -> bool:  # schedule.cpp:67-90
+    s = _c_strategy(_as_strategy(cfg))
+    r = L.load().dss_check_mixing(C.byref(s), t)
+    if r < 0:
+        _raise(-r, L.global_error())
+    return r == 1
+
+
+def round_outcome(strategy: SyncStrategy, t: int, payload_dim: int) -> SyncRoundOutcome:
+    s = _c_strategy(strategy)
+    o = L.dss_outcome()
+    _check_global(L.load().dss_round_outcome(C.byref(s), t, payload_dim, C.byref(o)))
+    return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
+
+
+# ---------------------------------------------------------------------------
+class DsSyncEngine:
+    """Device-resident DS-Sync / BSP workers on one GPU (one context).
+
+    Workers ``first_rank .. first_rank + local_workers - 1`` live in HBM as
+    worker-major rows.  ``step`` runs one fused iteration on the device.
+    """
+
+    def __init__(self, strategy: SyncStrategy, optimizer: OptimizerKind, dim: int,
+                 hp: Optional[OptimizerHyperparams] = None, dtype: str = "f32", device: int = 0,
+                 rank: int = 0, n_gpus: int = 1, path: int = 0):
+        hp = hp or OptimizerHyperparams()
+        self.lib = L.load()
+        self.strategy = strategy
+        self.optimizer = OptimizerKind(optimizer)
+        self.dim = int(dim)
+        self.dtype = np.float64 if dtype in ("f64", np.float64) else np.float32
+        cfg = L.dss_config()
+        cfg.strategy = _c_strategy(strategy)
+        cfg.optimizer = int(optimizer)
+        cfg.hp = L.dss_hparams(hp.momentum, hp.beta1, hp.beta2, hp.epsilon, hp.weight_decay)
+        cfg.dtype = L.DSS_F64 if self.dtype == np.float64 else L.DSS_F32
+        cfg.dim = self.dim
+        cfg.device = device
+        cfg.rank = rank
+        cfg.n_gpus = n_gpus
+        cfg.path = path
+        h = C.c_void_p()
+        st = self.lib.dss_create(C.byref(cfg), C.byref(h))
+        if st != L.DSS_OK:
+            _raise(st, L.global_error())
+        self.h = h
+        first, count = C.c_int(), C.c_int()
+        self.lib.dss_local_workers(self.h, C.byref(first), C.byref(count))
+        self.first_rank, self.local_workers = first.value, count.value
+        self.n_gpus = n_gpus
+        self.rank = rank
+
+    # -- lifecycle --
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.dss_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _ck(self, st: int):
+        if st != L.DSS_OK:
+            buf = C.create_string_buffer(2048)
+            r, it = C.c_int(-1), C.c_long(-1)
+            self.lib.dss_last_error(self.h, buf, len(buf), C.byref(r), C.byref(it))
+            _raise(st, buf.value.decode(), r.value, it.value)
+
+    # -- data movement --
+    def _arr(self, x) -> np.ndarray:
+        return np.ascontiguousarray(x, dtype=self.dtype)
+
+    def upload(self, buffer: int, rank: int, host) -> None:
+        a = self._arr(host)
+        self._ck(self.lib.dss_upload(self.h, buffer, rank, a.ctypes.data, a.size))
+
+    def download(self, buffer: int, rank: int) -> np.ndarray:
+        out = np.empty(self.dim, dtype=self.dtype)
+        self._ck(self.lib.dss_download(self.h, buffer, rank, out.ctypes.data, self.dim))
+        return out
+
+    def upload_all(self, buffer: int, host) -> None:
+        """host: [local_workers, dim] (pinned memory makes this asynchronous)."""
+        if isinstance(host, np.ndarray):
+            a = self._arr(host)
+            assert a.shape == (self.local_workers, self.dim)
+            self._keep = a
+            ptr = a.ctypes.data
+        else:  # any object exposing data_ptr() (e.g. a pinned torch tensor)
+            ptr = host.data_ptr()
+        self._ck(self.lib.dss_upload_all(self.h, buffer, ptr))
+
+    def download_all(self, buffer: int, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.local_workers, self.dim), dtype=self.dtype)
+        ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
+        self._ck(self.lib.dss_download_all(self.h, buffer, ptr))
+        return out
+
+    def broadcast_row(self, buffer: int, row) -> None:
+        a = self._arr(row)
+        self._ck(self.lib.dss_broadcast_row(self.h, buffer, a.ctypes.data))
+
+    def device_ptr(self, buffer: int, rank: int) -> int:
+        p = C.c_void_p()
+        self._ck(self.lib.dss_device_ptr(self.h, buffer, rank, C.byref(p)))
+        return p.value
+
+    @property
+    def row_stride(self) -> int:
+        return self.lib.dss_row_stride(self.h)
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        self._ck(self.lib.dss_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def set_step_count(self, rank: int, n: int) -> None:
+        self._ck(self.lib.dss_set_step_count(self.h, rank, n))
+
+    def step_count(self, rank: int) -> int:
+        return self.lib.dss_get_step_count(self.h, rank)
+
+    # -- hot path --
+    def step(self, t: int, alpha: float, check: bool = False) -> SyncRoundOutcome:
+        o = L.dss_outcome()
+        self._ck(self.lib.dss_step(self.h, t, alpha, 1 if check else 0, C.byref(o)))
+        return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
+
+    def sync_round(self, t: int, check: bool = True) -> SyncRoundOutcome:
+        o = L.dss_outcome()
+        self._ck(self.lib.dss_sync_round(self.h, t, 1 if check else 0, C.byref(o)))
+        return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
+
+    def apply_step(self, alpha: float, check: bool = True) -> None:
+        self._ck(self.lib.dss_apply_step(self.h, alpha, 1 if check else 0))
+
+    def quadratic_gradients(self, t: int, seed: int, mu: float, sigma: float) -> None:
+        self._ck(self.lib.dss_quadratic_gradients(self.h, t, seed, mu, sigma))
+
+    def quadratic_init(self, problem_seed: int, delta0: float) -> None:
+        self._ck(self.lib.dss_quadratic_init(self.h, problem_seed, delta0))
+
+    def set_optimum(self, wstar) -> None:
+        a = self._arr(wstar)
+        self._ck(self.lib.dss_set_optimum(self.h, a.ctypes.data, a.size))
+
+    def check(self) -> None:
+        self._ck(self.lib.dss_check(self.h))
+
+    def clear_error(self) -> None:
+        self._ck(self.lib.dss_clear_error(self.h))
+
+    # -- timing / accounting --
+    def enable_timing(self, on: bool = True) -> None:
+        self.lib.dss_enable_timing(self.h, 1 if on else 0)
+
+    def kernel_times(self):
+        tot, n, mx = C.c_double(), C.c_long(), C.c_double()
+        self._ck(self.lib.dss_kernel_times(self.h, C.byref(tot), C.byref(n), C.byref(mx)))
+        return tot.value, n.value, mx.value
+
+    @property
+    def launch_count(self) -> int:
+        return self.lib.dss_launch_count(self.h)
+
+    # -- multi-GPU --
+    def ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(L.IPC_BYTES)
+        self._ck(self.lib.dss_ipc_export(self.h, buf))
+        return buf.raw
+
+    def ipc_attach(self, all_handles: Sequence[bytes]) -> None:
+        blob = b"".join(all_handles)
+        assert len(blob) == L.IPC_BYTES * self.n_gpus
+        buf = C.create_string_buffer(blob, len(blob))
+        self._ck(self.lib.dss_ipc_attach(self.h, buf))
+
+    def barrier(self) -> None:
+        self._ck(self.lib.dss_barrier(self.h))
+
+
+# ---------------------------------------------------------------------------
+# Host-resident drop-ins for the reference's free functions.  Same semantics
+# as the reference (fp64); the arithmetic runs in the CUDA kernels.
+
+def apply_step(state: OptimizerState, params, grad, device: int = 0) -> StepResult:
+    """apply_step (optim.cpp:46-98) on the GPU: returns fresh params and state."""
+    w = np.asarray(params, dtype=np.float64)
+    g = np.asarray(grad, dtype=np.float64)
+    if w.shape != g.shape:
+        raise ValueError("apply_step: params and grad length mismatch")  # optim.cpp:30-32
+    a = state.hp.alpha
+    if not (a >= 0.0) or not np.isfinite(a):
+        raise ValueError("apply_step: alpha must be finite and >= 0")  # optim.cpp:33-35
+    for mom in (state.first_moment, state.second_moment):
+        if mom is not None and len(mom) and len(mom) != len(w):
+            raise ValueError("apply_step: moment buffer length mismatch")  # optim.cpp:36-41
+    if w.size == 0:
+        st = OptimizerState(state.kind, state.hp, state.first_moment, state.second_moment, state.step_count + 1)
+        return StepResult(w.copy(), st)
+    strat = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(1, 1))
+    with DsSyncEngine(strat, state.kind, w.size, state.hp, "f64", device) as e:
+        e.upload(L.BUF_PARAMS, 0, w)
+        e.upload(L.BUF_GRADS, 0, g)
+        kind = OptimizerKind(state.kind)
+        if kind != OptimizerKind.VANILLA_SGD and state.first_moment is not None and len(state.first_moment):
+            e.upload(L.BUF_MOMENT1, 0, state.first_moment)
+        if kind in (OptimizerKind.ADAM, OptimizerKind.ADAMW) and state.second_moment is not None \
+                and len(state.second_moment):
+            e.upload(L.BUF_MOMENT2, 0, state.second_moment)
+        e.set_step_count(0, state.step_count)
+        try:
+            e.apply_step(a, check=True)
+        except DivergenceError as err:
+            # the reference's apply_step throws std::runtime_error (optim.cpp:96)
+            raise RuntimeError("apply_step: non-finite value in result") from err
+        new = OptimizerState(kind, state.hp, None, None, state.step_count + 1)
+        if kind != OptimizerKind.VANILLA_SGD:
+            new.first_moment = e.download(L.BUF_MOMENT1, 0)
+        if kind in (OptimizerKind.ADAM, OptimizerKind.ADAMW):
+            new.second_moment = e.download(L.BUF_MOMENT2, 0)
+        return StepResult(e.download(L.BUF_PARAMS, 0), new)
+
+
+def sync_round(workers: List[WorkerState], strategy: SyncStrategy, t: int, device: int = 0) -> SyncRoundOutcome:
+    """sync_round (sync.cpp:268-282) on the GPU: averages params inside the
+    scheduled groups in place; optimizer state is never read or written."""
+    validate(strategy)
+    W = strategy.world.world_size
+    if len(workers) != W:
+        raise ValueError("sync_round: worker count does not match world_size")  # sync.cpp:271-273
+    d = len(workers[0].params)
+    for ws in workers:
+        if len(ws.params) != d:
+            raise ValueError("collective vectors must all have the same length")  # comm.cpp:67-69
+    if d == 0:
+        raise ValueError("collective vectors must be non-empty")  # comm.cpp:66
+    with DsSyncEngine(strategy, OptimizerKind.VANILLA_SGD, d, None, "f64", device) as e:
+        e.upload_all(L.BUF_PARAMS, np.stack([np.asarray(ws.params, dtype=np.float64) for ws in workers]))
+        out = e.sync_round(t, check=True)
+        res = e.download_all(L.BUF_PARAMS)
+    for k, ws in enumerate(workers):
+        ws.params = res[k].copy()
+    return out

@@ -1,0 +1,1235 @@
+// C-ABI implementation: device-resident worker state, the host driver of
+// the DS-Sync / BSP iteration, and kernel dispatch.
+//
+// Host driver restates run_training's DS branch (sync.cpp:347-374), BSP
+// branch (sync.cpp:375-428) and sync_round (sync.cpp:268-282) over
+// device-resident worker-major buffers.  One context per GPU (process).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "dssync_b200.h"
+#include "kernels.cuh"
+#include "schedule.hpp"
+
+using namespace dssb;
+
+namespace {
+
+thread_local std::string g_last_global_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct PeerError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+uint64_t mix64_host(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// Rng::for_stream (rng.cpp:20-26): the state the stream starts from.
+uint64_t stream_state(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t iteration) {
+  uint64_t s = mix64_host(seed + 0x9e3779b97f4a7c15ULL);
+  s = mix64_host(s ^ purpose);
+  s = mix64_host(s ^ rank);
+  s = mix64_host(s ^ iteration);
+  return s;
+}
+
+constexpr uint64_t kDataGen = 0x9e3779b97f4a7c15ULL;        // rng.hpp:40
+constexpr uint64_t kInitParams = 0xbf58476d1ce4e5b9ULL;     // rng.hpp:41
+constexpr uint64_t kGradientNoise = 0xa0761d6478bd642fULL;  // rng.hpp:44
+
+const char* collective_name(int topology) {
+  switch (topology) {
+    case DSS_TREE: return "tree_allreduce_avg";
+    case DSS_PS: return "ps_allreduce_avg";
+    default: return "ring_allreduce_avg";
+  }
+}
+
+// Device CSR table of groups for one launch of ds_group_kernel.
+struct GroupLaunch {
+  int size = 0;     // uniform group size of this launch (0 = mixed)
+  int groups = 0;
+  int* d_members = nullptr;
+  int* d_offsets = nullptr;
+};
+
+struct FoldLaunch {
+  int entries = 0;
+  int uniform_m = 0;  // src count if uniform, else 0
+  long max_len = 0;   // longest slice (elements)
+  FoldEntry* d_entries = nullptr;
+  void** d_src = nullptr;
+  void** d_dst = nullptr;
+};
+
+struct ParityPlan {
+  bool built = false;
+  bool any_spanning = false;  // identical on every GPU
+  std::vector<GroupLaunch> local;      // fused step+fold launches
+  GroupLaunch spanning_step;           // singleton in-place steps of spanning members
+  FoldLaunch fold;                     // owned two-shot slices
+};
+
+}  // namespace
+
+struct dss_ctx {
+  dss_config cfg{};
+  int P = 0;            // local workers
+  int first = 0;        // first global rank here
+  long d = 0, d_pad = 0;
+  int esz = 4;
+  int sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+
+  void* w = nullptr;
+  void* g = nullptr;
+  void* m1 = nullptr;
+  void* m2 = nullptr;
+  void* mg = nullptr;     // mean gradient row (BSP over several GPUs)
+  void* wstar = nullptr;  // quadratic optimum row
+  unsigned long long* d_err = nullptr;
+  unsigned long long* d_timeout = nullptr;
+  unsigned long long* flags = nullptr;  // [G] barrier words, written by peers
+  unsigned long long** d_peer_flags = nullptr;
+  unsigned long long* h_err = nullptr;  // pinned readback
+
+  std::vector<long> step_count;
+  std::vector<void*> peer_w, peer_g, peer_mg;
+  std::vector<unsigned long long*> peer_flag;
+  std::vector<void*> opened;  // IPC mappings to close
+  bool attached = false;
+  unsigned long long epoch = 0;
+  bool pending_remote = false;
+
+  ParityPlan step_plan[2];   // DS (or BSP at [0])
+  ParityPlan sync_plan[2];   // sync_round (no step)
+  GroupLaunch apply_launch;  // singleton groups of every local worker
+
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  long launches = 0;
+
+  int last_status = DSS_OK;
+  std::string last_error;
+  int last_rank = -1;
+  long last_iteration = -1;
+
+  std::vector<void*> allocations;
+};
+
+namespace {
+
+int fail(dss_ctx* c, int status, const std::string& msg, int rank = -1, long it = -1) {
+  if (c) {
+    c->last_status = status;
+    c->last_error = msg;
+    c->last_rank = rank;
+    c->last_iteration = it;
+  }
+  g_last_global_error = msg;
+  return status;
+}
+
+template <typename F>
+int guard(dss_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    return fail(c, DSS_EINVAL, e.what());
+  } catch (const CudaError& e) {
+    return fail(c, DSS_ECUDA, e.what());
+  } catch (const PeerError& e) {
+    return fail(c, DSS_ENCCL, e.what());
+  } catch (const std::exception& e) {
+    return fail(c, DSS_ERUNTIME, e.what());
+  }
+}
+
+void* dalloc(dss_ctx* c, size_t bytes) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, bytes), "cudaMalloc");
+  ck(cudaMemsetAsync(p, 0, bytes, c->stream), "cudaMemset");
+  c->allocations.push_back(p);
+  return p;
+}
+
+template <typename T>
+T* upload_table(dss_ctx* c, const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = static_cast<T*>(dalloc(c, v.size() * sizeof(T)));
+  ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream),
+     "table upload");
+  ck(cudaStreamSynchronize(c->stream), "table upload sync");
+  return p;
+}
+
+GroupLaunch make_group_launch(dss_ctx* c, const std::vector<std::vector<int>>& groups) {
+  GroupLaunch gl;
+  if (groups.empty()) return gl;
+  std::vector<int> members, offsets{0};
+  gl.size = static_cast<int>(groups[0].size());
+  for (const auto& g : groups) {
+    if (static_cast<int>(g.size()) != gl.size) gl.size = 0;
+    members.insert(members.end(), g.begin(), g.end());
+    offsets.push_back(static_cast<int>(members.size()));
+  }
+  gl.groups = static_cast<int>(groups.size());
+  gl.d_members = upload_table(c, members);
+  gl.d_offsets = upload_table(c, offsets);
+  return gl;
+}
+
+// Local-group launches bucketed by group size so each uses a templated,
+// fully unrolled member loop.
+std::vector<GroupLaunch> make_bucketed(dss_ctx* c, const std::vector<std::vector<int>>& groups) {
+  std::vector<GroupLaunch> out;
+  std::vector<int> sizes;
+  for (const auto& g : groups) {
+    if (std::find(sizes.begin(), sizes.end(), static_cast<int>(g.size())) == sizes.end()) {
+      sizes.push_back(static_cast<int>(g.size()));
+    }
+  }
+  for (int s : sizes) {
+    std::vector<std::vector<int>> b;
+    for (const auto& g : groups) {
+      if (static_cast<int>(g.size()) == s) b.push_back(g);
+    }
+    out.push_back(make_group_launch(c, b));
+  }
+  return out;
+}
+
+bool multi(const dss_ctx* c) { return c->cfg.n_gpus > 1; }
+bool force_fold(const dss_ctx* c) { return c->cfg.path == 1 && !multi(c); }
+
+void* row_ptr(dss_ctx* c, const std::vector<void*>& bases, int rank) {
+  const int gpu = rank / c->P;
+  const int lr = rank - gpu * c->P;
+  return static_cast<char*>(bases[static_cast<size_t>(gpu)]) +
+         static_cast<size_t>(lr) * c->d_pad * c->esz;
+}
+
+// Build the launch tables of one parity.  with_step: DS iteration (local
+// steps fused); otherwise sync_round (fold only).
+ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
+  ParityPlan pp;
+  const dss_strategy& s = c->cfg.strategy;
+  const Partition part = make_partition(s, t);
+  const int G = multi(c) ? c->cfg.n_gpus : 1;
+  std::vector<std::vector<int>> local, span_members;
+  std::vector<Slice> owned;
+
+  if (force_fold(c)) {
+    // Every multi-member group takes the two-shot path with one virtual
+    // owner per member (slices split m ways), all on this device.
+    for (int gi = 0; gi < part.n_groups(); ++gi) {
+      const int* mem = part.group(gi);
+      const int m = part.size(gi);
+      if (m == 1) {
+        local.push_back({mem[0]});
+        continue;
+      }
+      pp.any_spanning = true;
+      for (int j = 0; j < m; ++j) span_members.push_back({mem[j]});
+      for (int j = 0; j < m; ++j) {
+        Slice sl;
+        sl.group = gi;
+        slice_range(c->d_pad, m, j, &sl.lo, &sl.hi);
+        if (sl.hi > sl.lo) owned.push_back(sl);
+      }
+    }
+  } else {
+    const GpuPlan gp = make_plan(part, s.world_size, G, multi(c) ? c->cfg.rank : 0, c->d_pad);
+    pp.any_spanning = gp.any_spanning_globally;
+    for (int gi : gp.local_groups) {
+      local.emplace_back(part.group(gi), part.group(gi) + part.size(gi));
+    }
+    for (int r : gp.spanning_local_members) span_members.push_back({r});
+    owned = gp.owned;
+  }
+
+  pp.local = make_bucketed(c, local);
+  if (with_step) pp.spanning_step = make_group_launch(c, span_members);
+
+  if (!owned.empty()) {
+    std::vector<FoldEntry> entries;
+    std::vector<void*> src, dst;
+    std::vector<void*> wb = multi(c) ? c->peer_w : std::vector<void*>{c->w};
+    FoldLaunch& fl = pp.fold;
+    fl.uniform_m = part.size(owned[0].group);
+    for (const Slice& sl : owned) {
+      const int* mem = part.group(sl.group);
+      const int m = part.size(sl.group);
+      if (m != fl.uniform_m) fl.uniform_m = 0;
+      FoldEntry e{};
+      e.src_beg = static_cast<int>(src.size());
+      e.src_cnt = m;
+      e.dst_beg = static_cast<int>(dst.size());
+      e.dst_cnt = m;
+      e.lo = sl.lo;
+      e.hi = sl.hi;
+      e.err_rank = mem[0];
+      e.err_phase = s.kind == DSS_BSP ? 0 : 1;
+      for (int j = 0; j < m; ++j) {
+        void* p = row_ptr(c, wb, mem[j]);
+        src.push_back(p);
+        dst.push_back(p);
+      }
+      fl.max_len = std::max(fl.max_len, sl.hi - sl.lo);
+      entries.push_back(e);
+    }
+    fl.entries = static_cast<int>(entries.size());
+    fl.d_entries = upload_table(c, entries);
+    fl.d_src = upload_table(c, src);
+    fl.d_dst = upload_table(c, dst);
+  }
+  pp.built = true;
+  return pp;
+}
+
+// BSP across GPUs: this GPU's owned slice of the world group folds all W
+// gradients (peer rows) and writes the mean gradient slice into every GPU's
+// mean-gradient row.
+ParityPlan build_bsp_multi_plan(dss_ctx* c) {
+  ParityPlan pp;
+  const int G = c->cfg.n_gpus;
+  const int W = c->cfg.strategy.world_size;
+  pp.any_spanning = true;
+  std::vector<std::vector<int>> singles;
+  for (int k = 0; k < c->P; ++k) singles.push_back({c->first + k});
+  pp.spanning_step = make_group_launch(c, singles);
+  Slice sl;
+  slice_range(c->d_pad, G, c->cfg.rank, &sl.lo, &sl.hi);
+  if (sl.hi > sl.lo) {
+    FoldEntry e{};
+    std::vector<void*> src, dst;
+    e.src_beg = 0;
+    e.src_cnt = W;
+    e.dst_beg = 0;
+    e.dst_cnt = G;
+    e.lo = sl.lo;
+    e.hi = sl.hi;
+    e.err_rank = 0;
+    e.err_phase = 0;
+    for (int k = 0; k < W; ++k) src.push_back(row_ptr(c, c->peer_g, k));
+    for (int q = 0; q < G; ++q) dst.push_back(c->peer_mg[static_cast<size_t>(q)]);
+    pp.fold.entries = 1;
+    pp.fold.uniform_m = W;
+    pp.fold.max_len = sl.hi - sl.lo;
+    pp.fold.d_entries = upload_table(c, std::vector<FoldEntry>{e});
+    pp.fold.d_src = upload_table(c, src);
+    pp.fold.d_dst = upload_table(c, dst);
+  }
+  pp.built = true;
+  return pp;
+}
+
+void build_plans(dss_ctx* c) {
+  const dss_strategy& s = c->cfg.strategy;
+  if (s.kind == DSS_DS_SYNC) {
+    for (int p = 0; p < 2; ++p) c->step_plan[p] = build_plan(c, p, true);
+  } else if (multi(c)) {
+    c->step_plan[0] = build_bsp_multi_plan(c);
+  }
+  for (int p = 0; p < 2; ++p) c->sync_plan[p] = build_plan(c, p, false);
+}
+
+// ---- launch helpers ---------------------------------------------------------
+
+struct TimedLaunch {
+  dss_ctx* c;
+  cudaEvent_t b = nullptr, e = nullptr;
+  explicit TimedLaunch(dss_ctx* cc) : c(cc) {
+    ++c->launches;
+    if (!c->timing) return;
+    for (cudaEvent_t* ev : {&b, &e}) {
+      if (!c->ev_pool.empty()) {
+        *ev = c->ev_pool.back();
+        c->ev_pool.pop_back();
+      } else {
+        ck(cudaEventCreate(ev), "cudaEventCreate");
+      }
+    }
+    ck(cudaEventRecord(b, c->stream), "cudaEventRecord");
+  }
+  ~TimedLaunch() {
+    if (!c->timing) return;
+    cudaEventRecord(e, c->stream);
+    c->ev_pending.emplace_back(b, e);
+  }
+};
+
+int grid_x(const dss_ctx* c, long nvec, int ys) {
+  const long want = static_cast<long>(c->sms) * (2048 / kThreads);
+  long gx = (want + ys - 1) / ys;
+  const long need = (nvec + kThreads - 1) / kThreads;
+  gx = std::min(gx, need);
+  return static_cast<int>(std::max(1L, std::min(gx, 65535L)));
+}
+
+template <typename T>
+StepConsts<T> consts(const dss_ctx* c, double alpha) {
+  const dss_hparams& h = c->cfg.hp;
+  StepConsts<T> k;
+  k.alpha = static_cast<T>(alpha);
+  k.wd = static_cast<T>(h.weight_decay);
+  k.mom = static_cast<T>(h.momentum);
+  k.b1 = static_cast<T>(h.beta1);
+  k.omb1 = static_cast<T>(1.0 - h.beta1);
+  k.b2 = static_cast<T>(h.beta2);
+  k.omb2 = static_cast<T>(1.0 - h.beta2);
+  k.eps = static_cast<T>(h.epsilon);
+  k.awd = static_cast<T>(alpha * h.weight_decay);
+  return k;
+}
+
+template <typename Args>
+void fill_bias(const dss_ctx* c, Args& a) {
+  const dss_hparams& h = c->cfg.hp;
+  for (int k = 0; k < c->P; ++k) {
+    const double t = static_cast<double>(c->step_count[static_cast<size_t>(k)] + 1);
+    a.bc1[k] = 1.0 - std::pow(h.beta1, t);  // optim.cpp:76-77
+    a.bc2[k] = 1.0 - std::pow(h.beta2, t);  // optim.cpp:78
+  }
+}
+
+template <typename T, int OPT, int M>
+void launch_group_t(dss_ctx* c, const GroupArgs<T>& a, int groups) {
+  dim3 grid(grid_x(c, a.nvec, groups), groups);
+  TimedLaunch tl(c);
+  ds_group_kernel<T, OPT, M><<<grid, kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "ds_group_kernel launch");
+}
+
+template <typename T, int OPT>
+void launch_group_m(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
+  switch (gl.size) {
+    case 1: launch_group_t<T, OPT, 1>(c, a, gl.groups); break;
+    case 2: launch_group_t<T, OPT, 2>(c, a, gl.groups); break;
+    case 3: launch_group_t<T, OPT, 3>(c, a, gl.groups); break;
+    case 4: launch_group_t<T, OPT, 4>(c, a, gl.groups); break;
+    case 8: launch_group_t<T, OPT, 8>(c, a, gl.groups); break;
+    default: launch_group_t<T, OPT, 0>(c, a, gl.groups); break;
+  }
+}
+
+// opt < 0: fold only (sync_round); otherwise the optimizer kind.
+template <typename T>
+void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha,
+                   const void* g, long g_ld, int step_phase, int sync_phase) {
+  if (gl.groups == 0) return;
+  GroupArgs<T> a{};
+  a.w = static_cast<T*>(c->w);
+  a.g = static_cast<const T*>(g);
+  a.m1 = static_cast<T*>(c->m1);
+  a.m2 = static_cast<T*>(c->m2);
+  a.ld = c->d_pad;
+  a.g_ld = g_ld;
+  a.nvec = c->d_pad / Vec<T>::n;
+  a.first_rank = c->first;
+  a.members = gl.d_members;
+  a.offsets = gl.d_offsets;
+  a.step_phase = step_phase;
+  a.sync_phase = sync_phase;
+  a.t = t;
+  a.c = consts<T>(c, alpha);
+  fill_bias(c, a);
+  a.err = c->d_err;
+  switch (opt) {
+    case kOptNone: launch_group_m<T, kOptNone>(c, a, gl); break;
+    case kSgd: launch_group_m<T, kSgd>(c, a, gl); break;
+    case kMomentum: launch_group_m<T, kMomentum>(c, a, gl); break;
+    case kAdam: launch_group_m<T, kAdam>(c, a, gl); break;
+    case kAdamW: launch_group_m<T, kAdamW>(c, a, gl); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+}
+
+void launch_groups_any(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha,
+                       const void* g, long g_ld, int step_phase, int sync_phase = 1) {
+  if (c->cfg.dtype == DSS_F64) {
+    launch_groups<double>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase);
+  } else {
+    launch_groups<float>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase);
+  }
+}
+
+template <typename T, int M>
+void launch_fold_t(dss_ctx* c, const FoldLaunch& fl, long t) {
+  FoldArgs<T> a{};
+  a.src = reinterpret_cast<T* const*>(fl.d_src);
+  a.dst = reinterpret_cast<T* const*>(fl.d_dst);
+  a.entries = fl.d_entries;
+  a.t = t;
+  a.err = c->d_err;
+  dim3 grid(grid_x(c, fl.max_len / Vec<T>::n, fl.entries), fl.entries);
+  TimedLaunch tl(c);
+  fold_kernel<T, M><<<grid, kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "fold_kernel launch");
+}
+
+template <typename T>
+void launch_fold(dss_ctx* c, const FoldLaunch& fl, long t) {
+  if (fl.entries == 0) return;
+  switch (fl.uniform_m) {
+    case 2: launch_fold_t<T, 2>(c, fl, t); break;
+    case 4: launch_fold_t<T, 4>(c, fl, t); break;
+    case 8: launch_fold_t<T, 8>(c, fl, t); break;
+    default: launch_fold_t<T, 0>(c, fl, t); break;
+  }
+}
+
+void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
+  if (c->cfg.dtype == DSS_F64) {
+    launch_fold<double>(c, fl, t);
+  } else {
+    launch_fold<float>(c, fl, t);
+  }
+}
+
+template <typename T, int OPT, int WT>
+void launch_bsp_t(dss_ctx* c, const BspArgs<T>& a) {
+  dim3 grid(grid_x(c, a.nvec, 1), 1);
+  TimedLaunch tl(c);
+  bsp_kernel<T, OPT, WT><<<grid, kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "bsp_kernel launch");
+}
+
+template <typename T, int OPT>
+void launch_bsp_w(dss_ctx* c, const BspArgs<T>& a) {
+  switch (a.nw) {
+    case 2: launch_bsp_t<T, OPT, 2>(c, a); break;
+    case 4: launch_bsp_t<T, OPT, 4>(c, a); break;
+    case 8: launch_bsp_t<T, OPT, 8>(c, a); break;
+    default: launch_bsp_t<T, OPT, 0>(c, a); break;
+  }
+}
+
+template <typename T>
+void launch_bsp(dss_ctx* c, long t, double alpha) {
+  BspArgs<T> a{};
+  a.w = static_cast<T*>(c->w);
+  a.g = static_cast<const T*>(c->g);
+  a.m1 = static_cast<T*>(c->m1);
+  a.m2 = static_cast<T*>(c->m2);
+  a.ld = c->d_pad;
+  a.nvec = c->d_pad / Vec<T>::n;
+  a.nw = c->P;
+  a.t = t;
+  a.c = consts<T>(c, alpha);
+  fill_bias(c, a);
+  a.err = c->d_err;
+  switch (c->cfg.optimizer) {
+    case kSgd: launch_bsp_w<T, kSgd>(c, a); break;
+    case kMomentum: launch_bsp_w<T, kMomentum>(c, a); break;
+    case kAdam: launch_bsp_w<T, kAdam>(c, a); break;
+    case kAdamW: launch_bsp_w<T, kAdamW>(c, a); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+}
+
+void barrier(dss_ctx* c) {
+  if (!multi(c)) return;
+  if (!c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
+  ++c->epoch;
+  TimedLaunch tl(c);
+  barrier_kernel<<<1, 32 * ((c->cfg.n_gpus + 31) / 32), 0, c->stream>>>(
+      c->d_peer_flags, c->flags, c->cfg.rank, c->cfg.n_gpus, c->epoch, c->d_timeout);
+  ck(cudaGetLastError(), "barrier_kernel launch");
+}
+
+// Peers may still be writing group means into our rows (two-shot phase 2 of
+// the previous round): wait for them before touching the rows again.
+void quiesce(dss_ctx* c) {
+  if (c->pending_remote && multi(c)) barrier(c);
+  c->pending_remote = false;
+}
+
+void bump_steps(dss_ctx* c) {
+  for (auto& s : c->step_count) ++s;
+}
+
+int check_impl(dss_ctx* c) {
+  ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+  ck(cudaMemcpy(c->h_err, c->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost), "err readback");
+  unsigned long long timeout = 0;
+  if (c->d_timeout) {
+    ck(cudaMemcpy(&timeout, c->d_timeout, sizeof(timeout), cudaMemcpyDeviceToHost), "timeout readback");
+  }
+  if (timeout) return fail(c, DSS_ENCCL, "cross-GPU barrier timed out (peer did not arrive)");
+  const unsigned long long key = *c->h_err;
+  if (key == ~0ull) return DSS_OK;
+  const long t = static_cast<long>(key >> 34);
+  const int phase = static_cast<int>((key >> 32) & 3);
+  const int rank = static_cast<int>(key & 0xffffffffu);
+  std::string what;
+  const bool bsp = c->cfg.strategy.kind == DSS_BSP;
+  const bool local_step = bsp ? phase == 1 : phase == 0;
+  if (local_step) {
+    what = "apply_step: non-finite value in result";  // optim.cpp:96 via sync.cpp:257-261
+  } else {
+    what = std::string(collective_name(c->cfg.strategy.topology)) + ": non-finite value in result";
+  }
+  // DivergenceError text (errors.hpp:17-19)
+  const std::string msg = "worker " + std::to_string(rank) + " diverged at iteration " +
+                          std::to_string(t) + ": " + what;
+  return fail(c, DSS_EDIVERGED, msg, rank, t);
+}
+
+int check_rank(dss_ctx* c, int rank, int* lr) {
+  if (rank < c->first || rank >= c->first + c->P) {
+    throw std::invalid_argument("rank " + std::to_string(rank) + " is not hosted on this GPU");
+  }
+  *lr = rank - c->first;
+  return DSS_OK;
+}
+
+void* buffer_base(dss_ctx* c, int buffer) {
+  switch (buffer) {
+    case DSS_BUF_PARAMS: return c->w;
+    case DSS_BUF_GRADS: return c->g;
+    case DSS_BUF_MOMENT1:
+      if (!c->m1) throw std::invalid_argument("optimizer has no first moment buffer");
+      return c->m1;
+    case DSS_BUF_MOMENT2:
+      if (!c->m2) throw std::invalid_argument("optimizer has no second moment buffer");
+      return c->m2;
+    default: throw std::invalid_argument("unknown buffer id");
+  }
+}
+
+}  // namespace
+
+// ============================ schedule (host) ===============================
+
+extern "C" int dss_validate_world(int world_size, int group_size, int rectangular) {
+  return guard(nullptr, [&]() -> int {
+    validate_world(world_size, group_size, rectangular != 0);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_validate_strategy(const dss_strategy* s) {
+  return guard(nullptr, [&]() -> int {
+    if (!s) throw std::invalid_argument("null strategy");
+    validate_strategy(*s);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_is_square_mode(int world_size, int group_size) {
+  return is_square_mode(world_size, group_size) ? 1 : 0;
+}
+
+extern "C" int dss_partition(const dss_strategy* s, long t, int* members, int* offsets, int* n_groups) {
+  return guard(nullptr, [&]() -> int {
+    if (!s || !members || !offsets || !n_groups) throw std::invalid_argument("null argument");
+    if (s->kind == DSS_BSP) validate_strategy(*s);
+    const Partition p = make_partition(*s, t);
+    std::copy(p.members.begin(), p.members.end(), members);
+    std::copy(p.offsets.begin(), p.offsets.end(), offsets);
+    *n_groups = p.n_groups();
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_group_of(const dss_strategy* s, long t, int rank, int* members, int* count) {
+  return guard(nullptr, [&]() -> int {
+    if (!s || !members || !count) throw std::invalid_argument("null argument");
+    const std::vector<int> g = group_of(*s, t, rank);
+    std::copy(g.begin(), g.end(), members);
+    *count = static_cast<int>(g.size());
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_check_mixing(const dss_strategy* s, long t) {
+  int result = 0;
+  const int st = guard(nullptr, [&]() -> int {
+    if (!s) throw std::invalid_argument("null strategy");
+    result = check_mixing(*s, t) ? 1 : 0;
+    return DSS_OK;
+  });
+  return st == DSS_OK ? result : -st;
+}
+
+extern "C" int dss_round_outcome(const dss_strategy* s, long t, long payload_dim, dss_outcome* out) {
+  return guard(nullptr, [&]() -> int {
+    if (!s || !out) throw std::invalid_argument("null argument");
+    validate_strategy(*s);
+    *out = round_outcome(*s, t, payload_dim);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_plan(const dss_strategy* s, long t, long dim, int n_gpus, int rank,
+                        dss_plan_summary* out, long* slice_lo, long* slice_hi, int* slice_group,
+                        int max_slices) {
+  return guard(nullptr, [&]() -> int {
+    if (!s || !out) throw std::invalid_argument("null argument");
+    validate_strategy(*s);
+    if (n_gpus < 1 || s->world_size % n_gpus != 0) {
+      throw std::invalid_argument("world_size must be a multiple of n_gpus");
+    }
+    if (rank < 0 || rank >= n_gpus) throw std::invalid_argument("gpu rank out of range");
+    const Partition p = make_partition(*s, t);
+    const GpuPlan gp = make_plan(p, s->world_size, n_gpus, rank, pad_dim(dim));
+    out->local_groups = static_cast<int>(gp.local_groups.size());
+    out->spanning_groups = static_cast<int>(gp.spanning_groups.size());
+    out->owned_slices = static_cast<int>(gp.owned.size());
+    out->owned_elems = 0;
+    for (size_t i = 0; i < gp.owned.size(); ++i) {
+      out->owned_elems += gp.owned[i].hi - gp.owned[i].lo;
+      if (static_cast<int>(i) < max_slices) {
+        if (slice_lo) slice_lo[i] = gp.owned[i].lo;
+        if (slice_hi) slice_hi[i] = gp.owned[i].hi;
+        if (slice_group) slice_group[i] = gp.owned[i].group;
+      }
+    }
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_last_global_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::snprintf(buf, len, "%s", g_last_global_error.c_str());
+  }
+  return DSS_OK;
+}
+
+// ============================== context =====================================
+
+extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
+  if (!cfg || !out) return fail(nullptr, DSS_EINVAL, "null argument");
+  *out = nullptr;
+  auto c = std::make_unique<dss_ctx>();
+  int st = guard(c.get(), [&]() -> int {
+    c->cfg = *cfg;
+    const dss_strategy& s = cfg->strategy;
+    validate_strategy(s);
+    if (cfg->dim < 1) throw std::invalid_argument("dim must be >= 1");
+    if (cfg->dtype != DSS_F32 && cfg->dtype != DSS_F64) throw std::invalid_argument("unknown dtype");
+    if (cfg->optimizer < DSS_VANILLA_SGD || cfg->optimizer > DSS_ADAMW) {
+      throw std::invalid_argument("unknown optimizer kind");
+    }
+    if (cfg->n_gpus < 1 || s.world_size % cfg->n_gpus != 0) {
+      throw std::invalid_argument("world_size must be a multiple of n_gpus");
+    }
+    if (cfg->rank < 0 || cfg->rank >= cfg->n_gpus) throw std::invalid_argument("rank out of range");
+    c->P = s.world_size / cfg->n_gpus;
+    if (c->P > kMaxLocal) {
+      throw std::invalid_argument("at most " + std::to_string(kMaxLocal) + " workers per GPU");
+    }
+    c->first = cfg->rank * c->P;
+    c->d = cfg->dim;
+    c->d_pad = pad_dim(cfg->dim);
+    c->esz = cfg->dtype == DSS_F64 ? 8 : 4;
+    c->step_count.assign(static_cast<size_t>(c->P), 0);
+
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (cfg->device < 0 || cfg->device >= ndev) throw CudaError("no CUDA device " + std::to_string(cfg->device));
+    ck(cudaSetDevice(cfg->device), "cudaSetDevice");
+    ck(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg->device), "sm count");
+    ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own_stream;
+
+    const size_t rows = static_cast<size_t>(c->P) * c->d_pad * c->esz;
+    c->w = dalloc(c.get(), rows);
+    c->g = dalloc(c.get(), rows);
+    if (cfg->optimizer != DSS_VANILLA_SGD) c->m1 = dalloc(c.get(), rows);
+    if (cfg->optimizer == DSS_ADAM || cfg->optimizer == DSS_ADAMW) c->m2 = dalloc(c.get(), rows);
+    c->mg = dalloc(c.get(), static_cast<size_t>(c->d_pad) * c->esz);
+    c->wstar = dalloc(c.get(), static_cast<size_t>(c->d_pad) * c->esz);
+    c->d_err = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
+    ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream), "err init");
+    c->d_timeout = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
+    c->flags = static_cast<unsigned long long*>(
+        dalloc(c.get(), sizeof(unsigned long long) * static_cast<size_t>(std::max(cfg->n_gpus, 32))));
+    ck(cudaMallocHost(&c->h_err, sizeof(unsigned long long)), "cudaMallocHost");
+
+    std::vector<std::vector<int>> singles;
+    for (int k = 0; k < c->P; ++k) singles.push_back({c->first + k});
+    c->apply_launch = make_group_launch(c.get(), singles);
+    if (!multi(c.get())) build_plans(c.get());
+    ck(cudaStreamSynchronize(c->stream), "create sync");
+    return DSS_OK;
+  });
+  if (st != DSS_OK) {
+    g_last_global_error = c->last_error;
+    dss_destroy(c.release());
+    return st;
+  }
+  *out = c.release();
+  return DSS_OK;
+}
+
+extern "C" int dss_destroy(dss_ctx* c) {
+  if (!c) return DSS_OK;
+  if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (void* p : c->allocations) cudaFree(p);
+  for (auto& pr : c->ev_pending) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+  return DSS_OK;
+}
+
+extern "C" int dss_set_stream(dss_ctx* c, void* s) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(c->stream), "stream switch sync");
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_local_workers(const dss_ctx* c, int* first_rank, int* count) {
+  if (!c || !first_rank || !count) return DSS_EINVAL;
+  *first_rank = c->first;
+  *count = c->P;
+  return DSS_OK;
+}
+
+extern "C" long dss_row_stride(const dss_ctx* c) { return c ? c->d_pad : -1; }
+extern "C" int dss_elem_size(const dss_ctx* c) { return c ? c->esz : -1; }
+
+extern "C" int dss_device_ptr(dss_ctx* c, int buffer, int rank, void** out) {
+  if (!c || !out) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    int lr = 0;
+    check_rank(c, rank, &lr);
+    *out = static_cast<char*>(buffer_base(c, buffer)) + static_cast<size_t>(lr) * c->d_pad * c->esz;
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_upload(dss_ctx* c, int buffer, int rank, const void* host, long n) {
+  if (!c || !host) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    int lr = 0;
+    check_rank(c, rank, &lr);
+    if (n < 0 || n > c->d) throw std::invalid_argument("upload length exceeds dim");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    char* dst = static_cast<char*>(buffer_base(c, buffer)) + static_cast<size_t>(lr) * c->d_pad * c->esz;
+    ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(n) * c->esz, cudaMemcpyHostToDevice, c->stream),
+       "upload");
+    ck(cudaStreamSynchronize(c->stream), "upload sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_download(dss_ctx* c, int buffer, int rank, void* host, long n) {
+  if (!c || !host) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    int lr = 0;
+    check_rank(c, rank, &lr);
+    if (n < 0 || n > c->d) throw std::invalid_argument("download length exceeds dim");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    const char* src = static_cast<const char*>(buffer_base(c, buffer)) + static_cast<size_t>(lr) * c->d_pad * c->esz;
+    ck(cudaMemcpyAsync(host, src, static_cast<size_t>(n) * c->esz, cudaMemcpyDeviceToHost, c->stream),
+       "download");
+    ck(cudaStreamSynchronize(c->stream), "download sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_upload_all(dss_ctx* c, int buffer, const void* host) {
+  if (!c || !host) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    const size_t row = static_cast<size_t>(c->d) * c->esz;
+    ck(cudaMemcpy2DAsync(buffer_base(c, buffer), static_cast<size_t>(c->d_pad) * c->esz, host, row, row,
+                         static_cast<size_t>(c->P), cudaMemcpyHostToDevice, c->stream),
+       "upload_all");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_download_all(dss_ctx* c, int buffer, void* host) {
+  if (!c || !host) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    const size_t row = static_cast<size_t>(c->d) * c->esz;
+    ck(cudaMemcpy2DAsync(host, row, buffer_base(c, buffer), static_cast<size_t>(c->d_pad) * c->esz, row,
+                         static_cast<size_t>(c->P), cudaMemcpyDeviceToHost, c->stream),
+       "download_all");
+    ck(cudaStreamSynchronize(c->stream), "download_all sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_broadcast_row(dss_ctx* c, int buffer, const void* host_row) {
+  if (!c || !host_row) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    char* base = static_cast<char*>(buffer_base(c, buffer));
+    const size_t row = static_cast<size_t>(c->d) * c->esz;
+    for (int k = 0; k < c->P; ++k) {
+      ck(cudaMemcpyAsync(base + static_cast<size_t>(k) * c->d_pad * c->esz, host_row, row,
+                         cudaMemcpyHostToDevice, c->stream),
+         "broadcast_row");
+    }
+    ck(cudaStreamSynchronize(c->stream), "broadcast sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_set_step_count(dss_ctx* c, int rank, long step_count) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    int lr = 0;
+    check_rank(c, rank, &lr);
+    if (step_count < 0) throw std::invalid_argument("step_count must be >= 0");
+    c->step_count[static_cast<size_t>(lr)] = step_count;
+    return DSS_OK;
+  });
+}
+
+extern "C" long dss_get_step_count(const dss_ctx* c, int rank) {
+  if (!c || rank < c->first || rank >= c->first + c->P) return -1;
+  return c->step_count[static_cast<size_t>(rank - c->first)];
+}
+
+// ------------------------------- hot path ------------------------------------
+
+extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome* out) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (t < 0) throw std::invalid_argument("iteration must be >= 0");
+    // run_training (sync.cpp:324-328) / check_step_args (optim.cpp:33-35)
+    if (!std::isfinite(alpha) || alpha < 0.0) {
+      throw std::invalid_argument("learning rate at t=" + std::to_string(t) + " must be finite and >= 0");
+    }
+    if (multi(c) && !c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const dss_strategy& s = c->cfg.strategy;
+    const int opt = c->cfg.optimizer;
+    if (s.kind == DSS_DS_SYNC) {
+      const ParityPlan& pp = c->step_plan[t & 1];
+      quiesce(c);
+      // Local groups: fused apply_step + ordered fold + broadcast.
+      for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
+      if (pp.any_spanning) {
+        // Members of spanning groups step in place, then (after every GPU
+        // has stepped) each owner folds its slice over NVLink.
+        launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->g, c->d_pad, 0);
+        if (multi(c)) barrier(c);
+        launch_fold_any(c, pp.fold, t);
+        c->pending_remote = multi(c);
+      }
+    } else if (!multi(c)) {
+      if (c->cfg.dtype == DSS_F64) {
+        launch_bsp<double>(c, t, alpha);
+      } else {
+        launch_bsp<float>(c, t, alpha);
+      }
+    } else {
+      // BSP over GPUs: barrier (gradients final everywhere), ordered fold of
+      // all W gradients into every GPU's mean-gradient row, barrier, local
+      // apply_step of every replica with the shared mean gradient.
+      const ParityPlan& pp = c->step_plan[0];
+      c->pending_remote = false;
+      barrier(c);
+      launch_fold_any(c, pp.fold, t);
+      barrier(c);
+      launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->mg, 0, 1);
+    }
+    bump_steps(c);
+    if (out) *out = round_outcome(s, t, c->d);
+    if (check) return check_impl(c);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_sync_round(dss_ctx* c, long t, int check, dss_outcome* out) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    const dss_strategy& s = c->cfg.strategy;
+    validate_strategy(s);  // sync.cpp:270
+    if (t < 0 && s.kind == DSS_DS_SYNC) throw std::invalid_argument("iteration must be >= 0");
+    if (multi(c) && !c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const ParityPlan& pp = c->sync_plan[s.kind == DSS_DS_SYNC ? (t & 1) : 0];
+    quiesce(c);
+    const int phase = s.kind == DSS_BSP ? 0 : 1;  // collective failure: members[0] (sync.cpp:233-235)
+    for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, kOptNone, t, 0.0, nullptr, 0, 0, phase);
+    if (pp.any_spanning) {
+      if (multi(c)) barrier(c);
+      launch_fold_any(c, pp.fold, t);
+      c->pending_remote = multi(c);
+    }
+    if (out) *out = round_outcome(s, t, c->d);
+    if (check) return check_impl(c);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_apply_step(dss_ctx* c, double alpha, int check) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (!std::isfinite(alpha) || alpha < 0.0) {
+      throw std::invalid_argument("apply_step: alpha must be finite and >= 0");  // optim.cpp:33-35
+    }
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    launch_groups_any(c, c->apply_launch, c->cfg.optimizer, 0, alpha, c->g, c->d_pad, 0);
+    bump_steps(c);
+    if (check) return check_impl(c);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_quadratic_gradients(dss_ctx* c, long t, uint64_t seed, double mu, double sigma) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (!(mu > 0.0)) throw std::invalid_argument("quadratic requires problem.mu > 0");
+    if (sigma < 0.0) throw std::invalid_argument("problem.sigma must be >= 0");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    const double scale = sigma > 0.0 ? sigma / std::sqrt(static_cast<double>(c->d)) : 0.0;
+    auto run = [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      GradArgs<T> a{};
+      a.w = static_cast<const T*>(c->w);
+      a.g = static_cast<T*>(c->g);
+      a.wstar = static_cast<const T*>(c->wstar);
+      a.ld = c->d_pad;
+      a.d = c->d;
+      a.nlocal = c->P;
+      a.mu = mu;
+      a.scale = scale;
+      for (int k = 0; k < c->P; ++k) {
+        a.s0[k] = stream_state(seed, kGradientNoise, static_cast<uint64_t>(c->first + k), static_cast<uint64_t>(t));
+      }
+      dim3 grid(grid_x(c, c->d_pad, c->P), c->P);
+      TimedLaunch tl(c);
+      quad_grad_kernel<T><<<grid, kThreads, 0, c->stream>>>(a);
+      ck(cudaGetLastError(), "quad_grad_kernel launch");
+    };
+    if (c->cfg.dtype == DSS_F64) {
+      run(static_cast<double*>(nullptr));
+    } else {
+      run(static_cast<float*>(nullptr));
+    }
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_quadratic_init(dss_ctx* c, uint64_t problem_seed, double delta0) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (!(delta0 > 0.0)) throw std::invalid_argument("problem.delta0 must be > 0");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    double *ws = nullptr, *u = nullptr, *ss = nullptr;
+    ck(cudaMalloc(&ws, sizeof(double) * c->d), "cudaMalloc");
+    ck(cudaMalloc(&u, sizeof(double) * c->d), "cudaMalloc");
+    ck(cudaMalloc(&ss, sizeof(double)), "cudaMalloc");
+    ck(cudaMemsetAsync(ss, 0, sizeof(double), c->stream), "memset");
+    const int gx = grid_x(c, c->d, 1);
+    gaussian_fill_kernel<<<gx, kThreads, 0, c->stream>>>(ws, c->d, stream_state(problem_seed, kDataGen, 1, 0));
+    gaussian_fill_kernel<<<gx, kThreads, 0, c->stream>>>(u, c->d, stream_state(problem_seed, kInitParams, 0, 0));
+    sumsq_kernel<<<gx, kThreads, 0, c->stream>>>(u, c->d, ss);
+    const double r = std::sqrt(delta0);
+    const int gp = grid_x(c, c->d_pad, 1);
+    if (c->cfg.dtype == DSS_F64) {
+      compose_init_kernel<double><<<gp, kThreads, 0, c->stream>>>(ws, u, ss, c->d, c->d_pad, r,
+                                                                 static_cast<double*>(c->wstar),
+                                                                 static_cast<double*>(c->w));
+      broadcast_row_kernel<double><<<grid_x(c, c->d_pad * c->P, 1), kThreads, 0, c->stream>>>(
+          static_cast<double*>(c->w), c->d_pad, c->P, static_cast<double*>(c->w));
+    } else {
+      compose_init_kernel<float><<<gp, kThreads, 0, c->stream>>>(ws, u, ss, c->d, c->d_pad, r,
+                                                                static_cast<float*>(c->wstar),
+                                                                static_cast<float*>(c->w));
+      broadcast_row_kernel<float><<<grid_x(c, c->d_pad * c->P, 1), kThreads, 0, c->stream>>>(
+          static_cast<float*>(c->w), c->d_pad, c->P, static_cast<float*>(c->w));
+    }
+    ck(cudaGetLastError(), "init kernels");
+    ck(cudaStreamSynchronize(c->stream), "init sync");
+    cudaFree(ws);
+    cudaFree(u);
+    cudaFree(ss);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_set_optimum(dss_ctx* c, const void* host, long n) {
+  if (!c || !host) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (n < 0 || n > c->d) throw std::invalid_argument("optimum length exceeds dim");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaMemcpyAsync(c->wstar, host, static_cast<size_t>(n) * c->esz, cudaMemcpyHostToDevice, c->stream),
+       "set_optimum");
+    ck(cudaStreamSynchronize(c->stream), "set_optimum sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_check(dss_ctx* c) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    return check_impl(c);
+  });
+}
+
+extern "C" int dss_clear_error(dss_ctx* c) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream), "err reset");
+    ck(cudaMemsetAsync(c->d_timeout, 0, sizeof(unsigned long long), c->stream), "timeout reset");
+    ck(cudaStreamSynchronize(c->stream), "err reset sync");
+    c->last_status = DSS_OK;
+    c->last_error.clear();
+    c->last_rank = -1;
+    c->last_iteration = -1;
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_last_error(const dss_ctx* c, char* buf, size_t len, int* rank, long* iteration) {
+  if (!c) {
+    if (buf && len) std::snprintf(buf, len, "%s", g_last_global_error.c_str());
+    return DSS_EINVAL;
+  }
+  if (buf && len) std::snprintf(buf, len, "%s", c->last_error.c_str());
+  if (rank) *rank = c->last_rank;
+  if (iteration) *iteration = c->last_iteration;
+  return c->last_status;
+}
+
+extern "C" int dss_enable_timing(dss_ctx* c, int on) {
+  if (!c) return DSS_EINVAL;
+  c->timing = on != 0;
+  return DSS_OK;
+}
+
+extern "C" int dss_kernel_times(dss_ctx* c, double* total_ms, long* launches, double* max_launch_ms) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(c->stream), "timing sync");
+    double tot = 0.0, mx = 0.0;
+    for (auto& pr : c->ev_pending) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "cudaEventElapsedTime");
+      tot += ms;
+      mx = std::max(mx, static_cast<double>(ms));
+      c->ev_pool.push_back(pr.first);
+      c->ev_pool.push_back(pr.second);
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = static_cast<long>(c->ev_pending.size());
+    if (max_launch_ms) *max_launch_ms = mx;
+    c->ev_pending.clear();
+    return DSS_OK;
+  });
+}
+
+extern "C" long dss_launch_count(const dss_ctx* c) { return c ? c->launches : -1; }
+
+// ------------------------------- multi-GPU -----------------------------------
+
+extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
+  if (!c || !out) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    cudaIpcMemHandle_t h[4];
+    ck(cudaIpcGetMemHandle(&h[0], c->w), "cudaIpcGetMemHandle(params)");
+    ck(cudaIpcGetMemHandle(&h[1], c->g), "cudaIpcGetMemHandle(grads)");
+    ck(cudaIpcGetMemHandle(&h[2], c->mg), "cudaIpcGetMemHandle(mean grad)");
+    ck(cudaIpcGetMemHandle(&h[3], c->flags), "cudaIpcGetMemHandle(flags)");
+    std::memcpy(out, h, sizeof(h));
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
+  if (!c || !all) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (!multi(c)) throw std::invalid_argument("dss_ipc_attach needs n_gpus > 1");
+    if (c->attached) throw std::invalid_argument("already attached");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const int G = c->cfg.n_gpus;
+    c->peer_w.assign(static_cast<size_t>(G), nullptr);
+    c->peer_g.assign(static_cast<size_t>(G), nullptr);
+    c->peer_mg.assign(static_cast<size_t>(G), nullptr);
+    c->peer_flag.assign(static_cast<size_t>(G), nullptr);
+    const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
+    for (int r = 0; r < G; ++r) {
+      if (r == c->cfg.rank) {
+        c->peer_w[static_cast<size_t>(r)] = c->w;
+        c->peer_g[static_cast<size_t>(r)] = c->g;
+        c->peer_mg[static_cast<size_t>(r)] = c->mg;
+        c->peer_flag[static_cast<size_t>(r)] = c->flags;
+        continue;
+      }
+      void* p[4];
+      for (int b = 0; b < 4; ++b) {
+        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 4 + b], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          throw PeerError("cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
+        }
+        c->opened.push_back(p[b]);
+      }
+      c->peer_w[static_cast<size_t>(r)] = p[0];
+      c->peer_g[static_cast<size_t>(r)] = p[1];
+      c->peer_mg[static_cast<size_t>(r)] = p[2];
+      c->peer_flag[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[3]);
+    }
+    c->d_peer_flags = upload_table(c, c->peer_flag);
+    build_plans(c);
+    c->attached = true;
+    barrier(c);
+    ck(cudaStreamSynchronize(c->stream), "attach sync");
+    return check_impl(c) == DSS_OK ? DSS_OK : c->last_status;
+  });
+}
+
+extern "C" int dss_barrier(dss_ctx* c) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    barrier(c);
+    return DSS_OK;
+  });
+}

@@ -1,0 +1,540 @@
+// sm_100a kernels of the DS-Sync step.
+//
+// Bandwidth-bound elementwise/reduction work: no tensor cores.  Every
+// kernel streams worker rows with 128-bit vector loads/stores, one thread
+// per vector, grid sized in multiples of the 148 SMs.  The reduction axis is
+// the *member* axis (group size <= 8 typically) and its order is pinned by
+// the reference (param.hpp:21-24): acc = x_0; acc += x_k ascending;
+// acc *= 1/m.  One thread owns an element vector and folds all members in
+// registers in that order, so no tree/shuffle ever re-associates the sum.
+//
+// All arithmetic goes through explicit round-to-nearest intrinsics
+// (__fadd_rn/__dmul_rn ...), which are never contracted into FMA, matching
+// the reference's SSE2 build without FMA contraction.  The file
+// is also compiled with -fmad=false.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dssb {
+
+constexpr int kThreads = 256;
+constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel params
+
+enum OptKind : int { kOptNone = -1, kSgd = 0, kMomentum = 1, kAdam = 2, kAdamW = 3 };
+
+// ---- exact scalar ops ------------------------------------------------------
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ bool finite_(float a) { return isfinite(a); }
+__device__ __forceinline__ bool finite_(double a) { return isfinite(a); }
+
+// ---- 16-byte vectors ---------------------------------------------------------
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  using type = float4;
+  static constexpr int n = 4;
+};
+template <> struct Vec<double> {
+  using type = double2;
+  static constexpr int n = 2;
+};
+
+template <typename T> struct Pack {
+  T v[Vec<T>::n];
+};
+
+// Streaming loads/stores (evict-first): every byte is touched once per
+// iteration and the working set is far larger than L2.
+template <typename T>
+__device__ __forceinline__ Pack<T> ldv(const T* p) {
+  Pack<T> r;
+  typename Vec<T>::type x = __ldcs(reinterpret_cast<const typename Vec<T>::type*>(p));
+  static_assert(sizeof(x) == sizeof(r), "pack");
+  *reinterpret_cast<typename Vec<T>::type*>(r.v) = x;
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void stv(T* p, const Pack<T>& r) {
+  __stcs(reinterpret_cast<typename Vec<T>::type*>(p),
+         *reinterpret_cast<const typename Vec<T>::type*>(r.v));
+}
+// Peer/remote rows: cache-global accesses (no L1 allocation); peer
+// addresses bypass the local L2 anyway.
+template <typename T>
+__device__ __forceinline__ Pack<T> ldv_cg(const T* p) {
+  Pack<T> r;
+  *reinterpret_cast<typename Vec<T>::type*>(r.v) =
+      __ldcg(reinterpret_cast<const typename Vec<T>::type*>(p));
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void stv_cg(T* p, const Pack<T>& r) {
+  __stcg(reinterpret_cast<typename Vec<T>::type*>(p),
+         *reinterpret_cast<const typename Vec<T>::type*>(r.v));
+}
+
+// ---- optimizer constants for one launch (rounded once from double) ---------
+template <typename T> struct StepConsts {
+  T alpha;   // a
+  T wd;      // weight_decay
+  T mom;     // momentum
+  T b1, omb1;  // beta1, 1 - beta1 (computed in double, optim.cpp:84)
+  T b2, omb2;  // beta2, 1 - beta2
+  T eps;
+  T awd;     // a * weight_decay (optim.cpp:89, left-to-right)
+};
+
+// apply_step for one element (optim.cpp:56-91).  Operator order is the
+// reference's, left to right:
+//   sgd:      ge = g + wd*w;               w' = w - a*ge
+//   momentum: ge = g + wd*w; b = mom*b + ge; w' = w - a*b
+//   adam(w):  ge = adam ? g + wd*w : g
+//             m = b1*m + (1-b1)*ge;  v = b2*v + ((1-b2)*ge)*ge
+//             w' = w - (a*(m/bc1)) / (sqrt(v/bc2) + eps);  adamw: w' -= (a*wd)*w
+template <typename T, int OPT>
+__device__ __forceinline__ T step_elem(T w, T g, T& m1, T& m2, const StepConsts<T>& c, T bc1, T bc2) {
+  if constexpr (OPT == kSgd) {
+    const T ge = add_(g, mul_(c.wd, w));
+    return sub_(w, mul_(c.alpha, ge));
+  } else if constexpr (OPT == kMomentum) {
+    const T ge = add_(g, mul_(c.wd, w));
+    m1 = add_(mul_(c.mom, m1), ge);
+    return sub_(w, mul_(c.alpha, m1));
+  } else {
+    const T ge = (OPT == kAdam) ? add_(g, mul_(c.wd, w)) : g;
+    m1 = add_(mul_(c.b1, m1), mul_(c.omb1, ge));
+    m2 = add_(mul_(c.b2, m2), mul_(mul_(c.omb2, ge), ge));
+    const T mhat = div_(m1, bc1);
+    const T vhat = div_(m2, bc2);
+    T out = sub_(w, div_(mul_(c.alpha, mhat), add_(sqrt_(vhat), c.eps)));
+    if constexpr (OPT == kAdamW) out = sub_(out, mul_(c.awd, w));
+    return out;
+  }
+}
+
+// ---- divergence latch ----------------------------------------------------
+// key = t << 34 | phase << 32 | rank; atomicMin keeps the earliest iteration,
+// then phase (DS: 0 local step before 1 group sync, sync.cpp:348-370; BSP:
+// 0 gradient collective before 1 step, sync.cpp:389-421), then lowest rank
+// (sync.cpp:126-128).
+__device__ __forceinline__ unsigned long long err_key(long t, int phase, int rank) {
+  return (static_cast<unsigned long long>(t) << 34) |
+         (static_cast<unsigned long long>(phase) << 32) | static_cast<unsigned int>(rank);
+}
+
+__device__ __forceinline__ void latch_error(unsigned long long* err, unsigned long long key) {
+  // warp-aggregate: one atomic per warp that saw a failure
+  const unsigned mask = __activemask();
+  unsigned long long k = key;
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(mask, k, off);
+    k = o < k ? o : k;
+  }
+  if ((threadIdx.x & 31) == (__ffs(mask) - 1) && k != ~0ull) atomicMin(err, k);
+}
+
+// ---- fused DS-Sync group step ---------------------------------------------
+template <typename T> struct GroupArgs {
+  T* w;           // [P][ld] local params (row = global rank - first_rank)
+  const T* g;     // [P][ld] gradients; g_ld == 0 -> one shared row (BSP multi-GPU)
+  T* m1;
+  T* m2;
+  long ld;
+  long g_ld;
+  long nvec;      // vectors per row to process
+  int first_rank;
+  const int* members;  // CSR over the groups of this launch (global ranks)
+  const int* offsets;
+  int step_phase;      // error phase for a failed local step
+  int sync_phase;      // error phase for a failed group mean
+  long t;
+  StepConsts<T> c;
+  double bc1[kMaxLocal];  // per local worker bias corrections (optim.cpp:76-78)
+  double bc2[kMaxLocal];
+  unsigned long long* err;
+};
+
+// blockIdx.y = group of this launch; threads stride over the row's vectors.
+// Per element vector: for each member in ascending order load w, g, state;
+// step; store state; fold.  Then scale once and store the mean to every
+// member: each element of every array is read once and written once.
+template <typename T, int OPT, int M>
+__global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  const int beg = a.offsets[blockIdx.y];
+  const int m = M > 0 ? M : a.offsets[blockIdx.y + 1] - beg;
+  const int lead = a.members[beg];
+  // 1.0 / m in double, rounded once to T (param.cpp:49 / comm.cpp:107)
+  const T inv = static_cast<T>(1.0 / static_cast<double>(m));
+  unsigned long long bad = ~0ull;
+
+  // Per-member row offsets hoisted out of the element loop (registers for
+  // the templated group sizes).
+  constexpr int RM = M > 0 ? M : 1;
+  long row[RM], grow[RM];
+  int rank[RM];
+  T bc1[RM], bc2[RM];
+  if constexpr (M > 0) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      rank[j] = a.members[beg + j];
+      const int lr = rank[j] - a.first_rank;
+      row[j] = static_cast<long>(lr) * a.ld;
+      grow[j] = static_cast<long>(lr) * a.g_ld;
+      bc1[j] = static_cast<T>(a.bc1[lr]);
+      bc2[j] = static_cast<T>(a.bc2[lr]);
+    }
+  }
+
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < a.nvec; e += stride) {
+    const long off = e * VN;
+    Pack<T> acc;
+#pragma unroll(M > 0 ? M : 4)
+    for (int j = 0; j < m; ++j) {
+      long rj, gj;
+      T b1j, b2j;
+      int rk;
+      if constexpr (M > 0) {
+        rj = row[j];
+        gj = grow[j];
+        b1j = bc1[j];
+        b2j = bc2[j];
+        rk = rank[j];
+      } else {
+        rk = a.members[beg + j];
+        const int lr = rk - a.first_rank;
+        rj = static_cast<long>(lr) * a.ld;
+        gj = static_cast<long>(lr) * a.g_ld;
+        b1j = static_cast<T>(a.bc1[lr]);
+        b2j = static_cast<T>(a.bc2[lr]);
+      }
+      Pack<T> x = ldv(a.w + rj + off);
+      if constexpr (OPT != kOptNone) {
+        const Pack<T> gv = ldv(a.g + gj + off);
+        Pack<T> s1, s2;
+        if constexpr (OPT != kSgd) s1 = ldv(a.m1 + rj + off);
+        if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + rj + off);
+        bool ok = true;
+#pragma unroll
+        for (int l = 0; l < VN; ++l) {
+          x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1j, b2j);
+          ok = ok && finite_(x.v[l]);
+        }
+        if constexpr (OPT != kSgd) stv(a.m1 + rj + off, s1);
+        if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj + off, s2);
+        if (!ok) {
+          const unsigned long long k = err_key(a.t, a.step_phase, rk);
+          bad = k < bad ? k : bad;
+        }
+      }
+      if (j == 0) {
+        acc = x;
+      } else {
+#pragma unroll
+        for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+      }
+    }
+    if (M != 1) {
+      bool ok = true;
+#pragma unroll
+      for (int l = 0; l < VN; ++l) {
+        acc.v[l] = mul_(acc.v[l], inv);
+        ok = ok && finite_(acc.v[l]);
+      }
+      if (!ok) {
+        const unsigned long long k = err_key(a.t, a.sync_phase, lead);
+        bad = k < bad ? k : bad;
+      }
+    }
+#pragma unroll(M > 0 ? M : 4)
+    for (int j = 0; j < m; ++j) {
+      long rj;
+      if constexpr (M > 0) {
+        rj = row[j];
+      } else {
+        rj = static_cast<long>(a.members[beg + j] - a.first_rank) * a.ld;
+      }
+      stv(a.w + rj + off, acc);
+    }
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
+// ---- fused BSP step on one GPU --------------------------------------------
+// gm = (sum_k g_k ascending) * (1/W) (sync.cpp:389-402 via mean_of order),
+// then every worker w_k' = apply_step(w_k, gm) (sync.cpp:406-421).
+template <typename T> struct BspArgs {
+  T* w;
+  const T* g;
+  T* m1;
+  T* m2;
+  long ld;
+  long nvec;
+  int nw;  // W (all local)
+  long t;
+  StepConsts<T> c;
+  double bc1[kMaxLocal];
+  double bc2[kMaxLocal];
+  unsigned long long* err;
+};
+
+template <typename T, int OPT, int WT>
+__global__ void __launch_bounds__(kThreads) bsp_kernel(const BspArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  const int nw = WT > 0 ? WT : a.nw;
+  const T inv = static_cast<T>(1.0 / static_cast<double>(nw));
+  unsigned long long bad = ~0ull;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < a.nvec; e += stride) {
+    const long off = e * VN;
+    Pack<T> gm = ldv(a.g + off);
+#pragma unroll(WT > 0 ? WT : 4)
+    for (int k = 1; k < nw; ++k) {
+      const Pack<T> x = ldv(a.g + static_cast<long>(k) * a.ld + off);
+#pragma unroll
+      for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], x.v[l]);
+    }
+    bool okm = true;
+#pragma unroll
+    for (int l = 0; l < VN; ++l) {
+      gm.v[l] = mul_(gm.v[l], inv);
+      okm = okm && finite_(gm.v[l]);
+    }
+    if (!okm) {  // collective failure -> DivergenceError(0, t) (sync.cpp:399-401)
+      const unsigned long long k = err_key(a.t, 0, 0);
+      bad = k < bad ? k : bad;
+    }
+#pragma unroll(WT > 0 ? WT : 4)
+    for (int k = 0; k < nw; ++k) {
+      const long r = static_cast<long>(k) * a.ld + off;
+      Pack<T> x = ldv(a.w + r);
+      Pack<T> s1, s2;
+      if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
+      if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+      const T b1 = static_cast<T>(a.bc1[k]);
+      const T b2 = static_cast<T>(a.bc2[k]);
+      bool ok = true;
+#pragma unroll
+      for (int l = 0; l < VN; ++l) {
+        x.v[l] = step_elem<T, OPT>(x.v[l], gm.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
+        ok = ok && finite_(x.v[l]);
+      }
+      stv(a.w + r, x);
+      if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
+      if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+      if (!ok) {
+        const unsigned long long kk = err_key(a.t, 1, k);
+        bad = kk < bad ? kk : bad;
+      }
+    }
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
+// ---- ordered fold + broadcast over (possibly peer-mapped) rows ------------
+// Two-shot slice owner: for e in [lo, hi): acc = src_0; acc += src_j
+// ascending; acc *= 1/m; store to every dst.  src/dst are device pointers to
+// row starts; for a group spanning GPUs they are NVLink peer mappings, so
+// this kernel is the cross-GPU collective itself (P2P loads and stores over
+// NVSwitch from inside the kernel, no NCCL).
+struct FoldEntry {
+  int src_beg, src_cnt;  // into the src pointer table
+  int dst_beg, dst_cnt;  // into the dst pointer table
+  long lo, hi;           // element range (multiples of the vector width)
+  int err_rank;          // members[0] (sync.cpp:233-235) or 0 for BSP (sync.cpp:401)
+  int err_phase;
+};
+
+template <typename T> struct FoldArgs {
+  T* const* src;
+  T* const* dst;
+  const FoldEntry* entries;
+  long t;
+  unsigned long long* err;
+};
+
+template <typename T, int M>
+__global__ void __launch_bounds__(kThreads) fold_kernel(const FoldArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  const FoldEntry en = a.entries[blockIdx.y];
+  const int m = M > 0 ? M : en.src_cnt;
+  const T inv = static_cast<T>(1.0 / static_cast<double>(m));
+  unsigned long long bad = ~0ull;
+  const long v0 = en.lo / VN, v1 = en.hi / VN;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = v0 + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < v1; e += stride) {
+    const long off = e * VN;
+    Pack<T> acc = ldv_cg(a.src[en.src_beg] + off);
+#pragma unroll(M > 0 ? M - 1 : 4)
+    for (int j = 1; j < m; ++j) {
+      const Pack<T> x = ldv_cg(a.src[en.src_beg + j] + off);
+#pragma unroll
+      for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+    }
+    bool ok = true;
+#pragma unroll
+    for (int l = 0; l < VN; ++l) {
+      acc.v[l] = mul_(acc.v[l], inv);
+      ok = ok && finite_(acc.v[l]);
+    }
+    if (!ok) {
+      const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
+      bad = k < bad ? k : bad;
+    }
+    for (int q = 0; q < en.dst_cnt; ++q) {
+      stv_cg(a.dst[en.dst_beg + q] + off, acc);
+    }
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
+// ---- cross-GPU barrier over NVLink-mapped flag words ------------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Thread j tells GPU j "rank reached epoch", then waits until GPU j has told
+// us the same.  Bounded spin (~20 s of globaltimer) so a broken peer cannot
+// wedge the GPU: on timeout the barrier latches a failure instead.
+__global__ void barrier_kernel(unsigned long long* const* peer_flags, unsigned long long* my_flags,
+                               int rank, int n, unsigned long long epoch, unsigned long long* timeout) {
+  const int j = threadIdx.x;
+  if (j >= n) return;
+  __threadfence_system();
+  st_release_sys(peer_flags[j] + rank, epoch);
+  unsigned long long start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  while (ld_acquire_sys(my_flags + j) < epoch) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start > 20000000000ull) {
+      atomicExch(timeout, 1ull);
+      break;
+    }
+  }
+  __threadfence_system();
+}
+
+// ---- synthetic gradients: SplitMix64 + Box-Muller (rng.cpp:8-51) -----------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// i-th gaussian of the stream whose state after for_stream is s0: draws
+// 2i and 2i+1 (0-based), draw j = mix64(s0 + (j+1) * phi) (rng.cpp:28-31).
+__device__ __forceinline__ double gaussian_at(uint64_t s0, uint64_t i) {
+  const uint64_t phi = 0x9e3779b97f4a7c15ULL;
+  const uint64_t x = mix64(s0 + (2 * i + 1) * phi);
+  const uint64_t y = mix64(s0 + (2 * i + 2) * phi);
+  const double u1 = __dsub_rn(1.0, __dmul_rn(static_cast<double>(x >> 11), 0x1.0p-53));
+  const double u2 = __dmul_rn(static_cast<double>(y >> 11), 0x1.0p-53);
+  // sqrt(-2 log u1) * cos(2 pi u2), the argument rounded as (2.0*pi)*u2
+  return __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))),
+                   cos(__dmul_rn(6.283185307179586232, u2)));
+}
+
+template <typename T> struct GradArgs {
+  const T* w;
+  T* g;
+  const T* wstar;
+  long ld;
+  long d;      // real dimension (padding gets g = 0)
+  int nlocal;
+  double mu;
+  double scale;  // sigma / sqrt(d); 0 disables noise
+  uint64_t s0[kMaxLocal];  // for_stream(seed, kGradientNoise, rank, t) per local worker
+};
+
+// g_i = (0 + mu*(w_i - w*_i)) + scale * gaussian_i   (problems.cpp:173-193 with
+// A = mu*I: the dense matvec over exact zeros reduces to +0 + mu*x_i).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) quad_grad_kernel(const GradArgs<T> a) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  const int k = blockIdx.y;
+  const T* w = a.w + static_cast<long>(k) * a.ld;
+  T* g = a.g + static_cast<long>(k) * a.ld;
+  const T mu = static_cast<T>(a.mu);
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.ld; i += stride) {
+    if (i >= a.d) {
+      g[i] = T(0);
+      continue;
+    }
+    T grad = add_(T(0), mul_(mu, sub_(w[i], a.wstar[i])));
+    if (a.scale > 0.0) {
+      const double n = __dmul_rn(a.scale, gaussian_at(a.s0[k], static_cast<uint64_t>(i)));
+      grad = add_(grad, static_cast<T>(n));
+    }
+    g[i] = grad;
+  }
+}
+
+// Gaussian fill of one row (w* or the init direction u), in double.
+__global__ void gaussian_fill_kernel(double* out, long d, uint64_t s0) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < d; i += stride) {
+    out[i] = gaussian_at(s0, static_cast<uint64_t>(i));
+  }
+}
+
+__global__ void sumsq_kernel(const double* x, long d, double* out) {
+  __shared__ double part[kThreads / 32];
+  double acc = 0.0;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < d; i += stride) {
+    acc += x[i] * x[i];
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) s += part[i];
+    atomicAdd(out, s);
+  }
+}
+
+// w*_T = T(w*), row_T = T(w* + r * (u / |u|)) (problems.cpp:106-113,161-165)
+template <typename T>
+__global__ void compose_init_kernel(const double* wstar, const double* u, const double* sumsq, long d,
+                                    long ld, double r, T* wstar_out, T* row_out) {
+  const double n = __dsqrt_rn(*sumsq);
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < ld; i += stride) {
+    if (i < d) {
+      wstar_out[i] = static_cast<T>(wstar[i]);
+      row_out[i] = static_cast<T>(__dadd_rn(wstar[i], __dmul_rn(r, __ddiv_rn(u[i], n))));
+    } else {
+      wstar_out[i] = T(0);
+      row_out[i] = T(0);
+    }
+  }
+}
+
+template <typename T>
+__global__ void broadcast_row_kernel(T* base, long ld, int rows, const T* src) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  const long n = ld * rows;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    base[i] = src[i % ld];
+  }
+}
+
+}  // namespace dssb

@@ -1,0 +1,241 @@
+// Host schedule: restates /root/reference/proj/src/schedule.cpp:8-90 and
+// sync.cpp:47-66,131-141 (same rules, same error wording), plus the
+// rectangular W = N*K extension and the multi-GPU two-shot plan.
+#include "schedule.hpp"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace dssb {
+
+namespace {
+
+bool is_power_of_two(long n) { return n > 0 && (n & (n - 1)) == 0; }
+
+}  // namespace
+
+void validate_world(int world_size, int group_size, bool rectangular) {
+  // schedule.cpp:9-16
+  if (world_size < 1) {
+    throw std::invalid_argument("world_size must be >= 1 (got " + std::to_string(world_size) + ")");
+  }
+  if (group_size < 1) {
+    throw std::invalid_argument("group_size must be >= 1 (got " + std::to_string(group_size) + ")");
+  }
+  const long n = group_size;
+  if (rectangular) {
+    if (world_size % group_size != 0) {
+      throw std::invalid_argument(
+          "rectangular schedule needs world_size to be a multiple of group_size (got world_size=" +
+          std::to_string(world_size) + ", group_size=" + std::to_string(group_size) + ")");
+    }
+    return;
+  }
+  // schedule.cpp:17-23
+  if (world_size != n * n && world_size != group_size) {
+    throw std::invalid_argument(
+        "world_size must equal group_size^2, or group_size for a single full group (got "
+        "world_size=" +
+        std::to_string(world_size) + ", group_size=" + std::to_string(group_size) + ")");
+  }
+}
+
+bool is_square_mode(int world_size, int group_size) {
+  // schedule.cpp:26-29
+  const long n = group_size;
+  return world_size == n * n && world_size != group_size;
+}
+
+void validate_strategy(const dss_strategy& s) {
+  // sync.cpp:47-66
+  validate_world(s.world_size, s.group_size, s.rectangular != 0);
+  if (s.kind == DSS_BSP && s.group_size != s.world_size) {
+    throw std::invalid_argument(
+        "bsp runs one group spanning the world; set group_size equal to world_size");
+  }
+  if (s.kind == DSS_DS_SYNC && s.topology == DSS_PS) {
+    throw std::invalid_argument("ds-sync has no parameter-server variant; use topology ring or tree");
+  }
+  if (s.topology == DSS_TREE && !is_power_of_two(s.group_size)) {
+    throw std::invalid_argument("tree topology requires power-of-two groups (group_size=" +
+                                std::to_string(s.group_size) + ")");
+  }
+  if (s.topology == DSS_TREE && s.rectangular && s.world_size != s.group_size &&
+      !is_power_of_two(s.world_size / s.group_size)) {
+    throw std::invalid_argument("tree topology requires power-of-two groups (comb size=" +
+                                std::to_string(s.world_size / s.group_size) + ")");
+  }
+  if (s.topology == DSS_PS && s.num_servers < 1) {
+    throw std::invalid_argument("ps topology needs num_servers >= 1 (got " +
+                                std::to_string(s.num_servers) + ")");
+  }
+  if (s.kind != DSS_BSP && s.kind != DSS_DS_SYNC) throw std::invalid_argument("unknown strategy");
+  if (s.topology < DSS_RING || s.topology > DSS_PS) throw std::invalid_argument("unknown topology");
+}
+
+Partition make_partition(const dss_strategy& s, long t) {
+  const int W = s.world_size;
+  Partition part;
+  part.iteration = t;
+  if (s.kind == DSS_BSP) {
+    // partition_for (sync.cpp:131-139): one all-world group, no validation
+    // beyond the caller's validate(strategy).
+    part.members.resize(static_cast<size_t>(W));
+    for (int x = 0; x < W; ++x) part.members[static_cast<size_t>(x)] = x;
+    part.offsets = {0, W};
+    return part;
+  }
+  validate_world(W, s.group_size, s.rectangular != 0);  // schedule.cpp:32
+  if (t < 0) throw std::invalid_argument("iteration must be >= 0");  // schedule.cpp:33
+
+  const int n = s.group_size;
+  const bool single = (W == n);  // single-group layout (schedule.cpp:38-43)
+  if (single || W == 1) {
+    part.members.resize(static_cast<size_t>(W));
+    for (int x = 0; x < W; ++x) part.members[static_cast<size_t>(x)] = x;
+    part.offsets = {0, W};
+    return part;
+  }
+  // Square mode: g(x) = t even ? x / n : x % n (schedule.cpp:45-50).  The
+  // rectangular extension uses the same rule with W = n * k: k blocks of n
+  // on even t, n combs of k on odd t.  Visiting x ascending and bucketing
+  // keeps every group ascending by construction (schedule.cpp:52).
+  const int k = W / n;
+  const bool even = (t % 2 == 0);
+  const int groups = even ? k : n;
+  const int size = even ? n : k;
+  part.members.resize(static_cast<size_t>(W));
+  part.offsets.resize(static_cast<size_t>(groups) + 1);
+  for (int g = 0; g <= groups; ++g) part.offsets[static_cast<size_t>(g)] = g * size;
+  std::vector<int> fill(static_cast<size_t>(groups), 0);
+  for (int x = 0; x < W; ++x) {
+    const int g = even ? x / n : x % n;
+    part.members[static_cast<size_t>(g * size + fill[static_cast<size_t>(g)]++)] = x;
+  }
+  return part;
+}
+
+std::vector<int> group_of(const dss_strategy& s, long t, int rank) {
+  // schedule.cpp:56-65
+  if (rank < 0 || rank >= s.world_size) {
+    throw std::invalid_argument("rank out of range: " + std::to_string(rank));
+  }
+  const Partition p = make_partition(s, t);
+  for (int g = 0; g < p.n_groups(); ++g) {
+    const int* b = p.group(g);
+    if (std::find(b, b + p.size(g), rank) != b + p.size(g)) return std::vector<int>(b, b + p.size(g));
+  }
+  throw std::logic_error("partition does not cover rank");
+}
+
+bool check_mixing(const dss_strategy& s, long t) {
+  // schedule.cpp:67-90: every group at t meets every group at t+1 in exactly
+  // one worker (linear merge of two sorted lists).
+  const Partition now = make_partition(s, t);
+  const Partition next = make_partition(s, t + 1);
+  for (int a = 0; a < now.n_groups(); ++a) {
+    for (int b = 0; b < next.n_groups(); ++b) {
+      const int* x = now.group(a);
+      const int* y = next.group(b);
+      int i = 0, j = 0, common = 0;
+      while (i < now.size(a) && j < next.size(b)) {
+        if (x[i] == y[j]) {
+          ++common;
+          ++i;
+          ++j;
+        } else if (x[i] < y[j]) {
+          ++i;
+        } else {
+          ++j;
+        }
+      }
+      if (common != 1) return false;
+    }
+  }
+  return true;
+}
+
+namespace {
+
+// Serial steps and messages of one collective over m members (comm.cpp).
+void collective_counts(int topology, long m, int servers, long dim, long* steps, long* msgs) {
+  if (topology == DSS_RING) {  // comm.cpp:78-123: 2m-1 hops, lone member none
+    *steps = m == 1 ? 0 : 2 * m - 1;
+    *msgs = *steps;
+  } else if (topology == DSS_TREE) {  // comm.cpp:125-214
+    if (m == 1) {
+      *steps = 0;
+      *msgs = 0;
+      return;
+    }
+    long depth = 0;
+    while ((1L << depth) < m) ++depth;
+    *steps = 3 * depth;
+    *msgs = m * depth + 2 * (m - 1);
+  } else {  // ps, comm.cpp:216-289: 2m serial steps, every non-empty slice pushed and pulled
+    const long nonempty = std::min<long>(servers, dim);
+    *steps = 2 * m;
+    *msgs = 2 * m * nonempty;
+  }
+}
+
+}  // namespace
+
+dss_outcome round_outcome(const dss_strategy& s, long t, long payload_dim) {
+  // sync_round (sync.cpp:276-281): max serial steps over groups, sum of messages.
+  const Partition p = make_partition(s, t);
+  dss_outcome out{0, 0};
+  for (int g = 0; g < p.n_groups(); ++g) {
+    long steps = 0, msgs = 0;
+    collective_counts(s.topology, p.size(g), s.num_servers, payload_dim, &steps, &msgs);
+    out.critical_path_steps = std::max(out.critical_path_steps, steps);
+    out.total_messages += msgs;
+  }
+  return out;
+}
+
+void slice_range(long d_pad, int s, int j, long* lo, long* hi) {
+  // Near-equal contiguous slices (sizes differ by at most one chunk), the
+  // same split rule the reference's parameter servers use (comm.cpp:229-236).
+  const long chunks = d_pad / kRowAlign;
+  const long base = chunks / s;
+  const long rem = chunks % s;
+  const long c0 = j * base + std::min<long>(j, rem);
+  const long c1 = c0 + base + (j < rem ? 1 : 0);
+  *lo = c0 * kRowAlign;
+  *hi = c1 * kRowAlign;
+}
+
+GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad) {
+  GpuPlan plan;
+  const int per = world_size / n_gpus;
+  for (int g = 0; g < part.n_groups(); ++g) {
+    const int* mem = part.group(g);
+    const int m = part.size(g);
+    std::vector<int> gpus;  // ascending, distinct (members are ascending)
+    for (int j = 0; j < m; ++j) {
+      const int gpu = mem[j] / per;
+      if (gpus.empty() || gpus.back() != gpu) gpus.push_back(gpu);
+    }
+    if (gpus.size() > 1) plan.any_spanning_globally = true;
+    const auto it = std::find(gpus.begin(), gpus.end(), rank);
+    if (it == gpus.end()) continue;
+    if (gpus.size() == 1) {
+      plan.local_groups.push_back(g);
+      continue;
+    }
+    plan.spanning_groups.push_back(g);
+    for (int j = 0; j < m; ++j) {
+      if (mem[j] / per == rank) plan.spanning_local_members.push_back(mem[j]);
+    }
+    Slice sl;
+    sl.group = g;
+    slice_range(d_pad, static_cast<int>(gpus.size()), static_cast<int>(it - gpus.begin()), &sl.lo,
+                &sl.hi);
+    if (sl.hi > sl.lo) plan.owned.push_back(sl);
+  }
+  std::sort(plan.spanning_local_members.begin(), plan.spanning_local_members.end());
+  return plan;
+}
+
+}  // namespace dssb

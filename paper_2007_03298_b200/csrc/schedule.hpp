@@ -1,0 +1,77 @@
+// Host-side divide-and-shuffle schedule and the multi-GPU launch plan.
+//
+// The schedule is computed on the host exactly as the reference computes it
+// (/root/reference/proj/src/schedule.cpp:8-90, sync.cpp:47-66,131-141) so
+// group membership is bit-exact every iteration; the device only ever sees
+// the resulting CSR tables.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dssync_b200.h"
+
+namespace dssb {
+
+// Row padding in elements: 64 elements = 256 B (f32) / 512 B (f64), so every
+// worker row starts on a 256-B boundary and holds whole 16/32-B vectors.
+constexpr long kRowAlign = 64;
+
+inline long pad_dim(long d) { return (d + kRowAlign - 1) / kRowAlign * kRowAlign; }
+
+// CSR partition: groups[g] = members[offsets[g] .. offsets[g+1]), ascending.
+struct Partition {
+  long iteration = 0;
+  std::vector<int> members;
+  std::vector<int> offsets;
+  int n_groups() const { return static_cast<int>(offsets.size()) - 1; }
+  int size(int g) const { return offsets[g + 1] - offsets[g]; }
+  const int* group(int g) const { return members.data() + offsets[g]; }
+};
+
+// validate(WorldConfig) (schedule.cpp:8-24).  rectangular relaxes the
+// shape rule to W % N == 0 (builder extension).
+void validate_world(int world_size, int group_size, bool rectangular);
+bool is_square_mode(int world_size, int group_size);
+// validate(SyncStrategy) (sync.cpp:47-66).
+void validate_strategy(const dss_strategy& s);
+
+// make_partition (schedule.cpp:31-54) for DS-Sync; partition_for
+// (sync.cpp:131-141) returns the single all-world group under BSP.
+Partition make_partition(const dss_strategy& s, long t);
+std::vector<int> group_of(const dss_strategy& s, long t, int rank);
+bool check_mixing(const dss_strategy& s, long t);
+
+// Closed-form SyncRoundOutcome (comm.cpp:78-289 step/message counts).
+dss_outcome round_outcome(const dss_strategy& s, long t, long payload_dim);
+
+// ---------------------------------------------------------------------------
+// Multi-GPU plan.  W workers packed contiguously over G GPUs, P = W / G per
+// GPU, gpu(k) = k / P.  A group whose members all sit on one
+// GPU is folded there by the fused step kernel.  A group spanning S GPUs is
+// two-shot: every member GPU steps its own members in place, then the GPU at
+// position j of the group's (ascending) GPU list owns the j-th of S
+// near-equal slices of the padded row (in kRowAlign chunks) and folds that
+// slice over all members in ascending rank order, writing the mean to every
+// member.  One owner per element keeps the reference's fold order exactly.
+struct Slice {
+  int group = 0;  // index in the Partition
+  long lo = 0;    // element range [lo, hi) of the padded row
+  long hi = 0;
+};
+
+struct GpuPlan {
+  std::vector<int> local_groups;     // groups entirely on this GPU
+  std::vector<int> spanning_groups;  // groups with members here and elsewhere
+  std::vector<int> spanning_local_members;  // this GPU's members of spanning groups (ascending)
+  std::vector<Slice> owned;          // slices this GPU folds
+  bool any_spanning_globally = false;  // some group spans GPUs (barrier needed)
+};
+
+GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad);
+
+// [lo, hi) of the j-th of s near-equal chunk-aligned slices of [0, d_pad).
+void slice_range(long d_pad, int s, int j, long* lo, long* hi);
+
+}  // namespace dssb

@@ -1,0 +1,185 @@
+"""Generate the golden fixtures from the UNMODIFIED reference.
+
+Runs only in the build container (needs /root/reference and oracle/_ref).
+Every array here is produced by the reference library itself
+(oracle/_ref/libdssync_ref.so = /root/reference/proj/src compiled as-is,
+driven through its public API by oracle/ref_shim.cpp); the fixtures are
+committed so the GPU box, which has no /root/reference, can check the CUDA
+path bit for bit.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle.oracle import Reference  # noqa: E402
+
+K_DATA_GEN = 0x9e3779b97f4a7c15
+K_INIT_PARAMS = 0xbf58476d1ce4e5b9
+K_GRADIENT_NOISE = 0xa0761d6478bd642f
+
+OPTS = {"vanilla-sgd": 0, "sgd-momentum": 1, "adam": 2, "adamw": 3}
+
+
+def partitions(R: Reference) -> dict:
+    out = {"cases": [], "invalid": [], "mixing": []}
+    for W, N in [(1, 1), (4, 2), (4, 4), (9, 3), (9, 9), (16, 4), (25, 5), (36, 6), (64, 8)]:
+        for t in range(0, 11):
+            out["cases"].append({"W": W, "N": N, "t": t, "groups": R.make_partition(W, N, t)})
+            out["mixing"].append({"W": W, "N": N, "t": t, "mixing": R.check_mixing(W, N, t)})
+    # test_schedule.cpp:103-113 plus the C2/C3 shapes
+    for W, N in [(6, 2), (4, 3), (0, 0), (4, -2), (8, 2), (8, 4), (32, 4), (32, 8)]:
+        try:
+            R.make_partition(W, N, 0)
+            msg = None
+        except ValueError as e:
+            msg = str(e)
+        out["invalid"].append({"W": W, "N": N, "error": msg})
+    try:
+        R.make_partition(4, 2, -1)
+        out["negative_t"] = None
+    except ValueError as e:
+        out["negative_t"] = str(e)
+    return out
+
+
+def apply_steps(R: Reference) -> dict:
+    rng = np.random.default_rng(11)
+    arrs = {}
+    cases = []
+    # hand values of test_optim.cpp:23-109 and random rows
+    hand = [
+        ("vanilla-sgd", 0.1, 0.0, 0, [1.0, 2.0], [0.5, -1.0]),
+        ("vanilla-sgd", 0.1, 0.5, 0, [2.0], [1.0]),
+        ("sgd-momentum", 0.1, 0.0, 0, [1.0], [1.0]),
+        ("adam", 0.1, 0.0, 0, [1.0], [2.0]),
+        ("adamw", 0.1, 0.1, 0, [1.0], [0.0]),
+        ("adam", 0.1, 0.1, 0, [1.0], [0.0]),
+        ("sgd-momentum", 0.0, 0.0, 0, [0.25, -0.5], [1.0, 1.0]),
+    ]
+    for i in range(12):
+        opt = list(OPTS)[i % 4]
+        d = int(rng.integers(1, 70))
+        hand.append((opt, float(rng.uniform(0.001, 0.2)), [0.0, 0.01][i % 2], int(rng.integers(0, 20)),
+                     rng.standard_normal(d).tolist(), rng.standard_normal(d).tolist()))
+    for j, (opt, alpha, wd, sc, w, g) in enumerate(hand):
+        w = np.array(w, np.float64)
+        g = np.array(g, np.float64)
+        d = w.size
+        m1 = np.zeros(d) if sc == 0 else rng.standard_normal(d) * 0.1
+        m2 = np.zeros(d) if sc == 0 else np.abs(rng.standard_normal(d)) * 0.01
+        hp = R.hp_array(weight_decay=wd)
+        arrs[f"c{j}_w"], arrs[f"c{j}_g"], arrs[f"c{j}_m1"], arrs[f"c{j}_m2"] = w.copy(), g.copy(), m1.copy(), m2.copy()
+        rc, sc_out = R.apply_step(OPTS[opt], hp, alpha, sc, w, g, m1, m2)
+        assert rc == 0, R.error()
+        arrs[f"c{j}_w_out"], arrs[f"c{j}_m1_out"], arrs[f"c{j}_m2_out"] = w, m1, m2
+        cases.append({"id": j, "opt": opt, "alpha": alpha, "weight_decay": wd, "step_count": sc,
+                      "step_count_out": sc_out})
+    return {"cases": cases}, arrs
+
+
+def trajectories(R: Reference) -> tuple[dict, dict]:
+    """run_training on the isotropic quadratic (A = mu*I), DS and BSP, with
+    every per-iteration gradient recorded (the replay is verified against
+    run_training itself)."""
+    meta, arrs = [], {}
+    d, mu, sigma, delta0, pseed, rseed, T = 37, 1.0, 0.5, 4.0, 7, 1, 6
+    hp_by_opt = {"vanilla-sgd": (0.05, 0.0), "sgd-momentum": (0.05, 1e-4), "adam": (0.01, 0.0),
+                 "adamw": (0.01, 0.01)}
+    shapes = [("ds", 4, 2), ("ds", 9, 3), ("ds", 16, 4), ("bsp", 4, 4), ("bsp", 8, 8), ("ds", 4, 4)]
+    for kind, W, N in shapes:
+        for opt, (alpha, wd) in hp_by_opt.items():
+            hp = R.hp_array(weight_decay=wd)
+            grads, params, match = R.quadratic_run(1 if kind == "ds" else 0, 0, W, N, d, mu, sigma, delta0,
+                                                   pseed, rseed, T, OPTS[opt], hp, alpha)
+            assert match, f"replay != run_training for {kind} {W}x{N} {opt}"
+            key = f"{kind}_{W}x{N}_{opt}"
+            arrs[key + "_grads"] = grads
+            arrs[key + "_params"] = params
+            meta.append({"key": key, "kind": kind, "W": W, "N": N, "opt": opt, "alpha": alpha,
+                         "weight_decay": wd, "d": d, "T": T})
+    wstar, w0 = R.quadratic_init(pseed, d, mu, delta0)
+    arrs["quad_wstar"], arrs["quad_w0"] = wstar, w0
+    return {"trajectories": meta, "quadratic": {"d": d, "mu": mu, "sigma": sigma, "delta0": delta0,
+                                                 "problem_seed": pseed, "run_seed": rseed}}, arrs
+
+
+def logistic_c1(R: Reference) -> tuple[dict, dict]:
+    """Config C1 (acceptance.cpp:239-258): W=4 groups of 2, logistic d=20
+    M=2000 l2=0.05 seed 11, batch 8, vanilla SGD, step_decay_lr(1, 0.5, 75)."""
+    T = 300
+    hp = R.hp_array()
+    arrs, meta = {}, []
+    for kind, N in (("ds", 2), ("bsp", 4)):
+        grads, params, alphas, match = R.logistic_run(1 if kind == "ds" else 0, 4, N, 20, 2000, 0.05, 11, 1, 8, T,
+                                                      0, hp, 1.0, 0.5, 75)
+        assert match, "logistic replay != run_training"
+        arrs[f"c1_{kind}_grads"] = grads
+        arrs[f"c1_{kind}_params"] = params
+        arrs[f"c1_{kind}_alphas"] = alphas
+        meta.append({"kind": kind, "W": 4, "N": N, "d": 20, "T": T})
+    return {"c1": meta}, arrs
+
+
+def sync_rounds(R: Reference) -> tuple[dict, dict]:
+    rng = np.random.default_rng(19)
+    arrs, meta = {}, []
+    for kind, topo, W, N in [(1, 0, 4, 2), (1, 1, 4, 2), (1, 0, 9, 3), (1, 0, 16, 4), (0, 0, 4, 4), (0, 2, 5, 5),
+                             (1, 1, 64, 8)]:
+        d = int(rng.integers(1, 40))
+        w = rng.standard_normal((W, d))
+        for t in range(3):
+            arrs[f"s{len(meta)}_in"] = w.copy()
+            rc, counts, _ = R.sync_round(kind, topo, W, N, t, w, servers=3)
+            assert rc == 0, R.error()
+            arrs[f"s{len(meta)}_out"] = w.copy()
+            meta.append({"id": len(meta), "kind": kind, "topology": topo, "W": W, "N": N, "t": t, "d": d,
+                         "num_servers": 3, "critical_path_steps": counts[0], "total_messages": counts[1]})
+    return {"sync_rounds": meta}, arrs
+
+
+def rng_vectors(R: Reference) -> tuple[dict, dict]:
+    arrs = {}
+    st = np.array([0], np.uint64)
+    import ctypes as C
+    s = C.c_uint64(0)
+    first = R.lib.ref_next_u64(C.byref(s))
+    for rank in range(4):
+        for t in range(3):
+            arrs[f"noise_r{rank}_t{t}"] = R.gaussians(1, K_GRADIENT_NOISE, rank, t, 512)
+    arrs["wstar_stream"] = R.gaussians(7, K_DATA_GEN, 1, 0, 512)
+    arrs["init_stream"] = R.gaussians(7, K_INIT_PARAMS, 0, 0, 512)
+    del st
+    return {"splitmix_seed0_first": f"{first:#x}"}, arrs
+
+
+def main():
+    R = Reference()
+    meta = {"generated_by": "tests/golden/make_golden.py from oracle/_ref (unmodified /root/reference/proj/src)"}
+    meta["partitions"] = partitions(R)
+    m, a1 = apply_steps(R)
+    meta["apply_step"] = m
+    m, a2 = trajectories(R)
+    meta.update(m)
+    m, a3 = logistic_c1(R)
+    meta.update(m)
+    m, a4 = sync_rounds(R)
+    meta.update(m)
+    m, a5 = rng_vectors(R)
+    meta.update(m)
+    with open(os.path.join(HERE, "golden.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    np.savez_compressed(os.path.join(HERE, "golden.npz"), **a1, **a2, **a3, **a4, **a5)
+    print("wrote", os.path.join(HERE, "golden.json"), os.path.join(HERE, "golden.npz"))
+
+
+if __name__ == "__main__":
+    main()
