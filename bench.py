@@ -235,7 +235,9 @@ def our_arm(args, cfg):
     P = W // G
     peak, peak_kind = load_peaks()
     hp = OptimizerHyperparams(weight_decay=cfg["wd"])
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for the engine, torch's events and NCCL plumbing
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     def make(kind):
         s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W), 1,
@@ -392,7 +394,7 @@ def our_arm(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -150,8 +150,9 @@ int dss_plan(const dss_strategy* s, long t, long dim, int n_gpus, int rank,
 int dss_create(const dss_config* cfg, dss_ctx** out);
 int dss_destroy(dss_ctx* ctx);
 
-/* Run all device work on this stream (e.g. the caller's current stream).
- * NULL restores the context's own stream. */
+/* Run all device work on exactly this stream (e.g. the caller's current
+ * stream); NULL means the CUDA legacy default stream.  Contexts start on a
+ * private non-blocking stream. */
 int dss_set_stream(dss_ctx* ctx, void* cuda_stream);
 
 /* First global rank hosted here and how many (P = W / n_gpus). */

@@ -334,6 +334,7 @@ class DsSyncEngine:
         return self.lib.dss_row_stride(self.h)
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
+        """Run on exactly this cudaStream_t (0/None = legacy default stream)."""
         self._ck(self.lib.dss_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
 
     def set_step_count(self, rank: int, n: int) -> None:

@@ -809,7 +809,7 @@ extern "C" int dss_set_stream(dss_ctx* c, void* s) {
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     ck(cudaStreamSynchronize(c->stream), "stream switch sync");
-    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    c->stream = static_cast<cudaStream_t>(s);  // exactly this stream; NULL = legacy default stream
     return DSS_OK;
   });
 }

@@ -200,49 +200,78 @@ __global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < a.nvec; e += stride) {
     const long off = e * VN;
     Pack<T> acc;
-#pragma unroll(M > 0 ? M : 4)
-    for (int j = 0; j < m; ++j) {
-      long rj, gj;
-      T b1j, b2j;
-      int rk;
-      if constexpr (M > 0) {
-        rj = row[j];
-        gj = grow[j];
-        b1j = bc1[j];
-        b2j = bc2[j];
-        rk = rank[j];
-      } else {
-        rk = a.members[beg + j];
+    if constexpr (M > 0) {
+      // Templated group size: issue every member's loads first (w, g and
+      // optimizer state of all M members in flight at once), then step,
+      // store state and fold in ascending member order.  Without this split
+      // a member's state stores would pin the next member's loads behind
+      // them (the compiler cannot prove the rows do not alias).
+      Pack<T> xs[M], gs[M], s1[M], s2[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        xs[j] = ldv(a.w + row[j] + off);
+        if constexpr (OPT != kOptNone) gs[j] = ldv(a.g + grow[j] + off);
+        if constexpr (OPT != kOptNone && OPT != kSgd) s1[j] = ldv(a.m1 + row[j] + off);
+        if constexpr (OPT == kAdam || OPT == kAdamW) s2[j] = ldv(a.m2 + row[j] + off);
+      }
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        if constexpr (OPT != kOptNone) {
+          bool ok = true;
+#pragma unroll
+          for (int l = 0; l < VN; ++l) {
+            xs[j].v[l] = step_elem<T, OPT>(xs[j].v[l], gs[j].v[l], s1[j].v[l], s2[j].v[l], a.c, bc1[j], bc2[j]);
+            ok = ok && finite_(xs[j].v[l]);
+          }
+          if constexpr (OPT != kSgd) stv(a.m1 + row[j] + off, s1[j]);
+          if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + row[j] + off, s2[j]);
+          if (!ok) {
+            const unsigned long long k = err_key(a.t, a.step_phase, rank[j]);
+            bad = k < bad ? k : bad;
+          }
+        }
+        if (j == 0) {
+          acc = xs[0];
+        } else {
+#pragma unroll
+          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], xs[j].v[l]);
+        }
+      }
+    } else {
+      // Any group size: stream members one at a time (acc in registers).
+#pragma unroll 4
+      for (int j = 0; j < m; ++j) {
+        const int rk = a.members[beg + j];
         const int lr = rk - a.first_rank;
-        rj = static_cast<long>(lr) * a.ld;
-        gj = static_cast<long>(lr) * a.g_ld;
-        b1j = static_cast<T>(a.bc1[lr]);
-        b2j = static_cast<T>(a.bc2[lr]);
-      }
-      Pack<T> x = ldv(a.w + rj + off);
-      if constexpr (OPT != kOptNone) {
-        const Pack<T> gv = ldv(a.g + gj + off);
-        Pack<T> s1, s2;
-        if constexpr (OPT != kSgd) s1 = ldv(a.m1 + rj + off);
-        if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + rj + off);
-        bool ok = true;
+        const long rj = static_cast<long>(lr) * a.ld;
+        const long gj = static_cast<long>(lr) * a.g_ld;
+        Pack<T> x = ldv(a.w + rj + off);
+        if constexpr (OPT != kOptNone) {
+          const T b1j = static_cast<T>(a.bc1[lr]);
+          const T b2j = static_cast<T>(a.bc2[lr]);
+          const Pack<T> gv = ldv(a.g + gj + off);
+          Pack<T> s1, s2;
+          if constexpr (OPT != kSgd) s1 = ldv(a.m1 + rj + off);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + rj + off);
+          bool ok = true;
 #pragma unroll
-        for (int l = 0; l < VN; ++l) {
-          x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1j, b2j);
-          ok = ok && finite_(x.v[l]);
+          for (int l = 0; l < VN; ++l) {
+            x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1j, b2j);
+            ok = ok && finite_(x.v[l]);
+          }
+          if constexpr (OPT != kSgd) stv(a.m1 + rj + off, s1);
+          if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj + off, s2);
+          if (!ok) {
+            const unsigned long long k = err_key(a.t, a.step_phase, rk);
+            bad = k < bad ? k : bad;
+          }
         }
-        if constexpr (OPT != kSgd) stv(a.m1 + rj + off, s1);
-        if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj + off, s2);
-        if (!ok) {
-          const unsigned long long k = err_key(a.t, a.step_phase, rk);
-          bad = k < bad ? k : bad;
-        }
-      }
-      if (j == 0) {
-        acc = x;
-      } else {
+        if (j == 0) {
+          acc = x;
+        } else {
 #pragma unroll
-        for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+        }
       }
     }
     if (M != 1) {
@@ -257,15 +286,12 @@ __global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a
         bad = k < bad ? k : bad;
       }
     }
-#pragma unroll(M > 0 ? M : 4)
-    for (int j = 0; j < m; ++j) {
-      long rj;
-      if constexpr (M > 0) {
-        rj = row[j];
-      } else {
-        rj = static_cast<long>(a.members[beg + j] - a.first_rank) * a.ld;
-      }
-      stv(a.w + rj + off, acc);
+    if constexpr (M > 0) {
+#pragma unroll
+      for (int j = 0; j < M; ++j) stv(a.w + row[j] + off, acc);
+    } else {
+#pragma unroll 4
+      for (int j = 0; j < m; ++j) stv(a.w + static_cast<long>(a.members[beg + j] - a.first_rank) * a.ld + off, acc);
     }
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
@@ -298,12 +324,34 @@ __global__ void __launch_bounds__(kThreads) bsp_kernel(const BspArgs<T> a) {
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < a.nvec; e += stride) {
     const long off = e * VN;
-    Pack<T> gm = ldv(a.g + off);
-#pragma unroll(WT > 0 ? WT : 4)
-    for (int k = 1; k < nw; ++k) {
-      const Pack<T> x = ldv(a.g + static_cast<long>(k) * a.ld + off);
+    Pack<T> gm;
+    constexpr int RW = WT > 0 ? WT : 1;
+    Pack<T> xs[RW], s1[RW], s2[RW];
+    if constexpr (WT > 0) {
+      // every load of the iteration in flight before the first store
+      Pack<T> gs[WT];
 #pragma unroll
-      for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], x.v[l]);
+      for (int k = 0; k < WT; ++k) {
+        const long r = static_cast<long>(k) * a.ld + off;
+        gs[k] = ldv(a.g + r);
+        xs[k] = ldv(a.w + r);
+        if constexpr (OPT != kSgd) s1[k] = ldv(a.m1 + r);
+        if constexpr (OPT == kAdam || OPT == kAdamW) s2[k] = ldv(a.m2 + r);
+      }
+      gm = gs[0];
+#pragma unroll
+      for (int k = 1; k < WT; ++k) {
+#pragma unroll
+        for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], gs[k].v[l]);
+      }
+    } else {
+      gm = ldv(a.g + off);
+#pragma unroll 4
+      for (int k = 1; k < nw; ++k) {
+        const Pack<T> x = ldv(a.g + static_cast<long>(k) * a.ld + off);
+#pragma unroll
+        for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], x.v[l]);
+      }
     }
     bool okm = true;
 #pragma unroll
@@ -318,21 +366,27 @@ __global__ void __launch_bounds__(kThreads) bsp_kernel(const BspArgs<T> a) {
 #pragma unroll(WT > 0 ? WT : 4)
     for (int k = 0; k < nw; ++k) {
       const long r = static_cast<long>(k) * a.ld + off;
-      Pack<T> x = ldv(a.w + r);
-      Pack<T> s1, s2;
-      if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
-      if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+      Pack<T> x, m1v, m2v;
+      if constexpr (WT > 0) {
+        x = xs[k];
+        m1v = s1[k];
+        m2v = s2[k];
+      } else {
+        x = ldv(a.w + r);
+        if constexpr (OPT != kSgd) m1v = ldv(a.m1 + r);
+        if constexpr (OPT == kAdam || OPT == kAdamW) m2v = ldv(a.m2 + r);
+      }
       const T b1 = static_cast<T>(a.bc1[k]);
       const T b2 = static_cast<T>(a.bc2[k]);
       bool ok = true;
 #pragma unroll
       for (int l = 0; l < VN; ++l) {
-        x.v[l] = step_elem<T, OPT>(x.v[l], gm.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
+        x.v[l] = step_elem<T, OPT>(x.v[l], gm.v[l], m1v.v[l], m2v.v[l], a.c, b1, b2);
         ok = ok && finite_(x.v[l]);
       }
       stv(a.w + r, x);
-      if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
-      if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+      if constexpr (OPT != kSgd) stv(a.m1 + r, m1v);
+      if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, m2v);
       if (!ok) {
         const unsigned long long kk = err_key(a.t, 1, k);
         bad = kk < bad ? kk : bad;
@@ -397,6 +451,9 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const FoldArgs<T> a) {
     }
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+  // Peer stores must be performed system-wide before the next cross-GPU
+  // barrier lets the owners of those rows read them.
+  __threadfence_system();
 }
 
 // ---- cross-GPU barrier over NVLink-mapped flag words ------------------------

@@ -1,0 +1,41 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed for the
+handshake only.
+
+The data path never goes through torch.distributed or NCCL: every GPU's
+worker rows are exported as CUDA IPC handles, exchanged once here, and the
+library's kernels then load/store peer rows directly over NVLink/NVSwitch
+(two-shot ordered fold) with flag barriers in peer memory.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+
+def exchange_handles(engine, group=None) -> List[bytes]:
+    """all_gather every rank's IPC handle blob (rank order)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    blobs: List[Optional[bytes]] = [None] * world
+    dist.all_gather_object(blobs, engine.ipc_export(), group=group)
+    for i, b in enumerate(blobs):
+        if not isinstance(b, (bytes, bytearray)):
+            raise RuntimeError(f"rank {i} sent no IPC handle")
+    return [bytes(b) for b in blobs]
+
+
+def attach(engine, group=None) -> None:
+    """Map every peer's rows into this context (collective: call on all ranks)."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) != engine.n_gpus:
+        raise ValueError("process group size must equal the engine's n_gpus")
+    if dist.get_rank(group) != engine.rank:
+        raise ValueError("engine rank must equal the process rank")
+    engine.ipc_attach(exchange_handles(engine, group))
+
+
+def local_slice(world_size: int, n_gpus: int, rank: int) -> range:
+    """Global worker ranks hosted by GPU `rank` (contiguous packing, gpu(k) = k / P)."""
+    if world_size % n_gpus:
+        raise ValueError("world_size must be a multiple of n_gpus")
+    per = world_size // n_gpus
+    return range(rank * per, (rank + 1) * per)

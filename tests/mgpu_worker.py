@@ -1,0 +1,104 @@
+"""Worker for the multi-GPU parity test (one process per GPU, launched by
+tests/test_multi_gpu.py through torch.distributed.run).
+
+Every rank builds the same seeded full [W][d] inputs, uploads its own rows,
+maps its peers' rows over NVLink (CUDA IPC), runs DS-Sync / BSP iterations
+whose spanning groups are folded by the in-kernel two-shot P2P path, and
+rank 0 checks the gathered result bit for bit against the fp32 oracle.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle.oracle import Oracle, hparams  # noqa: E402
+from paper_2007_03298_b200 import (BUF_GRADS, BUF_MOMENT1, BUF_PARAMS, DsSyncEngine,  # noqa: E402
+                                   OptimizerHyperparams, OptimizerKind, StrategyKind, SyncStrategy, Topology,
+                                   WorldConfig)
+from paper_2007_03298_b200.dist import attach, local_slice  # noqa: E402
+
+CASES = [
+    # kind, W, N, rect, opt, d
+    ("ds", 8, 2, True, 0, 100_003),   # C2 shape: pairs / quads spanning GPUs
+    ("ds", 8, 2, True, 1, 4097),
+    ("ds", 16, 4, False, 3, 5000),    # blocks local or spanning by G, combs spanning
+    ("ds", 32, 4, True, 1, 3001),     # C3 shape
+    ("ds", 4, 2, False, 2, 999),
+    ("bsp", 8, 8, False, 0, 70_001),
+    ("bsp", 4, 4, False, 3, 2049),
+]
+
+
+def run_case(kind, W, N, rect, opt, d, rank, G, orc):
+    s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
+                     WorldConfig(W, N), 1, rect)
+    wd = 0.01 if opt in (1, 3) else 0.0
+    hp = OptimizerHyperparams(weight_decay=wd)
+    rng = np.random.default_rng(1000 + W + opt)
+    w = rng.standard_normal((W, d)).astype(np.float32)
+    mine = local_slice(W, G, rank)
+    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", rank, rank, G)
+    attach(e)
+    e.upload_all(BUF_PARAMS, w[mine.start:mine.stop])
+    m1, m2 = np.zeros_like(w), np.zeros_like(w)
+    steps = np.zeros(W, np.int64)
+    alpha = 0.05 if opt < 2 else 0.01
+    for t in range(5):
+        g = rng.standard_normal((W, d)).astype(np.float32)
+        e.upload_all(BUF_GRADS, g[mine.start:mine.stop])
+        e.step(t, alpha)
+        if kind == "ds":
+            rc = orc.ds_step(W, N, t, opt, hparams(weight_decay=wd), alpha, steps, w, g, m1, m2, rect)
+        else:
+            rc = orc.bsp_step(t, opt, hparams(weight_decay=wd), alpha, steps, w, g, m1, m2)
+        assert rc[0] == 0
+        steps += 1
+    # sync-only round too (sync_round semantics over peers)
+    e.sync_round(5, check=False)
+    if kind == "ds":
+        orc.sync_round(W, N, 5, w, rect=rect)
+    else:
+        orc.sync_round(W, W, 5, w, kind=0)
+    e.check()
+    got = e.download_all(BUF_PARAMS)
+    got_m1 = e.download_all(BUF_MOMENT1) if opt >= 1 else None
+    parts = [None] * G
+    dist.all_gather_object(parts, (got, got_m1))
+    e.close()
+    if rank == 0:
+        full = np.concatenate([p[0] for p in parts])
+        ok = np.array_equal(full, w)
+        if opt >= 1:
+            ok = ok and np.array_equal(np.concatenate([p[1] for p in parts]), m1)
+        diff = float(np.abs(full - w).max())
+        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d}: {'OK' if ok else 'MISMATCH'} maxdiff={diff}",
+              flush=True)
+        return ok
+    return True
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    G = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo")
+    orc = Oracle()
+    ok = True
+    for case in CASES:
+        if case[1] % G:
+            continue
+        ok = run_case(*case, rank, G, orc) and ok
+    dist.barrier()
+    if rank == 0:
+        print("MGPU " + ("PASS" if ok else "FAIL"), flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

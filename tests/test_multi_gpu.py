@@ -1,0 +1,29 @@
+"""Multi-GPU parity: the two-shot in-kernel NVLink fold (one process per
+GPU) is bit-exact with the fp32 oracle.  Needs >= 2 GPUs (gpurun --gpus 2/4);
+skipped on single-GPU boxes."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _ngpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_two_shot_nvlink_bit_exact(G):
+    if _ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr=127.0.0.1", f"--master-port={29600 + G}", os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(p.stdout[-4000:])
+    print(p.stderr[-4000:])
+    assert p.returncode == 0 and "MGPU PASS" in p.stdout
