@@ -46,6 +46,9 @@ CONFIGS = {
                     "(WideResNet-28-10 size), SGD-momentum 0.9 wd=1e-4"),
     "c4": dict(W=64, N=8, rect=False, d=340_000_000, opt=3, alpha=3e-5, wd=0.01,
                desc="C4: W=64 virtual workers, groups of 8, d=340,000,000 fp32 (BERT-large size), AdamW"),
+    # one GPU's share of C4's block iteration: 8 workers, one group of 8, AdamW
+    "c4slice": dict(W=8, N=8, rect=False, d=340_000_000, opt=3, alpha=3e-5, wd=0.01,
+                    desc="C4 per-GPU slice: 8 workers in one group of 8, d=340,000,000 fp32, AdamW"),
 }
 BYTES_PER_ELEM = {0: 12, 1: 20, 2: 28, 3: 28}
 OPT_NAMES = ["vanilla-sgd", "sgd-momentum", "adam", "adamw"]
@@ -214,6 +217,114 @@ def cpu_baseline(cfg, seconds=12.0, sample_d=1 << 20):
 
 
 # ---------------------------------------------------------------------------
+def step_bytes(cfg, G, rank, d_pad):
+    """Algorithmic bytes one GPU moves per DS / BSP iteration, by kernel kind,
+    averaged over the two schedule parities (block / comb iterations).
+      group: fused apply_step + fold (local groups) or in-place step
+             (members of spanning groups): d * bytes_per_elem per member
+      fold:  two-shot owner slice L over m members: reads m*L*4, writes m*L*4;
+             the part touching other GPUs' rows crosses NVLink."""
+    from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    bpe = BYTES_PER_ELEM[cfg["opt"]]
+    P = W // G
+    mine = set(range(rank * P, (rank + 1) * P))
+    out = {"ds": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0},
+           "bsp": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0}}
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
+    chunks = d_pad // 64
+    for p in (0, 1):
+        for g in make_partition(s, p).groups:
+            here = [m for m in g if m in mine]
+            if not here:
+                continue
+            out["ds"]["group"] += 0.5 * len(here) * d * bpe
+            gpus = sorted({m // P for m in g})
+            if len(gpus) == 1:
+                continue
+            S, j = len(gpus), gpus.index(rank)
+            L = (chunks // S + (1 if j < chunks % S else 0)) * 64
+            out["ds"]["fold_hbm"] += 0.5 * 2 * len(here) * L * 4
+            out["ds"]["fold_nvlink"] += 0.5 * 2 * (len(g) - len(here)) * L * 4
+    if G == 1:
+        out["bsp"]["group"] = W * d * bpe
+    else:
+        L = (chunks // G + (1 if rank < chunks % G else 0)) * 64
+        out["bsp"]["fold_hbm"] = (P + 1) * L * 4
+        out["bsp"]["fold_nvlink"] = ((W - P) + (G - 1)) * L * 4
+        out["bsp"]["group"] = P * d * bpe
+    return out
+
+
+class NcclBaseline:
+    """Comparison baselines only (not bit-exact: NCCL's sum order is not the
+    ascending fold).  DS: our in-place apply_step, then per group a local
+    pre-sum of this GPU's member rows, one ncclAllReduce per distinct GPU set
+    (torch.distributed.new_group -> ncclCommSplit), x 1/m, copy back.
+    BSP: local pre-sum of the gradients, world ncclAllReduce, x 1/W, copy into
+    every local gradient row, our apply_step."""
+
+    def __init__(self, e, cfg, G, rank):
+        import torch
+        import torch.distributed as dist
+        from paper_2007_03298_b200 import (BUF_GRADS, BUF_PARAMS, StrategyKind, SyncStrategy, Topology,
+                                           WorldConfig, make_partition)
+        self.e, self.cfg, self.G, self.rank = e, cfg, G, rank
+        W, N, d = cfg["W"], cfg["N"], cfg["d"]
+        P = W // G
+        self.first = rank * P
+        self.rows = {k: self._view(e, BUF_PARAMS, k, d) for k in range(self.first, self.first + P)}
+        self.grads = {k: self._view(e, BUF_GRADS, k, d) for k in range(self.first, self.first + P)}
+        s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
+        self.plans = []
+        comms = {}
+        for p in (0, 1):
+            by_set = {}
+            for g in make_partition(s, p).groups:
+                gpus = tuple(sorted({m // P for m in g}))
+                by_set.setdefault(gpus, []).append(g)
+            plan = []
+            for gpus, groups in sorted(by_set.items()):
+                if gpus not in comms:
+                    comms[gpus] = dist.new_group(list(gpus)) if len(gpus) > 1 else None
+                if rank in gpus:
+                    plan.append((comms[gpus], len(gpus), groups))
+            self.plans.append(plan)
+        self.torch, self.dist = torch, dist
+
+    @staticmethod
+    def _view(e, buf, rank, n):
+        import torch
+
+        class _A:
+            def __init__(self, ptr):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                                 "version": 3}
+        return torch.as_tensor(_A(e.device_ptr(buf, rank)), device="cuda")
+
+    def ds_step(self, t, alpha):
+        torch, dist = self.torch, self.dist
+        self.e.apply_step(alpha, check=False)
+        for comm, S, groups in self.plans[t & 1]:
+            local = [[m for m in g if m in self.rows] for g in groups]
+            sums = torch.stack([torch.stack([self.rows[m] for m in lg]).sum(0) for lg in local])
+            if comm is not None:
+                dist.all_reduce(sums, group=comm)
+            for lg, g, v in zip(local, groups, sums):
+                v.mul_(1.0 / len(g))
+                for m in lg:
+                    self.rows[m].copy_(v)
+
+    def bsp_step(self, t, alpha):
+        torch, dist = self.torch, self.dist
+        acc = torch.stack(list(self.grads.values())).sum(0)
+        dist.all_reduce(acc)
+        acc.mul_(1.0 / self.cfg["W"])
+        for g in self.grads.values():
+            g.copy_(acc)
+        self.e.apply_step(alpha, check=False)
+
+
 def our_arm(args, cfg):
     import torch
     import torch.distributed as dist
@@ -233,6 +344,7 @@ def our_arm(args, cfg):
     if W % G:
         raise SystemExit(f"W={W} not divisible by {G} GPUs")
     P = W // G
+    d_pad = (d + 63) // 64 * 64
     peak, peak_kind = load_peaks()
     hp = OptimizerHyperparams(weight_decay=cfg["wd"])
     # one dedicated stream for the engine, torch's events and NCCL plumbing
@@ -245,31 +357,12 @@ def our_arm(args, cfg):
         e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, "f32", local, rank, G)
         e.set_stream(stream.cuda_stream)
         if G > 1:
-            hs = [None] * G
-            dist.all_gather_object(hs, e.ipc_export())
-            e.ipc_attach(hs)
+            from paper_2007_03298_b200.dist import attach
+            attach(e)
         e.quadratic_init(7, 4.0)
         e.quadratic_gradients(0, 1, 1.0, 0.5)
         torch.cuda.synchronize()
         return e
-
-    def timed(e, k0, K, per_launch=False):
-        e.enable_timing(per_launch)
-        if G > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for t in range(k0, k0 + K):
-            e.step(t, cfg["alpha"])
-        b.record(stream)
-        torch.cuda.synchronize()
-        if G > 1:
-            dist.barrier()
-        ms = a.elapsed_time(b)
-        kt = e.kernel_times() if per_launch else (0.0, 0, 0.0)
-        e.enable_timing(False)
-        return ms, kt
 
     def max_over_ranks(x):
         if G == 1:
@@ -278,28 +371,42 @@ def our_arm(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
+    def timed(fn, k0, K):
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for t in range(k0, k0 + K):
+            fn(t)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b)) / K
+
     res = {}
     clocks = ClockSampler(local)
     for kind, name in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
         e = make(kind)
         l0 = e.launch_count
+        step = lambda t: e.step(t, cfg["alpha"])  # noqa: E731
         for t in range(args.warmup):
-            e.step(t, cfg["alpha"])
+            step(t)
         e.check()
         if name == "ds":
             clocks.start()
             tc0 = time.time()
-        ms, _ = timed(e, args.warmup, args.steps)
+        ms = timed(step, args.warmup, args.steps)
         if name == "ds":
-            tc1 = time.time()
-            res["clocks"] = clocks.stop(tc0, tc1)
-        launches = e.launch_count - l0
-        ms = max_over_ranks(ms)
-        # per-launch event timing of the hot kernels (second pass)
-        ms2, (ktot, kn, kmax) = timed(e, args.warmup + args.steps, args.steps, per_launch=True)
+            res["clocks"] = clocks.stop(tc0, time.time())
+        launches = (e.launch_count - l0) / (args.warmup + args.steps)
+        # second pass: every hot kernel bracketed by events on its stream
+        e.enable_timing(True)
+        timed(step, args.warmup + args.steps, args.steps)
+        kinds = e.kernel_times_by_kind()
+        e.enable_timing(False)
         e.check()
-        res[name] = dict(ms=ms / args.steps, kernel_ms=ktot, kernel_launches=kn, kernel_max_ms=kmax,
-                         launches_per_step=launches / (args.warmup + args.steps))
+        res[name] = dict(ms=ms, kinds={k: (v[0] / args.steps, v[1] / args.steps) for k, v in kinds.items()},
+                         launches_per_step=launches)
         if name == "ds":
             # e2e through the C-ABI with host buffers: pinned H2D of every
             # local worker's gradient, the step, D2H of every worker's params.
@@ -307,28 +414,27 @@ def our_arm(args, cfg):
             hg = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
             hw = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
             e.download_all(BUF_GRADS, hg)
-            if G > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for t in range(K2):
+
+            def e2e(t):
                 e.upload_all(BUF_GRADS, hg)
-                e.step(args.warmup + 2 * args.steps + t, cfg["alpha"])
+                e.step(t, cfg["alpha"])
                 e.download_all(BUF_PARAMS, hw)
-            b.record(stream)
-            torch.cuda.synchronize()
-            e2e_ms = max_over_ranks(a.elapsed_time(b)) / K2
-            res["e2e"] = dict(ms=e2e_ms, h2d=P * d * 4 * G, d2h=P * d * 4 * G, wall=time.perf_counter() - t0)
+            res["e2e_ms"] = timed(e2e, args.warmup + 2 * args.steps, K2)
             e.check()
+        if G > 1 and not args.no_nccl:
+            nb = NcclBaseline(e, cfg, G, rank)
+            fn = (lambda t: nb.ds_step(t, cfg["alpha"])) if name == "ds" else (lambda t: nb.bsp_step(t, cfg["alpha"]))
+            for t in range(3):
+                fn(t)
+            res["nccl_" + name] = timed(fn, 3, max(3, args.steps // 2))
+            del nb
         e.close()
         del e
         torch.cuda.synchronize()
 
     if G > 1:
         dist.barrier()
+    nb_bytes = step_bytes(cfg, G, rank, d_pad)
     if rank != 0:
         if G > 1:
             dist.destroy_process_group()
@@ -337,17 +443,36 @@ def our_arm(args, cfg):
     ds, bsp = res["ds"], res["bsp"]
     ipsec = 1000.0 / ds["ms"]
     bpe = BYTES_PER_ELEM[cfg["opt"]]
-    alg_bytes_step = W * d * bpe  # whole job, all ranks
-    # dominant kernel: fused DS group kernel (1 GPU) — algorithmic bytes per
-    # launch = (bytes of the step on this GPU) / launches per step
-    k_ms_avg = ds["kernel_ms"] / max(ds["kernel_launches"], 1)
-    per_gpu_bytes = P * d * bpe
-    achieved = per_gpu_bytes * args.steps / (ds["kernel_ms"] / 1e3) / 1e9 if ds["kernel_ms"] else None
+
+    def kernel_rows(r, key):
+        rows = {}
+        for k, (ms_, n_) in r["kinds"].items():
+            if n_ == 0:
+                continue
+            row = {"ms_per_step": ms_, "launches_per_step": n_}
+            if k == "group" or k == "bsp":
+                b = nb_bytes[key]["group"]
+                row.update(alg_bytes_per_step=b, hbm_gbs=b / (ms_ / 1e3) / 1e9 if ms_ else None)
+            elif k == "fold":
+                row.update(alg_bytes_per_step=nb_bytes[key]["fold_hbm"] + nb_bytes[key]["fold_nvlink"],
+                           nvlink_bytes_per_step=nb_bytes[key]["fold_nvlink"],
+                           nvlink_gbs=nb_bytes[key]["fold_nvlink"] / (ms_ / 1e3) / 1e9 if ms_ else None)
+            rows[k] = row
+        return rows
+
+    ds_k = kernel_rows(ds, "ds")
+    dom = max(ds_k.items(), key=lambda kv: kv[1]["ms_per_step"])
+    # dominant kernel: its algorithmic bytes per launch / its mean launch time
+    dk, dv = dom
+    per_launch_ms = dv["ms_per_step"] / dv["launches_per_step"]
+    per_launch_bytes = dv.get("alg_bytes_per_step", 0.0) / dv["launches_per_step"]
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{args.config}_g{G}")
+            tr = json.load(open(prof)).get(f"{args.config}_g{G}")
+            traffic = tr["bytes_per_launch"] if tr else None
         except Exception:
             traffic = None
     out = {
@@ -368,22 +493,33 @@ def our_arm(args, cfg):
                    "l2": f"inputs larger than L2: {P * d * 4 / 1e6:.0f} MB per array per GPU"
                          if P * d * 4 > 126e6 else "inputs smaller than L2 (latency-bound config)"},
         "effective_gbs": W * d * 4 / (ds["ms"] / 1e3) / 1e9,
-        "hbm_gbs_algorithmic": alg_bytes_step / (ds["ms"] / 1e3) / 1e9,
+        "hbm_gbs_algorithmic": W * d * bpe / (ds["ms"] / 1e3) / 1e9,
         "bsp": {"iters_s": 1000.0 / bsp["ms"], "ms_per_step": bsp["ms"],
-                "effective_gbs": W * d * 4 / (bsp["ms"] / 1e3) / 1e9,
-                "ds_over_bsp": bsp["ms"] / ds["ms"]},
+                "effective_gbs": W * d * 4 / (bsp["ms"] / 1e3) / 1e9, "ds_speedup_over_bsp": bsp["ms"] / ds["ms"],
+                "kernels": kernel_rows(bsp, "bsp")},
+        "kernels": ds_k,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "peak_kind": peak_kind, "kernel": "ds_group_kernel (fused apply_step + ordered fold + broadcast)"
-                     if G == 1 else "DS step kernels (local step + two-shot NVLink fold)",
-                     "avg_launch_ms": k_ms_avg, "launches_per_step": ds["launches_per_step"],
-                     "alg_bytes_per_launch": per_gpu_bytes * args.steps / max(ds["kernel_launches"], 1)},
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": {"group": "ds_group_kernel (fused apply_step + ordered fold + broadcast)",
+                                "fold": "fold_kernel (two-shot ordered fold over NVLink peers)",
+                                "bsp": "bsp_kernel", "barrier": "barrier_kernel"}.get(dk, dk),
+                     "avg_launch_ms": per_launch_ms, "alg_bytes_per_launch": per_launch_bytes},
         "gpu_launches": int(round(ds["launches_per_step"] * args.steps)),
         "clocks": res.get("clocks"),
-        "e2e": {"value": 1000.0 / res["e2e"]["ms"], "unit": "iters/s", "h2d_bytes_per_step": res["e2e"]["h2d"],
-                "d2h_bytes_per_step": res["e2e"]["d2h"],
+        "e2e": {"value": 1000.0 / res["e2e_ms"], "unit": "iters/s", "h2d_bytes_per_step": P * d * 4 * G,
+                "d2h_bytes_per_step": P * d * 4 * G,
                 "path": "C-ABI dss_upload_all(grads, pinned) + dss_step + dss_download_all(params, pinned)"},
     }
+    if "fold" in ds_k and ds_k["fold"].get("nvlink_gbs"):
+        out["nvlink"] = {"achieved": ds_k["fold"]["nvlink_gbs"], "peak": 770.0, "unit": "GB/s",
+                         "frac": ds_k["fold"]["nvlink_gbs"] / 770.0,
+                         "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
+                         "note": "rank-0 fold kernel: remote reads + remote writes per owned slice / kernel time"}
+    if G > 1 and "nccl_ds" in res:
+        out["nccl_baselines"] = {
+            "ds_split_allreduce": {"iters_s": 1000.0 / res["nccl_ds"], "ms_per_step": res["nccl_ds"]},
+            "bsp_world_allreduce": {"iters_s": 1000.0 / res["nccl_bsp"], "ms_per_step": res["nccl_bsp"]},
+            "note": "torch.distributed NCCL (ncclCommSplit sub-communicators); tolerance-parity only"}
     if G == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(out))
@@ -401,6 +537,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=1 << 19)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -232,6 +232,17 @@ int dss_last_global_error(char* buf, size_t len);
  * totals over the launches since the last reset are returned. */
 int dss_enable_timing(dss_ctx* ctx, int on);
 int dss_kernel_times(dss_ctx* ctx, double* total_ms, long* launches, double* max_launch_ms);
+/* Same events split by kernel kind: arrays of DSS_KIND_COUNT entries
+ * (total ms, launches) since the last call to either timing query. */
+enum {
+  DSS_KIND_GROUP = 0,    /* ds_group_kernel: fused step + ordered fold (or in-place step) */
+  DSS_KIND_FOLD = 1,     /* fold_kernel: two-shot ordered fold over NVLink peers */
+  DSS_KIND_BSP = 2,      /* bsp_kernel: fused gradient fold + step */
+  DSS_KIND_BARRIER = 3,  /* barrier_kernel: cross-GPU flag barrier */
+  DSS_KIND_GRADIENT = 4, /* quad_grad_kernel: synthetic gradients */
+  DSS_KIND_COUNT = 5
+};
+int dss_kernel_times_by_kind(dss_ctx* ctx, double* total_ms, long* launches);
 /* gpu_launches: hot-path kernels launched since creation (all kinds). */
 long dss_launch_count(const dss_ctx* ctx);
 

@@ -16,6 +16,7 @@ DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2 = range(4)
 IPC_BYTES = 256
+KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient"]
 
 
 class dss_hparams(C.Structure):
@@ -81,6 +82,7 @@ SIGNATURES = {
     "dss_last_global_error": (C.c_int, [C.c_char_p, C.c_size_t]),
     "dss_enable_timing": (C.c_int, [_P, C.c_int]),
     "dss_kernel_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_long), C.POINTER(C.c_double)]),
+    "dss_kernel_times_by_kind": (C.c_int, [_P, _P, _P]),
     "dss_launch_count": (C.c_long, [_P]),
     "dss_ipc_export": (C.c_int, [_P, _P]),
     "dss_ipc_attach": (C.c_int, [_P, _P]),

@@ -382,6 +382,13 @@ class DsSyncEngine:
         self._ck(self.lib.dss_kernel_times(self.h, C.byref(tot), C.byref(n), C.byref(mx)))
         return tot.value, n.value, mx.value
 
+    def kernel_times_by_kind(self) -> dict:
+        """{kind: (total_ms, launches)} since the last timing query."""
+        ms = np.zeros(len(L.KIND_NAMES), np.float64)
+        n = np.zeros(len(L.KIND_NAMES), np.int64)
+        self._ck(self.lib.dss_kernel_times_by_kind(self.h, ms.ctypes.data, n.ctypes.data))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(L.KIND_NAMES)}
+
     @property
     def launch_count(self) -> int:
         return self.lib.dss_launch_count(self.h)

@@ -129,6 +129,9 @@ struct dss_ctx {
 
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+  std::vector<int> ev_kind;
+  double kind_ms[DSS_KIND_COUNT] = {};
+  long kind_n[DSS_KIND_COUNT] = {};
   std::vector<cudaEvent_t> ev_pool;
   long launches = 0;
 
@@ -361,8 +364,9 @@ void build_plans(dss_ctx* c) {
 
 struct TimedLaunch {
   dss_ctx* c;
+  int kind;
   cudaEvent_t b = nullptr, e = nullptr;
-  explicit TimedLaunch(dss_ctx* cc) : c(cc) {
+  TimedLaunch(dss_ctx* cc, int k) : c(cc), kind(k) {
     ++c->launches;
     if (!c->timing) return;
     for (cudaEvent_t* ev : {&b, &e}) {
@@ -379,6 +383,7 @@ struct TimedLaunch {
     if (!c->timing) return;
     cudaEventRecord(e, c->stream);
     c->ev_pending.emplace_back(b, e);
+    c->ev_kind.push_back(kind);
   }
 };
 
@@ -419,7 +424,7 @@ void fill_bias(const dss_ctx* c, Args& a) {
 template <typename T, int OPT, int M>
 void launch_group_t(dss_ctx* c, const GroupArgs<T>& a, int groups) {
   dim3 grid(grid_x(c, a.nvec, groups), groups);
-  TimedLaunch tl(c);
+  TimedLaunch tl(c, DSS_KIND_GROUP);
   ds_group_kernel<T, OPT, M><<<grid, kThreads, 0, c->stream>>>(a);
   ck(cudaGetLastError(), "ds_group_kernel launch");
 }
@@ -486,7 +491,7 @@ void launch_fold_t(dss_ctx* c, const FoldLaunch& fl, long t) {
   a.t = t;
   a.err = c->d_err;
   dim3 grid(grid_x(c, fl.max_len / Vec<T>::n, fl.entries), fl.entries);
-  TimedLaunch tl(c);
+  TimedLaunch tl(c, DSS_KIND_FOLD);
   fold_kernel<T, M><<<grid, kThreads, 0, c->stream>>>(a);
   ck(cudaGetLastError(), "fold_kernel launch");
 }
@@ -513,7 +518,7 @@ void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
 template <typename T, int OPT, int WT>
 void launch_bsp_t(dss_ctx* c, const BspArgs<T>& a) {
   dim3 grid(grid_x(c, a.nvec, 1), 1);
-  TimedLaunch tl(c);
+  TimedLaunch tl(c, DSS_KIND_BSP);
   bsp_kernel<T, OPT, WT><<<grid, kThreads, 0, c->stream>>>(a);
   ck(cudaGetLastError(), "bsp_kernel launch");
 }
@@ -555,7 +560,7 @@ void barrier(dss_ctx* c) {
   if (!multi(c)) return;
   if (!c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
   ++c->epoch;
-  TimedLaunch tl(c);
+  TimedLaunch tl(c, DSS_KIND_BARRIER);
   barrier_kernel<<<1, 32 * ((c->cfg.n_gpus + 31) / 32), 0, c->stream>>>(
       c->d_peer_flags, c->flags, c->cfg.rank, c->cfg.n_gpus, c->epoch, c->d_timeout);
   ck(cudaGetLastError(), "barrier_kernel launch");
@@ -1038,7 +1043,7 @@ extern "C" int dss_quadratic_gradients(dss_ctx* c, long t, uint64_t seed, double
         a.s0[k] = stream_state(seed, kGradientNoise, static_cast<uint64_t>(c->first + k), static_cast<uint64_t>(t));
       }
       dim3 grid(grid_x(c, c->d_pad, c->P), c->P);
-      TimedLaunch tl(c);
+      TimedLaunch tl(c, DSS_KIND_GRADIENT);
       quad_grad_kernel<T><<<grid, kThreads, 0, c->stream>>>(a);
       ck(cudaGetLastError(), "quad_grad_kernel launch");
     };
@@ -1142,24 +1147,58 @@ extern "C" int dss_enable_timing(dss_ctx* c, int on) {
   return DSS_OK;
 }
 
+namespace {
+void drain_events(dss_ctx* c) {
+  ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+  ck(cudaStreamSynchronize(c->stream), "timing sync");
+  for (size_t i = 0; i < c->ev_pending.size(); ++i) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, c->ev_pending[i].first, c->ev_pending[i].second), "cudaEventElapsedTime");
+    c->kind_ms[c->ev_kind[i]] += ms;
+    c->kind_n[c->ev_kind[i]] += 1;
+    c->ev_pool.push_back(c->ev_pending[i].first);
+    c->ev_pool.push_back(c->ev_pending[i].second);
+  }
+  c->ev_pending.clear();
+  c->ev_kind.clear();
+}
+}  // namespace
+
 extern "C" int dss_kernel_times(dss_ctx* c, double* total_ms, long* launches, double* max_launch_ms) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     ck(cudaStreamSynchronize(c->stream), "timing sync");
     double tot = 0.0, mx = 0.0;
-    for (auto& pr : c->ev_pending) {
+    for (size_t i = 0; i < c->ev_pending.size(); ++i) {
       float ms = 0.f;
-      ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "cudaEventElapsedTime");
+      ck(cudaEventElapsedTime(&ms, c->ev_pending[i].first, c->ev_pending[i].second), "cudaEventElapsedTime");
       tot += ms;
       mx = std::max(mx, static_cast<double>(ms));
-      c->ev_pool.push_back(pr.first);
-      c->ev_pool.push_back(pr.second);
+    }
+    const long n = static_cast<long>(c->ev_pending.size());
+    drain_events(c);
+    for (int k = 0; k < DSS_KIND_COUNT; ++k) {
+      c->kind_ms[k] = 0.0;
+      c->kind_n[k] = 0;
     }
     if (total_ms) *total_ms = tot;
-    if (launches) *launches = static_cast<long>(c->ev_pending.size());
+    if (launches) *launches = n;
     if (max_launch_ms) *max_launch_ms = mx;
-    c->ev_pending.clear();
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_kernel_times_by_kind(dss_ctx* c, double* total_ms, long* launches) {
+  if (!c || !total_ms || !launches) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    drain_events(c);
+    for (int k = 0; k < DSS_KIND_COUNT; ++k) {
+      total_ms[k] = c->kind_ms[k];
+      launches[k] = c->kind_n[k];
+      c->kind_ms[k] = 0.0;
+      c->kind_n[k] = 0;
+    }
     return DSS_OK;
   });
 }
