@@ -169,7 +169,7 @@ template <typename T> struct GroupArgs {
 // step; store state; fold.  Then scale once and store the mean to every
 // member: each element of every array is read once and written once.
 template <typename T, int OPT, int M>
-__global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, 2) ds_group_kernel(const GroupArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   const int beg = a.offsets[blockIdx.y];
   const int m = M > 0 ? M : a.offsets[blockIdx.y + 1] - beg;
@@ -178,22 +178,14 @@ __global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a
   const T inv = static_cast<T>(1.0 / static_cast<double>(m));
   unsigned long long bad = ~0ull;
 
-  // Per-member row offsets hoisted out of the element loop (registers for
-  // the templated group sizes).
+  // Per-member local row index hoisted out of the element loop (registers
+  // for the templated group sizes); 64-bit offsets and bias corrections are
+  // derived per use to keep register pressure low at M = 8.
   constexpr int RM = M > 0 ? M : 1;
-  long row[RM], grow[RM];
-  int rank[RM];
-  T bc1[RM], bc2[RM];
+  int lrow[RM];
   if constexpr (M > 0) {
 #pragma unroll
-    for (int j = 0; j < M; ++j) {
-      rank[j] = a.members[beg + j];
-      const int lr = rank[j] - a.first_rank;
-      row[j] = static_cast<long>(lr) * a.ld;
-      grow[j] = static_cast<long>(lr) * a.g_ld;
-      bc1[j] = static_cast<T>(a.bc1[lr]);
-      bc2[j] = static_cast<T>(a.bc2[lr]);
-    }
+    for (int j = 0; j < M; ++j) lrow[j] = a.members[beg + j] - a.first_rank;
   }
 
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
@@ -201,40 +193,55 @@ __global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a
     const long off = e * VN;
     Pack<T> acc;
     if constexpr (M > 0) {
-      // Templated group size: issue every member's loads first (w, g and
-      // optimizer state of all M members in flight at once), then step,
+      // Templated group size: issue a chunk of members' loads first (w, g
+      // and optimizer state of CH members in flight at once), then step,
       // store state and fold in ascending member order.  Without this split
       // a member's state stores would pin the next member's loads behind
-      // them (the compiler cannot prove the rows do not alias).
-      Pack<T> xs[M], gs[M], s1[M], s2[M];
+      // them (the compiler cannot prove the rows do not alias).  Stateful
+      // optimizers carry 3-4 arrays per member, so groups of 8 work in
+      // chunks of 4 members to stay within 128 registers (2 CTAs / SM).
+      constexpr int CH = (OPT == kMomentum || OPT == kAdam || OPT == kAdamW) && M > 4 ? 4 : M;
 #pragma unroll
-      for (int j = 0; j < M; ++j) {
-        xs[j] = ldv(a.w + row[j] + off);
-        if constexpr (OPT != kOptNone) gs[j] = ldv(a.g + grow[j] + off);
-        if constexpr (OPT != kOptNone && OPT != kSgd) s1[j] = ldv(a.m1 + row[j] + off);
-        if constexpr (OPT == kAdam || OPT == kAdamW) s2[j] = ldv(a.m2 + row[j] + off);
-      }
+      for (int c0 = 0; c0 < M; c0 += CH) {
+        Pack<T> xs[CH], gs[CH], s1[CH], s2[CH];
 #pragma unroll
-      for (int j = 0; j < M; ++j) {
-        if constexpr (OPT != kOptNone) {
-          bool ok = true;
-#pragma unroll
-          for (int l = 0; l < VN; ++l) {
-            xs[j].v[l] = step_elem<T, OPT>(xs[j].v[l], gs[j].v[l], s1[j].v[l], s2[j].v[l], a.c, bc1[j], bc2[j]);
-            ok = ok && finite_(xs[j].v[l]);
-          }
-          if constexpr (OPT != kSgd) stv(a.m1 + row[j] + off, s1[j]);
-          if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + row[j] + off, s2[j]);
-          if (!ok) {
-            const unsigned long long k = err_key(a.t, a.step_phase, rank[j]);
-            bad = k < bad ? k : bad;
-          }
+        for (int q = 0; q < CH; ++q) {
+          const int j = c0 + q;
+          const long rj = static_cast<long>(lrow[j]) * a.ld + off;
+          xs[q] = ldv(a.w + rj);
+          if constexpr (OPT != kOptNone) gs[q] = ldv(a.g + static_cast<long>(lrow[j]) * a.g_ld + off);
+          if constexpr (OPT != kOptNone && OPT != kSgd) s1[q] = ldv(a.m1 + rj);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2[q] = ldv(a.m2 + rj);
         }
-        if (j == 0) {
-          acc = xs[0];
-        } else {
 #pragma unroll
-          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], xs[j].v[l]);
+        for (int q = 0; q < CH; ++q) {
+          const int j = c0 + q;
+          if constexpr (OPT != kOptNone) {
+            const long rj = static_cast<long>(lrow[j]) * a.ld + off;
+            T b1j = T(1), b2j = T(1);
+            if constexpr (OPT == kAdam || OPT == kAdamW) {
+              b1j = static_cast<T>(a.bc1[lrow[j]]);
+              b2j = static_cast<T>(a.bc2[lrow[j]]);
+            }
+            bool ok = true;
+#pragma unroll
+            for (int l = 0; l < VN; ++l) {
+              xs[q].v[l] = step_elem<T, OPT>(xs[q].v[l], gs[q].v[l], s1[q].v[l], s2[q].v[l], a.c, b1j, b2j);
+              ok = ok && finite_(xs[q].v[l]);
+            }
+            if constexpr (OPT != kSgd) stv(a.m1 + rj, s1[q]);
+            if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj, s2[q]);
+            if (!ok) {
+              const unsigned long long k = err_key(a.t, a.step_phase, lrow[j] + a.first_rank);
+              bad = k < bad ? k : bad;
+            }
+          }
+          if (j == 0) {
+            acc = xs[q];
+          } else {
+#pragma unroll
+            for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], xs[q].v[l]);
+          }
         }
       }
     } else {
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) ds_group_kernel(const GroupArgs<T> a
     }
     if constexpr (M > 0) {
 #pragma unroll
-      for (int j = 0; j < M; ++j) stv(a.w + row[j] + off, acc);
+      for (int j = 0; j < M; ++j) stv(a.w + static_cast<long>(lrow[j]) * a.ld + off, acc);
     } else {
 #pragma unroll 4
       for (int j = 0; j < m; ++j) stv(a.w + static_cast<long>(a.members[beg + j] - a.first_rank) * a.ld + off, acc);
@@ -316,7 +323,7 @@ template <typename T> struct BspArgs {
 };
 
 template <typename T, int OPT, int WT>
-__global__ void __launch_bounds__(kThreads) bsp_kernel(const BspArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, 2) bsp_kernel(const BspArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   const int nw = WT > 0 ? WT : a.nw;
   const T inv = static_cast<T>(1.0 / static_cast<double>(nw));
@@ -325,18 +332,24 @@ __global__ void __launch_bounds__(kThreads) bsp_kernel(const BspArgs<T> a) {
   for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < a.nvec; e += stride) {
     const long off = e * VN;
     Pack<T> gm;
-    constexpr int RW = WT > 0 ? WT : 1;
-    Pack<T> xs[RW], s1[RW], s2[RW];
+    // params/state of the first BCH workers are loaded with the gradients;
+    // the rest stream behind (stateful optimizers at W = 8 would otherwise
+    // need > 128 registers)
+    constexpr int BCH = WT == 0 ? 1 : (OPT != kSgd && WT > 4 ? 4 : WT);
+    Pack<T> xs[BCH], s1[BCH], s2[BCH];
     if constexpr (WT > 0) {
-      // every load of the iteration in flight before the first store
+      // every gradient and the first chunk of params/state in flight before
+      // the first store
       Pack<T> gs[WT];
 #pragma unroll
       for (int k = 0; k < WT; ++k) {
         const long r = static_cast<long>(k) * a.ld + off;
         gs[k] = ldv(a.g + r);
-        xs[k] = ldv(a.w + r);
-        if constexpr (OPT != kSgd) s1[k] = ldv(a.m1 + r);
-        if constexpr (OPT == kAdam || OPT == kAdamW) s2[k] = ldv(a.m2 + r);
+        if (k < BCH) {
+          xs[k] = ldv(a.w + r);
+          if constexpr (OPT != kSgd) s1[k] = ldv(a.m1 + r);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2[k] = ldv(a.m2 + r);
+        }
       }
       gm = gs[0];
 #pragma unroll
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(kThreads) bsp_kernel(const BspArgs<T> a) {
     for (int k = 0; k < nw; ++k) {
       const long r = static_cast<long>(k) * a.ld + off;
       Pack<T> x, m1v, m2v;
-      if constexpr (WT > 0) {
+      if (WT > 0 && k < BCH) {
         x = xs[k];
         m1v = s1[k];
         m2v = s2[k];
