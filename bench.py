@@ -371,14 +371,17 @@ def our_arm(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
-    def timed(fn, k0, K):
+    def timed(fn, k0, K, batched=None):
         if G > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for t in range(k0, k0 + K):
-            fn(t)
+        if batched is not None:
+            batched(k0, K)  # K iterations in one library call (dss_steps)
+        else:
+            for t in range(k0, k0 + K):
+                fn(t)
         b.record(stream)
         torch.cuda.synchronize()
         return max_over_ranks(a.elapsed_time(b)) / K
@@ -389,19 +392,20 @@ def our_arm(args, cfg):
         e = make(kind)
         l0 = e.launch_count
         step = lambda t: e.step(t, cfg["alpha"])  # noqa: E731
+        steps = lambda k0, K: e.steps(k0, np.full(K, cfg["alpha"]))  # noqa: E731
         for t in range(args.warmup):
             step(t)
         e.check()
         if name == "ds":
             clocks.start()
             tc0 = time.time()
-        ms = timed(step, args.warmup, args.steps)
+        ms = timed(step, args.warmup, args.steps, batched=steps)
         if name == "ds":
             res["clocks"] = clocks.stop(tc0, time.time())
         launches = (e.launch_count - l0) / (args.warmup + args.steps)
         # second pass: every hot kernel bracketed by events on its stream
         e.enable_timing(True)
-        timed(step, args.warmup + args.steps, args.steps)
+        timed(step, args.warmup + args.steps, args.steps, batched=steps)
         kinds = e.kernel_times_by_kind()
         e.enable_timing(False)
         e.check()
@@ -538,10 +542,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--d", type=int, default=None, help="override the config's d (profiling runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.d:
+        cfg["d"] = args.d
+        cfg["desc"] += f" [d overridden to {args.d:,} for profiling]"
     if args.impl == "reference":
         reference_arm(args, cfg)
     else:

@@ -196,6 +196,11 @@ long dss_get_step_count(const dss_ctx* ctx, int rank);
  * DSS_EDIVERGED from dss_check() (or from this call when check != 0). */
 int dss_step(dss_ctx* ctx, long t, double alpha, int check, dss_outcome* out);
 
+/* n consecutive iterations t0 .. t0+n-1 (alphas[i] for iteration t0+i) in
+ * one call: the run_training loop body (sync.cpp:323-459, sync part) without
+ * a host round trip per iteration. */
+int dss_steps(dss_ctx* ctx, long t0, long n, const double* alphas, int check, dss_outcome* last);
+
 /* sync_round (sync.cpp:268-282): group averaging only, no optimizer step.
  * Optimizer state untouched. */
 int dss_sync_round(dss_ctx* ctx, long t, int check, dss_outcome* out);

@@ -11,6 +11,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdssync_b200.so")
+# Tuning experiments only: load a variant build of the same library
+# (paper_2007_03298_b200.build --variant); the product default is LIB_PATH.
+LIB_PATH = os.environ.get("DSS_LIB_VARIANT", LIB_PATH)
 
 DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
@@ -71,6 +74,7 @@ SIGNATURES = {
     "dss_set_step_count": (C.c_int, [_P, C.c_int, C.c_long]),
     "dss_get_step_count": (C.c_long, [_P, C.c_int]),
     "dss_step": (C.c_int, [_P, C.c_long, C.c_double, C.c_int, C.POINTER(dss_outcome)]),
+    "dss_steps": (C.c_int, [_P, C.c_long, C.c_long, _P, C.c_int, C.POINTER(dss_outcome)]),
     "dss_sync_round": (C.c_int, [_P, C.c_long, C.c_int, C.POINTER(dss_outcome)]),
     "dss_apply_step": (C.c_int, [_P, C.c_double, C.c_int]),
     "dss_quadratic_gradients": (C.c_int, [_P, C.c_long, C.c_uint64, C.c_double, C.c_double]),

@@ -349,6 +349,13 @@ class DsSyncEngine:
         self._ck(self.lib.dss_step(self.h, t, alpha, 1 if check else 0, C.byref(o)))
         return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
 
+    def steps(self, t0: int, alphas, check: bool = False) -> SyncRoundOutcome:
+        """len(alphas) consecutive iterations from t0 in one library call."""
+        a = np.ascontiguousarray(alphas, dtype=np.float64)
+        o = L.dss_outcome()
+        self._ck(self.lib.dss_steps(self.h, t0, a.size, a.ctypes.data, 1 if check else 0, C.byref(o)))
+        return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
+
     def sync_round(self, t: int, check: bool = True) -> SyncRoundOutcome:
         o = L.dss_outcome()
         self._ck(self.lib.dss_sync_round(self.h, t, 1 if check else 0, C.byref(o)))

@@ -46,32 +46,46 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+def build_lib(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+              defines: tuple = (), out: str = LIB) -> str:
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, "dssync_b200.h")]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and not _stale(out, deps):
+        return out
+    bdir = BUILD if out == LIB else os.path.join(BUILD, os.path.basename(out) + ".d")
+    os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     objs = []
     for src in SOURCES:
-        obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(bdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if ptxas_v and src.endswith(".cu"):
             cmd.insert(1, "-Xptxas=-v")
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
+
+
+def build_variant(name: str, defines: tuple) -> str:
+    """Tuning builds: build/variants/libdssync_b200_<name>.so (A/B runs via DSS_LIB_VARIANT)."""
+    vdir = os.path.join(ROOT, "build", "variants")
+    os.makedirs(vdir, exist_ok=True)
+    return build_lib(force=True, defines=defines, out=os.path.join(vdir, f"libdssync_b200_{name}.so"))
 
 
 if __name__ == "__main__":
-    build_lib(force="--force" in sys.argv, verbose=True, ptxas_v="--ptxas-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], tuple(sys.argv[i + 2:])
+        print(build_variant(name, defs))
+    else:
+        build_lib(force="--force" in sys.argv, verbose=True, ptxas_v="--ptxas-v" in sys.argv)
+        print(LIB)

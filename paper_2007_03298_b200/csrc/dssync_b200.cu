@@ -982,6 +982,16 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
   });
 }
 
+extern "C" int dss_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
+  if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
+  for (long i = 0; i < n; ++i) {
+    const int st = dss_step(c, t0 + i, alphas[i], 0, last);
+    if (st != DSS_OK) return st;
+  }
+  if (check) return dss_check(c);
+  return DSS_OK;
+}
+
 extern "C" int dss_sync_round(dss_ctx* c, long t, int check, dss_outcome* out) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
   return guard(c, [&]() -> int {

@@ -22,6 +22,22 @@ namespace dssb {
 constexpr int kThreads = 256;
 constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel params
 
+// Tuning knobs (compile-time; the defaults are the measured best, see
+// DESIGN.md).  Members whose loads are issued together before the first
+// state store, per optimizer, and the CTAs/SM the register cap targets.
+#ifndef DSS_CHUNK_MOMENTUM
+#define DSS_CHUNK_MOMENTUM 8
+#endif
+#ifndef DSS_CHUNK_ADAM
+#define DSS_CHUNK_ADAM 4
+#endif
+#ifndef DSS_MIN_BLOCKS
+#define DSS_MIN_BLOCKS 2
+#endif
+#ifndef DSS_MIN_BLOCKS_M8_MOMENTUM
+#define DSS_MIN_BLOCKS_M8_MOMENTUM 1
+#endif
+
 enum OptKind : int { kOptNone = -1, kSgd = 0, kMomentum = 1, kAdam = 2, kAdamW = 3 };
 
 // ---- exact scalar ops ------------------------------------------------------
@@ -168,8 +184,13 @@ template <typename T> struct GroupArgs {
 // Per element vector: for each member in ascending order load w, g, state;
 // step; store state; fold.  Then scale once and store the mean to every
 // member: each element of every array is read once and written once.
+template <int OPT, int M>
+constexpr int group_min_blocks() {
+  return (OPT == kMomentum && M == 8) ? DSS_MIN_BLOCKS_M8_MOMENTUM : DSS_MIN_BLOCKS;
+}
+
 template <typename T, int OPT, int M>
-__global__ void __launch_bounds__(kThreads, 2) ds_group_kernel(const GroupArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group_kernel(const GroupArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   const int beg = a.offsets[blockIdx.y];
   const int m = M > 0 ? M : a.offsets[blockIdx.y + 1] - beg;
@@ -200,7 +221,9 @@ __global__ void __launch_bounds__(kThreads, 2) ds_group_kernel(const GroupArgs<T
       // them (the compiler cannot prove the rows do not alias).  Stateful
       // optimizers carry 3-4 arrays per member, so groups of 8 work in
       // chunks of 4 members to stay within 128 registers (2 CTAs / SM).
-      constexpr int CH = (OPT == kMomentum || OPT == kAdam || OPT == kAdamW) && M > 4 ? 4 : M;
+      constexpr int CH = OPT == kMomentum ? (M > DSS_CHUNK_MOMENTUM ? DSS_CHUNK_MOMENTUM : M)
+                         : (OPT == kAdam || OPT == kAdamW) ? (M > DSS_CHUNK_ADAM ? DSS_CHUNK_ADAM : M)
+                                                           : M;
 #pragma unroll
       for (int c0 = 0; c0 < M; c0 += CH) {
         Pack<T> xs[CH], gs[CH], s1[CH], s2[CH];
@@ -323,7 +346,7 @@ template <typename T> struct BspArgs {
 };
 
 template <typename T, int OPT, int WT>
-__global__ void __launch_bounds__(kThreads, 2) bsp_kernel(const BspArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, DSS_MIN_BLOCKS) bsp_kernel(const BspArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   const int nw = WT > 0 ? WT : a.nw;
   const T inv = static_cast<T>(1.0 / static_cast<double>(nw));
@@ -358,9 +381,20 @@ __global__ void __launch_bounds__(kThreads, 2) bsp_kernel(const BspArgs<T> a) {
         for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], gs[k].v[l]);
       }
     } else {
+      // any W: gradients in batches of 8 loads in flight, folded in order
       gm = ldv(a.g + off);
-#pragma unroll 4
-      for (int k = 1; k < nw; ++k) {
+      int k = 1;
+      for (; k + 8 <= nw; k += 8) {
+        Pack<T> gb[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gb[q] = ldv(a.g + static_cast<long>(k + q) * a.ld + off);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+          for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], gb[q].v[l]);
+        }
+      }
+      for (; k < nw; ++k) {
         const Pack<T> x = ldv(a.g + static_cast<long>(k) * a.ld + off);
 #pragma unroll
         for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], x.v[l]);
@@ -376,19 +410,8 @@ __global__ void __launch_bounds__(kThreads, 2) bsp_kernel(const BspArgs<T> a) {
       const unsigned long long k = err_key(a.t, 0, 0);
       bad = k < bad ? k : bad;
     }
-#pragma unroll(WT > 0 ? WT : 4)
-    for (int k = 0; k < nw; ++k) {
+    auto step_store = [&](int k, Pack<T>& x, Pack<T>& m1v, Pack<T>& m2v) {
       const long r = static_cast<long>(k) * a.ld + off;
-      Pack<T> x, m1v, m2v;
-      if (WT > 0 && k < BCH) {
-        x = xs[k];
-        m1v = s1[k];
-        m2v = s2[k];
-      } else {
-        x = ldv(a.w + r);
-        if constexpr (OPT != kSgd) m1v = ldv(a.m1 + r);
-        if constexpr (OPT == kAdam || OPT == kAdamW) m2v = ldv(a.m2 + r);
-      }
       const T b1 = static_cast<T>(a.bc1[k]);
       const T b2 = static_cast<T>(a.bc2[k]);
       bool ok = true;
@@ -403,6 +426,47 @@ __global__ void __launch_bounds__(kThreads, 2) bsp_kernel(const BspArgs<T> a) {
       if (!ok) {
         const unsigned long long kk = err_key(a.t, 1, k);
         bad = kk < bad ? kk : bad;
+      }
+    };
+    if constexpr (WT > 0) {
+#pragma unroll
+      for (int k = 0; k < WT; ++k) {
+        Pack<T> x, m1v, m2v;
+        if (k < BCH) {
+          x = xs[k];
+          m1v = s1[k];
+          m2v = s2[k];
+        } else {
+          const long r = static_cast<long>(k) * a.ld + off;
+          x = ldv(a.w + r);
+          if constexpr (OPT != kSgd) m1v = ldv(a.m1 + r);
+          if constexpr (OPT == kAdam || OPT == kAdamW) m2v = ldv(a.m2 + r);
+        }
+        step_store(k, x, m1v, m2v);
+      }
+    } else {
+      // any W: workers in batches of 4 whose loads are all in flight before
+      // the batch's first store
+      int k = 0;
+      for (; k + 4 <= nw; k += 4) {
+        Pack<T> x[4], m1v[4], m2v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const long r = static_cast<long>(k + q) * a.ld + off;
+          x[q] = ldv(a.w + r);
+          if constexpr (OPT != kSgd) m1v[q] = ldv(a.m1 + r);
+          if constexpr (OPT == kAdam || OPT == kAdamW) m2v[q] = ldv(a.m2 + r);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) step_store(k + q, x[q], m1v[q], m2v[q]);
+      }
+      for (; k < nw; ++k) {
+        const long r = static_cast<long>(k) * a.ld + off;
+        Pack<T> x, m1v, m2v;
+        x = ldv(a.w + r);
+        if constexpr (OPT != kSgd) m1v = ldv(a.m1 + r);
+        if constexpr (OPT == kAdam || OPT == kAdamW) m2v = ldv(a.m2 + r);
+        step_store(k, x, m1v, m2v);
       }
     }
   }

@@ -6,9 +6,10 @@
 set -euo pipefail
 CFG=${1:-c2}
 KRE=${2:-ds_group_kernel}
+DOVR=${3:+--d $3}
 OUT=gpurun_out
 mkdir -p $OUT
-CMD="python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3"
+CMD="python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 $DOVR"
 
 # 1) launch list: every kernel with its device time (cold-cache, serialised)
 $CMD > $OUT/plain_$CFG.log 2>&1
@@ -18,5 +19,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 # 2) full section set on the dominant kernel, source-correlated (-lineinfo)
 $CMD > $OUT/plain2_$CFG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:$KRE -s 4 -c 2 \
-    -o $OUT/prof_${CFG} -f $CMD > $OUT/ncu_full_$CFG.log 2>&1
+    -o $OUT/prof_${CFG}_${KRE} -f $CMD > $OUT/ncu_full_${CFG}_${KRE}.log 2>&1
 echo done
