@@ -296,6 +296,7 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
       e.hi = sl.hi;
       e.err_rank = mem[0];
       e.err_phase = s.kind == DSS_BSP ? 0 : 1;
+      if (m > kMaxFold) throw std::invalid_argument("group spans more members than the fold kernel holds (64)");
       for (int j = 0; j < m; ++j) {
         void* p = row_ptr(c, wb, mem[j]);
         src.push_back(p);
@@ -337,6 +338,7 @@ ParityPlan build_bsp_multi_plan(dss_ctx* c) {
     e.hi = sl.hi;
     e.err_rank = 0;
     e.err_phase = 0;
+    if (W > kMaxFold) throw std::invalid_argument("multi-GPU BSP supports at most 64 workers");
     for (int k = 0; k < W; ++k) src.push_back(row_ptr(c, c->peer_g, k));
     for (int q = 0; q < G; ++q) dst.push_back(c->peer_mg[static_cast<size_t>(q)]);
     pp.fold.entries = 1;

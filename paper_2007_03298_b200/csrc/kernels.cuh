@@ -495,23 +495,58 @@ template <typename T> struct FoldArgs {
   unsigned long long* err;
 };
 
+constexpr int kMaxFold = 64;  // members (sources) / destinations per entry held in shared memory
+
 template <typename T, int M>
 __global__ void __launch_bounds__(kThreads) fold_kernel(const FoldArgs<T> a) {
   constexpr int VN = Vec<T>::n;
-  const FoldEntry en = a.entries[blockIdx.y];
+  // Entry and its peer-pointer lists are read once into shared memory: the
+  // element loop then has no dependent pointer loads in front of its NVLink
+  // accesses (the stores could alias the tables, so the compiler would
+  // otherwise reload them every iteration).
+  __shared__ FoldEntry en;
+  __shared__ T* s_src[kMaxFold];
+  __shared__ T* s_dst[kMaxFold];
+  if (threadIdx.x == 0) en = a.entries[blockIdx.y];
+  __syncthreads();
+  for (int q = threadIdx.x; q < en.src_cnt; q += blockDim.x) s_src[q] = a.src[en.src_beg + q];
+  for (int q = threadIdx.x; q < en.dst_cnt; q += blockDim.x) s_dst[q] = a.dst[en.dst_beg + q];
+  __syncthreads();
   const int m = M > 0 ? M : en.src_cnt;
+  const int nd = en.dst_cnt;
   const T inv = static_cast<T>(1.0 / static_cast<double>(m));
+  constexpr int RM = M > 0 ? M : 1;
+  T* src[RM];
+  if constexpr (M > 0) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) src[j] = s_src[j];
+  }
   unsigned long long bad = ~0ull;
   const long v0 = en.lo / VN, v1 = en.hi / VN;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long e = v0 + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < v1; e += stride) {
     const long off = e * VN;
-    Pack<T> acc = ldv_cg(a.src[en.src_beg] + off);
-#pragma unroll(M > 0 ? M - 1 : 4)
-    for (int j = 1; j < m; ++j) {
-      const Pack<T> x = ldv_cg(a.src[en.src_beg + j] + off);
+    Pack<T> acc;
+    if constexpr (M > 0) {
+      // all member loads (local and NVLink peer) in flight, then the
+      // ordered fold
+      Pack<T> x[M];
 #pragma unroll
-      for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+      for (int j = 0; j < M; ++j) x[j] = ldv_cg(src[j] + off);
+      acc = x[0];
+#pragma unroll
+      for (int j = 1; j < M; ++j) {
+#pragma unroll
+        for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x[j].v[l]);
+      }
+    } else {
+      acc = ldv_cg(s_src[0] + off);
+#pragma unroll 4
+      for (int j = 1; j < m; ++j) {
+        const Pack<T> x = ldv_cg(s_src[j] + off);
+#pragma unroll
+        for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+      }
     }
     bool ok = true;
 #pragma unroll
@@ -523,9 +558,7 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const FoldArgs<T> a) {
       const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
       bad = k < bad ? k : bad;
     }
-    for (int q = 0; q < en.dst_cnt; ++q) {
-      stv_cg(a.dst[en.dst_beg + q] + off, acc);
-    }
+    for (int q = 0; q < nd; ++q) stv_cg(s_dst[q] + off, acc);
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
   // Peer stores must be performed system-wide before the next cross-GPU

@@ -46,6 +46,49 @@ __global__ void multi_kernel(Multi m) {
   }
 }
 
+// Two-shot fold shapes: GPU g owns slice g of n rows (one per GPU); it
+// folds the slice over all rows (n-1 remote) and stores the result to all.
+struct Fold {
+  const float4* src[8];
+  float4* dst[8];
+  int k;
+  long lo, hi;  // vector range of the owned slice
+};
+template <int U>
+__global__ void fold_kernel(Fold f) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x * U;
+  for (long i = f.lo + (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) * U; i < f.hi; i += stride) {
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = __ldcg(f.src[0] + i + u);
+    for (int q = 1; q < f.k; ++q) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 x = __ldcg(f.src[q] + i + u);
+        acc[u].x += x.x; acc[u].y += x.y; acc[u].z += x.z; acc[u].w += x.w;
+      }
+    }
+    for (int q = 0; q < f.k; ++q) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcg(f.dst[q] + i + u, acc[u]);
+    }
+  }
+}
+// fold with all loads issued before any add (k <= 8 fixed at 4 here)
+__global__ void fold4_kernel(Fold f) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = f.lo + static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < f.hi; i += stride) {
+    float4 x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = __ldcg(f.src[q] + i);
+    float4 acc = x[0];
+#pragma unroll
+    for (int q = 1; q < 4; ++q) { acc.x += x[q].x; acc.y += x[q].y; acc.z += x[q].z; acc.w += x[q].w; }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) __stcg(f.dst[q] + i, acc);
+  }
+}
+
 int main(int argc, char** argv) {
   int n = 0;
   CK(cudaGetDeviceCount(&n));
@@ -70,7 +113,7 @@ int main(int argc, char** argv) {
     CK(cudaMemset(b[g], 0, bytes));
     CK(cudaStreamCreate(&st[g]));
   }
-  const char* modes[] = {"local", "read", "write", "mixed", "readall", "writeall"};
+  const char* modes[] = {"local", "read", "write", "mixed", "readall", "writeall", "fold1", "fold2", "fold4", "foldall4"};
   for (const char* mode : modes) {
     for (int blocks_per_sm : {4, 8, 16}) {
       std::vector<cudaEvent_t> e0(n), e1(n);
@@ -103,6 +146,19 @@ int main(int argc, char** argv) {
             m.src[1] = a[g];
             m.dst[1] = c[peer];
             multi_kernel<<<grid, 256, 0, st[g]>>>(m);
+          } else if (!std::strncmp(mode, "fold", 4)) {
+            Fold f{};
+            f.k = n;
+            for (int p = 0; p < n; ++p) {
+              f.src[p] = a[p];
+              f.dst[p] = b[p];
+            }
+            f.lo = nv / n * g;
+            f.hi = f.lo + nv / n;
+            if (!std::strcmp(mode, "fold1")) fold_kernel<1><<<grid, 256, 0, st[g]>>>(f);
+            else if (!std::strcmp(mode, "fold2")) fold_kernel<2><<<grid, 256, 0, st[g]>>>(f);
+            else if (!std::strcmp(mode, "fold4")) fold_kernel<4><<<grid, 256, 0, st[g]>>>(f);
+            else if (n == 4) fold4_kernel<<<grid, 256, 0, st[g]>>>(f);
           } else {
             Multi m{};
             m.k = 0;
@@ -138,6 +194,7 @@ int main(int argc, char** argv) {
       // launch in every non-local mode (mixed: half reads, half writes each
       // way).  local reports the HBM copy (read + write).
       double gbs = bytes / (worst / 1e3) / 1e9;
+      if (!std::strncmp(mode, "fold", 4)) gbs = gbs * (n - 1) / n;  // remote bytes each way per GPU
       std::printf("%-9s blocks/SM=%2d  %8.3f ms  %7.1f GB/s%s\n", mode, blocks_per_sm, worst,
                   !std::strcmp(mode, "local") ? 2 * gbs : gbs,
                   !std::strcmp(mode, "local") ? " (HBM r+w)" : " per direction, both directions loaded");
