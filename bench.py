@@ -415,14 +415,28 @@ def our_arm(args, cfg):
             # e2e through the C-ABI with host buffers: pinned H2D of every
             # local worker's gradient, the step, D2H of every worker's params.
             K2 = max(3, min(args.steps, args.e2e_steps))
-            hg = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
-            hw = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
-            e.download_all(BUF_GRADS, hg)
+            if P * d * 4 <= 2e9:
+                hg = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
+                hw = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
+                e.download_all(BUF_GRADS, hg)
 
-            def e2e(t):
-                e.upload_all(BUF_GRADS, hg)
-                e.step(t, cfg["alpha"])
-                e.download_all(BUF_PARAMS, hw)
+                def e2e(t):
+                    e.upload_all(BUF_GRADS, hg)
+                    e.step(t, cfg["alpha"])
+                    e.download_all(BUF_PARAMS, hw)
+            else:
+                # large rows: stream every worker row through one pinned
+                # staging row (same bytes per step, bounded host memory)
+                hrow = np.empty(d, dtype=np.float32)
+                hrow_t = torch.from_numpy(hrow).pin_memory()
+                first = rank * P
+
+                def e2e(t):
+                    for k in range(first, first + P):
+                        e._ck(e.lib.dss_upload(e.h, BUF_GRADS, k, hrow_t.data_ptr(), d))
+                    e.step(t, cfg["alpha"])
+                    for k in range(first, first + P):
+                        e._ck(e.lib.dss_download(e.h, BUF_PARAMS, k, hrow_t.data_ptr(), d))
             res["e2e_ms"] = timed(e2e, args.warmup + 2 * args.steps, K2)
             e.check()
         if G > 1 and not args.no_nccl:

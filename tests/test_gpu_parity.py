@@ -102,7 +102,8 @@ def test_sync_round_golden(cuda_device, golden):
 
 
 CASES = [("ds", 4, 2, False), ("ds", 9, 3, False), ("ds", 16, 4, False), ("ds", 8, 2, True), ("ds", 32, 4, True),
-         ("ds", 64, 8, False), ("ds", 6, 6, False), ("bsp", 8, 8, False), ("bsp", 3, 3, False)]
+         ("ds", 64, 8, False), ("ds", 6, 6, False), ("ds", 25, 5, False), ("ds", 35, 5, True), ("ds", 12, 12, False),
+         ("bsp", 8, 8, False), ("bsp", 3, 3, False), ("bsp", 32, 32, False), ("bsp", 13, 13, False)]
 
 
 @pytest.mark.parametrize("kind,W,N,rect", CASES)
@@ -275,6 +276,27 @@ def test_c2_full_size_rows_vs_oracle(cuda_device, oracle):
         e.sync_round(2)
         after = torch.stack([_torch_view(e, BUF_PARAMS, k, d).double() for k in range(W)]).mean(0)
         assert torch.max(torch.abs(after - before)).item() < 1e-6
+
+
+def test_batched_steps_equal_single_steps(cuda_device):
+    """dss_steps(t0, alphas) == the same iterations one dss_step at a time."""
+    rng = np.random.default_rng(9)
+    W, N, d = 16, 4, 3001
+    w = rng.standard_normal((W, d)).astype(np.float32)
+    g = rng.standard_normal((W, d)).astype(np.float32)
+    alphas = np.linspace(0.01, 0.05, 7)
+    outs = []
+    for batched in (False, True):
+        with engine_for("ds", W, N, 3, d, 0.01, "f32") as e:
+            e.upload_all(BUF_PARAMS, w)
+            e.upload_all(BUF_GRADS, g)
+            if batched:
+                e.steps(0, alphas, check=True)
+            else:
+                for t, a_t in enumerate(alphas):
+                    e.step(t, float(a_t))
+            outs.append((e.download_all(BUF_PARAMS), e.step_count(5)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1] == len(alphas)
 
 
 def test_timing_and_launch_accounting(cuda_device):
