@@ -97,10 +97,13 @@ typedef struct {
   int rank;             /* this GPU's index among n_gpus (process rank) */
   int n_gpus;           /* G; world_size must be a multiple of G.  Workers are packed
                            contiguously: gpu(k) = k / (W/G) */
-  int path;             /* 0 = auto.  1 = route every multi-member group through the
-                           cross-GPU two-shot path (step in place, then ordered slice
-                           fold) even on one GPU: exercises the multi-GPU kernels on a
-                           single device for parity tests.  Results are bit-identical. */
+  int path;             /* 0 = auto (two-shot for groups with one member per GPU, ordered
+                           chain fold when some GPU holds several members).
+                           1 = (one GPU) route every multi-member group through the
+                           two-shot kernels with virtual owners: exercises the multi-GPU
+                           fold on a single device for parity tests.
+                           2 = (several GPUs) every spanning group uses the chain fold.
+                           Results are bit-identical on every path. */
 } dss_config;
 
 typedef struct dss_ctx dss_ctx;
@@ -139,8 +142,9 @@ int dss_round_outcome(const dss_strategy* s, long t, long payload_dim, dss_outco
 typedef struct {
   int local_groups;      /* groups whose members all live on this GPU */
   int spanning_groups;   /* groups with members on this GPU and on others */
-  int owned_slices;      /* spanning groups in which this GPU owns a non-empty slice */
+  int owned_slices;      /* two-shot groups in which this GPU owns a non-empty slice */
   long owned_elems;      /* sum of owned slice lengths */
+  int chain_groups;      /* spanning groups folded by the ordered chain (several members on a GPU) */
 } dss_plan_summary;
 int dss_plan(const dss_strategy* s, long t, long dim, int n_gpus, int rank,
              dss_plan_summary* out, long* slice_lo, long* slice_hi, int* slice_group, int max_slices);
@@ -245,16 +249,17 @@ enum {
   DSS_KIND_BSP = 2,      /* bsp_kernel: fused gradient fold + step */
   DSS_KIND_BARRIER = 3,  /* barrier_kernel: cross-GPU flag barrier */
   DSS_KIND_GRADIENT = 4, /* quad_grad_kernel: synthetic gradients */
-  DSS_KIND_COUNT = 5
+  DSS_KIND_CHAIN = 5,    /* chain_partial/mean_kernel: ordered chain fold over NVLink */
+  DSS_KIND_COUNT = 6
 };
 int dss_kernel_times_by_kind(dss_ctx* ctx, double* total_ms, long* launches);
 /* gpu_launches: hot-path kernels launched since creation (all kinds). */
 long dss_launch_count(const dss_ctx* ctx);
 
 /* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
-/* CUDA IPC handles of this GPU's params, grads and flag buffers:
- * DSS_IPC_BYTES bytes written to out. */
-#define DSS_IPC_BYTES 256
+/* CUDA IPC handles of this GPU's params, grads, mean-gradient, barrier-flag,
+ * chain-row and chain-flag buffers: DSS_IPC_BYTES bytes written to out. */
+#define DSS_IPC_BYTES 384
 int dss_ipc_export(dss_ctx* ctx, void* out);
 /* Map every GPU's exported handles (n_gpus * DSS_IPC_BYTES bytes, rank
  * order, own entry ignored).  Must be called on every rank before the first

@@ -18,8 +18,8 @@ LIB_PATH = os.environ.get("DSS_LIB_VARIANT", LIB_PATH)
 DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2 = range(4)
-IPC_BYTES = 256
-KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient"]
+IPC_BYTES = 384
+KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain"]
 
 
 class dss_hparams(C.Structure):
@@ -44,7 +44,7 @@ class dss_config(C.Structure):
 
 class dss_plan_summary(C.Structure):
     _fields_ = [("local_groups", C.c_int), ("spanning_groups", C.c_int),
-                ("owned_slices", C.c_int), ("owned_elems", C.c_long)]
+                ("owned_slices", C.c_int), ("owned_elems", C.c_long), ("chain_groups", C.c_int)]
 
 
 # Every symbol declared in include/dssync_b200.h, with its signature.

@@ -83,12 +83,23 @@ struct FoldLaunch {
   void** d_dst = nullptr;
 };
 
+struct ChainLaunch {
+  int na = 0, nb = 0;              // kernel A / kernel B entries on this GPU
+  ChainEntry* d_a = nullptr;
+  ChainEntry* d_b = nullptr;
+  void** d_src = nullptr;          // member rows
+  void** d_dst = nullptr;          // mean destinations
+};
+
 struct ParityPlan {
   bool built = false;
   bool any_spanning = false;  // identical on every GPU
+  bool any_twoshot = false;   // identical on every GPU
+  bool any_chain = false;     // identical on every GPU
   std::vector<GroupLaunch> local;      // fused step+fold launches
   GroupLaunch spanning_step;           // singleton in-place steps of spanning members
   FoldLaunch fold;                     // owned two-shot slices
+  ChainLaunch chain;                   // ordered chain-fold groups
 };
 
 }  // namespace
@@ -114,6 +125,16 @@ struct dss_ctx {
   unsigned long long* flags = nullptr;  // [G] barrier words, written by peers
   unsigned long long** d_peer_flags = nullptr;
   unsigned long long* h_err = nullptr;  // pinned readback
+
+  // chain fold: receive rows [2 (partial, mean)][slots][d_pad] and their
+  // per-chunk epoch flags [2][slots][n_chunks], both peer-mapped
+  void* chain_buf = nullptr;
+  unsigned long long* chain_flags = nullptr;
+  int chain_slots = 0;
+  long chain_chunk = 0, chain_nchunks = 0;
+  unsigned long long chain_epoch = 0;
+  std::vector<void*> peer_chain_buf;
+  std::vector<unsigned long long*> peer_chain_flags;
 
   std::vector<long> step_count;
   std::vector<void*> peer_w, peer_g, peer_mg;
@@ -235,6 +256,81 @@ void* row_ptr(dss_ctx* c, const std::vector<void*>& bases, int rank) {
          static_cast<size_t>(lr) * c->d_pad * c->esz;
 }
 
+// Row of a rank hosted on THIS GPU inside a local buffer.
+void* row_ptr(dss_ctx* c, const std::vector<void*>&, int rank, void* local_base) {
+  return static_cast<char*>(local_base) + static_cast<size_t>(rank - c->first) * c->d_pad * c->esz;
+}
+
+bool force_chain(const dss_ctx* c) { return c->cfg.path == 2 && multi(c); }
+
+void* chain_row(dss_ctx* c, void* base, int region, int slot) {
+  return static_cast<char*>(base) +
+         (static_cast<size_t>(region) * c->chain_slots + slot) * c->d_pad * c->esz;
+}
+unsigned long long* chain_flag(dss_ctx* c, unsigned long long* base, int region, int slot) {
+  return base + (static_cast<size_t>(region) * c->chain_slots + slot) * c->chain_nchunks;
+}
+
+// Chain-fold launch tables for this GPU's roles.  members of role i are
+// rows of `member_base` (local); its mean lands in dsts[i] (local rows).
+ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* member_base,
+                        const std::vector<std::vector<void*>>& dsts, int err_phase) {
+  ChainLaunch cl;
+  std::vector<ChainEntry> ea, eb;
+  std::vector<void*> src, dst;
+  for (size_t i = 0; i < roles.size(); ++i) {
+    const ChainRole& r = roles[i];
+    if (r.slot >= c->chain_slots || r.next_slot >= c->chain_slots || r.mean_next_slot >= c->chain_slots) {
+      throw std::logic_error("chain slot out of range");
+    }
+    ChainEntry a{};
+    a.stage = r.stage;
+    a.last = r.stage == r.S - 1;
+    a.run_beg = static_cast<int>(src.size());
+    a.run_cnt = static_cast<int>(r.run.size());
+    for (int k : r.run) {
+      src.push_back(static_cast<char*>(member_base) + static_cast<size_t>(k - c->first) * c->d_pad * c->esz);
+    }
+    a.dst_beg = static_cast<int>(dst.size());
+    a.dst_cnt = static_cast<int>(dsts[i].size());
+    dst.insert(dst.end(), dsts[i].begin(), dsts[i].end());
+    a.recv = chain_row(c, c->chain_buf, 0, r.slot);
+    a.recv_flags = chain_flag(c, c->chain_flags, 0, r.slot);
+    if (!a.last) {
+      a.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.next_gpu)], 0, r.next_slot);
+      a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.next_gpu)], 0, r.next_slot);
+    } else {
+      a.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+      a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+    }
+    a.err_rank = r.first_member;
+    a.err_phase = err_phase;
+    a.m = r.m;
+    ea.push_back(a);
+    if (r.stage <= r.S - 2) {
+      ChainEntry b = a;
+      b.last = 0;
+      b.recv = chain_row(c, c->chain_buf, 1, r.slot);
+      b.recv_flags = chain_flag(c, c->chain_flags, 1, r.slot);
+      if (r.stage < r.S - 2) {
+        b.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+        b.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+      } else {
+        b.send = nullptr;
+        b.send_flags = nullptr;
+      }
+      eb.push_back(b);
+    }
+  }
+  cl.na = static_cast<int>(ea.size());
+  cl.nb = static_cast<int>(eb.size());
+  cl.d_a = upload_table(c, ea);
+  cl.d_b = upload_table(c, eb);
+  cl.d_src = upload_table(c, src);
+  cl.d_dst = upload_table(c, dst);
+  return cl;
+}
+
 // Build the launch tables of one parity.  with_step: DS iteration (local
 // steps fused); otherwise sync_round (fold only).
 ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
@@ -265,14 +361,26 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
       }
     }
   } else {
-    const GpuPlan gp = make_plan(part, s.world_size, G, multi(c) ? c->cfg.rank : 0, c->d_pad);
+    const GpuPlan gp = make_plan(part, s.world_size, G, multi(c) ? c->cfg.rank : 0, c->d_pad, force_chain(c));
     pp.any_spanning = gp.any_spanning_globally;
+    pp.any_twoshot = gp.any_twoshot_globally;
+    pp.any_chain = gp.any_chain_globally;
     for (int gi : gp.local_groups) {
       local.emplace_back(part.group(gi), part.group(gi) + part.size(gi));
     }
     for (int r : gp.spanning_local_members) span_members.push_back({r});
     owned = gp.owned;
+    if (!gp.chain.empty()) {
+      std::vector<std::vector<void*>> dsts;
+      for (const ChainRole& r : gp.chain) {
+        std::vector<void*> d;
+        for (int k : r.run) d.push_back(row_ptr(c, std::vector<void*>(static_cast<size_t>(G), nullptr), k, c->w));
+        dsts.push_back(d);
+      }
+      pp.chain = build_chain(c, gp.chain, c->w, dsts, s.kind == DSS_BSP ? 0 : 1);
+    }
   }
+  if (force_fold(c)) pp.any_twoshot = pp.any_spanning;
 
   pp.local = make_bucketed(c, local);
   if (with_step) pp.spanning_step = make_group_launch(c, span_members);
@@ -321,13 +429,21 @@ ParityPlan build_bsp_multi_plan(dss_ctx* c) {
   ParityPlan pp;
   const int G = c->cfg.n_gpus;
   const int W = c->cfg.strategy.world_size;
+  const Partition part = make_partition(c->cfg.strategy, 0);  // one all-world group
+  const GpuPlan gp = make_plan(part, W, G, c->cfg.rank, c->d_pad, force_chain(c));
   pp.any_spanning = true;
+  pp.any_twoshot = gp.any_twoshot_globally;
+  pp.any_chain = gp.any_chain_globally;
   std::vector<std::vector<int>> singles;
   for (int k = 0; k < c->P; ++k) singles.push_back({c->first + k});
   pp.spanning_step = make_group_launch(c, singles);
-  Slice sl;
-  slice_range(c->d_pad, G, c->cfg.rank, &sl.lo, &sl.hi);
-  if (sl.hi > sl.lo) {
+  if (!gp.chain.empty()) {
+    // packed BSP: ordered chain over the gradient rows, mean into this GPU's
+    // mean-gradient row (every replica then steps with it)
+    pp.chain = build_chain(c, gp.chain, c->g, {std::vector<void*>{c->mg}}, 0);
+  }
+  if (!gp.owned.empty()) {
+    const Slice sl = gp.owned[0];
     FoldEntry e{};
     std::vector<void*> src, dst;
     e.src_beg = 0;
@@ -514,6 +630,45 @@ void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
     launch_fold<double>(c, fl, t);
   } else {
     launch_fold<float>(c, fl, t);
+  }
+}
+
+template <typename T>
+void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t) {
+  ++c->chain_epoch;  // same sequence on every GPU: flags compare against it
+  ChainArgs<T> a{};
+  a.src = reinterpret_cast<T* const*>(cl.d_src);
+  a.dst = reinterpret_cast<T* const*>(cl.d_dst);
+  a.chunk = c->chain_chunk;
+  a.len = c->d_pad;
+  a.n_chunks = c->chain_nchunks;
+  a.epoch = c->chain_epoch;
+  a.t = t;
+  a.err = c->d_err;
+  a.timeout = c->d_timeout;
+  if (cl.na > 0) {
+    a.entries = cl.d_a;
+    a.n_entries = cl.na;
+    const long units = c->chain_nchunks * cl.na;
+    TimedLaunch tl(c, DSS_KIND_CHAIN);
+    chain_partial_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * 4L)), kThreads, 0, c->stream>>>(a);
+    ck(cudaGetLastError(), "chain_partial_kernel launch");
+  }
+  if (cl.nb > 0) {
+    a.entries = cl.d_b;
+    a.n_entries = cl.nb;
+    const long units = c->chain_nchunks * cl.nb;
+    TimedLaunch tl(c, DSS_KIND_CHAIN);
+    chain_mean_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * 4L)), kThreads, 0, c->stream>>>(a);
+    ck(cudaGetLastError(), "chain_mean_kernel launch");
+  }
+}
+
+void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t) {
+  if (c->cfg.dtype == DSS_F64) {
+    launch_chain<double>(c, cl, t);
+  } else {
+    launch_chain<float>(c, cl, t);
   }
 }
 
@@ -707,6 +862,7 @@ extern "C" int dss_plan(const dss_strategy* s, long t, long dim, int n_gpus, int
     out->local_groups = static_cast<int>(gp.local_groups.size());
     out->spanning_groups = static_cast<int>(gp.spanning_groups.size());
     out->owned_slices = static_cast<int>(gp.owned.size());
+    out->chain_groups = static_cast<int>(gp.chain.size());
     out->owned_elems = 0;
     for (size_t i = 0; i < gp.owned.size(); ++i) {
       out->owned_elems += gp.owned[i].hi - gp.owned[i].lo;
@@ -781,7 +937,24 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     std::vector<std::vector<int>> singles;
     for (int k = 0; k < c->P; ++k) singles.push_back({c->first + k});
     c->apply_launch = make_group_launch(c.get(), singles);
-    if (!multi(c.get())) build_plans(c.get());
+    if (multi(c.get())) {
+      // chain-fold receive rows and flags, sized for the worst parity (the
+      // plan is global, so every GPU computes the same slot count)
+      int slots = 0;
+      for (long t = 0; t < (s.kind == DSS_DS_SYNC ? 2 : 1); ++t) {
+        const GpuPlan gp = make_plan(make_partition(s, t), s.world_size, cfg->n_gpus, cfg->rank, c->d_pad,
+                                     force_chain(c.get()));
+        slots = std::max(slots, gp.max_chain_slots);
+      }
+      c->chain_slots = slots;
+      c->chain_chunk = std::min<long>(c->d_pad, std::max<long>(2048, std::min<long>(65536, pad_dim(c->d_pad / 64))));
+      c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
+      c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
+      c->chain_flags = static_cast<unsigned long long*>(dalloc(
+          c.get(), std::max<size_t>(64, sizeof(unsigned long long) * 2 * slots * c->chain_nchunks)));
+    } else {
+      build_plans(c.get());
+    }
     ck(cudaStreamSynchronize(c->stream), "create sync");
     return DSS_OK;
   });
@@ -953,11 +1126,16 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
       // Local groups: fused apply_step + ordered fold + broadcast.
       for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
       if (pp.any_spanning) {
-        // Members of spanning groups step in place, then (after every GPU
-        // has stepped) each owner folds its slice over NVLink.
+        // Members of spanning groups step in place.  Two-shot groups: after
+        // every GPU has stepped, each owner folds its slice over NVLink.
+        // Chain groups: the ordered partial/mean passes (flag-synchronised
+        // per chunk, no barrier).
         launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->g, c->d_pad, 0);
-        if (multi(c)) barrier(c);
-        launch_fold_any(c, pp.fold, t);
+        if (pp.any_twoshot) {
+          if (multi(c)) barrier(c);
+          launch_fold_any(c, pp.fold, t);
+        }
+        if (pp.any_chain) launch_chain_any(c, pp.chain, t);
         c->pending_remote = multi(c);
       }
     } else if (!multi(c)) {
@@ -970,11 +1148,16 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
       // BSP over GPUs: barrier (gradients final everywhere), ordered fold of
       // all W gradients into every GPU's mean-gradient row, barrier, local
       // apply_step of every replica with the shared mean gradient.
+      // Packed GPUs (P >= 2) use the ordered chain over the gradient rows
+      // instead: every GPU forwards one partial row, not P rows.
       const ParityPlan& pp = c->step_plan[0];
       c->pending_remote = false;
       barrier(c);
-      launch_fold_any(c, pp.fold, t);
-      barrier(c);
+      if (pp.any_twoshot) {
+        launch_fold_any(c, pp.fold, t);
+        barrier(c);
+      }
+      if (pp.any_chain) launch_chain_any(c, pp.chain, t);
       launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->mg, 0, 1);
     }
     bump_steps(c);
@@ -1007,8 +1190,11 @@ extern "C" int dss_sync_round(dss_ctx* c, long t, int check, dss_outcome* out) {
     const int phase = s.kind == DSS_BSP ? 0 : 1;  // collective failure: members[0] (sync.cpp:233-235)
     for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, kOptNone, t, 0.0, nullptr, 0, 0, phase);
     if (pp.any_spanning) {
-      if (multi(c)) barrier(c);
-      launch_fold_any(c, pp.fold, t);
+      if (pp.any_twoshot) {
+        if (multi(c)) barrier(c);
+        launch_fold_any(c, pp.fold, t);
+      }
+      if (pp.any_chain) launch_chain_any(c, pp.chain, t);
       c->pending_remote = multi(c);
     }
     if (out) *out = round_outcome(s, t, c->d);
@@ -1224,11 +1410,14 @@ extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
-    cudaIpcMemHandle_t h[4];
+    if (!multi(c)) throw std::invalid_argument("dss_ipc_export needs n_gpus > 1");
+    cudaIpcMemHandle_t h[6];
     ck(cudaIpcGetMemHandle(&h[0], c->w), "cudaIpcGetMemHandle(params)");
     ck(cudaIpcGetMemHandle(&h[1], c->g), "cudaIpcGetMemHandle(grads)");
     ck(cudaIpcGetMemHandle(&h[2], c->mg), "cudaIpcGetMemHandle(mean grad)");
     ck(cudaIpcGetMemHandle(&h[3], c->flags), "cudaIpcGetMemHandle(flags)");
+    ck(cudaIpcGetMemHandle(&h[4], c->chain_buf), "cudaIpcGetMemHandle(chain rows)");
+    ck(cudaIpcGetMemHandle(&h[5], c->chain_flags), "cudaIpcGetMemHandle(chain flags)");
     std::memcpy(out, h, sizeof(h));
     return DSS_OK;
   });
@@ -1245,6 +1434,8 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
     c->peer_g.assign(static_cast<size_t>(G), nullptr);
     c->peer_mg.assign(static_cast<size_t>(G), nullptr);
     c->peer_flag.assign(static_cast<size_t>(G), nullptr);
+    c->peer_chain_buf.assign(static_cast<size_t>(G), nullptr);
+    c->peer_chain_flags.assign(static_cast<size_t>(G), nullptr);
     const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
     for (int r = 0; r < G; ++r) {
       if (r == c->cfg.rank) {
@@ -1252,11 +1443,13 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
         c->peer_g[static_cast<size_t>(r)] = c->g;
         c->peer_mg[static_cast<size_t>(r)] = c->mg;
         c->peer_flag[static_cast<size_t>(r)] = c->flags;
+        c->peer_chain_buf[static_cast<size_t>(r)] = c->chain_buf;
+        c->peer_chain_flags[static_cast<size_t>(r)] = c->chain_flags;
         continue;
       }
-      void* p[4];
-      for (int b = 0; b < 4; ++b) {
-        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 4 + b], cudaIpcMemLazyEnablePeerAccess);
+      void* p[6];
+      for (int b = 0; b < 6; ++b) {
+        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 6 + b], cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
           throw PeerError("cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
         }
@@ -1266,6 +1459,8 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
       c->peer_g[static_cast<size_t>(r)] = p[1];
       c->peer_mg[static_cast<size_t>(r)] = p[2];
       c->peer_flag[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[3]);
+      c->peer_chain_buf[static_cast<size_t>(r)] = p[4];
+      c->peer_chain_flags[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[5]);
     }
     c->d_peer_flags = upload_table(c, c->peer_flag);
     build_plans(c);

@@ -598,6 +598,161 @@ __global__ void barrier_kernel(unsigned long long* const* peer_flags, unsigned l
   __threadfence_system();
 }
 
+// ---- ordered chain fold across GPUs (comm.cpp:96-110) -------
+// A group spanning GPUs g_0 < ... < g_{S-1}, each holding a contiguous run
+// of its ascending members, is folded as the reference's ring does: the
+// partial leaves g_0 after its run, every next GPU *continues* the same
+// left-to-right fold with its own run (acc = (...(p + x_a) + x_{a+1}) ...),
+// the last GPU scales by 1/m.  The mean then travels g_{S-1} -> g_0 -> g_1
+// -> ... -> g_{S-2}.  Both passes are pipelined over chunks of the row with
+// per-chunk epoch flags in the receiver's memory (st.release.sys /
+// ld.acquire.sys), so each GPU moves ~2 rows over NVLink per group instead
+// of one per member, and the fold order is bit-exact.
+struct ChainEntry {
+  int stage;          // position j of this GPU in the group's GPU list
+  int last;           // j == S-1
+  int run_beg, run_cnt;   // this GPU's members: rows in the src pointer table
+  int dst_beg, dst_cnt;   // where the mean lands on this GPU
+  void* recv;         // local partial-receive row (j > 0) / mean-receive row (kernel B)
+  unsigned long long* recv_flags;  // local flags [n_chunks]
+  void* send;         // next GPU's receive row (remote), or nullptr
+  unsigned long long* send_flags;  // next GPU's flags (remote), or nullptr
+  int err_rank;
+  int err_phase;
+  int m;              // group size (1/m)
+};
+
+template <typename T> struct ChainArgs {
+  T* const* src;      // member rows (local)
+  T* const* dst;      // mean destinations (local)
+  const ChainEntry* entries;
+  int n_entries;
+  long chunk;         // elements per chunk (multiple of 64)
+  long len;           // row length (d_pad)
+  long n_chunks;
+  unsigned long long epoch;
+  long t;
+  unsigned long long* err;
+  unsigned long long* timeout;
+};
+
+__device__ __forceinline__ bool chain_wait(const unsigned long long* flag, unsigned long long epoch,
+                                           unsigned long long* timeout) {
+  unsigned long long start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  while (ld_acquire_sys(flag) < epoch) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start > 20000000000ull) {
+      atomicExch(timeout, 1ull);
+      return false;
+    }
+  }
+  return true;
+}
+
+// Kernel A: the ordered partial pass.  Work unit = (chunk, entry), visited
+// chunk-major so every chain advances together.  A CTA only ever waits on a
+// flag written by the previous GPU's kernel A, which itself only waits on
+// GPUs before it: no cycle, no same-GPU dependency.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  __shared__ ChainEntry en;
+  __shared__ int ok_flag;
+  const long units = a.n_chunks * a.n_entries;
+  unsigned long long bad = ~0ull;
+  for (long u = blockIdx.x; u < units; u += gridDim.x) {
+    const long c = u / a.n_entries;
+    const int ei = static_cast<int>(u % a.n_entries);
+    if (threadIdx.x == 0) {
+      en = a.entries[ei];
+      ok_flag = 1;
+      if (en.stage > 0) ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
+    }
+    __syncthreads();
+    const long lo = c * a.chunk;
+    const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
+    const T inv = static_cast<T>(1.0 / static_cast<double>(en.m));
+    if (ok_flag) {
+      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+        const long off = e * VN;
+        Pack<T> acc;
+        int j0 = 0;
+        if (en.stage == 0) {
+          acc = ldv(a.src[en.run_beg] + off);
+          j0 = 1;
+        } else {
+          acc = ldv_cg(static_cast<const T*>(en.recv) + off);
+        }
+        for (int j = j0; j < en.run_cnt; ++j) {
+          const Pack<T> x = ldv(a.src[en.run_beg + j] + off);
+#pragma unroll
+          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+        }
+        if (!en.last) {
+          stv_cg(static_cast<T*>(en.send) + off, acc);
+        } else {
+          bool ok = true;
+#pragma unroll
+          for (int l = 0; l < VN; ++l) {
+            acc.v[l] = mul_(acc.v[l], inv);
+            ok = ok && finite_(acc.v[l]);
+          }
+          if (!ok) {
+            const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
+            bad = k < bad ? k : bad;
+          }
+          for (int q = 0; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, acc);
+          if (en.send) stv_cg(static_cast<T*>(en.send) + off, acc);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && en.send) {
+      __threadfence_system();
+      st_release_sys(en.send_flags + c, a.epoch);
+    }
+    __syncthreads();
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
+// Kernel B: the mean pass g_{S-1} -> g_0 -> ... -> g_{S-2}: wait for the
+// chunk, store it to this GPU's destinations, forward it.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  __shared__ ChainEntry en;
+  __shared__ int ok_flag;
+  const long units = a.n_chunks * a.n_entries;
+  for (long u = blockIdx.x; u < units; u += gridDim.x) {
+    const long c = u / a.n_entries;
+    const int ei = static_cast<int>(u % a.n_entries);
+    if (threadIdx.x == 0) {
+      en = a.entries[ei];
+      ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
+    }
+    __syncthreads();
+    const long lo = c * a.chunk;
+    const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
+    if (ok_flag) {
+      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+        const long off = e * VN;
+        const Pack<T> mean = ldv_cg(static_cast<const T*>(en.recv) + off);
+        for (int q = 0; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, mean);
+        if (en.send) stv_cg(static_cast<T*>(en.send) + off, mean);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && en.send) {
+      __threadfence_system();
+      st_release_sys(en.send_flags + c, a.epoch);
+    }
+    __syncthreads();
+  }
+}
+
 // ---- synthetic gradients: SplitMix64 + Box-Muller (rng.cpp:8-51) -----------
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;

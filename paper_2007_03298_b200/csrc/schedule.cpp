@@ -206,21 +206,40 @@ void slice_range(long d_pad, int s, int j, long* lo, long* hi) {
   *hi = c1 * kRowAlign;
 }
 
-GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad) {
+GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad, bool force_chain) {
   GpuPlan plan;
   const int per = world_size / n_gpus;
+  std::vector<int> slots_used(static_cast<size_t>(n_gpus), 0);
+  // chain slot of (gpu, group): index of the group among the chain groups
+  // that include that GPU, in ascending group order -- every rank computes
+  // the same table, so senders know their receivers' slots.
+  std::vector<std::vector<int>> slot_of(static_cast<size_t>(part.n_groups()));
   for (int g = 0; g < part.n_groups(); ++g) {
     const int* mem = part.group(g);
     const int m = part.size(g);
-    std::vector<int> gpus;  // ascending, distinct (members are ascending)
+    std::vector<int> gpus;   // ascending, distinct (members are ascending)
+    std::vector<int> count;  // members per GPU
     for (int j = 0; j < m; ++j) {
       const int gpu = mem[j] / per;
-      if (gpus.empty() || gpus.back() != gpu) gpus.push_back(gpu);
+      if (gpus.empty() || gpus.back() != gpu) {
+        gpus.push_back(gpu);
+        count.push_back(0);
+      }
+      ++count.back();
     }
-    if (gpus.size() > 1) plan.any_spanning_globally = true;
+    const bool spanning = gpus.size() > 1;
+    if (spanning) plan.any_spanning_globally = true;
+    const bool chain = spanning && (force_chain || *std::max_element(count.begin(), count.end()) >= 2);
+    slot_of[static_cast<size_t>(g)].assign(static_cast<size_t>(n_gpus), -1);
+    if (chain) {
+      plan.any_chain_globally = true;
+      for (int gpu : gpus) slot_of[static_cast<size_t>(g)][static_cast<size_t>(gpu)] = slots_used[static_cast<size_t>(gpu)]++;
+    } else if (spanning) {
+      plan.any_twoshot_globally = true;
+    }
     const auto it = std::find(gpus.begin(), gpus.end(), rank);
     if (it == gpus.end()) continue;
-    if (gpus.size() == 1) {
+    if (!spanning) {
       plan.local_groups.push_back(g);
       continue;
     }
@@ -228,12 +247,39 @@ GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, l
     for (int j = 0; j < m; ++j) {
       if (mem[j] / per == rank) plan.spanning_local_members.push_back(mem[j]);
     }
+    const int S = static_cast<int>(gpus.size());
+    const int pos = static_cast<int>(it - gpus.begin());
+    if (chain) {
+      ChainRole r;
+      r.group = g;
+      r.stage = pos;
+      r.S = S;
+      r.m = m;
+      r.first_member = mem[0];
+      for (int j = 0; j < m; ++j) {
+        if (mem[j] / per == rank) r.run.push_back(mem[j]);
+      }
+      if (pos + 1 < S) r.next_gpu = gpus[static_cast<size_t>(pos + 1)];
+      if (pos == S - 1) {
+        r.mean_next_gpu = gpus[0];
+      } else if (pos + 1 <= S - 2) {
+        r.mean_next_gpu = gpus[static_cast<size_t>(pos + 1)];
+      }
+      plan.chain.push_back(r);
+      continue;
+    }
     Slice sl;
     sl.group = g;
-    slice_range(d_pad, static_cast<int>(gpus.size()), static_cast<int>(it - gpus.begin()), &sl.lo,
-                &sl.hi);
+    slice_range(d_pad, S, pos, &sl.lo, &sl.hi);
     if (sl.hi > sl.lo) plan.owned.push_back(sl);
   }
+  for (ChainRole& r : plan.chain) {
+    const auto& so = slot_of[static_cast<size_t>(r.group)];
+    r.slot = so[static_cast<size_t>(rank)];
+    if (r.next_gpu >= 0) r.next_slot = so[static_cast<size_t>(r.next_gpu)];
+    if (r.mean_next_gpu >= 0) r.mean_next_slot = so[static_cast<size_t>(r.mean_next_gpu)];
+  }
+  plan.max_chain_slots = *std::max_element(slots_used.begin(), slots_used.end());
   std::sort(plan.spanning_local_members.begin(), plan.spanning_local_members.end());
   return plan;
 }

@@ -61,15 +61,39 @@ struct Slice {
   long hi = 0;
 };
 
+// A spanning group with several members on some GPU is folded by the
+// ordered chain instead (kernels.cuh chain_*): this GPU's role in it.
+struct ChainRole {
+  int group = 0;        // index in the Partition
+  int slot = 0;         // this GPU's receive-buffer slot for the group
+  int stage = 0;        // position j in the group's ascending GPU list
+  int S = 0;            // GPUs spanned
+  int m = 0;            // members
+  int first_member = 0;
+  std::vector<int> run; // this GPU's members, ascending (contiguous in the fold order)
+  int next_gpu = -1;    // partial pass successor (stage j+1), -1 at the last stage
+  int next_slot = -1;
+  int mean_next_gpu = -1;  // mean pass successor: last -> g_0 -> g_1 -> ... -> g_{S-2}
+  int mean_next_slot = -1;
+};
+
 struct GpuPlan {
   std::vector<int> local_groups;     // groups entirely on this GPU
   std::vector<int> spanning_groups;  // groups with members here and elsewhere
   std::vector<int> spanning_local_members;  // this GPU's members of spanning groups (ascending)
-  std::vector<Slice> owned;          // slices this GPU folds
-  bool any_spanning_globally = false;  // some group spans GPUs (barrier needed)
+  std::vector<Slice> owned;          // two-shot slices this GPU folds
+  std::vector<ChainRole> chain;      // chain-fold groups this GPU takes part in
+  bool any_spanning_globally = false;  // some group spans GPUs
+  bool any_twoshot_globally = false;   // some spanning group is two-shot (barrier before the fold)
+  bool any_chain_globally = false;
+  int max_chain_slots = 0;           // over all GPUs: receive slots needed
 };
 
-GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad);
+// force_chain: every spanning group takes the chain path (tests); otherwise
+// only groups with >= 2 members on some GPU (where the chain moves fewer
+// NVLink bytes than the two-shot).
+GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad,
+                  bool force_chain = false);
 
 // [lo, hi) of the j-th of s near-equal chunk-aligned slices of [0, d_pad).
 void slice_range(long d_pad, int s, int j, long* lo, long* hi);

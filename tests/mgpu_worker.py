@@ -31,10 +31,12 @@ CASES = [
     ("ds", 4, 2, False, 2, 999),
     ("bsp", 8, 8, False, 0, 70_001),
     ("bsp", 4, 4, False, 3, 2049),
+    ("bsp", 16, 16, False, 1, 300_007),  # packed BSP: chain over gradient rows
+    ("ds", 64, 8, False, 0, 20_000),     # C4 shape
 ]
 
 
-def run_case(kind, W, N, rect, opt, d, rank, G, orc):
+def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0):
     s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
                      WorldConfig(W, N), 1, rect)
     wd = 0.01 if opt in (1, 3) else 0.0
@@ -42,7 +44,7 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc):
     rng = np.random.default_rng(1000 + W + opt)
     w = rng.standard_normal((W, d)).astype(np.float32)
     mine = local_slice(W, G, rank)
-    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", rank, rank, G)
+    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", rank, rank, G, path=path)
     attach(e)
     e.upload_all(BUF_PARAMS, w[mine.start:mine.stop])
     m1, m2 = np.zeros_like(w), np.zeros_like(w)
@@ -76,7 +78,8 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc):
         if opt >= 1:
             ok = ok and np.array_equal(np.concatenate([p[1] for p in parts]), m1)
         diff = float(np.abs(full - w).max())
-        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d}: {'OK' if ok else 'MISMATCH'} maxdiff={diff}",
+        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d} path={path}: "
+              f"{'OK' if ok else 'MISMATCH'} maxdiff={diff}",
               flush=True)
         return ok
     return True
@@ -92,7 +95,8 @@ def main():
     for case in CASES:
         if case[1] % G:
             continue
-        ok = run_case(*case, rank, G, orc) and ok
+        for path in (0, 2):  # auto (two-shot / chain by shape) and chain forced everywhere
+            ok = run_case(*case, rank, G, orc, path) and ok
     dist.barrier()
     if rank == 0:
         print("MGPU " + ("PASS" if ok else "FAIL"), flush=True)

@@ -27,7 +27,7 @@ class FakeEngine:
         self.attached = None
 
     def ipc_export(self):
-        return bytes([self.rank]) * 256
+        return bytes([self.rank]) * 384
 
     def ipc_attach(self, handles):
         self.attached = handles
@@ -46,7 +46,7 @@ def _worker(rank, world, port, q):
 
         e = FakeEngine(rank, world)
         attach(e)
-        assert e.attached == [bytes([r]) * 256 for r in range(world)]
+        assert e.attached == [bytes([r]) * 384 for r in range(world)]
         assert list(local_slice(8 * world, world, rank)) == list(range(8 * rank, 8 * rank + 8))
 
         results = {}
@@ -64,6 +64,8 @@ def _worker(rank, world, port, q):
                 mine = list(zip(grp[:n].tolist(), lo[:n].tolist(), hi[:n].tolist()))
                 allv = [None] * world
                 dist.all_gather_object(allv, mine)
+                chains = [None] * world
+                dist.all_gather_object(chains, out.chain_groups)
                 # every spanning group's slices tile [0, d_pad) exactly once
                 d_pad = (12345 + 63) // 64 * 64
                 by_group = {}
@@ -75,7 +77,7 @@ def _worker(rank, world, port, q):
                     assert ivs[0][0] == 0 and ivs[-1][1] == d_pad, (W, N, t, g)
                     for x, y in zip(ivs, ivs[1:]):
                         assert x[1] == y[0]
-                results[(W, N, t)] = len(by_group)
+                results[(W, N, t)] = (len(by_group), tuple(chains))
         q.put((rank, "ok", results))
     except Exception as ex:  # pragma: no cover - reported to the parent
         q.put((rank, repr(ex), None))

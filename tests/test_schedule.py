@@ -145,10 +145,12 @@ def _plan(s, t, d, G, r):
 
 
 @pytest.mark.parametrize("W,N,rect,G", [(8, 2, True, 8), (8, 2, True, 2), (32, 4, True, 8), (64, 8, False, 8),
-                                        (16, 4, False, 8), (8, 2, True, 4), (4, 2, False, 2)])
+                                        (16, 4, False, 8), (8, 2, True, 4), (4, 2, False, 2), (32, 4, True, 4)])
 def test_multi_gpu_plan_covers_every_element_once(W, N, rect, G):
-    """Two-shot ownership: for each group spanning GPUs, the owned slices of
-    its GPUs tile [0, d_pad) exactly once; GPU-local groups own nothing."""
+    """Every spanning group is folded exactly one way: two-shot (its GPUs'
+    owned slices tile [0, d_pad) exactly once) when it has one member per
+    GPU, the ordered chain (no slices; every member GPU takes part) when
+    some GPU holds several of its members.  GPU-local groups own nothing."""
     d = 1000 + 3
     d_pad = (d + 63) // 64 * 64
     s = ds(W, N, rect=rect)
@@ -156,20 +158,27 @@ def test_multi_gpu_plan_covers_every_element_once(W, N, rect, G):
         part = make_partition(s, t)
         per = W // G
         cover = {}
-        n_local = 0
+        n_local = n_chain = 0
         for r in range(G):
             summ, slices = _plan(s, t, d, G, r)
             n_local += summ.local_groups
+            n_chain += summ.chain_groups
             for g, lo, hi in slices:
                 cover.setdefault(g, []).append((lo, hi))
+        want_chain = 0
         for gi, members in enumerate(part.groups):
             gpus = sorted({m // per for m in members})
             if len(gpus) == 1:
                 assert gi not in cover
+                continue
+            if max(sum(1 for m in members if m // per == g) for g in gpus) >= 2:
+                assert gi not in cover
+                want_chain += len(gpus)
                 continue
             ivs = sorted(cover[gi])
             assert ivs[0][0] == 0 and ivs[-1][1] == d_pad
             for (a0, a1), (b0, b1) in zip(ivs, ivs[1:]):
                 assert a1 == b0
             assert len(ivs) <= len(gpus)
+        assert n_chain == want_chain
         assert n_local == sum(1 for g in part.groups if len({m // per for m in g}) == 1)
