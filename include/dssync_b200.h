@@ -225,6 +225,18 @@ int dss_quadratic_init(dss_ctx* ctx, uint64_t problem_seed, double delta0);
 /* Upload an explicit optimum w* (dim elements of the context dtype). */
 int dss_set_optimum(dss_ctx* ctx, const void* host, long n);
 
+/* ---- per-iteration trace (run_training post-round, sync.cpp:430-458) ---- */
+/* global_mean_params = mean_of_ptrs over all W workers' params
+ * (param.cpp:59-70): ascending fold x 1/W, bit-exact; dim elements of the
+ * context dtype written to host_mean on every rank (collective on multi-GPU). */
+int dss_global_mean(dss_ctx* ctx, void* host_mean);
+/* post_sync_loss of every local worker, full_loss of the isotropic quadratic
+ * 0.5 * sum_i (w_i - w*_i) * (mu * (w_i - w*_i)) (problems.cpp:195-200), as an
+ * fp64 device reduction (tolerance parity: the sum order is parallel).
+ * losses: local_workers doubles.  suboptimality (optional) = full_loss of the
+ * row written by the last dss_global_mean (true_suboptimality, sync.cpp:585). */
+int dss_quadratic_losses(dss_ctx* ctx, double mu, double* losses, double* suboptimality);
+
 /* Latched divergence check (synchronizes).  DSS_OK or DSS_EDIVERGED. */
 int dss_check(dss_ctx* ctx);
 /* Clear latched divergence flags. */

@@ -172,7 +172,7 @@ class Reference:
         L.ref_quadratic_init.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _P, _P] + E
         L.ref_quadratic_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_double, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _P, C.c_double,
-                                        _P, _P, C.POINTER(C.c_int)] + E
+                                        _P, _P, C.POINTER(C.c_int)] + E + [_P, _P, _P]
         L.ref_logistic_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                        C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double, C.c_double,
                                        C.c_long, _P, _P, _P, C.POINTER(C.c_int)] + E
@@ -242,14 +242,21 @@ class Reference:
             raise RuntimeError(self.error())
         return wstar, w0
 
-    def quadratic_run(self, kind, topo, W, N, d, mu, sigma, delta0, problem_seed, run_seed, T, opt, hp, alpha):
+    def quadratic_run(self, kind, topo, W, N, d, mu, sigma, delta0, problem_seed, run_seed, T, opt, hp, alpha,
+                      trace=False):
         grads = np.zeros((T, W, d), _D)
         params = np.zeros((T, W, d), _D)
         match = C.c_int()
+        tg = np.zeros((T, d), _D) if trace else None
+        tl = np.zeros((T, W), _D) if trace else None
+        ts = np.zeros((T, 5), _D) if trace else None
         rc = self.lib.ref_quadratic_run(kind, topo, W, N, d, mu, sigma, delta0, problem_seed, run_seed, T, opt,
-                                        _ptr(hp), alpha, _ptr(grads), _ptr(params), C.byref(match), *self._e())
+                                        _ptr(hp), alpha, _ptr(grads), _ptr(params), C.byref(match), *self._e(),
+                                        _ptr(tg), _ptr(tl), _ptr(ts))
         if rc:
             raise RuntimeError(self.error())
+        if trace:
+            return grads, params, bool(match.value), (tg, tl, ts)
         return grads, params, bool(match.value)
 
     def logistic_run(self, kind, W, N, d, M, l2, problem_seed, run_seed, batch, T, opt, hp, alpha0, factor, every):

@@ -334,11 +334,15 @@ int ref_quadratic_init(uint64_t seed, int d, double mu, double delta0, double* w
 //   grads_out  [T][W][d]  the stochastic gradient each worker used at t
 //   params_out [T][W][d]  every worker's params after iteration t
 // The replay is then checked against run_training itself (same options):
-// *matches = 1 iff final params agree bit for bit.
+// *matches = 1 iff final params agree bit for bit.  When trace_* are given,
+// run_training's IterationTrace (sync.hpp:63-74) is recorded per t:
+//   trace_gmean [T][d], trace_loss [T][W], trace_scalars [T][5] =
+//   {mean_post_sync_loss, suboptimality, critical_path_steps,
+//    total_messages, simulated_comm_time}.
 int ref_quadratic_run(int kind, int topo, int W, int N, int d, double mu, double sigma, double delta0,
                       uint64_t problem_seed, uint64_t run_seed, int T, int opt, const double* hp,
                       double alpha, double* grads_out, double* params_out, int* matches, char* err,
-                      int errlen) {
+                      int errlen, double* trace_gmean, double* trace_loss, double* trace_scalars) {
   return guarded(err, errlen, nullptr, nullptr, [&] {
     DatasetSpec s;
     s.kind = "quadratic";
@@ -386,6 +390,19 @@ int ref_quadratic_run(int kind, int topo, int W, int N, int d, double mu, double
     *matches = 1;
     for (int k = 0; k < W; ++k) {
       if (rr.final_workers[static_cast<size_t>(k)].params != ws[static_cast<size_t>(k)].params) *matches = 0;
+    }
+    if (trace_gmean) {
+      for (int t = 0; t < T; ++t) {
+        const IterationTrace& tr = rr.traces[static_cast<size_t>(t)];
+        std::memcpy(trace_gmean + static_cast<long>(t) * d, tr.global_mean_params.data(), sizeof(double) * static_cast<size_t>(d));
+        for (int k = 0; k < W; ++k) trace_loss[static_cast<long>(t) * W + k] = tr.post_sync_loss[static_cast<size_t>(k)];
+        double* sc = trace_scalars + static_cast<long>(t) * 5;
+        sc[0] = tr.mean_post_sync_loss;
+        sc[1] = tr.suboptimality;
+        sc[2] = static_cast<double>(tr.critical_path_steps);
+        sc[3] = static_cast<double>(tr.total_messages);
+        sc[4] = tr.simulated_comm_time;
+      }
     }
   });
 }

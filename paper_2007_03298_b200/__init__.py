@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     DivergenceError,
     DsSyncEngine,
     GroupPartition,
+    IterationTrace,
     OptimizerHyperparams,
     OptimizerKind,
     OptimizerState,
@@ -22,6 +23,7 @@ from .api import (  # noqa: F401
     apply_step,
     check_mixing,
     group_of,
+    iteration_trace,
     is_square_mode,
     make_partition,
     round_outcome,

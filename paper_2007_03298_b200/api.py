@@ -148,6 +148,40 @@ class SyncRoundOutcome:  # sync.hpp:119-122
     total_messages: int = 0
 
 
+@dataclass
+class IterationTrace:  # sync.hpp:63-74
+    t: int = 0
+    post_sync_loss: Optional[np.ndarray] = None
+    mean_post_sync_loss: float = 0.0
+    suboptimality: float = 0.0
+    critical_path_steps: int = 0
+    total_messages: int = 0
+    simulated_comm_time: float = 0.0
+    global_mean_params: Optional[np.ndarray] = None
+
+
+def iteration_trace(engine: "DsSyncEngine", t: int, outcome: SyncRoundOutcome, mu: float,
+                    data_size: float = 0.0, bandwidth: float = 1.0, losses_all=None) -> IterationTrace:
+    """run_training's post-round bookkeeping (sync.cpp:430-458) on the device
+    state: global mean (bit-exact ordered fold), per-worker quadratic losses
+    (fp64 device reduction), closed-form comm counts.  On several GPUs pass
+    losses_all = every worker's loss gathered in rank order."""
+    gmean = engine.global_mean()
+    losses, sub = engine.quadratic_losses(mu)
+    if losses_all is not None:
+        losses = np.asarray(losses_all, dtype=np.float64)
+    acc = 0.0
+    for x in losses:  # sync.cpp:582-584: ascending sum, then a division
+        acc += float(x)
+    W = engine.strategy.world.world_size
+    payload = data_size if data_size > 0.0 else 8.0 * engine.dim  # sync.cpp:314-318
+    bw = bandwidth
+    if engine.strategy.topology == Topology.PS:  # effective_bandwidth (sync.cpp:215-221)
+        bw = bandwidth * engine.strategy.num_servers / W
+    return IterationTrace(t, losses, acc / W, sub, outcome.critical_path_steps, outcome.total_messages,
+                          outcome.critical_path_steps * payload / bw, gmean)
+
+
 # ---------------------------------------------------------------------------
 def _raise(status: int, msg: str, rank: int = -1, iteration: int = -1):
     if status == L.DSS_OK:
@@ -373,6 +407,20 @@ class DsSyncEngine:
     def set_optimum(self, wstar) -> None:
         a = self._arr(wstar)
         self._ck(self.lib.dss_set_optimum(self.h, a.ctypes.data, a.size))
+
+    def global_mean(self) -> np.ndarray:
+        """mean_of_ptrs over all W workers (param.cpp:59-70), bit-exact."""
+        out = np.empty(self.dim, dtype=self.dtype)
+        self._ck(self.lib.dss_global_mean(self.h, out.ctypes.data))
+        return out
+
+    def quadratic_losses(self, mu: float, with_suboptimality: bool = True):
+        """(post_sync_loss of each local worker, full_loss at the last global mean)."""
+        losses = np.empty(self.local_workers, dtype=np.float64)
+        sub = C.c_double()
+        self._ck(self.lib.dss_quadratic_losses(self.h, mu, losses.ctypes.data,
+                                               C.byref(sub) if with_suboptimality else None))
+        return losses, (sub.value if with_suboptimality else None)
 
     def check(self) -> None:
         self._ck(self.lib.dss_check(self.h))

@@ -146,6 +146,8 @@ struct dss_ctx {
 
   ParityPlan step_plan[2];   // DS (or BSP at [0])
   ParityPlan sync_plan[2];   // sync_round (no step)
+  ParityPlan mean_plan;      // ordered fold of every worker's params into mg (trace)
+  double* d_loss = nullptr;  // [P + 1] loss accumulators (trace)
   GroupLaunch apply_launch;  // singleton groups of every local worker
 
   bool timing = false;
@@ -468,6 +470,72 @@ ParityPlan build_bsp_multi_plan(dss_ctx* c) {
   return pp;
 }
 
+// global_mean_params = mean_of_ptrs over all W workers (param.cpp:59-70):
+// one all-world group over the params rows, mean into mg (every GPU).
+ParityPlan build_mean_plan(dss_ctx* c) {
+  ParityPlan pp;
+  const int W = c->cfg.strategy.world_size;
+  dss_strategy world = c->cfg.strategy;
+  world.kind = DSS_BSP;
+  world.group_size = W;
+  world.rectangular = 0;
+  const Partition part = make_partition(world, 0);
+  if (!multi(c)) {
+    if (W > kMaxFold) throw std::invalid_argument("global mean supports at most 64 workers per GPU");
+    FoldEntry e{};
+    std::vector<void*> src, dst{c->mg};
+    e.src_beg = 0;
+    e.src_cnt = W;
+    e.dst_beg = 0;
+    e.dst_cnt = 1;
+    e.lo = 0;
+    e.hi = c->d_pad;
+    e.err_rank = 0;
+    e.err_phase = 1;
+    for (int k = 0; k < W; ++k) src.push_back(static_cast<char*>(c->w) + static_cast<size_t>(k) * c->d_pad * c->esz);
+    pp.any_spanning = true;
+    pp.any_twoshot = true;
+    pp.fold.entries = 1;
+    pp.fold.uniform_m = W;
+    pp.fold.max_len = c->d_pad;
+    pp.fold.d_entries = upload_table(c, std::vector<FoldEntry>{e});
+    pp.fold.d_src = upload_table(c, src);
+    pp.fold.d_dst = upload_table(c, dst);
+    pp.built = true;
+    return pp;
+  }
+  const int G = c->cfg.n_gpus;
+  const GpuPlan gp = make_plan(part, W, G, c->cfg.rank, c->d_pad, force_chain(c));
+  pp.any_spanning = true;
+  pp.any_twoshot = gp.any_twoshot_globally;
+  pp.any_chain = gp.any_chain_globally;
+  if (!gp.chain.empty()) pp.chain = build_chain(c, gp.chain, c->w, {std::vector<void*>{c->mg}}, 1);
+  if (!gp.owned.empty()) {
+    if (W > kMaxFold) throw std::invalid_argument("global mean supports at most 64 workers");
+    const Slice sl = gp.owned[0];
+    FoldEntry e{};
+    std::vector<void*> src, dst;
+    e.src_beg = 0;
+    e.src_cnt = W;
+    e.dst_beg = 0;
+    e.dst_cnt = G;
+    e.lo = sl.lo;
+    e.hi = sl.hi;
+    e.err_rank = 0;
+    e.err_phase = 1;
+    for (int k = 0; k < W; ++k) src.push_back(row_ptr(c, c->peer_w, k));
+    for (int q = 0; q < G; ++q) dst.push_back(c->peer_mg[static_cast<size_t>(q)]);
+    pp.fold.entries = 1;
+    pp.fold.uniform_m = W;
+    pp.fold.max_len = sl.hi - sl.lo;
+    pp.fold.d_entries = upload_table(c, std::vector<FoldEntry>{e});
+    pp.fold.d_src = upload_table(c, src);
+    pp.fold.d_dst = upload_table(c, dst);
+  }
+  pp.built = true;
+  return pp;
+}
+
 void build_plans(dss_ctx* c) {
   const dss_strategy& s = c->cfg.strategy;
   if (s.kind == DSS_DS_SYNC) {
@@ -476,6 +544,7 @@ void build_plans(dss_ctx* c) {
     c->step_plan[0] = build_bsp_multi_plan(c);
   }
   for (int p = 0; p < 2; ++p) c->sync_plan[p] = build_plan(c, p, false);
+  if (c->cfg.strategy.world_size <= kMaxFold || multi(c)) c->mean_plan = build_mean_plan(c);
 }
 
 // ---- launch helpers ---------------------------------------------------------
@@ -651,7 +720,8 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t) {
     a.n_entries = cl.na;
     const long units = c->chain_nchunks * cl.na;
     TimedLaunch tl(c, DSS_KIND_CHAIN);
-    chain_partial_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * 4L)), kThreads, 0, c->stream>>>(a);
+    chain_partial_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                              kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
   }
   if (cl.nb > 0) {
@@ -659,7 +729,8 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t) {
     a.n_entries = cl.nb;
     const long units = c->chain_nchunks * cl.nb;
     TimedLaunch tl(c, DSS_KIND_CHAIN);
-    chain_mean_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * 4L)), kThreads, 0, c->stream>>>(a);
+    chain_mean_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                           kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_mean_kernel launch");
   }
 }
@@ -947,7 +1018,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         slots = std::max(slots, gp.max_chain_slots);
       }
       c->chain_slots = slots;
-      c->chain_chunk = std::min<long>(c->d_pad, std::max<long>(2048, std::min<long>(65536, pad_dim(c->d_pad / 64))));
+      c->chain_chunk = std::min<long>(c->d_pad, DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
       c->chain_flags = static_cast<unsigned long long*>(dalloc(
@@ -1301,6 +1372,63 @@ extern "C" int dss_set_optimum(dss_ctx* c, const void* host, long n) {
     ck(cudaMemcpyAsync(c->wstar, host, static_cast<size_t>(n) * c->esz, cudaMemcpyHostToDevice, c->stream),
        "set_optimum");
     ck(cudaStreamSynchronize(c->stream), "set_optimum sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_global_mean(dss_ctx* c, void* host_mean) {
+  if (!c || !host_mean) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (!c->mean_plan.built) throw std::invalid_argument("global mean supports at most 64 workers per GPU");
+    if (multi(c) && !c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const ParityPlan& pp = c->mean_plan;
+    quiesce(c);
+    if (pp.any_twoshot) {
+      if (multi(c)) barrier(c);
+      launch_fold_any(c, pp.fold, 0);
+      if (multi(c)) barrier(c);
+    }
+    if (pp.any_chain) {
+      if (multi(c)) barrier(c);
+      launch_chain_any(c, pp.chain, 0);
+      if (multi(c)) c->pending_remote = true;
+    }
+    ck(cudaMemcpyAsync(host_mean, c->mg, static_cast<size_t>(c->d) * c->esz, cudaMemcpyDeviceToHost, c->stream),
+       "global mean download");
+    ck(cudaStreamSynchronize(c->stream), "global mean sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, double* losses, double* suboptimality) {
+  if (!c || !losses) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    if (!c->d_loss) c->d_loss = static_cast<double*>(dalloc(c, sizeof(double) * (c->P + 1)));
+    const int rows = c->P + (suboptimality ? 1 : 0);
+    std::vector<void*> ptrs;
+    for (int k = 0; k < c->P; ++k) ptrs.push_back(static_cast<char*>(c->w) + static_cast<size_t>(k) * c->d_pad * c->esz);
+    if (suboptimality) ptrs.push_back(c->mg);  // after dss_global_mean
+    void** d_ptrs = upload_table(c, ptrs);
+    ck(cudaMemsetAsync(c->d_loss, 0, sizeof(double) * (c->P + 1), c->stream), "loss reset");
+    dim3 grid(grid_x(c, c->d, rows), rows);
+    if (c->cfg.dtype == DSS_F64) {
+      quad_loss_kernel<double><<<grid, kThreads, 0, c->stream>>>(reinterpret_cast<const double* const*>(d_ptrs),
+                                                                 static_cast<const double*>(c->wstar), c->d, mu, c->d_loss);
+    } else {
+      quad_loss_kernel<float><<<grid, kThreads, 0, c->stream>>>(reinterpret_cast<const float* const*>(d_ptrs),
+                                                                static_cast<const float*>(c->wstar), c->d, mu, c->d_loss);
+    }
+    ck(cudaGetLastError(), "quad_loss_kernel launch");
+    std::vector<double> h(static_cast<size_t>(rows));
+    ck(cudaMemcpyAsync(h.data(), c->d_loss, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream), "loss readback");
+    ck(cudaStreamSynchronize(c->stream), "loss sync");
+    cudaFree(d_ptrs);
+    c->allocations.erase(std::find(c->allocations.begin(), c->allocations.end(), static_cast<void*>(d_ptrs)));
+    for (int k = 0; k < c->P; ++k) losses[k] = h[static_cast<size_t>(k)];
+    if (suboptimality) *suboptimality = h[static_cast<size_t>(c->P)];
     return DSS_OK;
   });
 }

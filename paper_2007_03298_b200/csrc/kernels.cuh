@@ -37,6 +37,15 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_MIN_BLOCKS_M8_MOMENTUM
 #define DSS_MIN_BLOCKS_M8_MOMENTUM 1
 #endif
+// Chain fold pipelining: elements per chunk (one flag each) and resident
+// CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
+// start one round after stage j instead of after the whole row.
+#ifndef DSS_CHAIN_CHUNK
+#define DSS_CHAIN_CHUNK 4096
+#endif
+#ifndef DSS_CHAIN_CTAS_PER_SM
+#define DSS_CHAIN_CTAS_PER_SM 2
+#endif
 
 enum OptKind : int { kOptNone = -1, kSgd = 0, kMomentum = 1, kAdam = 2, kAdamW = 3 };
 
@@ -847,6 +856,30 @@ __global__ void compose_init_kernel(const double* wstar, const double* u, const 
       wstar_out[i] = T(0);
       row_out[i] = T(0);
     }
+  }
+}
+
+// full_loss of the isotropic quadratic per row (problems.cpp:195-200 with
+// A = mu*I): 0.5 * sum_i (w_i - w*_i) * (mu * (w_i - w*_i)), accumulated in
+// fp64 (a parallel sum: tolerance parity, not order-exact).  blockIdx.y =
+// row; out[row] += block partial.
+template <typename T>
+__global__ void quad_loss_kernel(const T* const* rows, const T* wstar, long d, double mu, double* out) {
+  __shared__ double part[kThreads / 32];
+  const T* w = rows[blockIdx.y];
+  double acc = 0.0;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < d; i += stride) {
+    const double diff = static_cast<double>(w[i]) - static_cast<double>(wstar[i]);
+    acc += diff * (mu * diff);
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) s += part[i];
+    atomicAdd(out + blockIdx.y, 0.5 * s);
   }
 }
 

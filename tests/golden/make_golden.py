@@ -98,12 +98,17 @@ def trajectories(R: Reference) -> tuple[dict, dict]:
     for kind, W, N in shapes:
         for opt, (alpha, wd) in hp_by_opt.items():
             hp = R.hp_array(weight_decay=wd)
-            grads, params, match = R.quadratic_run(1 if kind == "ds" else 0, 0, W, N, d, mu, sigma, delta0,
-                                                   pseed, rseed, T, OPTS[opt], hp, alpha)
+            grads, params, match, (tg, tl, ts) = R.quadratic_run(1 if kind == "ds" else 0, 0, W, N, d, mu, sigma,
+                                                                 delta0, pseed, rseed, T, OPTS[opt], hp, alpha,
+                                                                 trace=True)
             assert match, f"replay != run_training for {kind} {W}x{N} {opt}"
             key = f"{kind}_{W}x{N}_{opt}"
             arrs[key + "_grads"] = grads
             arrs[key + "_params"] = params
+            # run_training's IterationTrace per t (sync.cpp:430-458)
+            arrs[key + "_trace_gmean"] = tg
+            arrs[key + "_trace_loss"] = tl
+            arrs[key + "_trace_scalars"] = ts
             meta.append({"key": key, "kind": kind, "W": W, "N": N, "opt": opt, "alpha": alpha,
                          "weight_decay": wd, "d": d, "T": T})
     wstar, w0 = R.quadratic_init(pseed, d, mu, delta0)

@@ -46,6 +46,35 @@ def test_golden_trajectories_bit_exact(cuda_device, golden, path):
                 assert np.array_equal(got, params[t]), (m["key"], t, np.abs(got - params[t]).max())
 
 
+def test_trace_parity(cuda_device, golden):
+    """run_training's IterationTrace (sync.cpp:430-458) on the device:
+    global_mean_params bit-exact (ordered fold over all W workers), critical
+    path / messages / simulated comm time exact, post-sync losses, their mean
+    and the suboptimality within 1e-12 relative (fp64 device reduction in a
+    parallel order, vs the reference's sequential dot)."""
+    from paper_2007_03298_b200 import iteration_trace
+    meta, a = golden
+    mu = meta["quadratic"]["mu"]
+    for m in meta["trajectories"]:
+        key = m["key"]
+        grads = a[key + "_grads"]
+        tg, tl, ts = a[key + "_trace_gmean"], a[key + "_trace_loss"], a[key + "_trace_scalars"]
+        T, W, d = grads.shape
+        with engine_for(m["kind"], W, m["N"], OPTS[m["opt"]], d, m["weight_decay"], "f64") as e:
+            e.set_optimum(a["quad_wstar"])
+            e.broadcast_row(BUF_PARAMS, a["quad_w0"])
+            for t in range(T):
+                e.upload_all(BUF_GRADS, grads[t])
+                out = e.step(t, m["alpha"], check=True)
+                tr = iteration_trace(e, t, out, mu)
+                assert np.array_equal(tr.global_mean_params, tg[t]), (key, t)
+                np.testing.assert_allclose(tr.post_sync_loss, tl[t], rtol=1e-12, atol=0)
+                assert tr.mean_post_sync_loss == pytest.approx(ts[t][0], rel=1e-12)
+                assert tr.suboptimality == pytest.approx(ts[t][1], rel=1e-12)
+                assert (tr.critical_path_steps, tr.total_messages) == (int(ts[t][2]), int(ts[t][3]))
+                assert tr.simulated_comm_time == ts[t][4]
+
+
 def test_c1_logistic_bit_exact(cuda_device, golden):
     """Config C1 (4 workers, 2 groups of 2, logistic d=20, SGD, step-decay lr,
     300 iterations) on the device: bit-exact every iteration."""
