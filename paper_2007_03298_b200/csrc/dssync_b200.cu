@@ -1017,6 +1017,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
                                      force_chain(c.get()));
         slots = std::max(slots, gp.max_chain_slots);
       }
+      dss_strategy world = s;  // the all-world group of the global-mean trace
+      world.kind = DSS_BSP;
+      world.group_size = s.world_size;
+      world.rectangular = 0;
+      slots = std::max(slots, make_plan(make_partition(world, 0), s.world_size, cfg->n_gpus, cfg->rank, c->d_pad,
+                                        force_chain(c.get())).max_chain_slots);
       c->chain_slots = slots;
       c->chain_chunk = std::min<long>(c->d_pad, DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;

@@ -46,6 +46,11 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 2
 #endif
+// 1: full system fence before each chunk's release flag; 0: rely on the
+// cumulativity of st.release.sys after the CTA barrier (lighter).
+#ifndef DSS_CHAIN_FENCE
+#define DSS_CHAIN_FENCE 1
+#endif
 
 enum OptKind : int { kOptNone = -1, kSgd = 0, kMomentum = 1, kAdam = 2, kAdamW = 3 };
 
@@ -719,7 +724,7 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
     }
     __syncthreads();
     if (threadIdx.x == 0 && en.send) {
-      __threadfence_system();
+      if (DSS_CHAIN_FENCE) __threadfence_system();
       st_release_sys(en.send_flags + c, a.epoch);
     }
     __syncthreads();
@@ -755,7 +760,7 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
     }
     __syncthreads();
     if (threadIdx.x == 0 && en.send) {
-      __threadfence_system();
+      if (DSS_CHAIN_FENCE) __threadfence_system();
       st_release_sys(en.send_flags + c, a.epoch);
     }
     __syncthreads();
