@@ -41,15 +41,15 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.
 #ifndef DSS_CHAIN_CHUNK
-#define DSS_CHAIN_CHUNK 4096
+#define DSS_CHAIN_CHUNK 8192
 #endif
 #ifndef DSS_CHAIN_CTAS_PER_SM
-#define DSS_CHAIN_CTAS_PER_SM 2
+#define DSS_CHAIN_CTAS_PER_SM 8
 #endif
 // 1: full system fence before each chunk's release flag; 0: rely on the
 // cumulativity of st.release.sys after the CTA barrier (lighter).
 #ifndef DSS_CHAIN_FENCE
-#define DSS_CHAIN_FENCE 1
+#define DSS_CHAIN_FENCE 0
 #endif
 
 enum OptKind : int { kOptNone = -1, kSgd = 0, kMomentum = 1, kAdam = 2, kAdamW = 3 };
