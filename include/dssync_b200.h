@@ -231,11 +231,13 @@ int dss_set_optimum(dss_ctx* ctx, const void* host, long n);
  * context dtype written to host_mean on every rank (collective on multi-GPU). */
 int dss_global_mean(dss_ctx* ctx, void* host_mean);
 /* post_sync_loss of every local worker, full_loss of the isotropic quadratic
- * 0.5 * sum_i (w_i - w*_i) * (mu * (w_i - w*_i)) (problems.cpp:195-200), as an
- * fp64 device reduction (tolerance parity: the sum order is parallel).
+ * 0.5 * sum_i (w_i - w*_i) * (mu * (w_i - w*_i)) (problems.cpp:195-200).
+ * exact = 0: parallel fp64 device reduction (tolerance parity);
+ * exact = 1: the reference's sequential operation order, bit-exact (one
+ * thread per row: for traces / metrics files, not for huge d).
  * losses: local_workers doubles.  suboptimality (optional) = full_loss of the
  * row written by the last dss_global_mean (true_suboptimality, sync.cpp:585). */
-int dss_quadratic_losses(dss_ctx* ctx, double mu, double* losses, double* suboptimality);
+int dss_quadratic_losses(dss_ctx* ctx, double mu, int exact, double* losses, double* suboptimality);
 
 /* Latched divergence check (synchronizes).  DSS_OK or DSS_EDIVERGED. */
 int dss_check(dss_ctx* ctx);

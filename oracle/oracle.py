@@ -172,7 +172,8 @@ class Reference:
         L.ref_quadratic_init.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _P, _P] + E
         L.ref_quadratic_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_double, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _P, C.c_double,
-                                        _P, _P, C.POINTER(C.c_int)] + E + [_P, _P, _P]
+                                        _P, _P, C.POINTER(C.c_int)] + E + [_P, _P, _P, C.c_char_p, C.c_long]
+        L.ref_format_doubles.argtypes = [_P, C.c_long, C.c_char_p, C.c_long]
         L.ref_logistic_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                        C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double, C.c_double,
                                        C.c_long, _P, _P, _P, C.POINTER(C.c_int)] + E
@@ -235,6 +236,12 @@ class Reference:
         self.lib.ref_gaussians(seed, purpose, rank, it, n, _ptr(out))
         return out
 
+    def format_doubles(self, values):
+        v = np.ascontiguousarray(values, _D)
+        buf = C.create_string_buffer(64 * (v.size + 1))
+        assert self.lib.ref_format_doubles(_ptr(v), v.size, buf, len(buf)) == 0
+        return buf.value.decode().split("\n")[:-1]
+
     def quadratic_init(self, seed, d, mu, delta0):
         wstar, w0 = np.zeros(d, _D), np.zeros(d, _D)
         rc = self.lib.ref_quadratic_init(seed, d, mu, delta0, _ptr(wstar), _ptr(w0), *self._e())
@@ -250,13 +257,14 @@ class Reference:
         tg = np.zeros((T, d), _D) if trace else None
         tl = np.zeros((T, W), _D) if trace else None
         ts = np.zeros((T, 5), _D) if trace else None
+        csv = C.create_string_buffer(1 << 16) if trace else None
         rc = self.lib.ref_quadratic_run(kind, topo, W, N, d, mu, sigma, delta0, problem_seed, run_seed, T, opt,
                                         _ptr(hp), alpha, _ptr(grads), _ptr(params), C.byref(match), *self._e(),
-                                        _ptr(tg), _ptr(tl), _ptr(ts))
+                                        _ptr(tg), _ptr(tl), _ptr(ts), csv, len(csv) if trace else 0)
         if rc:
             raise RuntimeError(self.error())
         if trace:
-            return grads, params, bool(match.value), (tg, tl, ts)
+            return grads, params, bool(match.value), (tg, tl, ts, csv.value.decode())
         return grads, params, bool(match.value)
 
     def logistic_run(self, kind, W, N, d, M, l2, problem_seed, run_seed, batch, T, opt, hp, alpha0, factor, every):

@@ -18,6 +18,7 @@
 
 #include "dssync/comm.hpp"
 #include "dssync/errors.hpp"
+#include "dssync/metrics.hpp"
 #include "dssync/optim.hpp"
 #include "dssync/param.hpp"
 #include "dssync/problems.hpp"
@@ -298,6 +299,18 @@ int ref_bsp_iteration(int topo, int servers, int W, long d, long t, int opt, con
   });
 }
 
+// format_double (metrics.cpp:13-17) of n values, '\n'-joined into buf.
+int ref_format_doubles(const double* v, long n, char* buf, long len) {
+  std::string out;
+  for (long i = 0; i < n; ++i) {
+    out += format_double(v[i]);
+    out += '\n';
+  }
+  if (static_cast<long>(out.size()) + 1 > len) return 1;
+  std::memcpy(buf, out.c_str(), out.size() + 1);
+  return 0;
+}
+
 // Gaussians of stream (seed, purpose, rank, it) (rng.cpp:20-51).
 void ref_gaussians(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t it, long n, double* out) {
   Rng r = Rng::for_stream(seed, purpose, rank, it);
@@ -342,7 +355,8 @@ int ref_quadratic_init(uint64_t seed, int d, double mu, double delta0, double* w
 int ref_quadratic_run(int kind, int topo, int W, int N, int d, double mu, double sigma, double delta0,
                       uint64_t problem_seed, uint64_t run_seed, int T, int opt, const double* hp,
                       double alpha, double* grads_out, double* params_out, int* matches, char* err,
-                      int errlen, double* trace_gmean, double* trace_loss, double* trace_scalars) {
+                      int errlen, double* trace_gmean, double* trace_loss, double* trace_scalars,
+                      char* csv_out, long csv_len) {
   return guarded(err, errlen, nullptr, nullptr, [&] {
     DatasetSpec s;
     s.kind = "quadratic";
@@ -403,6 +417,11 @@ int ref_quadratic_run(int kind, int topo, int W, int N, int d, double mu, double
         sc[3] = static_cast<double>(tr.total_messages);
         sc[4] = tr.simulated_comm_time;
       }
+    }
+    if (csv_out) {  // the reference's own metrics file for this run (metrics.cpp:37-56)
+      const std::string csv = metrics_csv(rr.traces);
+      if (static_cast<long>(csv.size()) + 1 > csv_len) throw std::runtime_error("csv buffer too small");
+      std::memcpy(csv_out, csv.c_str(), csv.size() + 1);
     }
   });
 }

@@ -81,7 +81,7 @@ SIGNATURES = {
     "dss_quadratic_init": (C.c_int, [_P, C.c_uint64, C.c_double]),
     "dss_set_optimum": (C.c_int, [_P, _P, C.c_long]),
     "dss_global_mean": (C.c_int, [_P, _P]),
-    "dss_quadratic_losses": (C.c_int, [_P, C.c_double, _P, _P]),
+    "dss_quadratic_losses": (C.c_int, [_P, C.c_double, C.c_int, _P, _P]),
     "dss_check": (C.c_int, [_P]),
     "dss_clear_error": (C.c_int, [_P]),
     "dss_last_error": (C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_long)]),

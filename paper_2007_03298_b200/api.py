@@ -161,13 +161,14 @@ class IterationTrace:  # sync.hpp:63-74
 
 
 def iteration_trace(engine: "DsSyncEngine", t: int, outcome: SyncRoundOutcome, mu: float,
-                    data_size: float = 0.0, bandwidth: float = 1.0, losses_all=None) -> IterationTrace:
+                    data_size: float = 0.0, bandwidth: float = 1.0, losses_all=None,
+                    exact: bool = False) -> IterationTrace:
     """run_training's post-round bookkeeping (sync.cpp:430-458) on the device
     state: global mean (bit-exact ordered fold), per-worker quadratic losses
     (fp64 device reduction), closed-form comm counts.  On several GPUs pass
     losses_all = every worker's loss gathered in rank order."""
     gmean = engine.global_mean()
-    losses, sub = engine.quadratic_losses(mu)
+    losses, sub = engine.quadratic_losses(mu, exact=exact)
     if losses_all is not None:
         losses = np.asarray(losses_all, dtype=np.float64)
     acc = 0.0
@@ -414,11 +415,12 @@ class DsSyncEngine:
         self._ck(self.lib.dss_global_mean(self.h, out.ctypes.data))
         return out
 
-    def quadratic_losses(self, mu: float, with_suboptimality: bool = True):
-        """(post_sync_loss of each local worker, full_loss at the last global mean)."""
+    def quadratic_losses(self, mu: float, with_suboptimality: bool = True, exact: bool = False):
+        """(post_sync_loss of each local worker, full_loss at the last global mean).
+        exact=True evaluates in the reference's sequential order (bit-exact)."""
         losses = np.empty(self.local_workers, dtype=np.float64)
         sub = C.c_double()
-        self._ck(self.lib.dss_quadratic_losses(self.h, mu, losses.ctypes.data,
+        self._ck(self.lib.dss_quadratic_losses(self.h, mu, 1 if exact else 0, losses.ctypes.data,
                                                C.byref(sub) if with_suboptimality else None))
         return losses, (sub.value if with_suboptimality else None)
 

@@ -1407,7 +1407,7 @@ extern "C" int dss_global_mean(dss_ctx* c, void* host_mean) {
   });
 }
 
-extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, double* losses, double* suboptimality) {
+extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, int exact, double* losses, double* suboptimality) {
   if (!c || !losses) return fail(c, DSS_EINVAL, "null argument");
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
@@ -1420,7 +1420,17 @@ extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, double* losses, doubl
     void** d_ptrs = upload_table(c, ptrs);
     ck(cudaMemsetAsync(c->d_loss, 0, sizeof(double) * (c->P + 1), c->stream), "loss reset");
     dim3 grid(grid_x(c, c->d, rows), rows);
-    if (c->cfg.dtype == DSS_F64) {
+    if (exact) {
+      if (c->cfg.dtype == DSS_F64) {
+        quad_loss_exact_kernel<double><<<rows, 32, 0, c->stream>>>(reinterpret_cast<const double* const*>(d_ptrs),
+                                                                  static_cast<const double*>(c->wstar), c->d, mu,
+                                                                  c->d_loss);
+      } else {
+        quad_loss_exact_kernel<float><<<rows, 32, 0, c->stream>>>(reinterpret_cast<const float* const*>(d_ptrs),
+                                                                 static_cast<const float*>(c->wstar), c->d, mu,
+                                                                 c->d_loss);
+      }
+    } else if (c->cfg.dtype == DSS_F64) {
       quad_loss_kernel<double><<<grid, kThreads, 0, c->stream>>>(reinterpret_cast<const double* const*>(d_ptrs),
                                                                  static_cast<const double*>(c->wstar), c->d, mu, c->d_loss);
     } else {

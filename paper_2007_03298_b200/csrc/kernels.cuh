@@ -888,6 +888,22 @@ __global__ void quad_loss_kernel(const T* const* rows, const T* wstar, long d, d
   }
 }
 
+// The same loss in the reference's exact operation order (problems.cpp:
+// 195-200: diff = w - w*, matvec(mu*I) = mu*diff, dot sequential from 0.0,
+// times 0.5): one thread per row walks i ascending.  Bit-exact with the
+// reference; meant for traces and metrics files, not for huge d.
+template <typename T>
+__global__ void quad_loss_exact_kernel(const T* const* rows, const T* wstar, long d, double mu, double* out) {
+  if (threadIdx.x != 0) return;
+  const T* w = rows[blockIdx.x];
+  double acc = 0.0;
+  for (long i = 0; i < d; ++i) {
+    const double diff = __dsub_rn(static_cast<double>(w[i]), static_cast<double>(wstar[i]));
+    acc = __dadd_rn(acc, __dmul_rn(diff, __dadd_rn(0.0, __dmul_rn(mu, diff))));
+  }
+  out[blockIdx.x] = __dmul_rn(0.5, acc);
+}
+
 template <typename T>
 __global__ void broadcast_row_kernel(T* base, long ld, int rows, const T* src) {
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;

@@ -98,7 +98,7 @@ def trajectories(R: Reference) -> tuple[dict, dict]:
     for kind, W, N in shapes:
         for opt, (alpha, wd) in hp_by_opt.items():
             hp = R.hp_array(weight_decay=wd)
-            grads, params, match, (tg, tl, ts) = R.quadratic_run(1 if kind == "ds" else 0, 0, W, N, d, mu, sigma,
+            grads, params, match, (tg, tl, ts, csv) = R.quadratic_run(1 if kind == "ds" else 0, 0, W, N, d, mu, sigma,
                                                                  delta0, pseed, rseed, T, OPTS[opt], hp, alpha,
                                                                  trace=True)
             assert match, f"replay != run_training for {kind} {W}x{N} {opt}"
@@ -110,7 +110,7 @@ def trajectories(R: Reference) -> tuple[dict, dict]:
             arrs[key + "_trace_loss"] = tl
             arrs[key + "_trace_scalars"] = ts
             meta.append({"key": key, "kind": kind, "W": W, "N": N, "opt": opt, "alpha": alpha,
-                         "weight_decay": wd, "d": d, "T": T})
+                         "weight_decay": wd, "d": d, "T": T, "metrics_csv": csv})
     wstar, w0 = R.quadratic_init(pseed, d, mu, delta0)
     arrs["quad_wstar"], arrs["quad_w0"] = wstar, w0
     return {"trajectories": meta, "quadratic": {"d": d, "mu": mu, "sigma": sigma, "delta0": delta0,

@@ -75,6 +75,28 @@ def test_trace_parity(cuda_device, golden):
                 assert tr.simulated_comm_time == ts[t][4]
 
 
+def test_metrics_csv_byte_identical(cuda_device, golden):
+    """Device run -> IterationTrace (exact-order losses) -> metrics_csv is
+    byte-identical to the reference's own metrics file for the same run
+    (metrics.cpp:37-56, determinism contract acceptance.cpp:404-440)."""
+    from paper_2007_03298_b200 import iteration_trace
+    from paper_2007_03298_b200.metrics import metrics_csv
+    meta, a = golden
+    mu = meta["quadratic"]["mu"]
+    for m in meta["trajectories"]:
+        grads = a[m["key"] + "_grads"]
+        T, W, d = grads.shape
+        traces = []
+        with engine_for(m["kind"], W, m["N"], OPTS[m["opt"]], d, m["weight_decay"], "f64") as e:
+            e.set_optimum(a["quad_wstar"])
+            e.broadcast_row(BUF_PARAMS, a["quad_w0"])
+            for t in range(T):
+                e.upload_all(BUF_GRADS, grads[t])
+                out = e.step(t, m["alpha"], check=True)
+                traces.append(iteration_trace(e, t, out, mu, exact=True))
+        assert metrics_csv(traces) == m["metrics_csv"], m["key"]
+
+
 def test_c1_logistic_bit_exact(cuda_device, golden):
     """Config C1 (4 workers, 2 groups of 2, logistic d=20, SGD, step-decay lr,
     300 iterations) on the device: bit-exact every iteration."""
