@@ -56,7 +56,9 @@ typedef enum {
   DSS_BUF_PARAMS = 0,   /* WorkerState::params            (sync.hpp:57) */
   DSS_BUF_GRADS = 1,    /* GradSample::grad                (problems.hpp:31) */
   DSS_BUF_MOMENT1 = 2,  /* OptimizerState::first_moment    (optim.hpp:31) */
-  DSS_BUF_MOMENT2 = 3   /* OptimizerState::second_moment   (optim.hpp:32) */
+  DSS_BUF_MOMENT2 = 3,  /* OptimizerState::second_moment   (optim.hpp:32) */
+  DSS_BUF_STATS = 4,    /* WorkerState::running_stats      (sync.hpp:58), rows of stats_dim */
+  DSS_BUF_STATS_OBS = 5 /* GradSample::stats_observation   (problems.hpp:32), rows of stats_dim */
 } dss_buffer;
 
 /* OptimizerHyperparams (optim.hpp:16-23); alpha is passed per step. */
@@ -104,6 +106,10 @@ typedef struct {
                            fold on a single device for parity tests.
                            2 = (several GPUs) every spanning group uses the chain fold.
                            Results are bit-identical on every path. */
+  long stats_dim;       /* running_stats per worker (0 = none).  They travel with the
+                           params (DS, sync_round) or the gradients (BSP) through the same
+                           ordered group fold, without an optimizer step
+                           (sync.cpp:203-213, 386-411). */
 } dss_config;
 
 typedef struct dss_ctx dss_ctx;
@@ -213,6 +219,12 @@ int dss_sync_round(dss_ctx* ctx, long t, int check, dss_outcome* out);
  * no averaging. */
 int dss_apply_step(dss_ctx* ctx, double alpha, int check);
 
+/* fold_running_stats (sync.cpp:193-201) for every local worker:
+ * running_stats = 0.9 * running_stats + 0.1 * stats_observation (the
+ * DSS_BUF_STATS_OBS rows).  Call it where the reference does: after the local
+ * step's gradient (DS) / before the collective (BSP), i.e. before dss_step. */
+int dss_running_stats_update(dss_ctx* ctx);
+
 /* Synthetic gradients of the isotropic quadratic (problems.cpp:134-136,173-193):
  *   g_k = mu * (w_k - w*) + (sigma / sqrt(d)) * gaussian_i(seed, kGradientNoise, k, t)
  * with the reference's SplitMix64 stream (rng.cpp:20-51), counter-addressed. */
@@ -272,8 +284,9 @@ long dss_launch_count(const dss_ctx* ctx);
 
 /* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
 /* CUDA IPC handles of this GPU's params, grads, mean-gradient, barrier-flag,
- * chain-row and chain-flag buffers: DSS_IPC_BYTES bytes written to out. */
-#define DSS_IPC_BYTES 384
+ * chain-row, chain-flag and running-stats buffers: DSS_IPC_BYTES bytes
+ * written to out. */
+#define DSS_IPC_BYTES 448
 int dss_ipc_export(dss_ctx* ctx, void* out);
 /* Map every GPU's exported handles (n_gpus * DSS_IPC_BYTES bytes, rank
  * order, own entry ignored).  Must be called on every rank before the first

@@ -492,6 +492,94 @@ int ref_logistic_run(int kind, int W, int N, int d, int M, double l2, uint64_t p
   });
 }
 
+// Tiny-MLP run (problems.cpp:436-570: running statistics = EMA of the hidden
+// pre-activations, stats_dim = hidden), DS or BSP, replayed through the
+// public API with the fold_running_stats EMA restated (sync.cpp:193-201:
+// rs = 0.9*rs + 0.1*obs), recording per t:
+//   grads [T][W][dim], obs [T][W][h], params [T][W][dim], stats [T][W][h]
+// and checked against run_training's final params and running_stats.
+int ref_mlp_run(int kind, int W, int N, int d_in, int M, int hidden, uint64_t problem_seed, uint64_t run_seed,
+                int batch, int T, int opt, const double* hp, double alpha, double* grads_out, double* obs_out,
+                double* params_out, double* stats_out, double* w0_out, int* matches, char* err, int errlen) {
+  return guarded(err, errlen, nullptr, nullptr, [&] {
+    DatasetSpec s;
+    s.kind = "tiny-mlp";
+    s.d = d_in;
+    s.M = M;
+    s.hidden = hidden;
+    s.seed = problem_seed;
+    auto problem = make_problem(s);
+    const int dim = problem->dim();
+    const int h = problem->stats_dim();
+    const SyncStrategy strat = make_strategy(kind, 0, W, N, 1);
+    RunOptions o;
+    o.iterations = T;
+    o.seed = run_seed;
+    o.batch_size = batch;
+    o.optimizer = make_opt(opt, hp, alpha);
+    o.lr = constant_lr(alpha);
+    const std::vector<Shard> shards = make_shards(problem->dataset_size(), W, run_seed);
+    std::vector<WorkerState> ws(static_cast<size_t>(W));
+    for (int k = 0; k < W; ++k) {
+      ws[static_cast<size_t>(k)].rank = k;
+      ws[static_cast<size_t>(k)].params = problem->initial_params();
+      ws[static_cast<size_t>(k)].running_stats.assign(static_cast<size_t>(h), 0.0);
+      ws[static_cast<size_t>(k)].opt = o.optimizer;
+      ws[static_cast<size_t>(k)].shard = shards[static_cast<size_t>(k)];
+    }
+    std::memcpy(w0_out, ws[0].params.data(), sizeof(double) * static_cast<size_t>(dim));
+    auto ema = [](WorkerState& x, const ParamVector& obs) {
+      for (size_t i = 0; i < x.running_stats.size(); ++i) x.running_stats[i] = 0.9 * x.running_stats[i] + 0.1 * obs[i];
+    };
+    for (int t = 0; t < T; ++t) {
+      std::vector<GradSample> smp(static_cast<size_t>(W));
+      for (int k = 0; k < W; ++k) {
+        const WorkerState& x = ws[static_cast<size_t>(k)];
+        Rng br = Rng::for_stream(run_seed, streams::kBatch, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
+        std::vector<int> b(static_cast<size_t>(batch));
+        for (auto& idx : b) idx = x.shard.indices[br.uniform_below(x.shard.indices.size())];
+        Rng noise = Rng::for_stream(run_seed, streams::kGradientNoise, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
+        smp[static_cast<size_t>(k)] = problem->stochastic_gradient(x.params, b, noise);
+        std::memcpy(grads_out + (static_cast<long>(t) * W + k) * dim, smp[static_cast<size_t>(k)].grad.data(), sizeof(double) * static_cast<size_t>(dim));
+        std::memcpy(obs_out + (static_cast<long>(t) * W + k) * h, smp[static_cast<size_t>(k)].stats_observation.data(), sizeof(double) * static_cast<size_t>(h));
+      }
+      if (kind == 1) {  // DS: local step, EMA, then params ++ stats averaged in groups
+        for (int k = 0; k < W; ++k) {
+          local_step(ws[static_cast<size_t>(k)], smp[static_cast<size_t>(k)].grad, alpha, t);
+          ema(ws[static_cast<size_t>(k)], smp[static_cast<size_t>(k)].stats_observation);
+        }
+        sync_round(ws, strat, t);
+      } else {  // BSP: EMA, one collective on grad ++ stats, then the step with the mean grad
+        std::vector<int> members(static_cast<size_t>(W));
+        std::vector<ParamVector> in(static_cast<size_t>(W));
+        for (int k = 0; k < W; ++k) {
+          ema(ws[static_cast<size_t>(k)], smp[static_cast<size_t>(k)].stats_observation);
+          members[static_cast<size_t>(k)] = k;
+          in[static_cast<size_t>(k)] = smp[static_cast<size_t>(k)].grad;
+          in[static_cast<size_t>(k)].insert(in[static_cast<size_t>(k)].end(), ws[static_cast<size_t>(k)].running_stats.begin(),
+                                            ws[static_cast<size_t>(k)].running_stats.end());
+        }
+        const AllReduceResult r = ring_allreduce_avg(members, in);
+        for (int k = 0; k < W; ++k) {
+          const ParamVector& pl = r.values[static_cast<size_t>(k)];
+          ws[static_cast<size_t>(k)].running_stats.assign(pl.begin() + dim, pl.end());
+          local_step(ws[static_cast<size_t>(k)], ParamVector(pl.begin(), pl.begin() + dim), alpha, t);
+        }
+      }
+      for (int k = 0; k < W; ++k) {
+        std::memcpy(params_out + (static_cast<long>(t) * W + k) * dim, ws[static_cast<size_t>(k)].params.data(), sizeof(double) * static_cast<size_t>(dim));
+        std::memcpy(stats_out + (static_cast<long>(t) * W + k) * h, ws[static_cast<size_t>(k)].running_stats.data(), sizeof(double) * static_cast<size_t>(h));
+      }
+    }
+    const RunResult rr = run_training(*problem, strat, o);
+    *matches = 1;
+    for (int k = 0; k < W; ++k) {
+      if (rr.final_workers[static_cast<size_t>(k)].params != ws[static_cast<size_t>(k)].params) *matches = 0;
+      if (rr.final_workers[static_cast<size_t>(k)].running_stats != ws[static_cast<size_t>(k)].running_stats) *matches = 0;
+    }
+  });
+}
+
 // ---------------------------------------------------------------------------
 // CPU baseline: the reference's own per-iteration DS / BSP work on
 // resident WorkerStates — apply_step for every worker (sync.cpp:348-362,

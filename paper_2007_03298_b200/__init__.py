@@ -30,4 +30,4 @@ from .api import (  # noqa: F401
     sync_round,
     validate,
 )
-from ._lib import BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_PARAMS  # noqa: F401
+from ._lib import BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_PARAMS, BUF_STATS, BUF_STATS_OBS  # noqa: F401

@@ -17,8 +17,8 @@ LIB_PATH = os.environ.get("DSS_LIB_VARIANT", LIB_PATH)
 
 DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
-BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2 = range(4)
-IPC_BYTES = 384
+BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_STATS, BUF_STATS_OBS = range(6)
+IPC_BYTES = 448
 KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain"]
 
 
@@ -39,7 +39,7 @@ class dss_outcome(C.Structure):
 class dss_config(C.Structure):
     _fields_ = [("strategy", dss_strategy), ("optimizer", C.c_int), ("hp", dss_hparams),
                 ("dtype", C.c_int), ("dim", C.c_long), ("device", C.c_int), ("rank", C.c_int),
-                ("n_gpus", C.c_int), ("path", C.c_int)]
+                ("n_gpus", C.c_int), ("path", C.c_int), ("stats_dim", C.c_long)]
 
 
 class dss_plan_summary(C.Structure):
@@ -77,6 +77,7 @@ SIGNATURES = {
     "dss_steps": (C.c_int, [_P, C.c_long, C.c_long, _P, C.c_int, C.POINTER(dss_outcome)]),
     "dss_sync_round": (C.c_int, [_P, C.c_long, C.c_int, C.POINTER(dss_outcome)]),
     "dss_apply_step": (C.c_int, [_P, C.c_double, C.c_int]),
+    "dss_running_stats_update": (C.c_int, [_P]),
     "dss_quadratic_gradients": (C.c_int, [_P, C.c_long, C.c_uint64, C.c_double, C.c_double]),
     "dss_quadratic_init": (C.c_int, [_P, C.c_uint64, C.c_double]),
     "dss_set_optimum": (C.c_int, [_P, _P, C.c_long]),

@@ -136,10 +136,11 @@ class SyncStrategy:  # sync.hpp:34-39
 
 
 @dataclass
-class WorkerState:  # sync.hpp:55-61 (running_stats unused by the quadratic path)
+class WorkerState:  # sync.hpp:55-61
     rank: int = 0
     params: np.ndarray = field(default_factory=lambda: np.zeros(0))
     opt: OptimizerState = field(default_factory=OptimizerState)
+    running_stats: np.ndarray = field(default_factory=lambda: np.zeros(0))
 
 
 @dataclass
@@ -271,7 +272,7 @@ class DsSyncEngine:
 
     def __init__(self, strategy: SyncStrategy, optimizer: OptimizerKind, dim: int,
                  hp: Optional[OptimizerHyperparams] = None, dtype: str = "f32", device: int = 0,
-                 rank: int = 0, n_gpus: int = 1, path: int = 0):
+                 rank: int = 0, n_gpus: int = 1, path: int = 0, stats_dim: int = 0):
         hp = hp or OptimizerHyperparams()
         self.lib = L.load()
         self.strategy = strategy
@@ -288,6 +289,8 @@ class DsSyncEngine:
         cfg.rank = rank
         cfg.n_gpus = n_gpus
         cfg.path = path
+        cfg.stats_dim = stats_dim
+        self.stats_dim = int(stats_dim)
         h = C.c_void_p()
         st = self.lib.dss_create(C.byref(cfg), C.byref(h))
         if st != L.DSS_OK:
@@ -332,16 +335,20 @@ class DsSyncEngine:
         a = self._arr(host)
         self._ck(self.lib.dss_upload(self.h, buffer, rank, a.ctypes.data, a.size))
 
+    def _len(self, buffer: int) -> int:
+        return self.stats_dim if buffer in (L.BUF_STATS, L.BUF_STATS_OBS) else self.dim
+
     def download(self, buffer: int, rank: int) -> np.ndarray:
-        out = np.empty(self.dim, dtype=self.dtype)
-        self._ck(self.lib.dss_download(self.h, buffer, rank, out.ctypes.data, self.dim))
+        n = self._len(buffer)
+        out = np.empty(n, dtype=self.dtype)
+        self._ck(self.lib.dss_download(self.h, buffer, rank, out.ctypes.data, n))
         return out
 
     def upload_all(self, buffer: int, host) -> None:
-        """host: [local_workers, dim] (pinned memory makes this asynchronous)."""
+        """host: [local_workers, row length] (pinned memory makes this asynchronous)."""
         if isinstance(host, np.ndarray):
             a = self._arr(host)
-            assert a.shape == (self.local_workers, self.dim)
+            assert a.shape == (self.local_workers, self._len(buffer))
             self._keep = a
             ptr = a.ctypes.data
         else:  # any object exposing data_ptr() (e.g. a pinned torch tensor)
@@ -350,7 +357,7 @@ class DsSyncEngine:
 
     def download_all(self, buffer: int, out=None) -> np.ndarray:
         if out is None:
-            out = np.empty((self.local_workers, self.dim), dtype=self.dtype)
+            out = np.empty((self.local_workers, self._len(buffer)), dtype=self.dtype)
         ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
         self._ck(self.lib.dss_download_all(self.h, buffer, ptr))
         return out
@@ -398,6 +405,10 @@ class DsSyncEngine:
 
     def apply_step(self, alpha: float, check: bool = True) -> None:
         self._ck(self.lib.dss_apply_step(self.h, alpha, 1 if check else 0))
+
+    def running_stats_update(self) -> None:
+        """fold_running_stats (sync.cpp:193-201) from the BUF_STATS_OBS rows."""
+        self._ck(self.lib.dss_running_stats_update(self.h))
 
     def quadratic_gradients(self, t: int, seed: int, mu: float, sigma: float) -> None:
         self._ck(self.lib.dss_quadratic_gradients(self.h, t, seed, mu, sigma))
@@ -510,22 +521,39 @@ def apply_step(state: OptimizerState, params, grad, device: int = 0) -> StepResu
 
 
 def sync_round(workers: List[WorkerState], strategy: SyncStrategy, t: int, device: int = 0) -> SyncRoundOutcome:
-    """sync_round (sync.cpp:268-282) on the GPU: averages params inside the
-    scheduled groups in place; optimizer state is never read or written."""
+    """sync_round (sync.cpp:268-282) on the GPU: params and running_stats
+    averaged inside the scheduled groups in place; optimizer state is never
+    read or written."""
     validate(strategy)
     W = strategy.world.world_size
     if len(workers) != W:
         raise ValueError("sync_round: worker count does not match world_size")  # sync.cpp:271-273
     d = len(workers[0].params)
-    for ws in workers:
-        if len(ws.params) != d:
-            raise ValueError("collective vectors must all have the same length")  # comm.cpp:67-69
-    if d == 0:
-        raise ValueError("collective vectors must be non-empty")  # comm.cpp:66
-    with DsSyncEngine(strategy, OptimizerKind.VANILLA_SGD, d, None, "f64", device) as e:
-        e.upload_all(L.BUF_PARAMS, np.stack([np.asarray(ws.params, dtype=np.float64) for ws in workers]))
+    sd = len(workers[0].running_stats)
+    for ws in workers:  # check_collective_args on the concatenated payload (comm.cpp:56-72)
+        if len(ws.params) + len(ws.running_stats) != d + sd:
+            raise ValueError("collective vectors must all have the same length")
+    if d + sd == 0:
+        raise ValueError("collective vectors must be non-empty")
+    if d == 0:  # a stats-only payload: fold it as the row
+        d, sd = sd, 0
+        rows = [np.asarray(ws.running_stats, dtype=np.float64) for ws in workers]
+        stats_only = True
+    else:
+        rows = [np.asarray(ws.params, dtype=np.float64) for ws in workers]
+        stats_only = False
+    with DsSyncEngine(strategy, OptimizerKind.VANILLA_SGD, d, None, "f64", device, stats_dim=sd) as e:
+        e.upload_all(L.BUF_PARAMS, np.stack(rows))
+        if sd:
+            e.upload_all(L.BUF_STATS, np.stack([np.asarray(ws.running_stats, dtype=np.float64) for ws in workers]))
         out = e.sync_round(t, check=True)
         res = e.download_all(L.BUF_PARAMS)
+        st = e.download_all(L.BUF_STATS) if sd else None
     for k, ws in enumerate(workers):
-        ws.params = res[k].copy()
+        if stats_only:
+            ws.running_stats = res[k].copy()
+        else:
+            ws.params = res[k].copy()
+            if sd:
+                ws.running_stats = st[k].copy()
     return out

@@ -119,6 +119,10 @@ struct dss_ctx {
   void* m1 = nullptr;
   void* m2 = nullptr;
   void* mg = nullptr;     // mean gradient row (BSP over several GPUs)
+  void* stats = nullptr;      // [P][s_pad] running statistics
+  void* stats_obs = nullptr;  // [P][s_pad] batch observations
+  long s = 0, s_pad = 0;
+  std::vector<void*> peer_stats;
   void* wstar = nullptr;  // quadratic optimum row
   unsigned long long* d_err = nullptr;
   unsigned long long* d_timeout = nullptr;
@@ -147,6 +151,7 @@ struct dss_ctx {
   ParityPlan step_plan[2];   // DS (or BSP at [0])
   ParityPlan sync_plan[2];   // sync_round (no step)
   ParityPlan mean_plan;      // ordered fold of every worker's params into mg (trace)
+  ParityPlan stats_plan[2];  // running-stats fold per parity (DS) / world group at [0] (BSP)
   double* d_loss = nullptr;  // [P + 1] loss accumulators (trace)
   GroupLaunch apply_launch;  // singleton groups of every local worker
 
@@ -536,6 +541,80 @@ ParityPlan build_mean_plan(dss_ctx* c) {
   return pp;
 }
 
+// Running statistics ride the same schedule as their payload (params for DS
+// and sync_round, the world group for BSP): local groups fold in the group
+// kernel (no step); groups spanning GPUs are tiny rows, always two-shot
+// slices over the peers' stats rows.
+ParityPlan build_stats_plan(dss_ctx* c, const Partition& part) {
+  ParityPlan pp;
+  const int G = multi(c) ? c->cfg.n_gpus : 1;
+  const int W = c->cfg.strategy.world_size;
+  std::vector<std::vector<int>> local;
+  std::vector<FoldEntry> entries;
+  std::vector<void*> src, dst;
+  long max_len = 0;
+  int uniform_m = -1;
+  for (int gi = 0; gi < part.n_groups(); ++gi) {
+    const int* mem = part.group(gi);
+    const int m = part.size(gi);
+    std::vector<int> gpus;
+    for (int j = 0; j < m; ++j) {
+      const int gpu = mem[j] / c->P;
+      if (gpus.empty() || gpus.back() != gpu) gpus.push_back(gpu);
+    }
+    if (gpus.size() > 1) pp.any_spanning = pp.any_twoshot = true;
+    const int me = multi(c) ? c->cfg.rank : 0;
+    const auto it = std::find(gpus.begin(), gpus.end(), me);
+    if (it == gpus.end()) continue;
+    if (gpus.size() == 1) {
+      local.emplace_back(mem, mem + m);
+      continue;
+    }
+    if (m > kMaxFold) throw std::invalid_argument("group spans more members than the fold kernel holds (64)");
+    long lo = 0, hi = 0;
+    slice_range(c->s_pad, static_cast<int>(gpus.size()), static_cast<int>(it - gpus.begin()), &lo, &hi);
+    if (hi <= lo) continue;
+    FoldEntry e{};
+    e.src_beg = static_cast<int>(src.size());
+    e.src_cnt = m;
+    e.dst_beg = static_cast<int>(dst.size());
+    e.dst_cnt = m;
+    e.lo = lo;
+    e.hi = hi;
+    e.err_rank = c->cfg.strategy.kind == DSS_BSP ? 0 : mem[0];
+    e.err_phase = c->cfg.strategy.kind == DSS_BSP ? 0 : 1;
+    for (int j = 0; j < m; ++j) {
+      const int gpu = mem[j] / c->P;
+      void* p = static_cast<char*>(c->peer_stats[static_cast<size_t>(gpu)]) +
+                static_cast<size_t>(mem[j] - gpu * c->P) * c->s_pad * c->esz;
+      src.push_back(p);
+      dst.push_back(p);
+    }
+    uniform_m = uniform_m < 0 ? m : (uniform_m == m ? m : 0);
+    max_len = std::max(max_len, hi - lo);
+    entries.push_back(e);
+  }
+  (void)G;
+  (void)W;
+  pp.local = make_bucketed(c, local);
+  if (!entries.empty()) {
+    pp.fold.entries = static_cast<int>(entries.size());
+    pp.fold.uniform_m = uniform_m < 0 ? 0 : uniform_m;
+    pp.fold.max_len = max_len;
+    pp.fold.d_entries = upload_table(c, entries);
+    pp.fold.d_src = upload_table(c, src);
+    pp.fold.d_dst = upload_table(c, dst);
+  }
+  pp.built = true;
+  return pp;
+}
+
+void build_stats_plans(dss_ctx* c) {
+  if (c->s == 0) return;
+  const dss_strategy& s = c->cfg.strategy;
+  for (int p = 0; p < (s.kind == DSS_DS_SYNC ? 2 : 1); ++p) c->stats_plan[p] = build_stats_plan(c, make_partition(s, p));
+}
+
 void build_plans(dss_ctx* c) {
   const dss_strategy& s = c->cfg.strategy;
   if (s.kind == DSS_DS_SYNC) {
@@ -545,6 +624,7 @@ void build_plans(dss_ctx* c) {
   }
   for (int p = 0; p < 2; ++p) c->sync_plan[p] = build_plan(c, p, false);
   if (c->cfg.strategy.world_size <= kMaxFold || multi(c)) c->mean_plan = build_mean_plan(c);
+  build_stats_plans(c);
 }
 
 // ---- launch helpers ---------------------------------------------------------
@@ -631,16 +711,16 @@ void launch_group_m(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
 // opt < 0: fold only (sync_round); otherwise the optimizer kind.
 template <typename T>
 void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha,
-                   const void* g, long g_ld, int step_phase, int sync_phase) {
+                   const void* g, long g_ld, int step_phase, int sync_phase, void* rows = nullptr, long rows_ld = 0) {
   if (gl.groups == 0) return;
   GroupArgs<T> a{};
-  a.w = static_cast<T*>(c->w);
+  a.w = static_cast<T*>(rows ? rows : c->w);  // rows: fold-only over another row set (running stats)
   a.g = static_cast<const T*>(g);
   a.m1 = static_cast<T*>(c->m1);
   a.m2 = static_cast<T*>(c->m2);
-  a.ld = c->d_pad;
+  a.ld = rows ? rows_ld : c->d_pad;
   a.g_ld = g_ld;
-  a.nvec = c->d_pad / Vec<T>::n;
+  a.nvec = a.ld / Vec<T>::n;
   a.first_rank = c->first;
   a.members = gl.d_members;
   a.offsets = gl.d_offsets;
@@ -661,11 +741,12 @@ void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double al
 }
 
 void launch_groups_any(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha,
-                       const void* g, long g_ld, int step_phase, int sync_phase = 1) {
+                       const void* g, long g_ld, int step_phase, int sync_phase = 1, void* rows = nullptr,
+                       long rows_ld = 0) {
   if (c->cfg.dtype == DSS_F64) {
-    launch_groups<double>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase);
+    launch_groups<double>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase, rows, rows_ld);
   } else {
-    launch_groups<float>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase);
+    launch_groups<float>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase, rows, rows_ld);
   }
 }
 
@@ -801,6 +882,23 @@ void quiesce(dss_ctx* c) {
   c->pending_remote = false;
 }
 
+// Fold the running statistics of iteration t (DS: the parity's groups; BSP:
+// the world).  barrier_done: a cross-GPU barrier already ordered every GPU's
+// stats update before this point in the current iteration.
+void fold_stats(dss_ctx* c, long t, bool barrier_done) {
+  if (c->s == 0) return;
+  const ParityPlan& sp = c->stats_plan[c->cfg.strategy.kind == DSS_DS_SYNC ? (t & 1) : 0];
+  const int phase = c->cfg.strategy.kind == DSS_BSP ? 0 : 1;
+  for (const GroupLaunch& gl : sp.local) {
+    launch_groups_any(c, gl, kOptNone, t, 0.0, nullptr, 0, 0, phase, c->stats, c->s_pad);
+  }
+  if (sp.any_twoshot) {
+    if (multi(c) && !barrier_done) barrier(c);
+    launch_fold_any(c, sp.fold, t);
+    c->pending_remote = multi(c);
+  }
+}
+
 void bump_steps(dss_ctx* c) {
   for (auto& s : c->step_count) ++s;
 }
@@ -840,16 +938,26 @@ int check_rank(dss_ctx* c, int rank, int* lr) {
   return DSS_OK;
 }
 
-void* buffer_base(dss_ctx* c, int buffer) {
+struct RowGeom {
+  void* base;
+  long len;  // logical row length (dim or stats_dim)
+  long ld;   // padded row stride
+};
+
+RowGeom geom(dss_ctx* c, int buffer) {
   switch (buffer) {
-    case DSS_BUF_PARAMS: return c->w;
-    case DSS_BUF_GRADS: return c->g;
+    case DSS_BUF_PARAMS: return {c->w, c->d, c->d_pad};
+    case DSS_BUF_GRADS: return {c->g, c->d, c->d_pad};
     case DSS_BUF_MOMENT1:
       if (!c->m1) throw std::invalid_argument("optimizer has no first moment buffer");
-      return c->m1;
+      return {c->m1, c->d, c->d_pad};
     case DSS_BUF_MOMENT2:
       if (!c->m2) throw std::invalid_argument("optimizer has no second moment buffer");
-      return c->m2;
+      return {c->m2, c->d, c->d_pad};
+    case DSS_BUF_STATS:
+    case DSS_BUF_STATS_OBS:
+      if (c->s == 0) throw std::invalid_argument("context has no running statistics (stats_dim = 0)");
+      return {buffer == DSS_BUF_STATS ? c->stats : c->stats_obs, c->s, c->s_pad};
     default: throw std::invalid_argument("unknown buffer id");
   }
 }
@@ -997,6 +1105,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     if (cfg->optimizer != DSS_VANILLA_SGD) c->m1 = dalloc(c.get(), rows);
     if (cfg->optimizer == DSS_ADAM || cfg->optimizer == DSS_ADAMW) c->m2 = dalloc(c.get(), rows);
     c->mg = dalloc(c.get(), static_cast<size_t>(c->d_pad) * c->esz);
+    if (cfg->stats_dim < 0) throw std::invalid_argument("stats_dim must be >= 0");
+    c->s = cfg->stats_dim;
+    c->s_pad = c->s > 0 ? pad_dim(c->s) : 0;
+    // running statistics rows (always allocated: an IPC handle needs a buffer)
+    c->stats = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(c->P) * c->s_pad * c->esz));
+    c->stats_obs = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(c->P) * c->s_pad * c->esz));
     c->wstar = dalloc(c.get(), static_cast<size_t>(c->d_pad) * c->esz);
     c->d_err = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
     ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream), "err init");
@@ -1030,6 +1144,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       c->chain_flags = static_cast<unsigned long long*>(dalloc(
           c.get(), std::max<size_t>(64, sizeof(unsigned long long) * 2 * slots * c->chain_nchunks)));
     } else {
+      c->peer_stats = {c->stats};
       build_plans(c.get());
     }
     ck(cudaStreamSynchronize(c->stream), "create sync");
@@ -1086,7 +1201,8 @@ extern "C" int dss_device_ptr(dss_ctx* c, int buffer, int rank, void** out) {
   return guard(c, [&]() -> int {
     int lr = 0;
     check_rank(c, rank, &lr);
-    *out = static_cast<char*>(buffer_base(c, buffer)) + static_cast<size_t>(lr) * c->d_pad * c->esz;
+    const RowGeom gm = geom(c, buffer);
+    *out = static_cast<char*>(gm.base) + static_cast<size_t>(lr) * gm.ld * c->esz;
     return DSS_OK;
   });
 }
@@ -1096,10 +1212,11 @@ extern "C" int dss_upload(dss_ctx* c, int buffer, int rank, const void* host, lo
   return guard(c, [&]() -> int {
     int lr = 0;
     check_rank(c, rank, &lr);
-    if (n < 0 || n > c->d) throw std::invalid_argument("upload length exceeds dim");
+    const RowGeom gm = geom(c, buffer);
+    if (n < 0 || n > gm.len) throw std::invalid_argument("upload length exceeds the row length");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
-    char* dst = static_cast<char*>(buffer_base(c, buffer)) + static_cast<size_t>(lr) * c->d_pad * c->esz;
+    char* dst = static_cast<char*>(gm.base) + static_cast<size_t>(lr) * gm.ld * c->esz;
     ck(cudaMemcpyAsync(dst, host, static_cast<size_t>(n) * c->esz, cudaMemcpyHostToDevice, c->stream),
        "upload");
     ck(cudaStreamSynchronize(c->stream), "upload sync");
@@ -1112,10 +1229,11 @@ extern "C" int dss_download(dss_ctx* c, int buffer, int rank, void* host, long n
   return guard(c, [&]() -> int {
     int lr = 0;
     check_rank(c, rank, &lr);
-    if (n < 0 || n > c->d) throw std::invalid_argument("download length exceeds dim");
+    const RowGeom gm = geom(c, buffer);
+    if (n < 0 || n > gm.len) throw std::invalid_argument("download length exceeds the row length");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
-    const char* src = static_cast<const char*>(buffer_base(c, buffer)) + static_cast<size_t>(lr) * c->d_pad * c->esz;
+    const char* src = static_cast<const char*>(gm.base) + static_cast<size_t>(lr) * gm.ld * c->esz;
     ck(cudaMemcpyAsync(host, src, static_cast<size_t>(n) * c->esz, cudaMemcpyDeviceToHost, c->stream),
        "download");
     ck(cudaStreamSynchronize(c->stream), "download sync");
@@ -1128,8 +1246,9 @@ extern "C" int dss_upload_all(dss_ctx* c, int buffer, const void* host) {
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
-    const size_t row = static_cast<size_t>(c->d) * c->esz;
-    ck(cudaMemcpy2DAsync(buffer_base(c, buffer), static_cast<size_t>(c->d_pad) * c->esz, host, row, row,
+    const RowGeom gm = geom(c, buffer);
+    const size_t row = static_cast<size_t>(gm.len) * c->esz;
+    ck(cudaMemcpy2DAsync(gm.base, static_cast<size_t>(gm.ld) * c->esz, host, row, row,
                          static_cast<size_t>(c->P), cudaMemcpyHostToDevice, c->stream),
        "upload_all");
     return DSS_OK;
@@ -1141,8 +1260,9 @@ extern "C" int dss_download_all(dss_ctx* c, int buffer, void* host) {
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
-    const size_t row = static_cast<size_t>(c->d) * c->esz;
-    ck(cudaMemcpy2DAsync(host, row, buffer_base(c, buffer), static_cast<size_t>(c->d_pad) * c->esz, row,
+    const RowGeom gm = geom(c, buffer);
+    const size_t row = static_cast<size_t>(gm.len) * c->esz;
+    ck(cudaMemcpy2DAsync(host, row, gm.base, static_cast<size_t>(gm.ld) * c->esz, row,
                          static_cast<size_t>(c->P), cudaMemcpyDeviceToHost, c->stream),
        "download_all");
     ck(cudaStreamSynchronize(c->stream), "download_all sync");
@@ -1155,10 +1275,11 @@ extern "C" int dss_broadcast_row(dss_ctx* c, int buffer, const void* host_row) {
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
-    char* base = static_cast<char*>(buffer_base(c, buffer));
-    const size_t row = static_cast<size_t>(c->d) * c->esz;
+    const RowGeom gm = geom(c, buffer);
+    char* base = static_cast<char*>(gm.base);
+    const size_t row = static_cast<size_t>(gm.len) * c->esz;
     for (int k = 0; k < c->P; ++k) {
-      ck(cudaMemcpyAsync(base + static_cast<size_t>(k) * c->d_pad * c->esz, host_row, row,
+      ck(cudaMemcpyAsync(base + static_cast<size_t>(k) * gm.ld * c->esz, host_row, row,
                          cudaMemcpyHostToDevice, c->stream),
          "broadcast_row");
     }
@@ -1215,12 +1336,14 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         if (pp.any_chain) launch_chain_any(c, pp.chain, t);
         c->pending_remote = multi(c);
       }
+      fold_stats(c, t, pp.any_twoshot);
     } else if (!multi(c)) {
       if (c->cfg.dtype == DSS_F64) {
         launch_bsp<double>(c, t, alpha);
       } else {
         launch_bsp<float>(c, t, alpha);
       }
+      fold_stats(c, t, false);
     } else {
       // BSP over GPUs: barrier (gradients final everywhere), ordered fold of
       // all W gradients into every GPU's mean-gradient row, barrier, local
@@ -1236,9 +1359,10 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
       }
       if (pp.any_chain) launch_chain_any(c, pp.chain, t);
       launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->mg, 0, 1);
+      fold_stats(c, t, true);
     }
     bump_steps(c);
-    if (out) *out = round_outcome(s, t, c->d);
+    if (out) *out = round_outcome(s, t, c->d + c->s);
     if (check) return check_impl(c);
     return DSS_OK;
   });
@@ -1274,8 +1398,28 @@ extern "C" int dss_sync_round(dss_ctx* c, long t, int check, dss_outcome* out) {
       if (pp.any_chain) launch_chain_any(c, pp.chain, t);
       c->pending_remote = multi(c);
     }
-    if (out) *out = round_outcome(s, t, c->d);
+    fold_stats(c, t, pp.any_twoshot);
+    if (out) *out = round_outcome(s, t, c->d + c->s);
     if (check) return check_impl(c);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_running_stats_update(dss_ctx* c) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (c->s == 0) return DSS_OK;  // the problem has no running statistics (sync.cpp:194)
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    const long n = static_cast<long>(c->P) * c->s_pad;
+    if (c->cfg.dtype == DSS_F64) {
+      stats_ema_kernel<double><<<grid_x(c, n, 1), kThreads, 0, c->stream>>>(static_cast<double*>(c->stats),
+                                                                          static_cast<const double*>(c->stats_obs), n);
+    } else {
+      stats_ema_kernel<float><<<grid_x(c, n, 1), kThreads, 0, c->stream>>>(static_cast<float*>(c->stats),
+                                                                         static_cast<const float*>(c->stats_obs), n);
+    }
+    ck(cudaGetLastError(), "stats_ema_kernel launch");
     return DSS_OK;
   });
 }
@@ -1555,13 +1699,14 @@ extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
     if (!multi(c)) throw std::invalid_argument("dss_ipc_export needs n_gpus > 1");
-    cudaIpcMemHandle_t h[6];
+    cudaIpcMemHandle_t h[7];
     ck(cudaIpcGetMemHandle(&h[0], c->w), "cudaIpcGetMemHandle(params)");
     ck(cudaIpcGetMemHandle(&h[1], c->g), "cudaIpcGetMemHandle(grads)");
     ck(cudaIpcGetMemHandle(&h[2], c->mg), "cudaIpcGetMemHandle(mean grad)");
     ck(cudaIpcGetMemHandle(&h[3], c->flags), "cudaIpcGetMemHandle(flags)");
     ck(cudaIpcGetMemHandle(&h[4], c->chain_buf), "cudaIpcGetMemHandle(chain rows)");
     ck(cudaIpcGetMemHandle(&h[5], c->chain_flags), "cudaIpcGetMemHandle(chain flags)");
+    ck(cudaIpcGetMemHandle(&h[6], c->stats), "cudaIpcGetMemHandle(running stats)");
     std::memcpy(out, h, sizeof(h));
     return DSS_OK;
   });
@@ -1580,6 +1725,7 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
     c->peer_flag.assign(static_cast<size_t>(G), nullptr);
     c->peer_chain_buf.assign(static_cast<size_t>(G), nullptr);
     c->peer_chain_flags.assign(static_cast<size_t>(G), nullptr);
+    c->peer_stats.assign(static_cast<size_t>(G), nullptr);
     const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
     for (int r = 0; r < G; ++r) {
       if (r == c->cfg.rank) {
@@ -1589,11 +1735,12 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
         c->peer_flag[static_cast<size_t>(r)] = c->flags;
         c->peer_chain_buf[static_cast<size_t>(r)] = c->chain_buf;
         c->peer_chain_flags[static_cast<size_t>(r)] = c->chain_flags;
+        c->peer_stats[static_cast<size_t>(r)] = c->stats;
         continue;
       }
-      void* p[6];
-      for (int b = 0; b < 6; ++b) {
-        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 6 + b], cudaIpcMemLazyEnablePeerAccess);
+      void* p[7];
+      for (int b = 0; b < 7; ++b) {
+        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 7 + b], cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
           throw PeerError("cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
         }
@@ -1605,6 +1752,7 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
       c->peer_flag[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[3]);
       c->peer_chain_buf[static_cast<size_t>(r)] = p[4];
       c->peer_chain_flags[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[5]);
+      c->peer_stats[static_cast<size_t>(r)] = p[6];
     }
     c->d_peer_flags = upload_table(c, c->peer_flag);
     build_plans(c);

@@ -904,6 +904,17 @@ __global__ void quad_loss_exact_kernel(const T* const* rows, const T* wstar, lon
   out[blockIdx.x] = __dmul_rn(0.5, acc);
 }
 
+// fold_running_stats (sync.cpp:193-201): rs = 0.9 * rs + 0.1 * obs, the
+// constants rounded once to T.
+template <typename T>
+__global__ void stats_ema_kernel(T* rs, const T* obs, long n) {
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  const T a = static_cast<T>(0.9), b = static_cast<T>(0.1);
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    rs[i] = add_(mul_(a, rs[i]), mul_(b, obs[i]));
+  }
+}
+
 template <typename T>
 __global__ void broadcast_row_kernel(T* base, long ld, int rows, const T* src) {
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;

@@ -134,6 +134,22 @@ def logistic_c1(R: Reference) -> tuple[dict, dict]:
     return {"c1": meta}, arrs
 
 
+def mlp_stats(R: Reference) -> tuple[dict, dict]:
+    """Running-statistics tail (sync.cpp:193-213): tiny-MLP (stats_dim =
+    hidden), DS W=4 N=2 and BSP W=4, Adam, as in acceptance.cpp:328-402."""
+    arrs, meta = {}, []
+    hp = R.hp_array()
+    for kind, N in (("ds", 2), ("bsp", 4)):
+        g, obs, p, st, w0, match = R.mlp_run(1 if kind == "ds" else 0, 4, N, 4, 24, 6, 71, 5, 2, 8, 2, hp, 0.01)
+        assert match, "mlp replay != run_training"
+        for name, arr in (("grads", g), ("obs", obs), ("params", p), ("stats", st)):
+            arrs[f"mlp_{kind}_{name}"] = arr
+        meta.append({"kind": kind, "W": 4, "N": N, "dim": g.shape[2], "stats_dim": obs.shape[2], "T": g.shape[0],
+                     "opt": "adam", "alpha": 0.01, "init": "tiny-mlp initial_params (seed 71)"})
+        arrs[f"mlp_{kind}_w0"] = w0
+    return {"mlp": meta}, arrs
+
+
 def sync_rounds(R: Reference) -> tuple[dict, dict]:
     rng = np.random.default_rng(19)
     arrs, meta = {}, []
@@ -178,6 +194,9 @@ def main():
     meta.update(m)
     m, a4 = sync_rounds(R)
     meta.update(m)
+    m, a6 = mlp_stats(R)
+    meta.update(m)
+    a4.update(a6)
     m, a5 = rng_vectors(R)
     meta.update(m)
     with open(os.path.join(HERE, "golden.json"), "w") as f:

@@ -17,7 +17,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle.oracle import Oracle, hparams  # noqa: E402
-from paper_2007_03298_b200 import (BUF_GRADS, BUF_MOMENT1, BUF_PARAMS, DsSyncEngine,  # noqa: E402
+from paper_2007_03298_b200 import (BUF_GRADS, BUF_MOMENT1, BUF_PARAMS, BUF_STATS, BUF_STATS_OBS,  # noqa: E402
+                                   DsSyncEngine,
                                    OptimizerHyperparams, OptimizerKind, StrategyKind, SyncStrategy, Topology,
                                    WorldConfig)
 from paper_2007_03298_b200.dist import attach, local_slice  # noqa: E402
@@ -36,7 +37,7 @@ CASES = [
 ]
 
 
-def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0):
+def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0):
     s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
                      WorldConfig(W, N), 1, rect)
     wd = 0.01 if opt in (1, 3) else 0.0
@@ -44,15 +45,27 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0):
     rng = np.random.default_rng(1000 + W + opt)
     w = rng.standard_normal((W, d)).astype(np.float32)
     mine = local_slice(W, G, rank)
-    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", rank, rank, G, path=path)
+    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", rank, rank, G, path=path, stats_dim=sd)
     attach(e)
     e.upload_all(BUF_PARAMS, w[mine.start:mine.stop])
+    rs = rng.standard_normal((W, sd)).astype(np.float32) if sd else None
+    if sd:
+        e.upload_all(BUF_STATS, rs[mine.start:mine.stop])
     m1, m2 = np.zeros_like(w), np.zeros_like(w)
     steps = np.zeros(W, np.int64)
     alpha = 0.05 if opt < 2 else 0.01
     for t in range(5):
         g = rng.standard_normal((W, d)).astype(np.float32)
         e.upload_all(BUF_GRADS, g[mine.start:mine.stop])
+        if sd:  # fold_running_stats EMA, then the stats ride the step's fold
+            obs = rng.standard_normal((W, sd)).astype(np.float32)
+            e.upload_all(BUF_STATS_OBS, obs[mine.start:mine.stop])
+            e.running_stats_update()
+            rs = (np.float32(0.9) * rs + np.float32(0.1) * obs).astype(np.float32)
+            if kind == "ds":
+                orc.sync_round(W, N, t, rs, rect=rect)
+            else:
+                orc.sync_round(W, W, t, rs, kind=0)
         e.step(t, alpha)
         if kind == "ds":
             rc = orc.ds_step(W, N, t, opt, hparams(weight_decay=wd), alpha, steps, w, g, m1, m2, rect)
@@ -64,21 +77,28 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0):
     e.sync_round(5, check=False)
     if kind == "ds":
         orc.sync_round(W, N, 5, w, rect=rect)
+        if sd:
+            orc.sync_round(W, N, 5, rs, rect=rect)
     else:
         orc.sync_round(W, W, 5, w, kind=0)
+        if sd:
+            orc.sync_round(W, W, 5, rs, kind=0)
     e.check()
     got = e.download_all(BUF_PARAMS)
     got_m1 = e.download_all(BUF_MOMENT1) if opt >= 1 else None
+    got_rs = e.download_all(BUF_STATS) if sd else None
     parts = [None] * G
-    dist.all_gather_object(parts, (got, got_m1))
+    dist.all_gather_object(parts, (got, got_m1, got_rs))
     e.close()
     if rank == 0:
         full = np.concatenate([p[0] for p in parts])
         ok = np.array_equal(full, w)
         if opt >= 1:
             ok = ok and np.array_equal(np.concatenate([p[1] for p in parts]), m1)
+        if sd:
+            ok = ok and np.array_equal(np.concatenate([p[2] for p in parts]), rs)
         diff = float(np.abs(full - w).max())
-        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d} path={path}: "
+        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d} path={path} stats={sd}: "
               f"{'OK' if ok else 'MISMATCH'} maxdiff={diff}",
               flush=True)
         return ok
@@ -97,6 +117,8 @@ def main():
             continue
         for path in (0, 2):  # auto (two-shot / chain by shape) and chain forced everywhere
             ok = run_case(*case, rank, G, orc, path) and ok
+    for case in (("ds", 8, 2, True, 2, 1001), ("bsp", 8, 8, False, 1, 777)):  # running-stats tail
+        ok = run_case(*case, rank, G, orc, 0, sd=6) and ok
     dist.barrier()
     if rank == 0:
         print("MGPU " + ("PASS" if ok else "FAIL"), flush=True)

@@ -97,6 +97,47 @@ def test_metrics_csv_byte_identical(cuda_device, golden):
         assert metrics_csv(traces) == m["metrics_csv"], m["key"]
 
 
+def test_running_stats_tail_bit_exact(cuda_device, golden):
+    """Running statistics (sync.cpp:193-213, 386-411): tiny-MLP (stats_dim =
+    hidden) under Adam, DS W=4 groups of 2 and BSP W=4, replayed on the device
+    from the reference's gradients and batch observations: the EMA update,
+    then params ++ stats through the group (DS) / world (BSP) fold.  Params
+    and running stats bit-exact after every iteration."""
+    from paper_2007_03298_b200 import BUF_STATS, BUF_STATS_OBS
+    meta, a = golden
+    for m in meta["mlp"]:
+        kind = m["kind"]
+        g, obs, p, st = (a[f"mlp_{kind}_{n}"] for n in ("grads", "obs", "params", "stats"))
+        T, W, dim = g.shape
+        s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
+                         WorldConfig(W, m["N"]))
+        with DsSyncEngine(s, OptimizerKind.ADAM, dim, OptimizerHyperparams(), "f64", 0,
+                          stats_dim=m["stats_dim"]) as e:
+            e.broadcast_row(BUF_PARAMS, a[f"mlp_{kind}_w0"])
+            for t in range(T):
+                e.upload_all(BUF_GRADS, g[t])
+                e.upload_all(BUF_STATS_OBS, obs[t])
+                e.running_stats_update()
+                e.step(t, m["alpha"], check=True)
+                assert np.array_equal(e.download_all(BUF_PARAMS), p[t]), (kind, t)
+                assert np.array_equal(e.download_all(BUF_STATS), st[t]), (kind, t)
+
+
+def test_sync_round_with_running_stats(cuda_device, oracle):
+    """sync_round averages params ++ running_stats as one payload
+    (sync.cpp:203-213): equal to the fold of the concatenated rows."""
+    rng = np.random.default_rng(4)
+    for W, N in ((4, 2), (9, 3), (16, 16)):
+        d, sd = 33, 5
+        workers = [WorkerState(k, rng.standard_normal(d), running_stats=rng.standard_normal(sd)) for k in range(W)]
+        cat = np.stack([np.concatenate([w.params, w.running_stats]) for w in workers])
+        kind = 0 if N == W else 1
+        oracle.sync_round(W, N, 1, cat, kind=kind)
+        sync_round(workers, strategy("ds" if kind else "bsp", W, N), 1)
+        got = np.stack([np.concatenate([w.params, w.running_stats]) for w in workers])
+        assert np.array_equal(got, cat)
+
+
 def test_c1_logistic_bit_exact(cuda_device, golden):
     """Config C1 (4 workers, 2 groups of 2, logistic d=20, SGD, step-decay lr,
     300 iterations) on the device: bit-exact every iteration."""
