@@ -89,6 +89,10 @@ struct ChainLaunch {
   ChainEntry* d_b = nullptr;
   void** d_src = nullptr;          // member rows
   void** d_dst = nullptr;          // mean destinations
+  int* d_src_lr = nullptr;         // local row index of each member
+  int* d_dst_lr = nullptr;         // local row index of each destination
+  int opt_mem = -1;                // fused step on the members (DS), kOptNone = fold only
+  int opt_dst = -1;                // fused step of the destinations with the mean (BSP)
 };
 
 struct ParityPlan {
@@ -281,10 +285,14 @@ unsigned long long* chain_flag(dss_ctx* c, unsigned long long* base, int region,
 // Chain-fold launch tables for this GPU's roles.  members of role i are
 // rows of `member_base` (local); its mean lands in dsts[i] (local rows).
 ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* member_base,
-                        const std::vector<std::vector<void*>>& dsts, int err_phase) {
+                        const std::vector<std::vector<void*>>& dsts, int err_phase, int opt_mem = kOptNone,
+                        int opt_dst = kOptNone, const std::vector<std::vector<int>>& dst_lrs = {}) {
   ChainLaunch cl;
+  cl.opt_mem = opt_mem;
+  cl.opt_dst = opt_dst;
   std::vector<ChainEntry> ea, eb;
   std::vector<void*> src, dst;
+  std::vector<int> src_lr, dst_lr;
   for (size_t i = 0; i < roles.size(); ++i) {
     const ChainRole& r = roles[i];
     if (r.slot >= c->chain_slots || r.next_slot >= c->chain_slots || r.mean_next_slot >= c->chain_slots) {
@@ -297,10 +305,14 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
     a.run_cnt = static_cast<int>(r.run.size());
     for (int k : r.run) {
       src.push_back(static_cast<char*>(member_base) + static_cast<size_t>(k - c->first) * c->d_pad * c->esz);
+      src_lr.push_back(k - c->first);
     }
     a.dst_beg = static_cast<int>(dst.size());
     a.dst_cnt = static_cast<int>(dsts[i].size());
     dst.insert(dst.end(), dsts[i].begin(), dsts[i].end());
+    for (size_t q = 0; q < dsts[i].size(); ++q) {
+      dst_lr.push_back(i < dst_lrs.size() && q < dst_lrs[i].size() ? dst_lrs[i][q] : 0);
+    }
     a.recv = chain_row(c, c->chain_buf, 0, r.slot);
     a.recv_flags = chain_flag(c, c->chain_flags, 0, r.slot);
     if (!a.last) {
@@ -335,6 +347,8 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
   cl.d_b = upload_table(c, eb);
   cl.d_src = upload_table(c, src);
   cl.d_dst = upload_table(c, dst);
+  cl.d_src_lr = upload_table(c, src_lr);
+  cl.d_dst_lr = upload_table(c, dst_lr);
   return cl;
 }
 
@@ -375,16 +389,30 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
     for (int gi : gp.local_groups) {
       local.emplace_back(part.group(gi), part.group(gi) + part.size(gi));
     }
-    for (int r : gp.spanning_local_members) span_members.push_back({r});
+    // Members of chain groups are stepped inside the chain's partial pass
+    // (fused step + ordered fold); only two-shot members step separately.
+    std::vector<int> chain_members;
+    for (const ChainRole& r : gp.chain) chain_members.insert(chain_members.end(), r.run.begin(), r.run.end());
+    for (int r : gp.spanning_local_members) {
+      const bool in_chain = std::find(chain_members.begin(), chain_members.end(), r) != chain_members.end();
+      if (!(with_step && in_chain)) span_members.push_back({r});
+    }
     owned = gp.owned;
     if (!gp.chain.empty()) {
       std::vector<std::vector<void*>> dsts;
+      std::vector<std::vector<int>> lrs;
       for (const ChainRole& r : gp.chain) {
         std::vector<void*> d;
-        for (int k : r.run) d.push_back(row_ptr(c, std::vector<void*>(static_cast<size_t>(G), nullptr), k, c->w));
+        std::vector<int> l;
+        for (int k : r.run) {
+          d.push_back(row_ptr(c, std::vector<void*>(static_cast<size_t>(G), nullptr), k, c->w));
+          l.push_back(k - c->first);
+        }
         dsts.push_back(d);
+        lrs.push_back(l);
       }
-      pp.chain = build_chain(c, gp.chain, c->w, dsts, s.kind == DSS_BSP ? 0 : 1);
+      pp.chain = build_chain(c, gp.chain, c->w, dsts, s.kind == DSS_BSP ? 0 : 1,
+                             with_step ? c->cfg.optimizer : kOptNone, kOptNone, lrs);
     }
   }
   if (force_fold(c)) pp.any_twoshot = pp.any_spanning;
@@ -445,9 +473,16 @@ ParityPlan build_bsp_multi_plan(dss_ctx* c) {
   for (int k = 0; k < c->P; ++k) singles.push_back({c->first + k});
   pp.spanning_step = make_group_launch(c, singles);
   if (!gp.chain.empty()) {
-    // packed BSP: ordered chain over the gradient rows, mean into this GPU's
-    // mean-gradient row (every replica then steps with it)
-    pp.chain = build_chain(c, gp.chain, c->g, {std::vector<void*>{c->mg}}, 0);
+    // packed BSP: ordered chain over the gradient rows; as each chunk of the
+    // mean gradient arrives, every local replica steps with it in place
+    // (fused fold -> step, no mean-gradient row round trip)
+    std::vector<void*> reps;
+    std::vector<int> lrs;
+    for (int k = 0; k < c->P; ++k) {
+      reps.push_back(static_cast<char*>(c->w) + static_cast<size_t>(k) * c->d_pad * c->esz);
+      lrs.push_back(k);
+    }
+    pp.chain = build_chain(c, gp.chain, c->g, {reps}, 0, kOptNone, c->cfg.optimizer, {lrs});
   }
   if (!gp.owned.empty()) {
     const Slice sl = gp.owned[0];
@@ -783,26 +818,15 @@ void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
   }
 }
 
-template <typename T>
-void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t) {
-  ++c->chain_epoch;  // same sequence on every GPU: flags compare against it
-  ChainArgs<T> a{};
-  a.src = reinterpret_cast<T* const*>(cl.d_src);
-  a.dst = reinterpret_cast<T* const*>(cl.d_dst);
-  a.chunk = c->chain_chunk;
-  a.len = c->d_pad;
-  a.n_chunks = c->chain_nchunks;
-  a.epoch = c->chain_epoch;
-  a.t = t;
-  a.err = c->d_err;
-  a.timeout = c->d_timeout;
+template <typename T, int OPTM, int OPTD>
+void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
   if (cl.na > 0) {
     a.entries = cl.d_a;
     a.n_entries = cl.na;
     const long units = c->chain_nchunks * cl.na;
     TimedLaunch tl(c, DSS_KIND_CHAIN);
-    chain_partial_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
-                              kThreads, 0, c->stream>>>(a);
+    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                                          kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
   }
   if (cl.nb > 0) {
@@ -810,17 +834,63 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t) {
     a.n_entries = cl.nb;
     const long units = c->chain_nchunks * cl.nb;
     TimedLaunch tl(c, DSS_KIND_CHAIN);
-    chain_mean_kernel<T><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
-                           kThreads, 0, c->stream>>>(a);
+    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                                 kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_mean_kernel launch");
   }
 }
 
-void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t) {
+template <typename T, int OPTM>
+void launch_chain_d(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
+  switch (cl.opt_dst) {
+    case kOptNone: launch_chain_t<T, OPTM, kOptNone>(c, cl, a); break;
+    case kSgd: launch_chain_t<T, kOptNone, kSgd>(c, cl, a); break;
+    case kMomentum: launch_chain_t<T, kOptNone, kMomentum>(c, cl, a); break;
+    case kAdam: launch_chain_t<T, kOptNone, kAdam>(c, cl, a); break;
+    case kAdamW: launch_chain_t<T, kOptNone, kAdamW>(c, cl, a); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+}
+
+template <typename T>
+void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
+  ++c->chain_epoch;  // same sequence on every GPU: flags compare against it
+  if (cl.opt_mem != kOptNone && cl.opt_dst != kOptNone) throw std::logic_error("chain: one fused step only");
+  ChainArgs<T> a{};
+  a.src = reinterpret_cast<T* const*>(cl.d_src);
+  a.dst = reinterpret_cast<T* const*>(cl.d_dst);
+  a.src_lr = cl.d_src_lr;
+  a.dst_lr = cl.d_dst_lr;
+  a.chunk = c->chain_chunk;
+  a.len = c->d_pad;
+  a.n_chunks = c->chain_nchunks;
+  a.epoch = c->chain_epoch;
+  a.t = t;
+  a.err = c->d_err;
+  a.timeout = c->d_timeout;
+  a.g = static_cast<const T*>(c->g);
+  a.m1 = static_cast<T*>(c->m1);
+  a.m2 = static_cast<T*>(c->m2);
+  a.ld = c->d_pad;
+  a.first_rank = c->first;
+  a.step_phase = c->cfg.strategy.kind == DSS_BSP ? 1 : 0;
+  a.c = consts<T>(c, alpha);
+  fill_bias(c, a);
+  switch (cl.opt_mem) {
+    case kOptNone: launch_chain_d<T, kOptNone>(c, cl, a); break;
+    case kSgd: launch_chain_t<T, kSgd, kOptNone>(c, cl, a); break;
+    case kMomentum: launch_chain_t<T, kMomentum, kOptNone>(c, cl, a); break;
+    case kAdam: launch_chain_t<T, kAdam, kOptNone>(c, cl, a); break;
+    case kAdamW: launch_chain_t<T, kAdamW, kOptNone>(c, cl, a); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+}
+
+void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha = 0.0) {
   if (c->cfg.dtype == DSS_F64) {
-    launch_chain<double>(c, cl, t);
+    launch_chain<double>(c, cl, t, alpha);
   } else {
-    launch_chain<float>(c, cl, t);
+    launch_chain<float>(c, cl, t, alpha);
   }
 }
 
@@ -1333,7 +1403,7 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
           if (multi(c)) barrier(c);
           launch_fold_any(c, pp.fold, t);
         }
-        if (pp.any_chain) launch_chain_any(c, pp.chain, t);
+        if (pp.any_chain) launch_chain_any(c, pp.chain, t, alpha);
         c->pending_remote = multi(c);
       }
       fold_stats(c, t, pp.any_twoshot);
@@ -1357,8 +1427,12 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         launch_fold_any(c, pp.fold, t);
         barrier(c);
       }
-      if (pp.any_chain) launch_chain_any(c, pp.chain, t);
-      launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->mg, 0, 1);
+      if (pp.any_chain) {
+        launch_chain_any(c, pp.chain, t, alpha);  // fold -> replica step, fused per chunk
+        c->pending_remote = true;
+      } else {
+        launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->mg, 0, 1);
+      }
       fold_stats(c, t, true);
     }
     bump_steps(c);

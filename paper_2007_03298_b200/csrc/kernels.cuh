@@ -639,6 +639,8 @@ struct ChainEntry {
 template <typename T> struct ChainArgs {
   T* const* src;      // member rows (local)
   T* const* dst;      // mean destinations (local)
+  const int* src_lr;  // local row index of each src entry (fused member step)
+  const int* dst_lr;  // local row index of each dst entry (fused BSP replica step)
   const ChainEntry* entries;
   int n_entries;
   long chunk;         // elements per chunk (multiple of 64)
@@ -648,6 +650,17 @@ template <typename T> struct ChainArgs {
   long t;
   unsigned long long* err;
   unsigned long long* timeout;
+  // fused optimizer step (DS: on the members before they are folded; BSP: on
+  // every local replica with the mean gradient as it arrives)
+  const T* g;
+  T* m1;
+  T* m2;
+  long ld;
+  int first_rank;
+  int step_phase;
+  StepConsts<T> c;
+  double bc1[kMaxLocal];
+  double bc2[kMaxLocal];
 };
 
 __device__ __forceinline__ bool chain_wait(const unsigned long long* flag, unsigned long long epoch,
@@ -665,11 +678,59 @@ __device__ __forceinline__ bool chain_wait(const unsigned long long* flag, unsig
   return true;
 }
 
+// apply_step of one local row's vector at `off` with gradient gv (in
+// registers); state read and written in place.  Returns the stepped params.
+template <typename T, int OPT>
+__device__ __forceinline__ Pack<T> chain_step(const ChainArgs<T>& a, T* wrow, int lr, long off, const Pack<T>& gv,
+                                              unsigned long long& bad, int phase) {
+  constexpr int VN = Vec<T>::n;
+  const long r = static_cast<long>(lr) * a.ld + off;
+  Pack<T> x = ldv(wrow + off);
+  Pack<T> s1, s2;
+  if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
+  if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+  const T b1 = static_cast<T>(a.bc1[lr]);
+  const T b2 = static_cast<T>(a.bc2[lr]);
+  bool ok = true;
+#pragma unroll
+  for (int l = 0; l < VN; ++l) {
+    x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
+    ok = ok && finite_(x.v[l]);
+  }
+  if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
+  if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+  if (!ok) {
+    const unsigned long long k = err_key(a.t, phase, a.first_rank + lr);
+    bad = k < bad ? k : bad;
+  }
+  return x;
+}
+
+// Deliver the mean vector of one element range on this GPU: store it to the
+// destinations (OPTD none) or step every local replica with it (BSP, OPTD).
+template <typename T, int OPTD>
+__device__ __forceinline__ void chain_deliver(const ChainArgs<T>& a, const ChainEntry& en, long off,
+                                              const Pack<T>& mean, unsigned long long& bad) {
+  for (int q = 0; q < en.dst_cnt; ++q) {
+    if constexpr (OPTD == kOptNone) {
+      stv(a.dst[en.dst_beg + q] + off, mean);
+    } else {
+      T* wrow = a.dst[en.dst_beg + q];
+      const Pack<T> x = chain_step<T, OPTD>(a, wrow, a.dst_lr[en.dst_beg + q], off, mean, bad, 1);
+      stv(wrow + off, x);
+    }
+  }
+}
+
 // Kernel A: the ordered partial pass.  Work unit = (chunk, entry), visited
 // chunk-major so every chain advances together.  A CTA only ever waits on a
 // flag written by the previous GPU's kernel A, which itself only waits on
-// GPUs before it: no cycle, no same-GPU dependency.
-template <typename T>
+// GPUs before it: no cycle, no same-GPU dependency.  OPTM != none fuses the
+// members' optimizer step into the pass (DS): the stepped params are folded
+// straight from registers and never written back -- each member row is read
+// once (w, g, state) and written once (state now, the mean later) while the
+// chunk's partial goes over NVLink.
+template <typename T, int OPTM, int OPTD>
 __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   __shared__ ChainEntry en;
@@ -694,13 +755,26 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
         Pack<T> acc;
         int j0 = 0;
         if (en.stage == 0) {
-          acc = ldv(a.src[en.run_beg] + off);
+          if constexpr (OPTM != kOptNone) {
+            const int lr = a.src_lr[en.run_beg];
+            acc = chain_step<T, OPTM>(a, a.src[en.run_beg], lr, off, ldv(a.g + static_cast<long>(lr) * a.ld + off),
+                                      bad, a.step_phase);
+          } else {
+            acc = ldv(a.src[en.run_beg] + off);
+          }
           j0 = 1;
         } else {
           acc = ldv_cg(static_cast<const T*>(en.recv) + off);
         }
         for (int j = j0; j < en.run_cnt; ++j) {
-          const Pack<T> x = ldv(a.src[en.run_beg + j] + off);
+          Pack<T> x;
+          if constexpr (OPTM != kOptNone) {
+            const int lr = a.src_lr[en.run_beg + j];
+            x = chain_step<T, OPTM>(a, a.src[en.run_beg + j], lr, off, ldv(a.g + static_cast<long>(lr) * a.ld + off),
+                                    bad, a.step_phase);
+          } else {
+            x = ldv(a.src[en.run_beg + j] + off);
+          }
 #pragma unroll
           for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
         }
@@ -717,7 +791,7 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
             const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
             bad = k < bad ? k : bad;
           }
-          for (int q = 0; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, acc);
+          chain_deliver<T, OPTD>(a, en, off, acc, bad);
           if (en.send) stv_cg(static_cast<T*>(en.send) + off, acc);
         }
       }
@@ -733,13 +807,14 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
 }
 
 // Kernel B: the mean pass g_{S-1} -> g_0 -> ... -> g_{S-2}: wait for the
-// chunk, store it to this GPU's destinations, forward it.
-template <typename T>
+// chunk, deliver it on this GPU (store, or step the replicas: BSP), forward.
+template <typename T, int OPTD>
 __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   __shared__ ChainEntry en;
   __shared__ int ok_flag;
   const long units = a.n_chunks * a.n_entries;
+  unsigned long long bad = ~0ull;
   for (long u = blockIdx.x; u < units; u += gridDim.x) {
     const long c = u / a.n_entries;
     const int ei = static_cast<int>(u % a.n_entries);
@@ -754,8 +829,8 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
       for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
         const long off = e * VN;
         const Pack<T> mean = ldv_cg(static_cast<const T*>(en.recv) + off);
-        for (int q = 0; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, mean);
         if (en.send) stv_cg(static_cast<T*>(en.send) + off, mean);
+        chain_deliver<T, OPTD>(a, en, off, mean, bad);
       }
     }
     __syncthreads();
@@ -765,6 +840,7 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
     }
     __syncthreads();
   }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
 
 // ---- synthetic gradients: SplitMix64 + Box-Muller (rng.cpp:8-51) -----------
