@@ -868,6 +868,7 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
   a.t = t;
   a.err = c->d_err;
   a.timeout = c->d_timeout;
+  a.stage = static_cast<T*>(c->mg);
   a.g = static_cast<const T*>(c->g);
   a.m1 = static_cast<T*>(c->m1);
   a.m2 = static_cast<T*>(c->m2);

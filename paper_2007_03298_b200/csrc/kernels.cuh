@@ -652,6 +652,7 @@ template <typename T> struct ChainArgs {
   unsigned long long* timeout;
   // fused optimizer step (DS: on the members before they are folded; BSP: on
   // every local replica with the mean gradient as it arrives)
+  T* stage;           // local row the mean is parked in before the replica step (BSP)
   const T* g;
   T* m1;
   T* m2;
@@ -791,8 +792,12 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
             const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
             bad = k < bad ? k : bad;
           }
-          chain_deliver<T, OPTD>(a, en, off, acc, bad);
           if (en.send) stv_cg(static_cast<T*>(en.send) + off, acc);
+          if constexpr (OPTD == kOptNone) {
+            chain_deliver<T, OPTD>(a, en, off, acc, bad);
+          } else {
+            stv(a.stage + off, acc);  // replicas step after the flag is out
+          }
         }
       }
     }
@@ -800,6 +805,16 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
     if (threadIdx.x == 0 && en.send) {
       if (DSS_CHAIN_FENCE) __threadfence_system();
       st_release_sys(en.send_flags + c, a.epoch);
+    }
+    if constexpr (OPTD != kOptNone) {
+      // the next GPU already has this chunk: now step the local replicas
+      // with it, off the inter-GPU critical path
+      if (ok_flag && en.last) {
+        for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+          const long off = e * VN;
+          chain_deliver<T, OPTD>(a, en, off, ldv(a.stage + off), bad);
+        }
+      }
     }
     __syncthreads();
   }
@@ -830,13 +845,22 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
         const long off = e * VN;
         const Pack<T> mean = ldv_cg(static_cast<const T*>(en.recv) + off);
         if (en.send) stv_cg(static_cast<T*>(en.send) + off, mean);
-        chain_deliver<T, OPTD>(a, en, off, mean, bad);
+        if constexpr (OPTD == kOptNone) chain_deliver<T, OPTD>(a, en, off, mean, bad);
       }
     }
     __syncthreads();
     if (threadIdx.x == 0 && en.send) {
       if (DSS_CHAIN_FENCE) __threadfence_system();
       st_release_sys(en.send_flags + c, a.epoch);
+    }
+    if constexpr (OPTD != kOptNone) {
+      // forwarded: now the (HBM-heavy) replica step, off the critical path
+      if (ok_flag) {
+        for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+          const long off = e * VN;
+          chain_deliver<T, OPTD>(a, en, off, ldv_cg(static_cast<const T*>(en.recv) + off), bad);
+        }
+      }
     }
     __syncthreads();
   }
