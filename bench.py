@@ -354,7 +354,7 @@ def our_arm(args, cfg):
     def make(kind):
         s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W), 1,
                          cfg["rect"] and kind == StrategyKind.DS_SYNC)
-        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, "f32", local, rank, G)
+        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, "f32", local, rank, G, path=args.path)
         e.set_stream(stream.cuda_stream)
         if G > 1:
             from paper_2007_03298_b200.dist import attach
@@ -508,6 +508,7 @@ def our_arm(args, cfg):
         "data": "synthetic: isotropic-quadratic gradients (SplitMix64/Box-Muller, seeds 7/1), device-resident",
         "config": {"workload": cfg["desc"], "W": W, "N": N, "d": d, "optimizer": OPT_NAMES[cfg["opt"]],
                    "rectangular": cfg["rect"], "workers_per_gpu": P, "parallelism": f"dp{G} (W/G workers per GPU)",
+                   "fold_path": {0: "auto", 2: "chain"}.get(args.path, args.path),
                    "l2": f"inputs larger than L2: {P * d * 4 / 1e6:.0f} MB per array per GPU"
                          if P * d * 4 > 126e6 else "inputs smaller than L2 (latency-bound config)"},
         "effective_gbs": W * d * 4 / (ds["ms"] / 1e3) / 1e9,
@@ -557,6 +558,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--d", type=int, default=None, help="override the config's d (profiling runs)")
+    ap.add_argument("--path", type=int, default=0, help="fold path: 0 auto, 2 chain for every spanning group")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -707,18 +707,62 @@ __device__ __forceinline__ Pack<T> chain_step(const ChainArgs<T>& a, T* wrow, in
   return x;
 }
 
+// Step up to 4 local rows (lr[q], params at wrow[q]) with gradients gv[q]
+// in one load phase: every row's params and state are in flight before the
+// first store (the per-row path would expose one HBM latency per row).
+template <typename T, int OPT, int B>
+__device__ __forceinline__ void chain_step_batch(const ChainArgs<T>& a, T* const* wrow, const int* lr, long off,
+                                                 const Pack<T>* gv, Pack<T>* out, unsigned long long& bad, int phase) {
+  constexpr int VN = Vec<T>::n;
+  Pack<T> x[B], s1[B], s2[B];
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const long r = static_cast<long>(lr[q]) * a.ld + off;
+    x[q] = ldv(wrow[q] + off);
+    if constexpr (OPT != kSgd) s1[q] = ldv(a.m1 + r);
+    if constexpr (OPT == kAdam || OPT == kAdamW) s2[q] = ldv(a.m2 + r);
+  }
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const long r = static_cast<long>(lr[q]) * a.ld + off;
+    const T b1 = static_cast<T>(a.bc1[lr[q]]);
+    const T b2 = static_cast<T>(a.bc2[lr[q]]);
+    bool ok = true;
+#pragma unroll
+    for (int l = 0; l < VN; ++l) {
+      x[q].v[l] = step_elem<T, OPT>(x[q].v[l], gv[q].v[l], s1[q].v[l], s2[q].v[l], a.c, b1, b2);
+      ok = ok && finite_(x[q].v[l]);
+    }
+    if constexpr (OPT != kSgd) stv(a.m1 + r, s1[q]);
+    if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2[q]);
+    if (!ok) {
+      const unsigned long long k = err_key(a.t, phase, a.first_rank + lr[q]);
+      bad = k < bad ? k : bad;
+    }
+    out[q] = x[q];
+  }
+}
+
 // Deliver the mean vector of one element range on this GPU: store it to the
-// destinations (OPTD none) or step every local replica with it (BSP, OPTD).
+// destinations (OPTD none) or step every local replica with it (BSP, OPTD),
+// replicas in batches of 4.
 template <typename T, int OPTD>
 __device__ __forceinline__ void chain_deliver(const ChainArgs<T>& a, const ChainEntry& en, long off,
                                               const Pack<T>& mean, unsigned long long& bad) {
-  for (int q = 0; q < en.dst_cnt; ++q) {
-    if constexpr (OPTD == kOptNone) {
-      stv(a.dst[en.dst_beg + q] + off, mean);
-    } else {
-      T* wrow = a.dst[en.dst_beg + q];
-      const Pack<T> x = chain_step<T, OPTD>(a, wrow, a.dst_lr[en.dst_beg + q], off, mean, bad, 1);
-      stv(wrow + off, x);
+  if constexpr (OPTD == kOptNone) {
+    for (int q = 0; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, mean);
+  } else {
+    const Pack<T> gv[4] = {mean, mean, mean, mean};
+    Pack<T> out[4];
+    int q = 0;
+    for (; q + 4 <= en.dst_cnt; q += 4) {
+      chain_step_batch<T, OPTD, 4>(a, a.dst + en.dst_beg + q, a.dst_lr + en.dst_beg + q, off, gv, out, bad, 1);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) stv(a.dst[en.dst_beg + q + b] + off, out[b]);
+    }
+    for (; q < en.dst_cnt; ++q) {
+      chain_step_batch<T, OPTD, 1>(a, a.dst + en.dst_beg + q, a.dst_lr + en.dst_beg + q, off, gv, out, bad, 1);
+      stv(a.dst[en.dst_beg + q] + off, out[0]);
     }
   }
 }
@@ -754,30 +798,48 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
       for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
         const long off = e * VN;
         Pack<T> acc;
-        int j0 = 0;
-        if (en.stage == 0) {
-          if constexpr (OPTM != kOptNone) {
-            const int lr = a.src_lr[en.run_beg];
-            acc = chain_step<T, OPTM>(a, a.src[en.run_beg], lr, off, ldv(a.g + static_cast<long>(lr) * a.ld + off),
-                                      bad, a.step_phase);
-          } else {
-            acc = ldv(a.src[en.run_beg] + off);
-          }
-          j0 = 1;
-        } else {
-          acc = ldv_cg(static_cast<const T*>(en.recv) + off);
-        }
-        for (int j = j0; j < en.run_cnt; ++j) {
-          Pack<T> x;
-          if constexpr (OPTM != kOptNone) {
-            const int lr = a.src_lr[en.run_beg + j];
-            x = chain_step<T, OPTM>(a, a.src[en.run_beg + j], lr, off, ldv(a.g + static_cast<long>(lr) * a.ld + off),
-                                    bad, a.step_phase);
-          } else {
-            x = ldv(a.src[en.run_beg + j] + off);
-          }
+        if constexpr (OPTM != kOptNone) {
+          // fused member step, members in load batches of up to 4, folded
+          // in ascending order straight from registers
+          int j = 0;
+          bool first = en.stage == 0;
+          if (!first) acc = ldv_cg(static_cast<const T*>(en.recv) + off);
+          while (j < en.run_cnt) {
+            const int nb = en.run_cnt - j >= 4 ? 4 : (en.run_cnt - j >= 2 ? 2 : 1);
+            Pack<T> gv[4], x[4];
+            const int* lrs = a.src_lr + en.run_beg + j;
+            for (int q = 0; q < nb; ++q) gv[q] = ldv(a.g + static_cast<long>(lrs[q]) * a.ld + off);
+            if (nb == 4) {
+              chain_step_batch<T, OPTM, 4>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
+            } else if (nb == 2) {
+              chain_step_batch<T, OPTM, 2>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
+            } else {
+              chain_step_batch<T, OPTM, 1>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
+            }
+            for (int q = 0; q < nb; ++q) {
+              if (first) {
+                acc = x[q];
+                first = false;
+              } else {
 #pragma unroll
-          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+                for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x[q].v[l]);
+              }
+            }
+            j += nb;
+          }
+        } else {
+          int j0 = 0;
+          if (en.stage == 0) {
+            acc = ldv(a.src[en.run_beg] + off);
+            j0 = 1;
+          } else {
+            acc = ldv_cg(static_cast<const T*>(en.recv) + off);
+          }
+          for (int j = j0; j < en.run_cnt; ++j) {
+            const Pack<T> x = ldv(a.src[en.run_beg + j] + off);
+#pragma unroll
+            for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+          }
         }
         if (!en.last) {
           stv_cg(static_cast<T*>(en.send) + off, acc);
