@@ -105,6 +105,8 @@ typedef struct {
                            two-shot kernels with virtual owners: exercises the multi-GPU
                            fold on a single device for parity tests.
                            2 = (several GPUs) every spanning group uses the chain fold.
+                           3 = (several GPUs) two-shot groups use the unfused pull fold
+                           (step, barrier, fold) instead of the fused push kernel.
                            Results are bit-identical on every path. */
   long stats_dim;       /* running_stats per worker (0 = none).  They travel with the
                            params (DS, sync_round) or the gradients (BSP) through the same
@@ -284,9 +286,9 @@ long dss_launch_count(const dss_ctx* ctx);
 
 /* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
 /* CUDA IPC handles of this GPU's params, grads, mean-gradient, barrier-flag,
- * chain-row, chain-flag and running-stats buffers: DSS_IPC_BYTES bytes
- * written to out. */
-#define DSS_IPC_BYTES 448
+ * chain-row, chain-flag, running-stats, push-staging and push-flag buffers:
+ * DSS_IPC_BYTES bytes written to out. */
+#define DSS_IPC_BYTES 576
 int dss_ipc_export(dss_ctx* ctx, void* out);
 /* Map every GPU's exported handles (n_gpus * DSS_IPC_BYTES bytes, rank
  * order, own entry ignored).  Must be called on every rank before the first

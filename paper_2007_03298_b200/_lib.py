@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("DSS_LIB_VARIANT", LIB_PATH)
 DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_STATS, BUF_STATS_OBS = range(6)
-IPC_BYTES = 448
+IPC_BYTES = 576
 KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain"]
 
 

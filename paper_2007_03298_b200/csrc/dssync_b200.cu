@@ -95,7 +95,16 @@ struct ChainLaunch {
   int opt_dst = -1;                // fused step of the destinations with the mean (BSP)
 };
 
+struct PushLaunch {
+  int items = 0, folds = 0;
+  PushItem* d_items = nullptr;
+  PushFold* d_folds = nullptr;
+  void** d_dst = nullptr;
+};
+
 struct ParityPlan {
+  PushLaunch push;                     // fused two-shot (DS step, one member per GPU)
+  bool any_push = false;               // identical on every GPU
   bool built = false;
   bool any_spanning = false;  // identical on every GPU
   bool any_twoshot = false;   // identical on every GPU
@@ -143,6 +152,12 @@ struct dss_ctx {
   unsigned long long chain_epoch = 0;
   std::vector<void*> peer_chain_buf;
   std::vector<unsigned long long*> peer_chain_flags;
+  // fused two-shot staging: each GPU's owned slices, S rows each, + flags
+  void* push_buf = nullptr;
+  unsigned long long* push_flags = nullptr;
+  std::vector<void*> peer_push_buf;
+  std::vector<unsigned long long*> peer_push_flags;
+  int push_occupancy = 0;
 
   std::vector<long> step_count;
   std::vector<void*> peer_w, peer_g, peer_mg;
@@ -273,6 +288,46 @@ void* row_ptr(dss_ctx* c, const std::vector<void*>&, int rank, void* local_base)
 }
 
 bool force_chain(const dss_ctx* c) { return c->cfg.path == 2 && multi(c); }
+bool use_push(const dss_ctx* c) { return multi(c) && c->cfg.path != 3; }  // path 3: unfused pull two-shot (A/B)
+
+// Staging layout of GPU q's owned two-shot slices at parity t: for each
+// owned slice (plan order) its group, S, [lo, hi), element offset in q's
+// staging buffer (S rows of hi-lo) and flag offset (S rows of n_chunks).
+struct OwnedSlot {
+  int group;
+  int S;
+  long lo, hi;
+  long stage_off;
+  long flag_off;
+  long nch;
+};
+std::vector<OwnedSlot> owned_layout(const dss_ctx* c, const Partition& part, int q, long chunk,
+                                    long* stage_total, long* flag_total) {
+  const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, c->cfg.n_gpus, q, c->d_pad, force_chain(c));
+  std::vector<OwnedSlot> out;
+  long so = 0, fo = 0;
+  for (const Slice& sl : gp.owned) {
+    OwnedSlot o{};
+    o.group = sl.group;
+    std::vector<int> gpus;
+    for (int j = 0; j < part.size(sl.group); ++j) {
+      const int gpu = part.group(sl.group)[j] / c->P;
+      if (gpus.empty() || gpus.back() != gpu) gpus.push_back(gpu);
+    }
+    o.S = static_cast<int>(gpus.size());
+    o.lo = sl.lo;
+    o.hi = sl.hi;
+    o.nch = (sl.hi - sl.lo + chunk - 1) / chunk;
+    o.stage_off = so;
+    o.flag_off = fo;
+    so += static_cast<long>(o.S) * (sl.hi - sl.lo);
+    fo += static_cast<long>(o.S) * o.nch;
+    out.push_back(o);
+  }
+  if (stage_total) *stage_total = so;
+  if (flag_total) *flag_total = fo;
+  return out;
+}
 
 void* chain_row(dss_ctx* c, void* base, int region, int slot) {
   return static_cast<char*>(base) +
@@ -352,6 +407,89 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
   return cl;
 }
 
+// Fused two-shot tables of parity t for this GPU (one member per GPU in
+// every two-shot group).
+PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
+  (void)t;
+  PushLaunch pl;
+  const int G = c->cfg.n_gpus;
+  const int me = c->cfg.rank;
+  const long CH = c->chain_chunk;
+  std::vector<std::vector<OwnedSlot>> lay(static_cast<size_t>(G));
+  for (int q = 0; q < G; ++q) lay[static_cast<size_t>(q)] = owned_layout(c, part, q, CH, nullptr, nullptr);
+  auto find_slot = [&](int q, int group) -> const OwnedSlot& {
+    for (const OwnedSlot& o : lay[static_cast<size_t>(q)]) {
+      if (o.group == group) return o;
+    }
+    throw std::logic_error("push: owner slot not found");
+  };
+  std::vector<PushItem> items;
+  std::vector<PushFold> folds;
+  std::vector<void*> dst;
+  const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, G, me, c->d_pad, force_chain(c));
+  for (int gi : gp.spanning_groups) {
+    bool chain = false;
+    for (const ChainRole& r : gp.chain) chain = chain || r.group == gi;
+    if (chain) continue;
+    const int* mem = part.group(gi);
+    const int m = part.size(gi);
+    std::vector<int> gpus;
+    int my_member = -1, j = -1;
+    for (int q = 0; q < m; ++q) {
+      const int gpu = mem[q] / c->P;
+      if (gpus.empty() || gpus.back() != gpu) gpus.push_back(gpu);
+      if (gpu == me) {
+        my_member = mem[q];
+        j = static_cast<int>(gpus.size()) - 1;
+      }
+    }
+    const int S = static_cast<int>(gpus.size());
+    if (S != m) throw std::logic_error("push two-shot needs one member per GPU");
+    for (int o = 0; o < S; ++o) {  // my member's chunks of every owner's slice
+      const OwnedSlot& sl = find_slot(gpus[static_cast<size_t>(o)], gi);
+      const long L = sl.hi - sl.lo;
+      char* stage = static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpus[static_cast<size_t>(o)])]) +
+                    static_cast<size_t>(sl.stage_off + static_cast<long>(j) * L) * c->esz;
+      unsigned long long* flags = c->peer_push_flags[static_cast<size_t>(gpus[static_cast<size_t>(o)])] +
+                                  sl.flag_off + static_cast<long>(j) * sl.nch;
+      for (long ch = 0; ch < sl.nch; ++ch) {
+        PushItem it{};
+        it.lr = my_member - c->first;
+        it.lo = sl.lo + ch * CH;
+        it.hi = std::min(sl.hi, it.lo + CH);
+        it.dst = stage + static_cast<size_t>(it.lo - sl.lo) * c->esz;
+        it.flag = flags + ch;
+        it.rank = my_member;
+        items.push_back(it);
+      }
+    }
+    const OwnedSlot& mine = find_slot(me, gi);  // the chunks I fold
+    const long L = mine.hi - mine.lo;
+    const int dst_beg = static_cast<int>(dst.size());
+    for (int q = 0; q < m; ++q) dst.push_back(row_ptr(c, c->peer_w, mem[q]));
+    for (long ch = 0; ch < mine.nch; ++ch) {
+      PushFold f{};
+      f.lo = mine.lo + ch * CH;
+      f.hi = std::min(mine.hi, f.lo + CH);
+      f.stage = static_cast<char*>(c->push_buf) + static_cast<size_t>(mine.stage_off + (f.lo - mine.lo)) * c->esz;
+      f.stage_ld = L;
+      f.flags = c->push_flags + mine.flag_off + ch;
+      f.flag_ld = mine.nch;
+      f.S = S;
+      f.dst_beg = dst_beg;
+      f.err_rank = mem[0];
+      folds.push_back(f);
+    }
+  }
+  // interleave phase-1 items so every CTA pushes to every owner early
+  pl.items = static_cast<int>(items.size());
+  pl.folds = static_cast<int>(folds.size());
+  pl.d_items = upload_table(c, items);
+  pl.d_folds = upload_table(c, folds);
+  pl.d_dst = upload_table(c, dst);
+  return pl;
+}
+
 // Build the launch tables of one parity.  with_step: DS iteration (local
 // steps fused); otherwise sync_round (fold only).
 ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
@@ -418,6 +556,16 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
   if (force_fold(c)) pp.any_twoshot = pp.any_spanning;
 
   pp.local = make_bucketed(c, local);
+  if (with_step && use_push(c) && pp.any_twoshot) {
+    // Fused two-shot: this GPU's two-shot members are stepped inside the
+    // push kernel; owned slices are folded there too.
+    pp.any_push = true;
+    pp.push = build_push(c, part, t);
+    std::vector<std::vector<int>> rest;  // chain members are stepped in the chain
+    (void)rest;
+    span_members.clear();
+    owned.clear();
+  }
   if (with_step) pp.spanning_step = make_group_launch(c, span_members);
 
   if (!owned.empty()) {
@@ -895,6 +1043,56 @@ void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha = 
   }
 }
 
+template <typename T, int OPT>
+void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
+  ++c->chain_epoch;  // flags compare against the shared epoch sequence
+  PushArgs<T> a{};
+  a.items = pl.d_items;
+  a.n_items = pl.items;
+  a.folds = pl.d_folds;
+  a.n_folds = pl.folds;
+  a.dst = reinterpret_cast<T* const*>(pl.d_dst);
+  a.w = static_cast<T*>(c->w);
+  a.g = static_cast<const T*>(c->g);
+  a.m1 = static_cast<T*>(c->m1);
+  a.m2 = static_cast<T*>(c->m2);
+  a.ld = c->d_pad;
+  a.first_rank = c->first;
+  a.t = t;
+  a.epoch = c->chain_epoch;
+  a.err = c->d_err;
+  a.timeout = c->d_timeout;
+  a.c = consts<T>(c, alpha);
+  fill_bias(c, a);
+  int occ = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, push_twoshot_kernel<T, OPT>, kThreads, 0), "occupancy");
+  // fully resident grid: phase-1 work can never wait behind spinning CTAs
+  const long grid = std::max(1L, std::min<long>(static_cast<long>(std::max(occ, 1)) * c->sms,
+                                                std::max(pl.items, pl.folds)));
+  TimedLaunch tl(c, DSS_KIND_FOLD);
+  push_twoshot_kernel<T, OPT><<<static_cast<int>(grid), kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "push_twoshot_kernel launch");
+}
+
+template <typename T>
+void launch_push(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
+  switch (c->cfg.optimizer) {
+    case kSgd: launch_push_t<T, kSgd>(c, pl, t, alpha); break;
+    case kMomentum: launch_push_t<T, kMomentum>(c, pl, t, alpha); break;
+    case kAdam: launch_push_t<T, kAdam>(c, pl, t, alpha); break;
+    case kAdamW: launch_push_t<T, kAdamW>(c, pl, t, alpha); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+}
+
+void launch_push_any(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
+  if (c->cfg.dtype == DSS_F64) {
+    launch_push<double>(c, pl, t, alpha);
+  } else {
+    launch_push<float>(c, pl, t, alpha);
+  }
+}
+
 template <typename T, int OPT, int WT>
 void launch_bsp_t(dss_ctx* c, const BspArgs<T>& a) {
   dim3 grid(grid_x(c, a.nvec, 1), 1);
@@ -1212,6 +1410,16 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       c->chain_chunk = std::min<long>(c->d_pad, DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
+      long ps = 0, pf = 0;  // fused two-shot staging of this GPU's owned slices, worst parity
+      for (long t = 0; t < (s.kind == DSS_DS_SYNC ? 2 : 1); ++t) {
+        long st = 0, fl = 0;
+        owned_layout(c.get(), make_partition(s, t), cfg->rank, c->chain_chunk, &st, &fl);
+        ps = std::max(ps, st);
+        pf = std::max(pf, fl);
+      }
+      c->push_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(ps) * c->esz));
+      c->push_flags = static_cast<unsigned long long*>(
+          dalloc(c.get(), std::max<size_t>(64, sizeof(unsigned long long) * static_cast<size_t>(pf))));
       c->chain_flags = static_cast<unsigned long long*>(dalloc(
           c.get(), std::max<size_t>(64, sizeof(unsigned long long) * 2 * slots * c->chain_nchunks)));
     } else {
@@ -1400,14 +1608,20 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         // Chain groups: the ordered partial/mean passes (flag-synchronised
         // per chunk, no barrier).
         launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->g, c->d_pad, 0);
-        if (pp.any_twoshot) {
+        bool barrier_done = false;
+        if (pp.any_push) {
+          launch_push_any(c, pp.push, t, alpha);  // fused step + push two-shot
+        } else if (pp.any_twoshot) {
           if (multi(c)) barrier(c);
+          barrier_done = true;
           launch_fold_any(c, pp.fold, t);
         }
         if (pp.any_chain) launch_chain_any(c, pp.chain, t, alpha);
         c->pending_remote = multi(c);
+        fold_stats(c, t, barrier_done);
+      } else {
+        fold_stats(c, t, false);
       }
-      fold_stats(c, t, pp.any_twoshot);
     } else if (!multi(c)) {
       if (c->cfg.dtype == DSS_F64) {
         launch_bsp<double>(c, t, alpha);
@@ -1774,7 +1988,7 @@ extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
     if (!multi(c)) throw std::invalid_argument("dss_ipc_export needs n_gpus > 1");
-    cudaIpcMemHandle_t h[7];
+    cudaIpcMemHandle_t h[9];
     ck(cudaIpcGetMemHandle(&h[0], c->w), "cudaIpcGetMemHandle(params)");
     ck(cudaIpcGetMemHandle(&h[1], c->g), "cudaIpcGetMemHandle(grads)");
     ck(cudaIpcGetMemHandle(&h[2], c->mg), "cudaIpcGetMemHandle(mean grad)");
@@ -1782,6 +1996,8 @@ extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
     ck(cudaIpcGetMemHandle(&h[4], c->chain_buf), "cudaIpcGetMemHandle(chain rows)");
     ck(cudaIpcGetMemHandle(&h[5], c->chain_flags), "cudaIpcGetMemHandle(chain flags)");
     ck(cudaIpcGetMemHandle(&h[6], c->stats), "cudaIpcGetMemHandle(running stats)");
+    ck(cudaIpcGetMemHandle(&h[7], c->push_buf), "cudaIpcGetMemHandle(push staging)");
+    ck(cudaIpcGetMemHandle(&h[8], c->push_flags), "cudaIpcGetMemHandle(push flags)");
     std::memcpy(out, h, sizeof(h));
     return DSS_OK;
   });
@@ -1801,6 +2017,8 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
     c->peer_chain_buf.assign(static_cast<size_t>(G), nullptr);
     c->peer_chain_flags.assign(static_cast<size_t>(G), nullptr);
     c->peer_stats.assign(static_cast<size_t>(G), nullptr);
+    c->peer_push_buf.assign(static_cast<size_t>(G), nullptr);
+    c->peer_push_flags.assign(static_cast<size_t>(G), nullptr);
     const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
     for (int r = 0; r < G; ++r) {
       if (r == c->cfg.rank) {
@@ -1811,11 +2029,13 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
         c->peer_chain_buf[static_cast<size_t>(r)] = c->chain_buf;
         c->peer_chain_flags[static_cast<size_t>(r)] = c->chain_flags;
         c->peer_stats[static_cast<size_t>(r)] = c->stats;
+        c->peer_push_buf[static_cast<size_t>(r)] = c->push_buf;
+        c->peer_push_flags[static_cast<size_t>(r)] = c->push_flags;
         continue;
       }
-      void* p[7];
-      for (int b = 0; b < 7; ++b) {
-        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 7 + b], cudaIpcMemLazyEnablePeerAccess);
+      void* p[9];
+      for (int b = 0; b < 9; ++b) {
+        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 9 + b], cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
           throw PeerError("cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
         }
@@ -1828,6 +2048,8 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
       c->peer_chain_buf[static_cast<size_t>(r)] = p[4];
       c->peer_chain_flags[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[5]);
       c->peer_stats[static_cast<size_t>(r)] = p[6];
+      c->peer_push_buf[static_cast<size_t>(r)] = p[7];
+      c->peer_push_flags[static_cast<size_t>(r)] = static_cast<unsigned long long*>(p[8]);
     }
     c->d_peer_flags = upload_table(c, c->peer_flag);
     build_plans(c);

@@ -929,6 +929,134 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
 
+// ---- fused two-shot (push) over NVLink ------------------------------------
+// For groups with one member per GPU.  One persistent kernel per iteration:
+//   phase 1  each GPU steps its member chunk by chunk and pushes the stepped
+//            chunk straight into the slice owner's staging row (row = the
+//            member's position j in the group), releasing a per-chunk flag;
+//   phase 2  the owner of each slice waits for the S flags of a chunk, folds
+//            rows 0..S-1 in ascending member order, scales, and stores the
+//            mean into every member's params row (peer stores).
+// The HBM step overlaps the NVLink push.  The grid is sized to be fully
+// resident, so every CTA finishes its phase-1 items before any CTA can spin
+// in phase 2 -- no CTA waits on work that cannot be scheduled.
+struct PushItem {        // phase 1: one chunk of my member, bound for one owner
+  int lr;                // my member's local row
+  long lo, hi;           // element range
+  void* dst;             // owner's staging row j, positioned at element lo
+  unsigned long long* flag;  // owner's flag for (slice, j, chunk)
+  int rank;              // member's global rank (error key)
+};
+struct PushFold {        // phase 2: one chunk of a slice this GPU owns
+  long lo, hi;           // element range
+  const void* stage;     // staging row 0 of the slice, positioned at lo
+  long stage_ld;         // elements between staging rows (slice length)
+  const unsigned long long* flags;  // flag of (row 0, this chunk); rows are flag_ld apart
+  long flag_ld;
+  int S;                 // rows (= members)
+  int dst_beg;           // S member param-row pointers in the dst table
+  int err_rank;          // members[0]
+};
+
+template <typename T> struct PushArgs {
+  const PushItem* items;
+  int n_items;
+  const PushFold* folds;
+  int n_folds;
+  T* const* dst;         // member param rows (local or peer)
+  T* w;
+  const T* g;
+  T* m1;
+  T* m2;
+  long ld;
+  int first_rank;
+  long t;
+  unsigned long long epoch;
+  unsigned long long* err;
+  unsigned long long* timeout;
+  StepConsts<T> c;
+  double bc1[kMaxLocal];
+  double bc2[kMaxLocal];
+};
+
+template <typename T, int OPT>
+__global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  __shared__ PushItem it;
+  __shared__ PushFold fo;
+  __shared__ int ok_flag;
+  unsigned long long bad = ~0ull;
+  // phase 1: step + push
+  for (int u = blockIdx.x; u < a.n_items; u += gridDim.x) {
+    if (threadIdx.x == 0) it = a.items[u];
+    __syncthreads();
+    const long r = static_cast<long>(it.lr) * a.ld;
+    const T b1 = static_cast<T>(a.bc1[it.lr]);
+    const T b2 = static_cast<T>(a.bc2[it.lr]);
+    for (long e = it.lo / VN + threadIdx.x; e < it.hi / VN; e += blockDim.x) {
+      const long off = e * VN;
+      Pack<T> x = ldv(a.w + r + off);
+      const Pack<T> gv = ldv(a.g + r + off);
+      Pack<T> s1, s2;
+      if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r + off);
+      if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r + off);
+      bool ok = true;
+#pragma unroll
+      for (int l = 0; l < VN; ++l) {
+        x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
+        ok = ok && finite_(x.v[l]);
+      }
+      if constexpr (OPT != kSgd) stv(a.m1 + r + off, s1);
+      if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r + off, s2);
+      if (!ok) {
+        const unsigned long long k = err_key(a.t, 0, it.rank);
+        bad = k < bad ? k : bad;
+      }
+      stv_cg(static_cast<T*>(it.dst) + (off - it.lo), x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(it.flag, a.epoch);
+    __syncthreads();
+  }
+  // phase 2: ordered fold of owned chunks
+  for (int u = blockIdx.x; u < a.n_folds; u += gridDim.x) {
+    if (threadIdx.x == 0) {
+      fo = a.folds[u];
+      ok_flag = 1;
+      for (int j = 0; j < fo.S && ok_flag; ++j) ok_flag = chain_wait(fo.flags + j * fo.flag_ld, a.epoch, a.timeout);
+    }
+    __syncthreads();
+    if (ok_flag) {
+      const T inv = static_cast<T>(1.0 / static_cast<double>(fo.S));
+      const T* st = static_cast<const T*>(fo.stage);
+      for (long e = fo.lo / VN + threadIdx.x; e < fo.hi / VN; e += blockDim.x) {
+        const long off = e * VN;
+        const long so = off - fo.lo;
+        Pack<T> acc = ldv_cg(st + so);
+        for (int j = 1; j < fo.S; ++j) {
+          const Pack<T> x = ldv_cg(st + j * fo.stage_ld + so);
+#pragma unroll
+          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+        }
+        bool ok = true;
+#pragma unroll
+        for (int l = 0; l < VN; ++l) {
+          acc.v[l] = mul_(acc.v[l], inv);
+          ok = ok && finite_(acc.v[l]);
+        }
+        if (!ok) {
+          const unsigned long long k = err_key(a.t, 1, fo.err_rank);
+          bad = k < bad ? k : bad;
+        }
+        for (int q = 0; q < fo.S; ++q) stv_cg(a.dst[fo.dst_beg + q] + off, acc);
+      }
+    }
+    __syncthreads();
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+  __threadfence_system();
+}
+
 // ---- synthetic gradients: SplitMix64 + Box-Muller (rng.cpp:8-51) -----------
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;

@@ -27,7 +27,7 @@ class FakeEngine:
         self.attached = None
 
     def ipc_export(self):
-        return bytes([self.rank]) * 448
+        return bytes([self.rank]) * 576
 
     def ipc_attach(self, handles):
         self.attached = handles
@@ -46,7 +46,7 @@ def _worker(rank, world, port, q):
 
         e = FakeEngine(rank, world)
         attach(e)
-        assert e.attached == [bytes([r]) * 448 for r in range(world)]
+        assert e.attached == [bytes([r]) * 576 for r in range(world)]
         assert list(local_slice(8 * world, world, rank)) == list(range(8 * rank, 8 * rank + 8))
 
         results = {}
