@@ -424,6 +424,7 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
     throw std::logic_error("push: owner slot not found");
   };
   std::vector<PushItem> items;
+  std::vector<std::pair<long, long>> item_keys;  // (chunk-major, owner) order key, index
   std::vector<PushFold> folds;
   std::vector<void*> dst;
   const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, G, me, c->d_pad, force_chain(c));
@@ -445,7 +446,8 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
     }
     const int S = static_cast<int>(gpus.size());
     if (S != m) throw std::logic_error("push two-shot needs one member per GPU");
-    for (int o = 0; o < S; ++o) {  // my member's chunks of every owner's slice
+    for (int oo = 0; oo < S; ++oo) {  // my member's chunks of every owner's slice
+      const int o = (oo + j) % S;       // start at a different owner on every GPU
       const OwnedSlot& sl = find_slot(gpus[static_cast<size_t>(o)], gi);
       const long L = sl.hi - sl.lo;
       char* stage = static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpus[static_cast<size_t>(o)])]) +
@@ -460,6 +462,7 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
         it.dst = stage + static_cast<size_t>(it.lo - sl.lo) * c->esz;
         it.flag = flags + ch;
         it.rank = my_member;
+        item_keys.push_back({ch * 64 + oo, static_cast<long>(items.size())});
         items.push_back(it);
       }
     }
@@ -481,7 +484,14 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
       folds.push_back(f);
     }
   }
-  // interleave phase-1 items so every CTA pushes to every owner early
+  // interleave phase-1 items chunk-major across owners (each GPU starting at
+  // a different owner) so every owner's inbound link is busy from the start
+  std::stable_sort(item_keys.begin(), item_keys.end(),
+                   [](const std::pair<long, long>& x, const std::pair<long, long>& y) { return x.first < y.first; });
+  std::vector<PushItem> ordered;
+  ordered.reserve(items.size());
+  for (const auto& k : item_keys) ordered.push_back(items[static_cast<size_t>(k.second)]);
+  items.swap(ordered);
   pl.items = static_cast<int>(items.size());
   pl.folds = static_cast<int>(folds.size());
   pl.d_items = upload_table(c, items);
