@@ -889,8 +889,39 @@ void launch_group_t(dss_ctx* c, const GroupArgs<T>& a, int groups) {
   ck(cudaGetLastError(), "ds_group_kernel launch");
 }
 
+// Shared-memory-staged variant for groups of 8 with stateful optimizers
+// (DSS_GROUP_BULK=1; default off until measured better).
+#ifndef DSS_GROUP_BULK
+#define DSS_GROUP_BULK 0
+#endif
+
+template <typename T, int OPT>
+void launch_group_bulk(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
+  constexpr int A = (OPT == kAdam || OPT == kAdamW) ? 4 : (OPT == kMomentum ? 3 : 2);
+  const size_t smem = static_cast<size_t>(kBulkStages) * 8 * A * kBulkTE * sizeof(T);
+  static bool attr_set = false;
+  if (!attr_set) {
+    ck(cudaFuncSetAttribute(ds_group_bulk_kernel<T, OPT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)),
+       "bulk smem attribute");
+    attr_set = true;
+  }
+  const int tiles = static_cast<int>((a.ld + kBulkTE - 1) / kBulkTE);
+  dim3 grid(std::max(1, std::min(tiles, (c->sms + gl.groups - 1) / gl.groups)), gl.groups);
+  TimedLaunch tl(c, DSS_KIND_GROUP);
+  ds_group_bulk_kernel<T, OPT, 8><<<grid, kThreads + 32, smem, c->stream>>>(a, c->d_timeout);
+  ck(cudaGetLastError(), "ds_group_bulk_kernel launch");
+}
+
 template <typename T, int OPT>
 void launch_group_m(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
+  if constexpr (OPT == kMomentum || OPT == kAdam || OPT == kAdamW) {
+    if (DSS_GROUP_BULK && std::is_same_v<T, float> && gl.size == 8 && a.g_ld == a.ld &&
+        a.w == static_cast<T*>(c->w)) {
+      launch_group_bulk<T, OPT>(c, a, gl);
+      return;
+    }
+  }
   switch (gl.size) {
     case 1: launch_group_t<T, OPT, 1>(c, a, gl.groups); break;
     case 2: launch_group_t<T, OPT, 2>(c, a, gl.groups); break;

@@ -341,6 +341,165 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
 
+// ---- shared-memory-staged group step (cp.async.bulk + mbarrier ring) -------
+// Same arithmetic as ds_group_kernel; for groups of 8 with stateful
+// optimizers, where holding every member's w/g/m/v in registers caps the
+// bytes in flight.  A producer warp streams each tile's member rows into a
+// ring of NS shared-memory stages with 1-D TMA bulk copies
+// (cp.async.bulk.shared::cluster.global, completion on an mbarrier); 8
+// consumer warps step + fold from shared memory and store the state and the
+// mean straight to HBM.
+#ifndef DSS_BULK_TE
+#define DSS_BULK_TE 256
+#endif
+#ifndef DSS_BULK_STAGES
+#define DSS_BULK_STAGES 4
+#endif
+constexpr int kBulkTE = DSS_BULK_TE;          // elements per tile row
+constexpr int kBulkStages = DSS_BULK_STAGES;  // ring depth
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait (~20 s): a broken pipeline latches a timeout instead of hanging
+__device__ __forceinline__ bool mbar_wait(unsigned long long* bar, unsigned parity, unsigned long long* timeout) {
+  unsigned long long start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+  while (!mbar_try_wait(bar, parity)) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - start > 20000000000ull) {
+      atomicExch(timeout, 1ull);
+      return false;
+    }
+  }
+  return true;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, int OPT, int M>
+__global__ void __launch_bounds__(kThreads + 32, 1) ds_group_bulk_kernel(const GroupArgs<T> a,
+                                                                         unsigned long long* timeout) {
+  constexpr int A = (OPT == kAdam || OPT == kAdamW) ? 4 : (OPT == kMomentum ? 3 : 2);  // w, g, m1, m2
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* stage = reinterpret_cast<T*>(smem_raw);  // [NS][M][A][TE]
+  __shared__ __align__(8) unsigned long long full[kBulkStages], empty[kBulkStages];
+  const int tiles_per_row = static_cast<int>((a.ld + kBulkTE - 1) / kBulkTE);
+  const long n_tiles = static_cast<long>(gridDim.y) * tiles_per_row;
+  const int grp = blockIdx.y;
+  const int beg = a.offsets[grp];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // tiles of this group handled by this CTA: x = blockIdx.x, blockIdx.x + gridDim.x, ...
+  const int n_mine = tiles_per_row > static_cast<int>(blockIdx.x)
+                         ? (tiles_per_row - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                         : 0;
+  (void)n_tiles;
+  if (threadIdx.x >= kThreads) {
+    // producer warp: one lane issues every bulk copy
+    if (threadIdx.x == kThreads) {
+      for (int i = 0; i < n_mine; ++i) {
+        const int s = i % kBulkStages;
+        const int r = i / kBulkStages;
+        if (r > 0 && !mbar_wait(&empty[s], static_cast<unsigned>((r - 1) & 1), timeout)) break;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const long e0 = static_cast<long>(blockIdx.x + i * gridDim.x) * kBulkTE;
+        const long len = a.ld - e0 < kBulkTE ? a.ld - e0 : kBulkTE;
+        const unsigned bytes = static_cast<unsigned>(len * sizeof(T));
+        mbar_expect_tx(&full[s], bytes * M * A);
+        T* st = stage + static_cast<long>(s) * M * A * kBulkTE;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          const long row = static_cast<long>(a.members[beg + j] - a.first_rank) * a.ld + e0;
+          bulk_g2s(st + (j * A + 0) * kBulkTE, a.w + row, bytes, &full[s]);
+          bulk_g2s(st + (j * A + 1) * kBulkTE, a.g + row, bytes, &full[s]);
+          if constexpr (A >= 3) bulk_g2s(st + (j * A + 2) * kBulkTE, a.m1 + row, bytes, &full[s]);
+          if constexpr (A >= 4) bulk_g2s(st + (j * A + 3) * kBulkTE, a.m2 + row, bytes, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  // consumers: thread x owns element e0 + x of every tile
+  const int lead = a.members[beg];
+  const T inv = static_cast<T>(1.0 / static_cast<double>(M));
+  int lr[M];
+  T b1[M], b2[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    lr[j] = a.members[beg + j] - a.first_rank;
+    b1[j] = static_cast<T>(a.bc1[lr[j]]);
+    b2[j] = static_cast<T>(a.bc2[lr[j]]);
+  }
+  unsigned long long bad = ~0ull;
+  for (int i = 0; i < n_mine; ++i) {
+    const int s = i % kBulkStages;
+    if (!mbar_wait(&full[s], static_cast<unsigned>((i / kBulkStages) & 1), timeout)) break;
+    const long e0 = static_cast<long>(blockIdx.x + i * gridDim.x) * kBulkTE;
+    const long len = a.ld - e0 < kBulkTE ? a.ld - e0 : kBulkTE;
+    const T* st = stage + static_cast<long>(s) * M * A * kBulkTE;
+    for (int x = threadIdx.x; x < len; x += kThreads) {
+      T acc = T(0);
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        T w = st[(j * A + 0) * kBulkTE + x];
+        const T gj = st[(j * A + 1) * kBulkTE + x];
+        T s1 = T(0), s2 = T(0);
+        if constexpr (A >= 3) s1 = st[(j * A + 2) * kBulkTE + x];
+        if constexpr (A >= 4) s2 = st[(j * A + 3) * kBulkTE + x];
+        w = step_elem<T, OPT>(w, gj, s1, s2, a.c, b1[j], b2[j]);
+        const long gi = static_cast<long>(lr[j]) * a.ld + e0 + x;
+        if constexpr (A >= 3) __stcs(a.m1 + gi, s1);
+        if constexpr (A >= 4) __stcs(a.m2 + gi, s2);
+        if (!finite_(w)) {
+          const unsigned long long k = err_key(a.t, a.step_phase, a.first_rank + lr[j]);
+          bad = k < bad ? k : bad;
+        }
+        acc = j == 0 ? w : add_(acc, w);
+      }
+      acc = mul_(acc, inv);
+      if (!finite_(acc)) {
+        const unsigned long long k = err_key(a.t, a.sync_phase, lead);
+        bad = k < bad ? k : bad;
+      }
+#pragma unroll
+      for (int j = 0; j < M; ++j) __stcs(a.w + static_cast<long>(lr[j]) * a.ld + e0 + x, acc);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
 // ---- fused BSP step on one GPU --------------------------------------------
 // gm = (sum_k g_k ascending) * (1/W) (sync.cpp:389-402 via mean_of order),
 // then every worker w_k' = apply_step(w_k, gm) (sync.cpp:406-421).
