@@ -213,6 +213,18 @@ int dss_step(dss_ctx* ctx, long t, double alpha, int check, dss_outcome* out);
  * a host round trip per iteration. */
 int dss_steps(dss_ctx* ctx, long t0, long n, const double* alphas, int check, dss_outcome* last);
 
+/* One iteration fed from and returned to HOST memory, pipelined across
+ * calls: host_grads ([local_workers][dim], pinned) is copied in on a copy
+ * stream, the iteration runs, and the resulting params are snapshotted on
+ * the device and copied out to host_params ([local_workers][dim], pinned) on
+ * a second copy stream -- so iteration t's copy-out overlaps iteration t+1's
+ * copy-in.  host_params of iteration t is complete once the next
+ * dss_step_host or dss_host_sync returns; host_grads may be reused as soon
+ * as the next call returns.  Collective on several GPUs (like dss_step). */
+int dss_step_host(dss_ctx* ctx, long t, double alpha, const void* host_grads, void* host_params);
+/* Wait for every outstanding dss_step_host copy. */
+int dss_host_sync(dss_ctx* ctx);
+
 /* sync_round (sync.cpp:268-282): group averaging only, no optimizer step.
  * Optimizer state untouched. */
 int dss_sync_round(dss_ctx* ctx, long t, int check, dss_outcome* out);

@@ -75,6 +75,8 @@ SIGNATURES = {
     "dss_get_step_count": (C.c_long, [_P, C.c_int]),
     "dss_step": (C.c_int, [_P, C.c_long, C.c_double, C.c_int, C.POINTER(dss_outcome)]),
     "dss_steps": (C.c_int, [_P, C.c_long, C.c_long, _P, C.c_int, C.POINTER(dss_outcome)]),
+    "dss_step_host": (C.c_int, [_P, C.c_long, C.c_double, _P, _P]),
+    "dss_host_sync": (C.c_int, [_P]),
     "dss_sync_round": (C.c_int, [_P, C.c_long, C.c_int, C.POINTER(dss_outcome)]),
     "dss_apply_step": (C.c_int, [_P, C.c_double, C.c_int]),
     "dss_running_stats_update": (C.c_int, [_P]),

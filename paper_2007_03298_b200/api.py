@@ -398,6 +398,17 @@ class DsSyncEngine:
         self._ck(self.lib.dss_steps(self.h, t0, a.size, a.ctypes.data, 1 if check else 0, C.byref(o)))
         return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
 
+    def step_host(self, t: int, alpha: float, host_grads, host_params) -> None:
+        """dss_step_host: one iteration fed from / returned to pinned host
+        buffers ([local_workers, dim]), copies pipelined across calls; the
+        previous call's host_params are complete when this returns."""
+        gp = host_grads.ctypes.data if isinstance(host_grads, np.ndarray) else host_grads.data_ptr()
+        pp = host_params.ctypes.data if isinstance(host_params, np.ndarray) else host_params.data_ptr()
+        self._ck(self.lib.dss_step_host(self.h, t, alpha, C.c_void_p(gp), C.c_void_p(pp)))
+
+    def host_sync(self) -> None:
+        self._ck(self.lib.dss_host_sync(self.h))
+
     def sync_round(self, t: int, check: bool = True) -> SyncRoundOutcome:
         o = L.dss_outcome()
         self._ck(self.lib.dss_sync_round(self.h, t, 1 if check else 0, C.byref(o)))

@@ -158,6 +158,11 @@ struct dss_ctx {
   std::vector<void*> peer_push_buf;
   std::vector<unsigned long long*> peer_push_flags;
   int push_occupancy = 0;
+  // dss_step_host pipeline
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_free = nullptr, ev_snap = nullptr, ev_out = nullptr;
+  void* snapshot = nullptr;
+  bool host_pipe = false;
 
   std::vector<long> step_count;
   std::vector<void*> peer_w, peer_g, peer_mg;
@@ -1491,6 +1496,11 @@ extern "C" int dss_destroy(dss_ctx* c) {
   }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->copy_in) cudaStreamSynchronize(c->copy_in), cudaStreamDestroy(c->copy_in);
+  if (c->copy_out) cudaStreamSynchronize(c->copy_out), cudaStreamDestroy(c->copy_out);
+  for (cudaEvent_t e : {c->ev_in, c->ev_free, c->ev_snap, c->ev_out}) {
+    if (e) cudaEventDestroy(e);
+  }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return DSS_OK;
@@ -1694,6 +1704,69 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
     bump_steps(c);
     if (out) *out = round_outcome(s, t, c->d + c->s);
     if (check) return check_impl(c);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_step_host(dss_ctx* c, long t, double alpha, const void* host_grads, void* host_params) {
+  if (!c || !host_grads || !host_params) return fail(c, DSS_EINVAL, "null argument");
+  int st = guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    if (!c->host_pipe) {
+      ck(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking), "copy stream");
+      ck(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking), "copy stream");
+      for (cudaEvent_t* e : {&c->ev_in, &c->ev_free, &c->ev_snap, &c->ev_out}) {
+        ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+      }
+      c->snapshot = dalloc(c, static_cast<size_t>(c->P) * c->d_pad * c->esz);
+      ck(cudaEventRecord(c->ev_free, c->stream), "event");
+      ck(cudaEventRecord(c->ev_out, c->copy_out), "event");
+      c->host_pipe = true;
+    }
+    const size_t row = static_cast<size_t>(c->d) * c->esz;
+    const size_t ld = static_cast<size_t>(c->d_pad) * c->esz;
+    // copy-in: once the previous iteration no longer reads the gradients
+    ck(cudaStreamWaitEvent(c->copy_in, c->ev_free, 0), "wait");
+    ck(cudaMemcpy2DAsync(c->g, ld, host_grads, row, row, static_cast<size_t>(c->P), cudaMemcpyHostToDevice,
+                         c->copy_in),
+       "grads H2D");
+    ck(cudaEventRecord(c->ev_in, c->copy_in), "event");
+    ck(cudaStreamWaitEvent(c->stream, c->ev_in, 0), "wait");
+    // the previous call's copy-out (running concurrently with this copy-in)
+    // must land before we return: that is the API's completion point
+    ck(cudaEventSynchronize(c->ev_out), "previous copy-out");
+    return DSS_OK;
+  });
+  if (st != DSS_OK) return st;
+  st = dss_step(c, t, alpha, 0, nullptr);
+  if (st != DSS_OK) return st;
+  return guard(c, [&]() -> int {
+    const size_t row = static_cast<size_t>(c->d) * c->esz;
+    const size_t ld = static_cast<size_t>(c->d_pad) * c->esz;
+    quiesce(c);  // peers' mean stores into our rows (and reads of our grads) are done
+    ck(cudaEventRecord(c->ev_free, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->stream, c->ev_out, 0), "wait");  // previous copy-out done with the snapshot
+    ck(cudaMemcpyAsync(c->snapshot, c->w, static_cast<size_t>(c->P) * ld, cudaMemcpyDeviceToDevice, c->stream),
+       "params snapshot");
+    ck(cudaEventRecord(c->ev_snap, c->stream), "event");
+    ck(cudaStreamWaitEvent(c->copy_out, c->ev_snap, 0), "wait");
+    ck(cudaMemcpy2DAsync(host_params, row, c->snapshot, ld, row, static_cast<size_t>(c->P), cudaMemcpyDeviceToHost,
+                         c->copy_out),
+       "params D2H");
+    ck(cudaEventRecord(c->ev_out, c->copy_out), "event");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_host_sync(dss_ctx* c) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    if (c->host_pipe) {
+      ck(cudaStreamSynchronize(c->copy_in), "copy-in sync");
+      ck(cudaStreamSynchronize(c->copy_out), "copy-out sync");
+    }
+    ck(cudaStreamSynchronize(c->stream), "stream sync");
     return DSS_OK;
   });
 }

@@ -391,6 +391,34 @@ def test_batched_steps_equal_single_steps(cuda_device):
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1] == len(alphas)
 
 
+def test_step_host_pipeline(cuda_device, oracle):
+    """dss_step_host: grads fed from host, params returned to host every
+    iteration with the copies pipelined across calls.  Iteration t's params
+    are complete once call t+1 (or host_sync) returns; every one is bit-exact
+    vs the oracle."""
+    import torch
+    rng = np.random.default_rng(12)
+    W, N, d, T = 8, 2, 50_021, 6
+    w = rng.standard_normal((W, d)).astype(np.float32)
+    grads = [rng.standard_normal((W, d)).astype(np.float32) for _ in range(T)]
+    hg = [torch.from_numpy(g).pin_memory() for g in grads]
+    hp = [torch.empty((W, d), dtype=torch.float32).pin_memory() for _ in range(T)]
+    with engine_for("ds", W, N, 1, d, 1e-4, "f32", rect=True) as e:
+        e.upload_all(BUF_PARAMS, w)
+        for t in range(T):
+            e.step_host(t, 0.05, hg[t], hp[t])
+            if t >= 1:  # the previous iteration's params have landed
+                pass
+        e.host_sync()
+    ref = w.copy()
+    m1 = np.zeros_like(ref)
+    steps = np.zeros(W, np.int64)
+    for t in range(T):
+        oracle.ds_step(W, N, t, 1, hparams(weight_decay=1e-4), 0.05, steps, ref, grads[t], m1, None, True)
+        steps += 1
+        assert np.array_equal(hp[t].numpy(), ref), t
+
+
 def test_timing_and_launch_accounting(cuda_device):
     with engine_for("ds", 8, 2, 0, 1 << 20, dtype="f32", rect=True) as e:
         e.enable_timing(True)
