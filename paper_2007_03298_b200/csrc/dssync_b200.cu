@@ -179,6 +179,14 @@ struct dss_ctx {
   double* d_loss = nullptr;  // [P + 1] loss accumulators (trace)
   GroupLaunch apply_launch;  // singleton groups of every local worker
 
+  // tiny-problem multi-iteration path (dss_steps)
+  int* d_small_members[2] = {nullptr, nullptr};
+  int* d_small_offsets[2] = {nullptr, nullptr};
+  int small_ngroups[2] = {0, 0};
+  double* d_small_buf = nullptr;  // [n] alphas, [n][P] bc1, [n][P] bc2
+  long small_cap = 0;
+  std::vector<double> h_small;
+
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
   std::vector<int> ev_kind;
@@ -1771,8 +1779,112 @@ extern "C" int dss_host_sync(dss_ctx* c) {
   });
 }
 
+namespace {
+
+// Worlds small enough that one CTA beats one launch per iteration.
+bool small_path(const dss_ctx* c, long n) {
+  const long bytes = static_cast<long>(c->P) * c->d_pad * c->esz;
+  return !multi(c) && c->cfg.path == 0 && c->s == 0 && n >= 2 && bytes <= 32768 && c->P <= kMaxLocal;
+}
+
+template <typename T, int OPT>
+void launch_small_t(dss_ctx* c, const SmallArgs<T>& a) {
+  TimedLaunch tl(c, c->cfg.strategy.kind == DSS_BSP ? DSS_KIND_BSP : DSS_KIND_GROUP);
+  small_steps_kernel<T, OPT><<<1, kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "small_steps_kernel launch");
+}
+
+template <typename T>
+void run_small(dss_ctx* c, long t0, long n, const double* alphas) {
+  const int P = c->P;
+  const dss_strategy& s = c->cfg.strategy;
+  if (!c->d_small_members[0]) {  // schedule tables of both parities, once
+    for (int p = 0; p < 2; ++p) {
+      const Partition part = make_partition(s, p);
+      c->d_small_members[p] = upload_table(c, part.members);
+      c->d_small_offsets[p] = upload_table(c, part.offsets);
+      c->small_ngroups[p] = part.n_groups();
+    }
+  }
+  const long need = n * (1 + 2L * P);
+  if (need > c->small_cap) {
+    c->d_small_buf = static_cast<double*>(dalloc(c, sizeof(double) * need));
+    c->small_cap = need;
+  }
+  c->h_small.resize(static_cast<size_t>(need));
+  double* ha = c->h_small.data();
+  double* h1 = ha + n;
+  double* h2 = h1 + n * P;
+  const dss_hparams& h = c->cfg.hp;
+  for (long i = 0; i < n; ++i) {
+    ha[i] = alphas[i];
+    for (int k = 0; k < P; ++k) {  // optim.cpp:76-78 per worker and iteration
+      const double tt = static_cast<double>(c->step_count[static_cast<size_t>(k)] + i + 1);
+      h1[i * P + k] = 1.0 - std::pow(h.beta1, tt);
+      h2[i * P + k] = 1.0 - std::pow(h.beta2, tt);
+    }
+  }
+  ck(cudaMemcpyAsync(c->d_small_buf, ha, sizeof(double) * need, cudaMemcpyHostToDevice, c->stream),
+     "small-path tables");
+  SmallArgs<T> a{};
+  a.w = static_cast<T*>(c->w);
+  a.g = static_cast<const T*>(c->g);
+  a.m1 = static_cast<T*>(c->m1);
+  a.m2 = static_cast<T*>(c->m2);
+  a.ld = c->d_pad;
+  a.nvec = c->d_pad / Vec<T>::n;
+  a.nw = P;
+  for (int p = 0; p < 2; ++p) {
+    a.members[p] = c->d_small_members[p];
+    a.offsets[p] = c->d_small_offsets[p];
+    a.ngroups[p] = c->small_ngroups[p];
+  }
+  a.bsp = s.kind == DSS_BSP ? 1 : 0;
+  a.t0 = t0;
+  a.n = static_cast<int>(n);
+  a.alpha = c->d_small_buf;
+  a.bc1 = c->d_small_buf + n;
+  a.bc2 = c->d_small_buf + n + n * P;
+  a.wd = h.weight_decay;
+  a.c = consts<T>(c, 0.0);
+  a.err = c->d_err;
+  switch (c->cfg.optimizer) {
+    case kSgd: launch_small_t<T, kSgd>(c, a); break;
+    case kMomentum: launch_small_t<T, kMomentum>(c, a); break;
+    case kAdam: launch_small_t<T, kAdam>(c, a); break;
+    case kAdamW: launch_small_t<T, kAdamW>(c, a); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+  // the host table buffer is reused by the next call: wait for the copy
+  ck(cudaStreamSynchronize(c->stream), "small-path sync");
+  for (auto& sc : c->step_count) sc += n;
+}
+
+}  // namespace
+
 extern "C" int dss_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
   if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
+  if (small_path(c, n)) {
+    const int st = guard(c, [&]() -> int {
+      if (t0 < 0) throw std::invalid_argument("iteration must be >= 0");
+      for (long i = 0; i < n; ++i) {
+        if (!std::isfinite(alphas[i]) || alphas[i] < 0.0) {
+          throw std::invalid_argument("learning rate at t=" + std::to_string(t0 + i) + " must be finite and >= 0");
+        }
+      }
+      ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+      if (c->cfg.dtype == DSS_F64) {
+        run_small<double>(c, t0, n, alphas);
+      } else {
+        run_small<float>(c, t0, n, alphas);
+      }
+      if (last) *last = round_outcome(c->cfg.strategy, t0 + n - 1, c->d + c->s);
+      return DSS_OK;
+    });
+    if (st != DSS_OK) return st;
+    if (check) return dss_check(c);
+    return DSS_OK;
+  }
   for (long i = 0; i < n; ++i) {
     const int st = dss_step(c, t0 + i, alphas[i], 0, last);
     if (st != DSS_OK) return st;

@@ -646,6 +646,147 @@ __global__ void __launch_bounds__(kThreads, DSS_MIN_BLOCKS) bsp_kernel(const Bsp
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
 
+// ---- many iterations of a tiny problem in one CTA ---------------------------
+// C1-sized worlds (W * d_pad of a few thousand elements) are launch-latency
+// bound: one CTA runs n consecutive DS (or BSP) iterations with a
+// __syncthreads() between them instead of a kernel launch.  The schedule of
+// both parities, per-iteration alpha (and alpha*wd) and per-worker bias
+// corrections live in device memory.  Same arithmetic as the other kernels.
+template <typename T> struct SmallArgs {
+  T* w;
+  const T* g;
+  T* m1;
+  T* m2;
+  long ld;
+  long nvec;
+  int nw;               // W (all local)
+  const int* members[2];
+  const int* offsets[2];
+  int ngroups[2];
+  int bsp;              // 1: world fold of the gradients, then every worker steps
+  long t0;
+  int n;
+  const double* alpha;  // [n]
+  const double* bc1;    // [n][nw]
+  const double* bc2;
+  double wd;
+  StepConsts<T> c;      // alpha / awd overwritten per iteration
+  unsigned long long* err;
+};
+
+template <typename T, int OPT>
+__global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  unsigned long long bad = ~0ull;
+  StepConsts<T> c = a.c;
+  for (int i = 0; i < a.n; ++i) {
+    const long t = a.t0 + i;
+    c.alpha = static_cast<T>(a.alpha[i]);
+    c.awd = static_cast<T>(a.alpha[i] * a.wd);
+    if (a.bsp) {
+      const T inv = static_cast<T>(1.0 / static_cast<double>(a.nw));
+      for (long e = threadIdx.x; e < a.nvec; e += blockDim.x) {
+        const long off = e * VN;
+        Pack<T> gm = ldv(a.g + off);
+        for (int k = 1; k < a.nw; ++k) {
+          const Pack<T> x = ldv(a.g + static_cast<long>(k) * a.ld + off);
+#pragma unroll
+          for (int l = 0; l < VN; ++l) gm.v[l] = add_(gm.v[l], x.v[l]);
+        }
+        bool okm = true;
+#pragma unroll
+        for (int l = 0; l < VN; ++l) {
+          gm.v[l] = mul_(gm.v[l], inv);
+          okm = okm && finite_(gm.v[l]);
+        }
+        if (!okm) {
+          const unsigned long long k = err_key(t, 0, 0);
+          bad = k < bad ? k : bad;
+        }
+        for (int k = 0; k < a.nw; ++k) {
+          const long r = static_cast<long>(k) * a.ld + off;
+          Pack<T> x = ldv(a.w + r);
+          Pack<T> s1, s2;
+          if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+          const T b1 = static_cast<T>(a.bc1[static_cast<long>(i) * a.nw + k]);
+          const T b2 = static_cast<T>(a.bc2[static_cast<long>(i) * a.nw + k]);
+          bool ok = true;
+#pragma unroll
+          for (int l = 0; l < VN; ++l) {
+            x.v[l] = step_elem<T, OPT>(x.v[l], gm.v[l], s1.v[l], s2.v[l], c, b1, b2);
+            ok = ok && finite_(x.v[l]);
+          }
+          stv(a.w + r, x);
+          if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
+          if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+          if (!ok) {
+            const unsigned long long kk = err_key(t, 1, k);
+            bad = kk < bad ? kk : bad;
+          }
+        }
+      }
+    } else {
+      const int p = static_cast<int>(t & 1);
+      const int* members = a.members[p];
+      const int* offsets = a.offsets[p];
+      const long units = static_cast<long>(a.ngroups[p]) * a.nvec;
+      for (long u = threadIdx.x; u < units; u += blockDim.x) {
+        const int grp = static_cast<int>(u / a.nvec);
+        const long off = (u % a.nvec) * VN;
+        const int beg = offsets[grp];
+        const int m = offsets[grp + 1] - beg;
+        Pack<T> acc;
+        for (int j = 0; j < m; ++j) {
+          const int k = members[beg + j];
+          const long r = static_cast<long>(k) * a.ld + off;
+          Pack<T> x = ldv(a.w + r);
+          const Pack<T> gv = ldv(a.g + r);
+          Pack<T> s1, s2;
+          if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+          const T b1 = static_cast<T>(a.bc1[static_cast<long>(i) * a.nw + k]);
+          const T b2 = static_cast<T>(a.bc2[static_cast<long>(i) * a.nw + k]);
+          bool ok = true;
+#pragma unroll
+          for (int l = 0; l < VN; ++l) {
+            x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], c, b1, b2);
+            ok = ok && finite_(x.v[l]);
+          }
+          if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
+          if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+          if (!ok) {
+            const unsigned long long kk = err_key(t, 0, k);
+            bad = kk < bad ? kk : bad;
+          }
+          if (j == 0) {
+            acc = x;
+          } else {
+#pragma unroll
+            for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+          }
+        }
+        if (m > 1) {
+          const T inv = static_cast<T>(1.0 / static_cast<double>(m));
+          bool ok = true;
+#pragma unroll
+          for (int l = 0; l < VN; ++l) {
+            acc.v[l] = mul_(acc.v[l], inv);
+            ok = ok && finite_(acc.v[l]);
+          }
+          if (!ok) {
+            const unsigned long long kk = err_key(t, 1, members[beg]);
+            bad = kk < bad ? kk : bad;
+          }
+        }
+        for (int j = 0; j < m; ++j) stv(a.w + static_cast<long>(members[beg + j]) * a.ld + off, acc);
+      }
+    }
+    __syncthreads();  // iteration t's rows are final before t+1 reads them
+  }
+  if (bad != ~0ull) atomicMin(a.err, bad);
+}
+
 // ---- ordered fold + broadcast over (possibly peer-mapped) rows ------------
 // Two-shot slice owner: for e in [lo, hi): acc = src_0; acc += src_j
 // ascending; acc *= 1/m; store to every dst.  src/dst are device pointers to

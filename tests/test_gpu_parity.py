@@ -391,6 +391,39 @@ def test_batched_steps_equal_single_steps(cuda_device):
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1] == len(alphas)
 
 
+@pytest.mark.parametrize("kind,W,N", [("ds", 4, 2), ("ds", 9, 3), ("bsp", 4, 4)])
+@pytest.mark.parametrize("opt", [0, 1, 2, 3])
+def test_small_world_multi_iteration_kernel(cuda_device, oracle, kind, W, N, opt):
+    """Tiny worlds (C1-sized): dss_steps runs all n iterations in one CTA
+    (one launch).  Bit-exact vs the f32 and f64 restatement iteration by
+    iteration semantics, incl. per-iteration learning rates and Adam bias
+    corrections."""
+    rng = np.random.default_rng(W * 7 + opt)
+    d = 20
+    wd = 0.01 if opt in (1, 3) else 0.0
+    for dtype, npt in (("f32", np.float32), ("f64", np.float64)):
+        w = rng.standard_normal((W, d)).astype(npt)
+        g = rng.standard_normal((W, d)).astype(npt)
+        alphas = np.array([0.05, 0.05, 0.025, 0.025, 0.0125, 0.01, 0.01], dtype=np.float64)
+        with engine_for(kind, W, N, opt, d, wd, dtype) as e:
+            e.upload_all(BUF_PARAMS, w)
+            e.upload_all(BUF_GRADS, g)
+            e.steps(3, alphas, check=True)
+            got = e.download_all(BUF_PARAMS)
+            assert e.step_count(0) == len(alphas)
+        ref = w.copy()
+        m1, m2 = np.zeros_like(ref), np.zeros_like(ref)
+        steps = np.zeros(W, np.int64)
+        for i, a_i in enumerate(alphas):
+            if kind == "ds":
+                rc = oracle.ds_step(W, N, 3 + i, opt, hparams(weight_decay=wd), float(a_i), steps, ref, g, m1, m2)
+            else:
+                rc = oracle.bsp_step(3 + i, opt, hparams(weight_decay=wd), float(a_i), steps, ref, g, m1, m2)
+            assert rc[0] == 0
+            steps += 1
+        assert np.array_equal(got, ref), (dtype, kind, opt)
+
+
 def test_step_host_pipeline(cuda_device, oracle):
     """dss_step_host: grads fed from host, params returned to host every
     iteration with the copies pipelined across calls.  Iteration t's params
