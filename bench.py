@@ -229,10 +229,19 @@ def step_bytes(cfg, G, rank, d_pad):
     bpe = BYTES_PER_ELEM[cfg["opt"]]
     P = W // G
     mine = set(range(rank * P, (rank + 1) * P))
-    out = {"ds": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0},
-           "bsp": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0}}
+    out = {"ds": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0},
+           "bsp": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0}}
     s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
     chunks = d_pad // 64
+
+    def chain_out(gpus):
+        # partial row out unless last stage; mean row out if this GPU forwards
+        # in the mean pass (last -> g0 -> ... -> g_{S-2})
+        S, j = len(gpus), gpus.index(rank)
+        partial = d * 4 if j < S - 1 else 0
+        mean = d * 4 if (j == S - 1 or j < S - 2) else 0
+        return partial + mean
+
     for p in (0, 1):
         for g in make_partition(s, p).groups:
             here = [m for m in g if m in mine]
@@ -242,12 +251,18 @@ def step_bytes(cfg, G, rank, d_pad):
             gpus = sorted({m // P for m in g})
             if len(gpus) == 1:
                 continue
+            if max(sum(1 for m in g if m // P == q) for q in gpus) >= 2:  # ordered chain
+                out["ds"]["chain_nvlink"] += 0.5 * chain_out(gpus)
+                continue
             S, j = len(gpus), gpus.index(rank)
             L = (chunks // S + (1 if j < chunks % S else 0)) * 64
             out["ds"]["fold_hbm"] += 0.5 * 2 * len(here) * L * 4
             out["ds"]["fold_nvlink"] += 0.5 * 2 * (len(g) - len(here)) * L * 4
     if G == 1:
         out["bsp"]["group"] = W * d * bpe
+    elif P >= 2:
+        out["bsp"]["chain_nvlink"] = chain_out(list(range(G)))
+        out["bsp"]["group"] = P * d * bpe
     else:
         L = (chunks // G + (1 if rank < chunks % G else 0)) * 64
         out["bsp"]["fold_hbm"] = (P + 1) * L * 4
@@ -480,11 +495,18 @@ def our_arm(args, cfg):
                 row.update(alg_bytes_per_step=nb_bytes[key]["fold_hbm"] + nb_bytes[key]["fold_nvlink"],
                            nvlink_bytes_per_step=nb_bytes[key]["fold_nvlink"],
                            nvlink_gbs=nb_bytes[key]["fold_nvlink"] / (ms_ / 1e3) / 1e9 if ms_ else None)
+            elif k == "chain":
+                # rank-0 outbound NVLink bytes of its chain roles (per-direction link load)
+                row.update(nvlink_bytes_per_step=nb_bytes[key]["chain_nvlink"],
+                           nvlink_gbs=nb_bytes[key]["chain_nvlink"] / (ms_ / 1e3) / 1e9 if ms_ else None)
             rows[k] = row
         return rows
 
     ds_k = kernel_rows(ds, "ds")
-    dom = max(ds_k.items(), key=lambda kv: kv[1]["ms_per_step"])
+    # HBM roofline: the HBM-bound kernel with the most time (at N > 1 the
+    # cross-GPU fold kernels are reported against NVLink in "nvlink")
+    hbm_k = {k: v for k, v in ds_k.items() if v.get("alg_bytes_per_step") and k in ("group", "bsp")} or ds_k
+    dom = max(hbm_k.items(), key=lambda kv: kv[1]["ms_per_step"])
     # dominant kernel: its algorithmic bytes per launch / its mean launch time
     dk, dv = dom
     per_launch_ms = dv["ms_per_step"] / dv["launches_per_step"]
@@ -527,7 +549,8 @@ def our_arm(args, cfg):
                      "kernel": {"group": "ds_group_kernel (fused apply_step + ordered fold + broadcast)",
                                 "fold": "fold_kernel (two-shot ordered fold over NVLink peers)",
                                 "bsp": "bsp_kernel", "barrier": "barrier_kernel"}.get(dk, dk),
-                     "avg_launch_ms": per_launch_ms, "alg_bytes_per_launch": per_launch_bytes},
+                     "avg_launch_ms": per_launch_ms, "alg_bytes_per_launch": per_launch_bytes,
+                     "share_of_step": dv["ms_per_step"] / ds["ms"] if ds["ms"] else None},
         "gpu_launches": int(round(ds["launches_per_step"] * args.steps)),
         "clocks": res.get("clocks"),
         "e2e": {"value": 1000.0 / res["e2e_ms"], "unit": "iters/s", "h2d_bytes_per_step": P * d * 4 * G,
@@ -536,11 +559,15 @@ def our_arm(args, cfg):
                         "copy streams, D2H of step t overlapping H2D of step t+1)" if P * d * 4 <= 2e9 else
                         "C-ABI dss_upload/dss_step/dss_download per row through one pinned staging row"},
     }
-    if "fold" in ds_k and ds_k["fold"].get("nvlink_gbs"):
-        out["nvlink"] = {"achieved": ds_k["fold"]["nvlink_gbs"], "peak": 770.0, "unit": "GB/s",
-                         "frac": ds_k["fold"]["nvlink_gbs"] / 770.0,
-                         "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
-                         "note": "rank-0 fold kernel: remote reads + remote writes per owned slice / kernel time"}
+    for kk, note in (("fold", "rank-0 two-shot kernel: remote reads + remote writes per owned slice (= per-direction "
+                               "link bytes in a symmetric fold) / kernel time"),
+                     ("chain", "rank-0 chain kernels: outbound partial + mean rows of its chain roles / kernel time "
+                               "(includes the fused optimizer step)")):
+        if kk in ds_k and ds_k[kk].get("nvlink_gbs"):
+            out.setdefault("nvlink", {"achieved": ds_k[kk]["nvlink_gbs"], "peak": 770.0, "unit": "GB/s",
+                                      "frac": ds_k[kk]["nvlink_gbs"] / 770.0, "kernel": kk,
+                                      "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
+                                      "note": note})
     if G > 1 and "nccl_ds" in res:
         out["nccl_baselines"] = {
             "ds_split_allreduce": {"iters_s": 1000.0 / res["nccl_ds"], "ms_per_step": res["nccl_ds"]},
