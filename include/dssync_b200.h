@@ -50,6 +50,7 @@ typedef enum { DSS_VANILLA_SGD = 0, DSS_SGD_MOMENTUM = 1, DSS_ADAM = 2, DSS_ADAM
 typedef enum { DSS_BSP = 0, DSS_DS_SYNC = 1 } dss_strategy_kind;  /* sync.hpp:14 */
 typedef enum { DSS_RING = 0, DSS_TREE = 1, DSS_PS = 2 } dss_topology; /* sync.hpp:15 */
 typedef enum { DSS_F32 = 0, DSS_F64 = 1 } dss_dtype;
+typedef enum { DSS_SAMPLING_REPLACEMENT = 0, DSS_SAMPLING_EPOCH = 1 } dss_sampling; /* sync.hpp SamplingMode */
 
 /* Worker-major device buffers, [local_workers][d_pad]. */
 typedef enum {
@@ -264,6 +265,36 @@ int dss_global_mean(dss_ctx* ctx, void* host_mean);
  * losses: local_workers doubles.  suboptimality (optional) = full_loss of the
  * row written by the last dss_global_mean (true_suboptimality, sync.cpp:585). */
 int dss_quadratic_losses(dss_ctx* ctx, double mu, int exact, double* losses, double* suboptimality);
+
+/* ---- logistic regression on the device (config C1 end to end) ----------- */
+/* LogisticProblem's synthetic dataset (problems.cpp:230-250), host, bit-exact:
+ * x: M*d doubles (row-major), y: M labels in {-1, +1}. */
+int dss_logistic_dataset(uint64_t seed, int d, int M, double* x, double* y);
+/* make_shards (problems.cpp:642-662), host, bit-exact: worker w owns
+ * indices[offsets[w] .. offsets[w+1]) (indices: M ints, offsets: workers+1). */
+int dss_make_shards(int dataset_size, int workers, uint64_t seed, int* indices, int* offsets);
+/* epoch_order (problems.cpp:664-674), host, bit-exact: out = size ints. */
+int dss_epoch_order(const int* shard, int size, uint64_t seed, int rank, long epoch, int* out);
+/* Upload the dataset (x: M*dim doubles, y: M) and shard it over the world
+ * with make_shards(M, world_size, run_seed) (sync.cpp:300); each iteration
+ * then samples batch_size examples per worker on the device (sample_batch,
+ * sync.cpp:153-179, DSS_SAMPLING_*) with the run seed's streams. */
+int dss_logistic_setup(dss_ctx* ctx, const double* x, const double* y, int M, double l2, int batch_size,
+                       int sampling, uint64_t run_seed);
+/* Gradient rows of every local worker at iteration t: checked_gradient +
+ * LogisticProblem::stochastic_gradient (sync.cpp:181-191, problems.cpp:265-290),
+ * computed in fp64 from the worker's params and stored in the context dtype.
+ * Batch indices are bit-exact; the gradient is within libdevice-vs-glibc exp
+ * rounding of the reference.  A non-finite gradient or batch loss latches
+ * DivergenceError(rank, t, "non-finite stochastic gradient") (see dss_check). */
+int dss_logistic_gradients(dss_ctx* ctx, long t);
+/* n iterations of (dss_logistic_gradients(t), dss_step(t, alphas[i])). */
+int dss_logistic_steps(dss_ctx* ctx, long t0, long n, const double* alphas, int check, dss_outcome* last);
+/* Indices sampled by the last dss_logistic_gradients: [local_workers][batch]. */
+int dss_logistic_batch(dss_ctx* ctx, int* out);
+/* LogisticProblem::full_loss (problems.cpp:292-305) of every local worker:
+ * exact = 1 in the reference's order (one thread per row), 0 parallel. */
+int dss_logistic_losses(dss_ctx* ctx, int exact, double* losses);
 
 /* Latched divergence check (synchronizes).  DSS_OK or DSS_EDIVERGED. */
 int dss_check(dss_ctx* ctx);

@@ -176,7 +176,10 @@ class Reference:
         L.ref_format_doubles.argtypes = [_P, C.c_long, C.c_char_p, C.c_long]
         L.ref_logistic_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                        C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double, C.c_double,
-                                       C.c_long, _P, _P, _P, C.POINTER(C.c_int)] + E
+                                       C.c_long, C.c_int, _P, _P, _P, _P, C.POINTER(C.c_int)] + E
+        L.ref_logistic_yx.argtypes = [C.c_uint64, C.c_int, C.c_int, _P] + E
+        L.ref_make_shards.argtypes = [C.c_int, C.c_int, C.c_uint64, _P, _P] + E
+        L.ref_epoch_order.argtypes = [_P, C.c_int, C.c_uint64, C.c_int, C.c_long, _P]
         L.ref_mlp_run.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double,
                                                   _P, _P, _P, _P, _P, C.POINTER(C.c_int)] + E
         L.ref_bench_create.restype = _P
@@ -283,14 +286,37 @@ class Reference:
             raise RuntimeError(self.error())
         return g, obs, p, st, w0, bool(match.value)
 
-    def logistic_run(self, kind, W, N, d, M, l2, problem_seed, run_seed, batch, T, opt, hp, alpha0, factor, every):
+    def logistic_run(self, kind, W, N, d, M, l2, problem_seed, run_seed, batch, T, opt, hp, alpha0, factor, every,
+                     sampling=0, with_batches=False):
         grads = np.zeros((T, W, d), _D)
         params = np.zeros((T, W, d), _D)
         alphas = np.zeros(T, _D)
+        batches = np.zeros((T, W, batch), np.int32)
         match = C.c_int()
         rc = self.lib.ref_logistic_run(kind, W, N, d, M, l2, problem_seed, run_seed, batch, T, opt, _ptr(hp), alpha0,
-                                       factor, every, _ptr(grads), _ptr(params), _ptr(alphas), C.byref(match),
-                                       *self._e())
+                                       factor, every, sampling, _ptr(grads), _ptr(params), _ptr(alphas),
+                                       _ptr(batches), C.byref(match), *self._e())
         if rc:
             raise RuntimeError(self.error())
+        if with_batches:
+            return grads, params, alphas, batches, bool(match.value)
         return grads, params, alphas, bool(match.value)
+
+    def logistic_yx(self, seed, d, M):
+        out = np.zeros((M, d), _D)
+        if self.lib.ref_logistic_yx(C.c_uint64(seed), d, M, _ptr(out), *self._e()):
+            raise RuntimeError(self.error())
+        return out
+
+    def make_shards(self, M, W, seed):
+        idx = np.zeros(M, np.int32)
+        off = np.zeros(W + 1, np.int32)
+        if self.lib.ref_make_shards(M, W, C.c_uint64(seed), _ptr(idx), _ptr(off), *self._e()):
+            raise RuntimeError(self.error())
+        return idx, off
+
+    def epoch_order(self, shard, seed, rank, epoch):
+        shard = np.ascontiguousarray(shard, np.int32)
+        out = np.zeros_like(shard)
+        self.lib.ref_epoch_order(_ptr(shard), shard.size, C.c_uint64(seed), rank, C.c_long(epoch), _ptr(out))
+        return out

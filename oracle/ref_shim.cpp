@@ -433,8 +433,8 @@ int ref_quadratic_run(int kind, int topo, int W, int N, int d, double mu, double
 // against run_training.
 int ref_logistic_run(int kind, int W, int N, int d, int M, double l2, uint64_t problem_seed,
                      uint64_t run_seed, int batch, int T, int opt, const double* hp, double alpha0,
-                     double factor, long every, double* grads_out, double* params_out, double* alphas_out,
-                     int* matches, char* err, int errlen) {
+                     double factor, long every, int sampling, double* grads_out, double* params_out,
+                     double* alphas_out, int* batches_out, int* matches, char* err, int errlen) {
   return guarded(err, errlen, nullptr, nullptr, [&] {
     DatasetSpec s;
     s.kind = "logistic";
@@ -450,6 +450,7 @@ int ref_logistic_run(int kind, int W, int N, int d, int M, double l2, uint64_t p
     o.batch_size = batch;
     o.optimizer = make_opt(opt, hp, alpha0);
     o.lr = step_decay_lr(alpha0, factor, every);
+    o.sampling = sampling ? SamplingMode::Epoch : SamplingMode::Replacement;
     const std::vector<Shard> shards = make_shards(problem->dataset_size(), W, run_seed);
     std::vector<WorkerState> ws(static_cast<size_t>(W));
     for (int k = 0; k < W; ++k) {
@@ -464,9 +465,20 @@ int ref_logistic_run(int kind, int W, int N, int d, int M, double l2, uint64_t p
       std::vector<ParamVector> grads(static_cast<size_t>(W));
       for (int k = 0; k < W; ++k) {
         const WorkerState& x = ws[static_cast<size_t>(k)];
-        Rng br = Rng::for_stream(run_seed, streams::kBatch, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
+        // sample_batch (sync.cpp:153-179), restated: it is not in a public header
         std::vector<int> b(static_cast<size_t>(batch));
-        for (auto& idx : b) idx = x.shard.indices[br.uniform_below(x.shard.indices.size())];
+        if (!sampling) {
+          Rng br = Rng::for_stream(run_seed, streams::kBatch, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
+          for (auto& idx : b) idx = x.shard.indices[br.uniform_below(x.shard.indices.size())];
+        } else {
+          const long size = static_cast<long>(x.shard.indices.size());
+          long pos = static_cast<long>(t) * batch;
+          for (auto& idx : b) {
+            idx = epoch_order(x.shard, run_seed, k, pos / size)[static_cast<size_t>(pos % size)];
+            ++pos;
+          }
+        }
+        std::memcpy(batches_out + (static_cast<long>(t) * W + k) * batch, b.data(), sizeof(int) * static_cast<size_t>(batch));
         Rng noise = Rng::for_stream(run_seed, streams::kGradientNoise, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
         grads[static_cast<size_t>(k)] = problem->stochastic_gradient(x.params, b, noise).grad;
         std::memcpy(grads_out + (static_cast<long>(t) * W + k) * d, grads[static_cast<size_t>(k)].data(), sizeof(double) * static_cast<size_t>(d));
@@ -490,6 +502,49 @@ int ref_logistic_run(int kind, int W, int N, int d, int M, double l2, uint64_t p
       if (rr.final_workers[static_cast<size_t>(k)].params != ws[static_cast<size_t>(k)].params) *matches = 0;
     }
   });
+}
+
+// y_i * x_i of the logistic dataset through the public Problem API: with
+// l2 = 0, w = 0 and the one-example batch {i}, stochastic_gradient is
+// (-y_i * 0.5) * x_i exactly (problems.cpp:265-290), so -2 * grad = y_i * x_i.
+// The model depends on the data only through these products.
+int ref_logistic_yx(uint64_t seed, int d, int M, double* out, char* err, int errlen) {
+  return guarded(err, errlen, nullptr, nullptr, [&] {
+    DatasetSpec s;
+    s.kind = "logistic";
+    s.d = d;
+    s.M = M;
+    s.mu = 0.0;
+    s.seed = seed;
+    auto problem = make_problem(s);
+    const ParamVector w(static_cast<size_t>(d), 0.0);
+    Rng noise(0);
+    for (int i = 0; i < M; ++i) {
+      const int b[1] = {i};
+      const GradSample g = problem->stochastic_gradient(w, std::span<const int>(b, 1), noise);
+      for (int j = 0; j < d; ++j) out[static_cast<long>(i) * d + j] = -2.0 * g.grad[static_cast<size_t>(j)];
+    }
+  });
+}
+
+int ref_make_shards(int M, int W, uint64_t seed, int* indices, int* offsets, char* err, int errlen) {
+  return guarded(err, errlen, nullptr, nullptr, [&] {
+    const std::vector<Shard> sh = make_shards(M, W, seed);
+    int n = 0;
+    offsets[0] = 0;
+    for (int w = 0; w < W; ++w) {
+      for (int i : sh[static_cast<size_t>(w)].indices) indices[n++] = i;
+      offsets[w + 1] = n;
+    }
+  });
+}
+
+int ref_epoch_order(const int* shard, int size, uint64_t seed, int rank, long epoch, int* out) {
+  Shard s;
+  s.indices.assign(shard, shard + size);
+  const std::vector<int> o = epoch_order(s, seed, rank, epoch);
+  for (int i = 0; i < size; ++i) out[i] = o[static_cast<size_t>(i)];
+  return 0;
 }
 
 // Tiny-MLP run (problems.cpp:436-570: running statistics = EMA of the hidden

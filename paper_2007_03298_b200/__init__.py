@@ -13,6 +13,8 @@ from .api import (  # noqa: F401
     OptimizerHyperparams,
     OptimizerKind,
     OptimizerState,
+    SamplingMode,
+    Shard,
     StepResult,
     StrategyKind,
     SyncRoundOutcome,
@@ -22,10 +24,13 @@ from .api import (  # noqa: F401
     WorldConfig,
     apply_step,
     check_mixing,
+    epoch_order,
     group_of,
     iteration_trace,
+    logistic_dataset,
     is_square_mode,
     make_partition,
+    make_shards,
     round_outcome,
     sync_round,
     validate,

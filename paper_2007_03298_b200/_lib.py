@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("DSS_LIB_VARIANT", LIB_PATH)
 DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_STATS, BUF_STATS_OBS = range(6)
+SAMPLING_REPLACEMENT, SAMPLING_EPOCH = 0, 1  # dss_sampling
 IPC_BYTES = 576
 KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain"]
 
@@ -85,6 +86,14 @@ SIGNATURES = {
     "dss_set_optimum": (C.c_int, [_P, _P, C.c_long]),
     "dss_global_mean": (C.c_int, [_P, _P]),
     "dss_quadratic_losses": (C.c_int, [_P, C.c_double, C.c_int, _P, _P]),
+    "dss_logistic_dataset": (C.c_int, [C.c_uint64, C.c_int, C.c_int, _P, _P]),
+    "dss_make_shards": (C.c_int, [C.c_int, C.c_int, C.c_uint64, _P, _P]),
+    "dss_epoch_order": (C.c_int, [_P, C.c_int, C.c_uint64, C.c_int, C.c_long, _P]),
+    "dss_logistic_setup": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64]),
+    "dss_logistic_gradients": (C.c_int, [_P, C.c_long]),
+    "dss_logistic_steps": (C.c_int, [_P, C.c_long, C.c_long, _P, C.c_int, _P]),
+    "dss_logistic_batch": (C.c_int, [_P, _P]),
+    "dss_logistic_losses": (C.c_int, [_P, C.c_int, _P]),
     "dss_check": (C.c_int, [_P]),
     "dss_clear_error": (C.c_int, [_P]),
     "dss_last_error": (C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_long)]),

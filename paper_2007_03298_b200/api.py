@@ -263,6 +263,41 @@ def round_outcome(strategy: SyncStrategy, t: int, payload_dim: int) -> SyncRound
 
 
 # ---------------------------------------------------------------------------
+class SamplingMode(enum.IntEnum):  # sync.hpp SamplingMode
+    REPLACEMENT = 0
+    EPOCH = 1
+
+
+@dataclass
+class Shard:  # problems.hpp Shard
+    owner: int
+    indices: List[int]
+
+
+def logistic_dataset(seed: int, d: int, M: int):
+    """LogisticProblem's synthetic data (problems.cpp:230-250), bit-exact:
+    (x [M, d] float64, y [M] in {-1, +1})."""
+    x = np.empty((M, d), dtype=np.float64)
+    y = np.empty(M, dtype=np.float64)
+    _check_global(L.load().dss_logistic_dataset(C.c_uint64(seed), d, M, x.ctypes.data, y.ctypes.data))
+    return x, y
+
+
+def make_shards(dataset_size: int, workers: int, seed: int) -> List[Shard]:  # problems.cpp:642-662
+    idx = np.empty(max(dataset_size, 0), dtype=np.int32)
+    off = np.empty(max(workers, 0) + 1, dtype=np.int32)
+    _check_global(L.load().dss_make_shards(dataset_size, workers, C.c_uint64(seed), idx.ctypes.data,
+                                           off.ctypes.data))
+    return [Shard(w, idx[off[w]:off[w + 1]].tolist()) for w in range(workers)]
+
+
+def epoch_order(shard: Shard, seed: int, rank: int, epoch: int) -> List[int]:  # problems.cpp:664-674
+    a = np.ascontiguousarray(shard.indices, dtype=np.int32)
+    out = np.empty_like(a)
+    _check_global(L.load().dss_epoch_order(a.ctypes.data, a.size, C.c_uint64(seed), rank, epoch, out.ctypes.data))
+    return out.tolist()
+
+
 class DsSyncEngine:
     """Device-resident DS-Sync / BSP workers on one GPU (one context).
 
@@ -445,6 +480,39 @@ class DsSyncEngine:
         self._ck(self.lib.dss_quadratic_losses(self.h, mu, 1 if exact else 0, losses.ctypes.data,
                                                C.byref(sub) if with_suboptimality else None))
         return losses, (sub.value if with_suboptimality else None)
+
+    # -- logistic regression on the device (config C1) --
+    def logistic_setup(self, x, y, l2: float, batch_size: int, sampling: int = SamplingMode.REPLACEMENT,
+                       run_seed: int = 1) -> None:
+        """Upload the dataset and shard it over the world (make_shards(M, W, run_seed))."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if x.ndim != 2 or x.shape[1] != self.dim or y.shape != (x.shape[0],):
+            raise ValueError("logistic: x must be [M, dim] and y [M]")
+        self._ck(self.lib.dss_logistic_setup(self.h, x.ctypes.data, y.ctypes.data, x.shape[0], l2, batch_size,
+                                             int(sampling), C.c_uint64(run_seed)))
+        self._logistic_batch = batch_size
+
+    def logistic_gradients(self, t: int) -> None:
+        self._ck(self.lib.dss_logistic_gradients(self.h, t))
+
+    def logistic_steps(self, t0: int, alphas, check: bool = False) -> SyncRoundOutcome:
+        """len(alphas) iterations of (device logistic gradient, step) from t0."""
+        a = np.ascontiguousarray(alphas, dtype=np.float64)
+        o = L.dss_outcome()
+        self._ck(self.lib.dss_logistic_steps(self.h, t0, a.size, a.ctypes.data, 1 if check else 0, C.byref(o)))
+        return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
+
+    def logistic_batch(self) -> np.ndarray:
+        out = np.empty((self.local_workers, self._logistic_batch), dtype=np.int32)
+        self._ck(self.lib.dss_logistic_batch(self.h, out.ctypes.data))
+        return out
+
+    def logistic_losses(self, exact: bool = False) -> np.ndarray:
+        """full_loss (problems.cpp:292-305) of every local worker."""
+        out = np.empty(self.local_workers, dtype=np.float64)
+        self._ck(self.lib.dss_logistic_losses(self.h, 1 if exact else 0, out.ctypes.data))
+        return out
 
     def check(self) -> None:
         self._ck(self.lib.dss_check(self.h))

@@ -25,11 +25,11 @@ NVCC_FLAGS = [
     # no FMA contraction anywhere on the parity path; the kernels
     # also use explicit __f*_rn / __d*_rn intrinsics
     "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
-    "-Xcompiler", "-fPIC,-O2,-Wall",
+    "-Xcompiler", "-fPIC,-O2,-Wall,-ffp-contract=off",
     "-I" + INCLUDE, "-I" + CSRC,
 ]
 
-SOURCES = ["dssync_b200.cu", "schedule.cpp"]
+SOURCES = ["dssync_b200.cu", "schedule.cpp", "problems.cpp"]
 
 
 def _nvcc() -> str:

@@ -18,6 +18,7 @@
 
 #include "dssync_b200.h"
 #include "kernels.cuh"
+#include "problems.hpp"
 #include "schedule.hpp"
 
 using namespace dssb;
@@ -138,6 +139,7 @@ struct dss_ctx {
   std::vector<void*> peer_stats;
   void* wstar = nullptr;  // quadratic optimum row
   unsigned long long* d_err = nullptr;
+  unsigned long long* d_gerr = nullptr;  // gradient-producer failures: t << 32 | rank
   unsigned long long* d_timeout = nullptr;
   unsigned long long* flags = nullptr;  // [G] barrier words, written by peers
   unsigned long long** d_peer_flags = nullptr;
@@ -177,6 +179,23 @@ struct dss_ctx {
   ParityPlan mean_plan;      // ordered fold of every worker's params into mg (trace)
   ParityPlan stats_plan[2];  // running-stats fold per parity (DS) / world group at [0] (BSP)
   double* d_loss = nullptr;  // [P + 1] loss accumulators (trace)
+
+  // logistic problem on the device (dss_logistic_setup)
+  struct {
+    bool ready = false;
+    double* x = nullptr;       // [M][d]
+    double* y = nullptr;       // [M]
+    int* shard = nullptr;      // local shards, concatenated
+    int* shard_off = nullptr;  // [P + 1]
+    int* order = nullptr;      // [P][max_shard]
+    long* order_epoch = nullptr;
+    int* batch = nullptr;      // [P][B]
+    long max_shard = 0;
+    int M = 0, B = 0, sampling = 0;
+    double l2 = 0.0;
+    uint64_t seed = 0;
+    std::vector<void*> mem;
+  } logi;
   GroupLaunch apply_launch;  // singleton groups of every local worker
 
   // tiny-problem multi-iteration path (dss_steps)
@@ -1234,15 +1253,33 @@ int check_impl(dss_ctx* c) {
     ck(cudaMemcpy(&timeout, c->d_timeout, sizeof(timeout), cudaMemcpyDeviceToHost), "timeout readback");
   }
   if (timeout) return fail(c, DSS_ENCCL, "cross-GPU barrier timed out (peer did not arrive)");
+  unsigned long long gkey = ~0ull;
+  ck(cudaMemcpy(&gkey, c->d_gerr, sizeof(gkey), cudaMemcpyDeviceToHost), "err readback");
   const unsigned long long key = *c->h_err;
-  if (key == ~0ull) return DSS_OK;
-  const long t = static_cast<long>(key >> 34);
+  if (key == ~0ull && gkey == ~0ull) return DSS_OK;
+  long t = static_cast<long>(key >> 34);
   const int phase = static_cast<int>((key >> 32) & 3);
-  const int rank = static_cast<int>(key & 0xffffffffu);
+  int rank = static_cast<int>(key & 0xffffffffu);
   std::string what;
   const bool bsp = c->cfg.strategy.kind == DSS_BSP;
   const bool local_step = bsp ? phase == 1 : phase == 0;
-  if (local_step) {
+  // A gradient failure (checked_gradient, sync.cpp:181-191) wins over an
+  // iteration-t step/collective failure unless it comes later in the
+  // reference's order: DS runs gradient + step per worker in rank order
+  // (sync.cpp:348-361), BSP computes every gradient before the collective.
+  bool grad = false;
+  if (gkey != ~0ull) {
+    const long gt = static_cast<long>(gkey >> 32);
+    const int gr = static_cast<int>(gkey & 0xffffffffu);
+    grad = key == ~0ull || gt < t || (gt == t && (bsp || !local_step || gr <= rank));
+    if (grad) {
+      t = gt;
+      rank = gr;
+    }
+  }
+  if (grad) {
+    what = "non-finite stochastic gradient";
+  } else if (local_step) {
     what = "apply_step: non-finite value in result";  // optim.cpp:96 via sync.cpp:257-261
   } else {
     what = std::string(collective_name(c->cfg.strategy.topology)) + ": non-finite value in result";
@@ -1437,6 +1474,8 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     c->wstar = dalloc(c.get(), static_cast<size_t>(c->d_pad) * c->esz);
     c->d_err = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
     ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream), "err init");
+    c->d_gerr = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
+    ck(cudaMemsetAsync(c->d_gerr, 0xff, sizeof(unsigned long long), c->stream), "err init");
     c->d_timeout = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
     c->flags = static_cast<unsigned long long*>(
         dalloc(c.get(), sizeof(unsigned long long) * static_cast<size_t>(std::max(cfg->n_gpus, 32))));
@@ -1492,6 +1531,10 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
   return DSS_OK;
 }
 
+namespace {
+void free_logistic(dss_ctx* c);
+}  // namespace
+
 extern "C" int dss_destroy(dss_ctx* c) {
   if (!c) return DSS_OK;
   if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
@@ -1504,6 +1547,7 @@ extern "C" int dss_destroy(dss_ctx* c) {
   }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->h_err) cudaFreeHost(c->h_err);
+  free_logistic(c);
   if (c->copy_in) cudaStreamSynchronize(c->copy_in), cudaStreamDestroy(c->copy_in);
   if (c->copy_out) cudaStreamSynchronize(c->copy_out), cudaStreamDestroy(c->copy_out);
   for (cudaEvent_t e : {c->ev_in, c->ev_free, c->ev_snap, c->ev_out}) {
@@ -2108,6 +2152,213 @@ extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, int exact, double* lo
   });
 }
 
+// ====================== logistic problem on the device ======================
+
+extern "C" int dss_logistic_dataset(uint64_t seed, int d, int M, double* x, double* y) {
+  if (!x || !y) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    std::vector<double> hx, hy;
+    logistic_dataset(seed, d, M, hx, hy);
+    std::memcpy(x, hx.data(), sizeof(double) * hx.size());
+    std::memcpy(y, hy.data(), sizeof(double) * hy.size());
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_make_shards(int dataset_size, int workers, uint64_t seed, int* indices, int* offsets) {
+  if (!indices || !offsets) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    std::vector<int> idx, off;
+    make_shards(dataset_size, workers, seed, idx, off);
+    std::copy(idx.begin(), idx.end(), indices);
+    std::copy(off.begin(), off.end(), offsets);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_epoch_order(const int* shard, int size, uint64_t seed, int rank, long epoch, int* out) {
+  if ((!shard || !out) && size > 0) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    if (size < 0) throw std::invalid_argument("epoch_order: size must be >= 0");
+    epoch_order(shard, size, seed, rank, epoch, out);
+    return DSS_OK;
+  });
+}
+
+namespace {
+
+void free_logistic(dss_ctx* c) {
+  for (void* p : c->logi.mem) cudaFree(p);
+  c->logi.mem.clear();
+  c->logi.ready = false;
+}
+
+template <typename P>
+P* logi_alloc(dss_ctx* c, size_t n) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(P)), "cudaMalloc");
+  c->logi.mem.push_back(p);
+  return static_cast<P*>(p);
+}
+
+// 3 d doubles (w, products, accumulators) + the broadcast scalar
+size_t logistic_smem(long d) { return sizeof(double) * (3 * static_cast<size_t>(d) + 2); }
+constexpr long kLogisticMaxDim = 9000;
+
+}  // namespace
+
+extern "C" int dss_logistic_setup(dss_ctx* c, const double* x, const double* y, int M, double l2, int batch_size,
+                                  int sampling, uint64_t run_seed) {
+  if (!c || !x || !y) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (M < 1) throw std::invalid_argument("logistic requires problem.M >= 1");
+    if (!(l2 >= 0.0)) throw std::invalid_argument("problem.mu must be >= 0");
+    if (batch_size < 1) throw std::invalid_argument("batch_size must be >= 1");
+    if (sampling != DSS_SAMPLING_REPLACEMENT && sampling != DSS_SAMPLING_EPOCH) {
+      throw std::invalid_argument("sampling must be replacement or epoch");
+    }
+    if (c->d > kLogisticMaxDim) throw std::invalid_argument("logistic on the device supports dim <= 9000");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(c->stream), "stream sync");
+    free_logistic(c);
+    // make_shards over the whole world (sync.cpp:300); keep this GPU's rows
+    std::vector<int> idx, off;
+    make_shards(M, c->cfg.strategy.world_size, run_seed, idx, off);
+    std::vector<int> local_off(static_cast<size_t>(c->P) + 1, 0);
+    long max_shard = 0;
+    for (int k = 0; k < c->P; ++k) {
+      const int n = off[static_cast<size_t>(c->first + k) + 1] - off[static_cast<size_t>(c->first + k)];
+      local_off[static_cast<size_t>(k) + 1] = local_off[static_cast<size_t>(k)] + n;
+      max_shard = std::max<long>(max_shard, n);
+    }
+    auto& L = c->logi;
+    const size_t xn = static_cast<size_t>(M) * c->d;
+    L.x = logi_alloc<double>(c, xn);
+    L.y = logi_alloc<double>(c, static_cast<size_t>(M));
+    L.shard = logi_alloc<int>(c, static_cast<size_t>(local_off.back()));
+    L.shard_off = logi_alloc<int>(c, local_off.size());
+    L.order = logi_alloc<int>(c, static_cast<size_t>(c->P) * max_shard);
+    L.order_epoch = logi_alloc<long>(c, static_cast<size_t>(c->P));
+    L.batch = logi_alloc<int>(c, static_cast<size_t>(c->P) * batch_size);
+    ck(cudaMemcpy(L.x, x, sizeof(double) * xn, cudaMemcpyHostToDevice), "logistic x upload");
+    ck(cudaMemcpy(L.y, y, sizeof(double) * M, cudaMemcpyHostToDevice), "logistic y upload");
+    ck(cudaMemcpy(L.shard, idx.data() + off[static_cast<size_t>(c->first)], sizeof(int) * local_off.back(),
+                  cudaMemcpyHostToDevice), "shard upload");
+    ck(cudaMemcpy(L.shard_off, local_off.data(), sizeof(int) * local_off.size(), cudaMemcpyHostToDevice),
+       "shard upload");
+    ck(cudaMemset(L.order_epoch, 0xff, sizeof(long) * c->P), "epoch init");  // -1
+    ck(cudaMemset(L.batch, 0, sizeof(int) * c->P * batch_size), "batch init");
+    if (logistic_smem(c->d) > 48 * 1024) {
+      ck(cudaFuncSetAttribute(logistic_grad_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(logistic_smem(c->d))), "smem attr");
+      ck(cudaFuncSetAttribute(logistic_grad_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(logistic_smem(c->d))), "smem attr");
+    }
+    L.max_shard = max_shard;
+    L.M = M;
+    L.B = batch_size;
+    L.sampling = sampling;
+    L.l2 = l2;
+    L.seed = run_seed;
+    L.ready = true;
+    return DSS_OK;
+  });
+}
+
+namespace {
+
+void launch_logistic(dss_ctx* c, long t) {
+  const auto& L = c->logi;
+  LogisticArgs a{};
+  a.x = L.x;
+  a.y = L.y;
+  a.shard = L.shard;
+  a.shard_off = L.shard_off;
+  a.order = L.order;
+  a.order_epoch = L.order_epoch;
+  a.batch = L.batch;
+  a.max_shard = L.max_shard;
+  a.ld = c->d_pad;
+  a.d = static_cast<int>(c->d);
+  a.B = L.B;
+  a.sampling = L.sampling;
+  a.l2 = L.l2;
+  a.seed = L.seed;
+  a.t = t;
+  a.first_rank = c->first;
+  a.gerr = c->d_gerr;
+  TimedLaunch tl(c, DSS_KIND_GRADIENT);
+  if (c->cfg.dtype == DSS_F64) {
+    logistic_grad_kernel<double><<<c->P, 128, logistic_smem(c->d), c->stream>>>(
+        a, static_cast<const double*>(c->w), static_cast<double*>(c->g));
+  } else {
+    logistic_grad_kernel<float><<<c->P, 128, logistic_smem(c->d), c->stream>>>(
+        a, static_cast<const float*>(c->w), static_cast<float*>(c->g));
+  }
+  ck(cudaGetLastError(), "logistic_grad_kernel launch");
+}
+
+}  // namespace
+
+extern "C" int dss_logistic_gradients(dss_ctx* c, long t) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (!c->logi.ready) throw std::invalid_argument("dss_logistic_setup has not been called");
+    if (t < 0) throw std::invalid_argument("iteration must be >= 0");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    launch_logistic(c, t);
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_logistic_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
+  if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
+  for (long i = 0; i < n; ++i) {
+    int st = dss_logistic_gradients(c, t0 + i);
+    if (st == DSS_OK) st = dss_step(c, t0 + i, alphas[i], 0, last);
+    if (st != DSS_OK) return st;
+  }
+  if (check) return dss_check(c);
+  return DSS_OK;
+}
+
+extern "C" int dss_logistic_batch(dss_ctx* c, int* out) {
+  if (!c || !out) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (!c->logi.ready) throw std::invalid_argument("dss_logistic_setup has not been called");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaMemcpyAsync(out, c->logi.batch, sizeof(int) * c->P * c->logi.B, cudaMemcpyDeviceToHost, c->stream),
+       "batch download");
+    ck(cudaStreamSynchronize(c->stream), "batch sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_logistic_losses(dss_ctx* c, int exact, double* losses) {
+  if (!c || !losses) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (!c->logi.ready) throw std::invalid_argument("dss_logistic_setup has not been called");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    if (!c->d_loss) c->d_loss = static_cast<double*>(dalloc(c, sizeof(double) * (c->P + 1)));
+    const auto& L = c->logi;
+    if (c->cfg.dtype == DSS_F64) {
+      logistic_loss_kernel<double><<<c->P, kThreads, 0, c->stream>>>(static_cast<const double*>(c->w), c->d_pad, L.x,
+                                                                     L.y, static_cast<int>(c->d), L.M, L.l2, exact,
+                                                                     c->d_loss);
+    } else {
+      logistic_loss_kernel<float><<<c->P, kThreads, 0, c->stream>>>(static_cast<const float*>(c->w), c->d_pad, L.x,
+                                                                    L.y, static_cast<int>(c->d), L.M, L.l2, exact,
+                                                                    c->d_loss);
+    }
+    ck(cudaGetLastError(), "logistic_loss_kernel launch");
+    ck(cudaMemcpyAsync(losses, c->d_loss, sizeof(double) * c->P, cudaMemcpyDeviceToHost, c->stream), "loss readback");
+    ck(cudaStreamSynchronize(c->stream), "loss sync");
+    return DSS_OK;
+  });
+}
+
 extern "C" int dss_check(dss_ctx* c) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
   return guard(c, [&]() -> int {
@@ -2121,6 +2372,7 @@ extern "C" int dss_clear_error(dss_ctx* c) {
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     ck(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream), "err reset");
+    ck(cudaMemsetAsync(c->d_gerr, 0xff, sizeof(unsigned long long), c->stream), "err reset");
     ck(cudaMemsetAsync(c->d_timeout, 0, sizeof(unsigned long long), c->stream), "timeout reset");
     ck(cudaStreamSynchronize(c->stream), "err reset sync");
     c->last_status = DSS_OK;

@@ -1514,4 +1514,195 @@ __global__ void broadcast_row_kernel(T* base, long ld, int rows, const T* src) {
   }
 }
 
+// ---- logistic regression with device batch sampling ------------------------
+// LogisticProblem::stochastic_gradient (problems.cpp:265-290) fed by
+// sample_batch (sync.cpp:153-179): one CTA per local worker.  Thread 0 draws
+// the batch from the worker's shard with the reference's SplitMix64 streams
+// (integer work: bit-exact indices), then the CTA walks the batch in order:
+// the products x_j * w_j in parallel, their sum sequentially from 0.0 (the
+// reference's dot order), and the per-feature accumulation -y*s*x_j in
+// parallel (each feature's sum keeps the reference's sample order).  Every
+// add/mul is an explicit _rn op; the only inexact step against the
+// reference is exp() in the sigmoid (CUDA's libdevice vs glibc, <= 1 ulp).
+
+__device__ __forceinline__ uint64_t stream_state_dev(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t it) {
+  uint64_t s = mix64(seed + 0x9e3779b97f4a7c15ULL);
+  s = mix64(s ^ purpose);
+  s = mix64(s ^ rank);
+  return mix64(s ^ it);
+}
+
+struct DevRng {  // Rng::next_u64 / uniform_below (rng.cpp:28-43)
+  uint64_t s;
+  __device__ __forceinline__ uint64_t next() {
+    s += 0x9e3779b97f4a7c15ULL;
+    return mix64(s);
+  }
+  __device__ __forceinline__ uint64_t below(uint64_t n) {
+    const uint64_t limit = ~0ULL - ~0ULL % n;
+    uint64_t v = next();
+    while (v >= limit) v = next();
+    return v % n;
+  }
+};
+
+constexpr uint64_t kBatchStream = 0xd6e8feb86659fd93ULL;       // rng.hpp:45
+constexpr uint64_t kEpochOrderStream = 0xe7037ed1a0b428dbULL;  // rng.hpp:47
+
+struct LogisticArgs {
+  const double* x;        // [M][d] row-major
+  const double* y;        // [M] labels in {-1, +1}
+  const int* shard;       // local workers' shards, concatenated
+  const int* shard_off;   // [P + 1]
+  int* order;             // [P][max_shard] cached epoch order (epoch sampling)
+  long* order_epoch;      // [P] epoch held in order (-1 = none)
+  int* batch;             // [P][B] the sampled indices
+  long max_shard;
+  long ld;                // row stride of w / g
+  int d, B, sampling;     // sampling: 0 replacement, 1 epoch
+  double l2;
+  uint64_t seed;
+  long t;
+  int first_rank;
+  unsigned long long* gerr;  // gradient failure latch: t << 32 | rank
+};
+
+__device__ __forceinline__ double softplus_dev(double z) {  // problems.cpp:338-341
+  return z > 0.0 ? __dadd_rn(z, log1p(exp(-z))) : log1p(exp(z));
+}
+
+// sample_batch (sync.cpp:153-179) for local worker k, into a.batch[k].
+__device__ void sample_batch_dev(const LogisticArgs& a, int k) {
+  const int rank = a.first_rank + k;
+  const int* sh = a.shard + a.shard_off[k];
+  const long size = a.shard_off[k + 1] - a.shard_off[k];
+  int* bt = a.batch + static_cast<long>(k) * a.B;
+  if (a.sampling == 0) {
+    DevRng r{stream_state_dev(a.seed, kBatchStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(a.t))};
+    for (int b = 0; b < a.B; ++b) bt[b] = sh[r.below(static_cast<uint64_t>(size))];
+    return;
+  }
+  int* ord = a.order + static_cast<long>(k) * a.max_shard;
+  long pos = a.t * a.B;
+  for (int b = 0; b < a.B; ++b, ++pos) {
+    const long epoch = pos / size;
+    if (a.order_epoch[k] != epoch) {  // epoch_order (problems.cpp:664-674)
+      for (long i = 0; i < size; ++i) ord[i] = sh[i];
+      DevRng r{stream_state_dev(a.seed, kEpochOrderStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(epoch))};
+      for (long i = size - 1; i > 0; --i) {
+        const long j = static_cast<long>(r.below(static_cast<uint64_t>(i + 1)));
+        const int tmp = ord[i];
+        ord[i] = ord[j];
+        ord[j] = tmp;
+      }
+      a.order_epoch[k] = epoch;
+    }
+    bt[b] = ord[pos % size];
+  }
+}
+
+// dynamic shared memory: wd[d], prod[d], acc[d] (doubles) + 2 scalars
+template <typename T>
+__global__ void __launch_bounds__(128) logistic_grad_kernel(const LogisticArgs a, const T* __restrict__ w,
+                                                            T* __restrict__ g) {
+  extern __shared__ double sh[];
+  const int k = blockIdx.x;
+  const int d = a.d;
+  double* wd = sh;
+  double* prod = sh + d;
+  double* acc = sh + 2 * d;
+  double* sval = sh + 3 * d;  // [0] = -y*s of the current sample
+  const T* wr = w + static_cast<long>(k) * a.ld;
+  if (threadIdx.x == 0) sample_batch_dev(a, k);
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    wd[j] = static_cast<double>(wr[j]);
+    acc[j] = 0.0;
+  }
+  __syncthreads();
+  const int* bt = a.batch + static_cast<long>(k) * a.B;
+  double loss = 0.0;  // thread 0 only
+  for (int b = 0; b < a.B; ++b) {
+    const int idx = bt[b];
+    const double* x = a.x + static_cast<long>(idx) * d;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) prod[j] = __dmul_rn(x[j], wd[j]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double y = a.y[idx];
+      double z = 0.0;
+      for (int j = 0; j < d; ++j) z = __dadd_rn(z, prod[j]);
+      const double nz = __dmul_rn(-y, z);
+      loss = __dadd_rn(loss, softplus_dev(nz));
+      const double s = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz)));  // sigmoid (problems.cpp:337)
+      sval[0] = __dmul_rn(-y, s);
+    }
+    __syncthreads();
+    const double ys = sval[0];
+    for (int j = threadIdx.x; j < d; j += blockDim.x) acc[j] = __dadd_rn(acc[j], __dmul_rn(ys, x[j]));
+  }
+  const double inv = __ddiv_rn(1.0, static_cast<double>(a.B));
+  bool bad = false;
+  T* gr = g + static_cast<long>(k) * a.ld;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double v = __dmul_rn(acc[j], inv);
+    if (a.l2 > 0.0) v = __dadd_rn(v, __dmul_rn(a.l2, wd[j]));
+    bad = bad || !isfinite(v);
+    gr[j] = static_cast<T>(v);
+  }
+  for (long j = d + threadIdx.x; j < a.ld; j += blockDim.x) gr[j] = T(0);
+  if (threadIdx.x == 0) {
+    loss = __dmul_rn(loss, inv);
+    if (a.l2 > 0.0) {
+      double dd = 0.0;
+      for (int j = 0; j < d; ++j) dd = __dadd_rn(dd, __dmul_rn(wd[j], wd[j]));
+      loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(0.5, a.l2), dd));
+    }
+    bad = bad || !isfinite(loss);
+  }
+  // checked_gradient (sync.cpp:181-191): DivergenceError(rank, t)
+  if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.first_rank + k));
+  }
+}
+
+// LogisticProblem::full_loss (problems.cpp:292-305) of local row blockIdx.x:
+// mean softplus(-y z) + 0.5 * l2 * |w|^2.  exact = 1: one thread in the
+// reference's order (libdevice exp/log1p: tolerance, not bit-exact);
+// exact = 0: a parallel fp64 reduction over the examples.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) logistic_loss_kernel(const T* w, long ld, const double* x, const double* y,
+                                                                 int d, int M, double l2, int exact, double* out) {
+  __shared__ double part[kThreads / 32];
+  const T* wr = w + static_cast<long>(blockIdx.x) * ld;
+  double acc = 0.0;
+  if (exact) {
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < M; ++i) {
+      const double* xi = x + static_cast<long>(i) * d;
+      double z = 0.0;
+      for (int j = 0; j < d; ++j) z = __dadd_rn(z, __dmul_rn(xi[j], static_cast<double>(wr[j])));
+      acc = __dadd_rn(acc, softplus_dev(__dmul_rn(-y[i], z)));
+    }
+  } else {
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+      const double* xi = x + static_cast<long>(i) * d;
+      double z = 0.0;
+      for (int j = 0; j < d; ++j) z = __dadd_rn(z, __dmul_rn(xi[j], static_cast<double>(wr[j])));
+      acc += softplus_dev(__dmul_rn(-y[i], z));
+    }
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    acc = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) acc += part[i];
+  }
+  acc = __ddiv_rn(acc, static_cast<double>(M));
+  if (l2 > 0.0) {
+    double dd = 0.0;
+    for (int j = 0; j < d; ++j) dd = __dadd_rn(dd, __dmul_rn(static_cast<double>(wr[j]), static_cast<double>(wr[j])));
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(0.5, l2), dd));
+  }
+  out[blockIdx.x] = acc;
+}
+
 }  // namespace dssb

@@ -1,0 +1,51 @@
+// Host-side problem setup for the device gradient producers: the
+// reference's SplitMix64 streams, the synthetic logistic dataset, the data
+// shards and the per-epoch shard orders.
+//
+// These run once per run (setup), not per iteration, and are bit-exact
+// restatements of the reference's host code.  They are compiled with the
+// host compiler and the same libm as the reference, and FMA contraction is
+// off:
+//   Rng                /root/reference/proj/src/rng.cpp:9-51
+//   logistic dataset   /root/reference/proj/src/problems.cpp:230-250
+//   make_shards        /root/reference/proj/src/problems.cpp:642-662
+//   epoch_order        /root/reference/proj/src/problems.cpp:664-674
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace dssb {
+
+// rng.hpp:42-47 stream purposes
+constexpr uint64_t kStreamDataGen = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t kStreamInitParams = 0xbf58476d1ce4e5b9ULL;
+constexpr uint64_t kStreamShard = 0x94d049bb133111ebULL;
+constexpr uint64_t kStreamBatch = 0xd6e8feb86659fd93ULL;
+constexpr uint64_t kStreamGradientNoise = 0xa0761d6478bd642fULL;
+constexpr uint64_t kStreamEpochOrder = 0xe7037ed1a0b428dbULL;
+
+class HostRng {
+ public:
+  explicit HostRng(uint64_t state) : state_(state) {}
+  static HostRng for_stream(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t iteration);
+  uint64_t next_u64();
+  double uniform01();
+  uint64_t uniform_below(uint64_t n);
+  double gaussian();
+
+ private:
+  uint64_t state_;
+};
+
+// Synthetic logistic data (problems.cpp:230-250): x is M x d row-major,
+// y in {-1, +1}.
+void logistic_dataset(uint64_t seed, int d, int M, std::vector<double>& x, std::vector<double>& y);
+
+// CSR shards: worker w owns indices[offsets[w] .. offsets[w+1]).
+void make_shards(int dataset_size, int workers, uint64_t seed, std::vector<int>& indices,
+                 std::vector<int>& offsets);
+
+void epoch_order(const int* shard, int size, uint64_t seed, int rank, long epoch, int* out);
+
+}  // namespace dssb

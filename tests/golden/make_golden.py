@@ -119,19 +119,48 @@ def trajectories(R: Reference) -> tuple[dict, dict]:
 
 def logistic_c1(R: Reference) -> tuple[dict, dict]:
     """Config C1 (acceptance.cpp:239-258): W=4 groups of 2, logistic d=20
-    M=2000 l2=0.05 seed 11, batch 8, vanilla SGD, step_decay_lr(1, 0.5, 75)."""
+    M=2000 l2=0.05 seed 11, batch 8, vanilla SGD, step_decay_lr(1, 0.5, 75);
+    replacement sampling (the default) and epoch sampling, with every
+    sampled batch recorded."""
     T = 300
     hp = R.hp_array()
     arrs, meta = {}, []
-    for kind, N in (("ds", 2), ("bsp", 4)):
-        grads, params, alphas, match = R.logistic_run(1 if kind == "ds" else 0, 4, N, 20, 2000, 0.05, 11, 1, 8, T,
-                                                      0, hp, 1.0, 0.5, 75)
+    for kind, N, sampling in (("ds", 2, 0), ("bsp", 4, 0), ("ds", 2, 1), ("bsp", 4, 1)):
+        tag = f"c1_{kind}" if sampling == 0 else f"c1e_{kind}"
+        grads, params, alphas, batches, match = R.logistic_run(1 if kind == "ds" else 0, 4, N, 20, 2000, 0.05, 11,
+                                                               1, 8, T, 0, hp, 1.0, 0.5, 75, sampling=sampling,
+                                                               with_batches=True)
         assert match, "logistic replay != run_training"
-        arrs[f"c1_{kind}_grads"] = grads
-        arrs[f"c1_{kind}_params"] = params
-        arrs[f"c1_{kind}_alphas"] = alphas
-        meta.append({"kind": kind, "W": 4, "N": N, "d": 20, "T": T})
+        arrs[f"{tag}_grads"] = grads
+        arrs[f"{tag}_params"] = params
+        arrs[f"{tag}_alphas"] = alphas
+        arrs[f"{tag}_batches"] = batches
+        meta.append({"tag": tag, "kind": kind, "W": 4, "N": N, "d": 20, "T": T, "batch": 8,
+                     "sampling": ["replacement", "epoch"][sampling]})
     return {"c1": meta}, arrs
+
+
+def logistic_data(R: Reference) -> tuple[dict, dict]:
+    """Pins for the host-side problem setup: y*x of the synthetic logistic
+    data (the model sees the data only through these products), make_shards
+    and epoch_order, all from the reference."""
+    import hashlib
+    arrs = {}
+    arrs["logi_yx_small"] = R.logistic_yx(5, 6, 40)
+    c1 = R.logistic_yx(11, 20, 2000)
+    meta = {"c1_yx_sha256": hashlib.sha256(np.ascontiguousarray(c1).tobytes()).hexdigest(), "shards": [],
+            "epoch_orders": []}
+    for M, W, seed in ((2000, 4, 1), (10, 3, 7), (7, 7, 2), (1001, 16, 3)):
+        idx, off = R.make_shards(M, W, seed)
+        key = f"shards_{M}_{W}_{seed}"
+        arrs[key + "_idx"], arrs[key + "_off"] = idx, off
+        meta["shards"].append({"M": M, "W": W, "seed": seed, "key": key})
+    idx, off = R.make_shards(2000, 4, 1)
+    for rank, epoch in ((0, 0), (1, 3), (3, 7)):
+        key = f"epoch_{rank}_{epoch}"
+        arrs[key] = R.epoch_order(idx[off[rank]:off[rank + 1]], 1, rank, epoch)
+        meta["epoch_orders"].append({"rank": rank, "epoch": epoch, "key": key, "shards": "shards_2000_4_1"})
+    return {"logistic_data": meta}, arrs
 
 
 def mlp_stats(R: Reference) -> tuple[dict, dict]:
@@ -192,6 +221,9 @@ def main():
     meta.update(m)
     m, a3 = logistic_c1(R)
     meta.update(m)
+    m, a7 = logistic_data(R)
+    meta.update(m)
+    a3.update(a7)
     m, a4 = sync_rounds(R)
     meta.update(m)
     m, a6 = mlp_stats(R)

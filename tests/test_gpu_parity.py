@@ -143,8 +143,8 @@ def test_c1_logistic_bit_exact(cuda_device, golden):
     300 iterations) on the device: bit-exact every iteration."""
     meta, a = golden
     for m in meta["c1"]:
-        kind = m["kind"]
-        grads, params, alphas = a[f"c1_{kind}_grads"], a[f"c1_{kind}_params"], a[f"c1_{kind}_alphas"]
+        kind, tag = m["kind"], m["tag"]
+        grads, params, alphas = a[f"{tag}_grads"], a[f"{tag}_params"], a[f"{tag}_alphas"]
         T, W, d = grads.shape
         with engine_for(kind, W, m["N"], 0, d) as e:
             for t in range(T):

@@ -110,8 +110,8 @@ def test_c1_logistic_matches_reference(oracle, golden):
     """Config C1 (acceptance.cpp:239-258) replayed from the reference's gradients."""
     meta, a = golden
     for m in meta["c1"]:
-        kind = m["kind"]
-        grads, params, alphas = a[f"c1_{kind}_grads"], a[f"c1_{kind}_params"], a[f"c1_{kind}_alphas"]
+        kind, tag = m["kind"], m["tag"]
+        grads, params, alphas = a[f"{tag}_grads"], a[f"{tag}_params"], a[f"{tag}_alphas"]
         T, W, d = grads.shape
         w = np.zeros((W, d))
         steps = np.zeros(W, np.int64)
