@@ -270,6 +270,16 @@ int dss_quadratic_losses(dss_ctx* ctx, double mu, int exact, double* losses, dou
 /* LogisticProblem's synthetic dataset (problems.cpp:230-250), host, bit-exact:
  * x: M*d doubles (row-major), y: M labels in {-1, +1}. */
 int dss_logistic_dataset(uint64_t seed, int d, int M, double* x, double* y);
+/* QuadraticProblem's optimum and start for A = mu*I (problems.cpp:157-165),
+ * host, bit-exact: wstar, w0 = d doubles each (cf. dss_quadratic_init, the
+ * device-side generator of the same rows for huge d). */
+int dss_quadratic_problem(uint64_t seed, int d, double delta0, double* wstar, double* w0);
+/* LogisticProblem::finish_setup (problems.cpp:346-416), host, bit-exact:
+ * the smoothness bound (power iteration on X^T X / 4M, + l2) and, when
+ * l2 > 0, the damped-Newton optimum w_opt (d doubles, optional) and
+ * f* = full_loss(w_opt) (NaN when l2 == 0: no optimum). */
+int dss_logistic_constants(const double* x, const double* y, int M, int d, double l2, double* smoothness,
+                           double* f_star, double* w_opt);
 /* make_shards (problems.cpp:642-662), host, bit-exact: worker w owns
  * indices[offsets[w] .. offsets[w+1]) (indices: M ints, offsets: workers+1). */
 int dss_make_shards(int dataset_size, int workers, uint64_t seed, int* indices, int* offsets);

@@ -177,7 +177,10 @@ class Reference:
         L.ref_logistic_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
                                        C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double, C.c_double,
                                        C.c_long, C.c_int, _P, _P, _P, _P, C.POINTER(C.c_int)] + E
+        L.ref_cmd_run.argtypes = [C.c_char_p, C.c_char_p] + E + [C.POINTER(C.c_int), C.POINTER(C.c_long)]
+        L.ref_parse_config.argtypes = [C.c_char_p] + E
         L.ref_logistic_yx.argtypes = [C.c_uint64, C.c_int, C.c_int, _P] + E
+        L.ref_load_csv.argtypes = [C.c_char_p, C.c_double, _P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)] + E
         L.ref_make_shards.argtypes = [C.c_int, C.c_int, C.c_uint64, _P, _P] + E
         L.ref_epoch_order.argtypes = [_P, C.c_int, C.c_uint64, C.c_int, C.c_long, _P]
         L.ref_mlp_run.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double,
@@ -302,11 +305,32 @@ class Reference:
             return grads, params, alphas, batches, bool(match.value)
         return grads, params, alphas, bool(match.value)
 
+    def cmd_run(self, config_path, out_dir):
+        """The reference's `dssync run` (main.cpp:34-55): (status, message, rank, iteration);
+        status 0 ok, 2 DivergenceError, 4 ConfigError, else another failure."""
+        rank, it = C.c_int(-1), C.c_long(-1)
+        rc = self.lib.ref_cmd_run(config_path.encode(), out_dir.encode(), *self._e(), C.byref(rank), C.byref(it))
+        return rc, (self.error() if rc else ""), rank.value, it.value
+
+    def parse_config(self, text):
+        """None when parse_run_config accepts text, else its ConfigError message."""
+        rc = self.lib.ref_parse_config(text.encode(), *self._e())
+        return self.error() if rc else None
+
     def logistic_yx(self, seed, d, M):
         out = np.zeros((M, d), _D)
         if self.lib.ref_logistic_yx(C.c_uint64(seed), d, M, _ptr(out), *self._e()):
             raise RuntimeError(self.error())
         return out
+
+    def load_csv(self, path, l2, cap=1 << 16):
+        """(error or None, y*x [M, d] or None)."""
+        out = np.zeros(cap, _D)
+        M, d = C.c_int(0), C.c_int(0)
+        rc = self.lib.ref_load_csv(path.encode(), l2, _ptr(out), cap, C.byref(M), C.byref(d), *self._e())
+        if rc:
+            return self.error(), None
+        return None, out[:M.value * d.value].reshape(M.value, d.value).copy()
 
     def make_shards(self, M, W, seed):
         idx = np.zeros(M, np.int32)

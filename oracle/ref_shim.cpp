@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "dssync/comm.hpp"
+#include "dssync/config.hpp"
 #include "dssync/errors.hpp"
 #include "dssync/metrics.hpp"
 #include "dssync/optim.hpp"
@@ -37,12 +38,15 @@ void put(char* buf, int len, const std::string& s) {
   }
 }
 
-// 0 ok, 1 invalid_argument, 2 DivergenceError, 3 runtime_error
+// 0 ok, 1 invalid_argument, 2 DivergenceError, 3 runtime_error, 4 ConfigError
 template <typename F>
 int guarded(char* err, int errlen, int* rank, long* it, F&& f) {
   try {
     f();
     return 0;
+  } catch (const ConfigError& e) {
+    put(err, errlen, e.what());
+    return 4;
   } catch (const DivergenceError& e) {
     if (rank) *rank = e.rank;
     if (it) *it = e.iteration;
@@ -527,6 +531,33 @@ int ref_logistic_yx(uint64_t seed, int d, int M, double* out, char* err, int err
   });
 }
 
+// load_logistic_csv through make_problem (problems.cpp:572-640): M, d and
+// y_i * x_i (as ref_logistic_yx) when out is non-null.
+int ref_load_csv(const char* path, double l2, double* out, int cap, int* M, int* d, char* err, int errlen) {
+  return guarded(err, errlen, nullptr, nullptr, [&] {
+    DatasetSpec s;
+    s.kind = "logistic";
+    s.csv = path;
+    s.mu = l2;
+    auto problem = make_problem(s);
+    *M = problem->dataset_size();
+    *d = problem->dim();
+    if (!out || static_cast<long>(*M) * *d > cap) return;
+    const ParamVector w(static_cast<size_t>(*d), 0.0);
+    const std::unique_ptr<Problem> p0 = [&] {
+      DatasetSpec z = s;
+      z.mu = 0.0;
+      return make_problem(z);
+    }();
+    Rng noise(0);
+    for (int i = 0; i < *M; ++i) {
+      const int b[1] = {i};
+      const GradSample g = p0->stochastic_gradient(w, std::span<const int>(b, 1), noise);
+      for (int j = 0; j < *d; ++j) out[static_cast<long>(i) * *d + j] = -2.0 * g.grad[static_cast<size_t>(j)];
+    }
+  });
+}
+
 int ref_make_shards(int M, int W, uint64_t seed, int* indices, int* offsets, char* err, int errlen) {
   return guarded(err, errlen, nullptr, nullptr, [&] {
     const std::vector<Shard> sh = make_shards(M, W, seed);
@@ -545,6 +576,31 @@ int ref_epoch_order(const int* shard, int size, uint64_t seed, int rank, long ep
   const std::vector<int> o = epoch_order(s, seed, rank, epoch);
   for (int i = 0; i < size; ++i) out[i] = o[static_cast<size_t>(i)];
   return 0;
+}
+
+// The reference's `dssync run` (tools/main.cpp:34-55) through its public
+// API: load_run_config, make_problem, build_run_options, run_training,
+// metrics_csv / summary_json / atomic_write_file into out_dir.
+int ref_cmd_run(const char* config_path, const char* out_dir, char* err, int errlen, int* rank, long* it) {
+  return guarded(err, errlen, rank, it, [&] {
+    const RunConfig cfg = load_run_config(config_path);
+    std::unique_ptr<Problem> problem = make_problem(cfg.problem);
+    std::vector<SeedOutcome> outcomes;
+    for (uint64_t seed : cfg.seeds) {
+      const RunOptions opts = build_run_options(cfg, *problem, seed);
+      const RunResult result = run_training(*problem, cfg.strategy, opts);
+      const IterationTrace& last = result.traces.back();
+      outcomes.push_back({seed, last.mean_post_sync_loss, last.suboptimality});
+      atomic_write_file(std::string(out_dir) + "/metrics_seed" + std::to_string(seed) + ".csv",
+                        metrics_csv(result.traces));
+    }
+    atomic_write_file(std::string(out_dir) + "/summary.json", summary_json(cfg, outcomes));
+  });
+}
+
+// parse_run_config only: 0 or 4 (ConfigError) with the message.
+int ref_parse_config(const char* text, char* err, int errlen) {
+  return guarded(err, errlen, nullptr, nullptr, [&] { (void)parse_run_config(text); });
 }
 
 // Tiny-MLP run (problems.cpp:436-570: running statistics = EMA of the hidden

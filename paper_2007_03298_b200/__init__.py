@@ -27,10 +27,12 @@ from .api import (  # noqa: F401
     epoch_order,
     group_of,
     iteration_trace,
+    logistic_constants,
     logistic_dataset,
     is_square_mode,
     make_partition,
     make_shards,
+    quadratic_problem,
     round_outcome,
     sync_round,
     validate,

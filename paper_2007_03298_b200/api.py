@@ -283,6 +283,27 @@ def logistic_dataset(seed: int, d: int, M: int):
     return x, y
 
 
+def quadratic_problem(seed: int, d: int, delta0: float):
+    """QuadraticProblem (A = mu*I) optimum w* and start w0 (problems.cpp:157-165), bit-exact."""
+    ws = np.empty(d, dtype=np.float64)
+    w0 = np.empty(d, dtype=np.float64)
+    _check_global(L.load().dss_quadratic_problem(C.c_uint64(seed), d, delta0, ws.ctypes.data, w0.ctypes.data))
+    return ws, w0
+
+
+def logistic_constants(x, y, l2: float):
+    """LogisticProblem's smoothness, optimum and f* (problems.cpp:346-416), bit-exact:
+    (smoothness, f_star or nan, w_opt or None)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    M, d = x.shape
+    sm, fs = C.c_double(), C.c_double()
+    w = np.empty(d, dtype=np.float64)
+    _check_global(L.load().dss_logistic_constants(x.ctypes.data, y.ctypes.data, M, d, l2, C.byref(sm), C.byref(fs),
+                                                  w.ctypes.data))
+    return sm.value, fs.value, (w if l2 > 0.0 else None)
+
+
 def make_shards(dataset_size: int, workers: int, seed: int) -> List[Shard]:  # problems.cpp:642-662
     idx = np.empty(max(dataset_size, 0), dtype=np.int32)
     off = np.empty(max(workers, 0) + 1, dtype=np.int32)

@@ -2165,6 +2165,30 @@ extern "C" int dss_logistic_dataset(uint64_t seed, int d, int M, double* x, doub
   });
 }
 
+extern "C" int dss_quadratic_problem(uint64_t seed, int d, double delta0, double* wstar, double* w0) {
+  if (!wstar || !w0) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    std::vector<double> ws, x0;
+    quadratic_problem(seed, d, delta0, ws, x0);
+    std::memcpy(wstar, ws.data(), sizeof(double) * ws.size());
+    std::memcpy(w0, x0.data(), sizeof(double) * x0.size());
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_logistic_constants(const double* x, const double* y, int M, int d, double l2,
+                                      double* smoothness, double* f_star, double* w_opt) {
+  if (!x || !y || !smoothness || !f_star) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    if (l2 < 0.0) throw std::invalid_argument("logistic l2 must be >= 0");
+    const LogisticConstants k = logistic_constants(x, y, M, d, l2);
+    *smoothness = k.smoothness;
+    *f_star = l2 > 0.0 ? k.f_star : std::nan("");
+    if (w_opt && l2 > 0.0) std::copy(k.w_opt.begin(), k.w_opt.end(), w_opt);
+    return DSS_OK;
+  });
+}
+
 extern "C" int dss_make_shards(int dataset_size, int workers, uint64_t seed, int* indices, int* offsets) {
   if (!indices || !offsets) return fail(nullptr, DSS_EINVAL, "null argument");
   return guard(nullptr, [&]() -> int {

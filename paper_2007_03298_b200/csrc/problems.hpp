@@ -7,7 +7,9 @@
 // host compiler and the same libm as the reference, and FMA contraction is
 // off:
 //   Rng                /root/reference/proj/src/rng.cpp:9-51
+//   quadratic w*, w0   /root/reference/proj/src/problems.cpp:157-165
 //   logistic dataset   /root/reference/proj/src/problems.cpp:230-250
+//   logistic L, f*     /root/reference/proj/src/problems.cpp:18-82,292-416
 //   make_shards        /root/reference/proj/src/problems.cpp:642-662
 //   epoch_order        /root/reference/proj/src/problems.cpp:664-674
 #pragma once
@@ -41,6 +43,21 @@ class HostRng {
 // Synthetic logistic data (problems.cpp:230-250): x is M x d row-major,
 // y in {-1, +1}.
 void logistic_dataset(uint64_t seed, int d, int M, std::vector<double>& x, std::vector<double>& y);
+
+// LogisticProblem::finish_setup (problems.cpp:346-416): the smoothness
+// bound (power iteration on X^T X / 4M, + l2) and, for l2 > 0, the optimum
+// by damped Newton (w_opt, f* = full_loss(w_opt)).  Setup-time host code.
+struct LogisticConstants {
+  double smoothness = 0.0;
+  double f_star = 0.0;
+  std::vector<double> w_opt;
+};
+LogisticConstants logistic_constants(const double* x, const double* y, int M, int d, double l2);
+
+// Isotropic quadratic (A = mu*I) optimum and start (problems.cpp:157-165):
+// w* = gaussians of (seed, kDataGen, 1, 0); w0 = w* + sqrt(delta0) * u, u the
+// normalised gaussians of (seed, kInitParams, 0, 0).
+void quadratic_problem(uint64_t seed, int d, double delta0, std::vector<double>& wstar, std::vector<double>& w0);
 
 // CSR shards: worker w owns indices[offsets[w] .. offsets[w+1]).
 void make_shards(int dataset_size, int workers, uint64_t seed, std::vector<int>& indices,

@@ -211,6 +211,122 @@ def rng_vectors(R: Reference) -> tuple[dict, dict]:
     return {"splitmix_seed0_first": f"{first:#x}"}, arrs
 
 
+CLI_CONFIGS = [
+    # (name, config, expected parity)
+    ("quad_ds_momentum", {"strategy": "ds-sync", "world_size": 4, "group_size": 2, "iterations": 40, "seeds": [1, 2],
+                          "problem": {"kind": "quadratic", "d": 16, "mu": 0.5, "L": 0.5, "sigma": 0.0, "delta0": 4.0,
+                                      "seed": 3},
+                          "optimizer": {"kind": "sgd-momentum", "momentum": 0.8, "weight_decay": 0.001},
+                          "lr": {"kind": "step-decay", "alpha": 0.2, "factor": 0.5, "every": 15}}, "bytes"),
+    ("quad_bsp_adam", {"strategy": "bsp", "world_size": 4, "iterations": 30, "seeds": [3],
+                       "problem": {"kind": "quadratic", "d": 33, "mu": 1.0, "L": 1.0, "delta0": 2.0, "seed": 5},
+                       "optimizer": {"kind": "adam"}, "lr": {"kind": "constant", "alpha": 0.05}}, "bytes"),
+    ("quad_bsp_ps_theorem", {"strategy": "bsp", "topology": "ps", "servers": 2, "world_size": 9, "iterations": 25,
+                            "seeds": [4, 5, 6], "cost_model": {"data_size": 1000.0, "bandwidth": 10.0},
+                            "problem": {"kind": "quadratic", "d": 7, "mu": 2.0, "L": 2.0, "delta0": 1.0, "seed": 9},
+                            "optimizer": {"kind": "adamw", "weight_decay": 0.01}, "lr": {"kind": "theorem"}}, "bytes"),
+    ("quad_ds_tree_noise", {"strategy": "ds-sync", "topology": "tree", "world_size": 16, "iterations": 30,
+                            "seeds": [7], "problem": {"kind": "quadratic", "d": 24, "mu": 1.0, "L": 1.0, "sigma": 0.5,
+                                                      "delta0": 4.0, "seed": 7},
+                            "lr": {"kind": "constant", "alpha": 0.1}}, "tolerance"),
+    ("logistic_ds_epoch", {"strategy": "ds-sync", "world_size": 4, "group_size": 2, "iterations": 60, "seeds": [1],
+                           "batch_size": 4, "sampling": "epoch",
+                           "problem": {"kind": "logistic", "d": 8, "M": 400, "mu": 0.05, "seed": 11},
+                           "lr": {"kind": "theorem"}}, "tolerance"),
+    ("logistic_bsp", {"strategy": "bsp", "world_size": 4, "iterations": 40, "seeds": [2, 3], "batch_size": 8,
+                      "problem": {"kind": "logistic", "d": 20, "M": 2000, "mu": 0.05, "seed": 11},
+                      "lr": {"kind": "step-decay", "alpha": 1.0, "factor": 0.5, "every": 10}}, "tolerance"),
+    ("quad_diverges", {"strategy": "ds-sync", "world_size": 4, "iterations": 10,
+                       "problem": {"kind": "quadratic", "d": 5, "mu": 1.0, "L": 1.0, "seed": 1},
+                       "lr": {"kind": "constant", "alpha": 1e300}}, "error"),
+]
+
+BAD_CONFIGS = [
+    "{", "[]", '{"world_size": 4}', '{"strategy": "x", "world_size": 4, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 5, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "bogus": 1}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic", "dd": 3}}',
+    '{"strategy": "ds-sync", "world_size": 4.0, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "topology": "mesh", "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "iterations": 0, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "seeds": [], "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "seeds": [1, -2], "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "sampling": "stratified", "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "svm"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic", "csv": "a.csv"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "optimizer": {"kind": "lion"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "optimizer": {"momentum": 1.0}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "optimizer": {"epsilon": 0}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "lr": {"kind": "cosine"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "lr": {"kind": "step-decay", '
+    '"factor": 1.5}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "lr": {"alpha": -1}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "cost_model": {"bandwidth": 0}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic"}, "check": {"samples": 1}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "logistic", "M": 3}}',
+    '{"strategy": "bsp", "world_size": 4, "group_size": 2, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 6, "group_size": 2, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "servers": 0, "topology": "ps", "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "execution": "async", "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "threads": -1, "problem": {"kind": "quadratic"}}',
+    '{"strategy": 3, "world_size": 4, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic", "seed": -1}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": {"kind": "quadratic", "mu": "x"}}',
+    '{"strategy": "ds-sync", "world_size": 4, "problem": "quadratic"}',
+    '{"strategy": "ds-sync", "world_size": 4, "batch_size": 0, "problem": {"kind": "quadratic"}}',
+    '{"strategy": "ds-sync", "world_size": 1, "group_size": 1, "problem": {"kind": "quadratic"}}',
+]
+
+
+CSV_CASES = [
+    "1.5, -2,1\n\n0.25,4e-1,0\r\n-1,0x10,-1\n",
+    "1,1\n3\n", "1,2,1\n1,2,3,1\n", "1,2,2\n", "1,x,1\n", "1,2z,1\n", "", "\n\n", "1,,1\n", "1,2,1,\n",
+    " 7 ,\t8\t,1\n", "1e999,1\n", "inf,-1\n", "nan,1\n", "1,-0\n", ",\n", "1,2,1", "1,2,+1\n", ".5,-.5,1\n",
+    "1,2,1\n\r\n",
+]
+
+
+def csv_cases(R: Reference) -> dict:
+    """load_logistic_csv (problems.cpp:584-640) on edge-case files: the
+    reference's error text, or y*x of the parsed rows."""
+    import tempfile
+    out = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for i, text in enumerate(CSV_CASES):
+            path = os.path.join(tmp, f"c{i}.csv")
+            with open(path, "w", newline="") as f:
+                f.write(text)
+            err, yx = R.load_csv(path, 0.1)
+            out.append({"text": text, "error": err.replace(path, "<path>") if err else None,
+                        "yx": None if yx is None else [[float(v) for v in row] for row in yx]})
+    return {"csv_cases": out}
+
+
+def cli_runs(R: Reference) -> dict:
+    """The reference's own `dssync run` (tools/main.cpp:34-55 through
+    oracle/ref_shim.cpp ref_cmd_run): metrics_seed*.csv and summary.json
+    texts per config, plus parse_run_config's verdict on malformed configs."""
+    import tempfile
+    runs = []
+    for name, cfg, parity in CLI_CONFIGS:
+        with tempfile.TemporaryDirectory() as tmp:
+            path = os.path.join(tmp, "cfg.json")
+            with open(path, "w") as f:
+                json.dump(cfg, f)
+            out = os.path.join(tmp, "out")
+            rc, msg, rank, it = R.cmd_run(path, out)
+            files = {}
+            if rc == 0:
+                for fn in sorted(os.listdir(out)):
+                    with open(os.path.join(out, fn)) as f:
+                        files[fn] = f.read()
+        runs.append({"name": name, "config": cfg, "parity": parity, "status": rc, "error": msg, "rank": rank,
+                     "iteration": it, "files": files})
+    bad = [{"text": t, "error": R.parse_config(t)} for t in BAD_CONFIGS]
+    return {"cli_runs": runs, "bad_configs": bad}
+
+
 def main():
     R = Reference()
     meta = {"generated_by": "tests/golden/make_golden.py from oracle/_ref (unmodified /root/reference/proj/src)"}
@@ -231,6 +347,8 @@ def main():
     a4.update(a6)
     m, a5 = rng_vectors(R)
     meta.update(m)
+    meta.update(cli_runs(R))
+    meta.update(csv_cases(R))
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **a1, **a2, **a3, **a4, **a5)
