@@ -127,6 +127,8 @@ struct dss_ctx {
   int sms = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // chain kernel B, concurrent with kernel A
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   void* w = nullptr;
   void* g = nullptr;
@@ -1041,23 +1043,45 @@ void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
 
 template <typename T, int OPTM, int OPTD>
 void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
+  ChainArgs<T> b = a;
+  b.entries = cl.d_b;
+  b.n_entries = cl.nb;
+  const long units_a = c->chain_nchunks * cl.na;
+  const long units_b = c->chain_nchunks * cl.nb;
+  TimedLaunch tl(c, DSS_KIND_CHAIN);  // spans both kernels; counts kernel A
+  if (cl.na == 0) --c->launches;
+  const bool concurrent = DSS_CHAIN_CONCURRENT && cl.na > 0 && cl.nb > 0;
+  if (concurrent) {
+    // Kernel B only waits on flags released by kernel A (here or on other
+    // GPUs), never the reverse: it may run beside A.  Its few resident CTAs
+    // leave A room on every SM, so a spinning B can never starve A.
+    if (!c->side) {
+      ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+      ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
+      ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
+    }
+    ck(cudaEventRecord(c->ev_fork, c->stream), "fork record");
+    ck(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork wait");
+    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units_b, c->sms * long{DSS_CHAIN_B_CTAS_PER_SM})),
+                                 kThreads, 0, c->side>>>(b);
+    ck(cudaGetLastError(), "chain_mean_kernel launch");
+    ++c->launches;
+  }
   if (cl.na > 0) {
     a.entries = cl.d_a;
     a.n_entries = cl.na;
-    const long units = c->chain_nchunks * cl.na;
-    TimedLaunch tl(c, DSS_KIND_CHAIN);
-    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units_a, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
                                           kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
   }
-  if (cl.nb > 0) {
-    a.entries = cl.d_b;
-    a.n_entries = cl.nb;
-    const long units = c->chain_nchunks * cl.nb;
-    TimedLaunch tl(c, DSS_KIND_CHAIN);
-    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
-                                 kThreads, 0, c->stream>>>(a);
+  if (concurrent) {
+    ck(cudaEventRecord(c->ev_join, c->side), "join record");
+    ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join wait");
+  } else if (cl.nb > 0) {
+    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units_b, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                                 kThreads, 0, c->stream>>>(b);
     ck(cudaGetLastError(), "chain_mean_kernel launch");
+    ++c->launches;
   }
 }
 
@@ -1551,6 +1575,10 @@ extern "C" int dss_destroy(dss_ctx* c) {
   if (c->copy_in) cudaStreamSynchronize(c->copy_in), cudaStreamDestroy(c->copy_in);
   if (c->copy_out) cudaStreamSynchronize(c->copy_out), cudaStreamDestroy(c->copy_out);
   for (cudaEvent_t e : {c->ev_in, c->ev_free, c->ev_snap, c->ev_out}) {
+    if (e) cudaEventDestroy(e);
+  }
+  if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join}) {
     if (e) cudaEventDestroy(e);
   }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

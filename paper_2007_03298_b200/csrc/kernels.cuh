@@ -46,6 +46,15 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 8
 #endif
+// 1: run the chain's mean pass (kernel B) concurrently with the partial
+// pass (kernel A) on a side stream, B with DSS_CHAIN_B_CTAS_PER_SM resident
+// CTAs per SM; 0: B after A on the context stream.
+#ifndef DSS_CHAIN_CONCURRENT
+#define DSS_CHAIN_CONCURRENT 1
+#endif
+#ifndef DSS_CHAIN_B_CTAS_PER_SM
+#define DSS_CHAIN_B_CTAS_PER_SM 2
+#endif
 // 1: full system fence before each chunk's release flag; 0: rely on the
 // cumulativity of st.release.sys after the CTA barrier (lighter).
 #ifndef DSS_CHAIN_FENCE
