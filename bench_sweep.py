@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--groups", default="2,4,8")
     ap.add_argument("--opt", default="sgd", choices=["sgd", "sync"])
     ap.add_argument("--mem-gb", type=float, default=150.0, help="per-GPU cap for the worker arrays")
+    ap.add_argument("--path", type=int, default=0, help="fold path (0 auto; 4 auto without one-shot)")
+    ap.add_argument("--no-nccl", action="store_true")
     args = ap.parse_args()
 
     import torch
@@ -80,10 +82,11 @@ def main():
             if P * d * 4 * 2 > args.mem_gb * 1e9:
                 continue
             K = int(max(5, min(2000, 4e9 / (P * nbytes * 3 + 1))))
-            row = {"N": N, "W": W, "bytes_per_worker": nbytes, "d": d, "n_gpus": G, "steps": K, "opt": args.opt}
+            row = {"N": N, "W": W, "bytes_per_worker": nbytes, "d": d, "n_gpus": G, "steps": K, "opt": args.opt,
+                   "path": args.path}
             for kind, key in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
                 s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W))
-                e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, d, None, "f32", local, rank, G)
+                e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, d, None, "f32", local, rank, G, path=args.path)
                 e.set_stream(stream.cuda_stream)
                 if G > 1:
                     from paper_2007_03298_b200.dist import attach
@@ -100,7 +103,7 @@ def main():
                 row[key + "_ms"] = ms
                 row[key + "_iters_s"] = 1000.0 / ms
                 row[key + "_eff_gbs"] = W * d * 4 / (ms / 1e3) / 1e9
-                if key == "bsp" and G > 1:
+                if key == "bsp" and G > 1 and not args.no_nccl:
                     grads = []
                     for k in range(rank * P, (rank + 1) * P):
                         ptr = e.device_ptr(BUF_GRADS, k)

@@ -108,6 +108,10 @@ typedef struct {
                            2 = (several GPUs) every spanning group uses the chain fold.
                            3 = (several GPUs) two-shot groups use the unfused pull fold
                            (step, barrier, fold) instead of the fused push kernel.
+                           4 = (several GPUs) as 0 but never one-shot: rows of at most
+                           1 MiB otherwise fold one-shot (every member GPU gathers every
+                           member row; no peer stores into params, no next-iteration
+                           barrier).
                            Results are bit-identical on every path. */
   long stats_dim;       /* running_stats per worker (0 = none).  They travel with the
                            params (DS, sync_round) or the gradients (BSP) through the same

@@ -97,6 +97,7 @@ struct ChainLaunch {
 };
 
 struct PushLaunch {
+  bool oneshot = false;
   int items = 0, folds = 0;
   PushItem* d_items = nullptr;
   PushFold* d_folds = nullptr;
@@ -162,6 +163,10 @@ struct dss_ctx {
   std::vector<void*> peer_push_buf;
   std::vector<unsigned long long*> peer_push_flags;
   int push_occupancy = 0;
+  // one-shot (small rows): double-buffered staging [2][P][G][d_pad] + flags [2][P][G][n_chunks]
+  bool oneshot = false;
+  long oneshot_half_elems = 0, oneshot_half_flags = 0;
+  unsigned long long oneshot_seq = 0;
   // dss_step_host pipeline
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   cudaEvent_t ev_in = nullptr, ev_free = nullptr, ev_snap = nullptr, ev_out = nullptr;
@@ -443,8 +448,11 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
 
 // Fused two-shot tables of parity t for this GPU (one member per GPU in
 // every two-shot group).
+PushLaunch build_oneshot(dss_ctx* c, const Partition& part);
+
 PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
   (void)t;
+  if (c->oneshot) return build_oneshot(c, part);
   PushLaunch pl;
   const int G = c->cfg.n_gpus;
   const int me = c->cfg.rank;
@@ -514,6 +522,7 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
       f.flag_ld = mine.nch;
       f.S = S;
       f.dst_beg = dst_beg;
+      f.n_dst = m;
       f.err_rank = mem[0];
       folds.push_back(f);
     }
@@ -529,6 +538,86 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
   pl.items = static_cast<int>(items.size());
   pl.folds = static_cast<int>(folds.size());
   pl.d_items = upload_table(c, items);
+  pl.d_folds = upload_table(c, folds);
+  pl.d_dst = upload_table(c, dst);
+  return pl;
+}
+
+// One-shot tables of parity t for this GPU: my member's stepped row goes to
+// every member GPU's staging (row lr_o * G + j on GPU o, lr_o the member's
+// local row there, j my position in the group); every GPU folds all S rows
+// of its own member in ascending order and keeps the mean locally.
+PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
+  PushLaunch pl;
+  pl.oneshot = true;
+  const int G = c->cfg.n_gpus;
+  const int me = c->cfg.rank;
+  const long CH = c->chain_chunk;
+  const long nch = c->chain_nchunks;
+  const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, G, me, c->d_pad, force_chain(c));
+  std::vector<PushItem> items;
+  std::vector<std::pair<long, long>> item_keys;
+  std::vector<PushFold> folds;
+  std::vector<void*> dst;
+  for (int gi : gp.spanning_groups) {
+    bool chain = false;
+    for (const ChainRole& r : gp.chain) chain = chain || r.group == gi;
+    if (chain) continue;
+    const int* mem = part.group(gi);
+    const int m = part.size(gi);
+    int j = -1, my_member = -1;
+    for (int q = 0; q < m; ++q) {
+      if (mem[q] / c->P == me) {
+        j = q;
+        my_member = mem[q];
+      }
+    }
+    if (j < 0) continue;
+    for (int oo = 0; oo < m; ++oo) {
+      const int o = (oo + j) % m;  // every GPU starts at a different destination
+      const int gpu = mem[o] / c->P;
+      const long row = static_cast<long>(mem[o] - gpu * c->P) * G + j;
+      char* stage = static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpu)]) +
+                    static_cast<size_t>(row * c->d_pad) * c->esz;
+      unsigned long long* flags = c->peer_push_flags[static_cast<size_t>(gpu)] + row * nch;
+      for (long ch = 0; ch < nch; ++ch) {
+        PushItem it{};
+        it.lr = my_member - c->first;
+        it.lo = ch * CH;
+        it.hi = std::min(c->d_pad, it.lo + CH);
+        it.dst = stage + static_cast<size_t>(it.lo) * c->esz;
+        it.flag = flags + ch;
+        it.rank = my_member;
+        item_keys.push_back({ch * 64 + oo, static_cast<long>(items.size())});
+        items.push_back(it);
+      }
+    }
+    const long row0 = static_cast<long>(my_member - c->first) * G;
+    const int dst_beg = static_cast<int>(dst.size());
+    dst.push_back(static_cast<char*>(c->w) + static_cast<size_t>(my_member - c->first) * c->d_pad * c->esz);
+    for (long ch = 0; ch < nch; ++ch) {
+      PushFold f{};
+      f.lo = ch * CH;
+      f.hi = std::min(c->d_pad, f.lo + CH);
+      f.stage = static_cast<char*>(c->push_buf) + static_cast<size_t>(row0 * c->d_pad + f.lo) * c->esz;
+      f.stage_ld = c->d_pad;
+      f.flags = c->push_flags + row0 * nch + ch;
+      f.flag_ld = nch;
+      f.S = m;
+      f.dst_beg = dst_beg;
+      f.n_dst = 1;
+      f.err_rank = mem[0];
+      folds.push_back(f);
+    }
+  }
+  std::stable_sort(item_keys.begin(), item_keys.end(),
+                   [](const std::pair<long, long>& x, const std::pair<long, long>& y) { return x.first < y.first; });
+  std::vector<PushItem> ordered;
+  ordered.reserve(items.size());
+  for (const auto& k : item_keys) ordered.push_back(items[static_cast<size_t>(k.second)]);
+  pl.items = static_cast<int>(ordered.size());
+  pl.folds = static_cast<int>(folds.size());
+  pl.d_items = upload_table(c, ordered);
   pl.d_folds = upload_table(c, folds);
   pl.d_dst = upload_table(c, dst);
   return pl;
@@ -1050,7 +1139,22 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
   const long units_b = c->chain_nchunks * cl.nb;
   TimedLaunch tl(c, DSS_KIND_CHAIN);  // spans both kernels; counts kernel A
   if (cl.na == 0) --c->launches;
-  const bool concurrent = DSS_CHAIN_CONCURRENT && cl.na > 0 && cl.nb > 0;
+  // Concurrency needs room for kernel A beside B's resident CTAs on every SM
+  // (otherwise spinning B CTAs could hold every slot A needs): only the
+  // light store-only B (DS), and only if the register files fit both.
+  bool concurrent = DSS_CHAIN_CONCURRENT && OPTD == kOptNone && cl.na > 0 && cl.nb > 0;
+  if (concurrent) {
+    static int regs_a = -1, regs_b = -1;
+    if (regs_a < 0) {
+      cudaFuncAttributes fa{}, fb{};
+      ck(cudaFuncGetAttributes(&fa, chain_partial_kernel<T, OPTM, OPTD>), "chain attrs");
+      ck(cudaFuncGetAttributes(&fb, chain_mean_kernel<T, OPTD>), "chain attrs");
+      regs_a = fa.numRegs;
+      regs_b = fb.numRegs;
+    }
+    auto cta_regs = [](int r) { return ((r + 7) / 8) * 8 * kThreads; };
+    concurrent = DSS_CHAIN_B_CTAS_PER_SM * cta_regs(regs_b) + cta_regs(regs_a) <= 65536;
+  }
   if (concurrent) {
     // Kernel B only waits on flags released by kernel A (here or on other
     // GPUs), never the reverse: it may run beside A.  Its few resident CTAs
@@ -1159,6 +1263,13 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   a.epoch = c->chain_epoch;
   a.err = c->d_err;
   a.timeout = c->d_timeout;
+  if (pl.oneshot) {
+    // alternate staging buffers: a GPU can only push launch n+2 after every
+    // peer pushed launch n+1, i.e. after every peer finished folding launch n
+    const long par = static_cast<long>(c->oneshot_seq++ & 1);
+    a.stage_shift = par * c->oneshot_half_elems * c->esz;
+    a.flag_shift = par * c->oneshot_half_flags;
+  }
   a.c = consts<T>(c, alpha);
   fill_bias(c, a);
   int occ = 0;
@@ -1490,6 +1601,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     if (cfg->optimizer == DSS_ADAM || cfg->optimizer == DSS_ADAMW) c->m2 = dalloc(c.get(), rows);
     c->mg = dalloc(c.get(), static_cast<size_t>(c->d_pad) * c->esz);
     if (cfg->stats_dim < 0) throw std::invalid_argument("stats_dim must be >= 0");
+    if (cfg->path < 0 || cfg->path > 4) throw std::invalid_argument("path must be 0..4");
     c->s = cfg->stats_dim;
     c->s_pad = c->s > 0 ? pad_dim(c->s) : 0;
     // running statistics rows (always allocated: an IPC handle needs a buffer)
@@ -1533,6 +1645,14 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         owned_layout(c.get(), make_partition(s, t), cfg->rank, c->chain_chunk, &st, &fl);
         ps = std::max(ps, st);
         pf = std::max(pf, fl);
+      }
+      c->oneshot = s.kind == DSS_DS_SYNC && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 &&
+                   c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
+      if (c->oneshot) {
+        c->oneshot_half_elems = static_cast<long>(c->P) * cfg->n_gpus * c->d_pad;
+        c->oneshot_half_flags = static_cast<long>(c->P) * cfg->n_gpus * c->chain_nchunks;
+        ps = std::max(ps, 2 * c->oneshot_half_elems);
+        pf = std::max(pf, 2 * c->oneshot_half_flags);
       }
       c->push_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(ps) * c->esz));
       c->push_flags = static_cast<unsigned long long*>(
@@ -1748,7 +1868,8 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
           launch_fold_any(c, pp.fold, t);
         }
         if (pp.any_chain) launch_chain_any(c, pp.chain, t, alpha);
-        c->pending_remote = multi(c);
+        // one-shot writes no peer params: the next iteration needs no barrier
+        c->pending_remote = multi(c) && (pp.any_chain || !(pp.any_push && pp.push.oneshot));
         fold_stats(c, t, barrier_done);
       } else {
         fold_stats(c, t, false);
@@ -1866,8 +1987,10 @@ void launch_small_t(dss_ctx* c, const SmallArgs<T>& a) {
   ck(cudaGetLastError(), "small_steps_kernel launch");
 }
 
+LogisticArgs logistic_args(dss_ctx* c, long t);
+
 template <typename T>
-void run_small(dss_ctx* c, long t0, long n, const double* alphas) {
+void run_small(dss_ctx* c, long t0, long n, const double* alphas, bool logistic = false) {
   const int P = c->P;
   const dss_strategy& s = c->cfg.strategy;
   if (!c->d_small_members[0]) {  // schedule tables of both parities, once
@@ -1920,6 +2043,10 @@ void run_small(dss_ctx* c, long t0, long n, const double* alphas) {
   a.wd = h.weight_decay;
   a.c = consts<T>(c, 0.0);
   a.err = c->d_err;
+  if (logistic) {
+    a.logistic = 1;
+    a.lg = logistic_args(c, t0);
+  }
   switch (c->cfg.optimizer) {
     case kSgd: launch_small_t<T, kSgd>(c, a); break;
     case kMomentum: launch_small_t<T, kMomentum>(c, a); break;
@@ -2319,7 +2446,7 @@ extern "C" int dss_logistic_setup(dss_ctx* c, const double* x, const double* y, 
 
 namespace {
 
-void launch_logistic(dss_ctx* c, long t) {
+LogisticArgs logistic_args(dss_ctx* c, long t) {
   const auto& L = c->logi;
   LogisticArgs a{};
   a.x = L.x;
@@ -2339,6 +2466,11 @@ void launch_logistic(dss_ctx* c, long t) {
   a.t = t;
   a.first_rank = c->first;
   a.gerr = c->d_gerr;
+  return a;
+}
+
+void launch_logistic(dss_ctx* c, long t) {
+  const LogisticArgs a = logistic_args(c, t);
   TimedLaunch tl(c, DSS_KIND_GRADIENT);
   if (c->cfg.dtype == DSS_F64) {
     logistic_grad_kernel<double><<<c->P, 128, logistic_smem(c->d), c->stream>>>(
@@ -2366,6 +2498,28 @@ extern "C" int dss_logistic_gradients(dss_ctx* c, long t) {
 
 extern "C" int dss_logistic_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
   if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
+  if (small_path(c, n) && c->logi.ready && c->d <= kSmallLogiMaxDim) {
+    // the whole run in one CTA: sampling, gradient, step and group fold
+    const int st = guard(c, [&]() -> int {
+      if (t0 < 0) throw std::invalid_argument("iteration must be >= 0");
+      for (long i = 0; i < n; ++i) {
+        if (!std::isfinite(alphas[i]) || alphas[i] < 0.0) {
+          throw std::invalid_argument("learning rate at t=" + std::to_string(t0 + i) + " must be finite and >= 0");
+        }
+      }
+      ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+      if (c->cfg.dtype == DSS_F64) {
+        run_small<double>(c, t0, n, alphas, true);
+      } else {
+        run_small<float>(c, t0, n, alphas, true);
+      }
+      if (last) *last = round_outcome(c->cfg.strategy, t0 + n - 1, c->d + c->s);
+      return DSS_OK;
+    });
+    if (st != DSS_OK) return st;
+    if (check) return dss_check(c);
+    return DSS_OK;
+  }
   for (long i = 0; i < n; ++i) {
     int st = dss_logistic_gradients(c, t0 + i);
     if (st == DSS_OK) st = dss_step(c, t0 + i, alphas[i], 0, last);

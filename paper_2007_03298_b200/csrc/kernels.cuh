@@ -46,6 +46,11 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 8
 #endif
+// Rows up to this many bytes fold one-shot over NVLink (every member GPU
+// gathers every member's row) instead of two-shot.
+#ifndef DSS_ONESHOT_MAX_BYTES
+#define DSS_ONESHOT_MAX_BYTES (1L << 20)
+#endif
 // 1: run the chain's mean pass (kernel B) concurrently with the partial
 // pass (kernel A) on a side stream, B with DSS_CHAIN_B_CTAS_PER_SM resident
 // CTAs per SM; 0: B after A on the context stream.
@@ -661,6 +666,95 @@ __global__ void __launch_bounds__(kThreads, DSS_MIN_BLOCKS) bsp_kernel(const Bsp
 // __syncthreads() between them instead of a kernel launch.  The schedule of
 // both parities, per-iteration alpha (and alpha*wd) and per-worker bias
 // corrections live in device memory.  Same arithmetic as the other kernels.
+__device__ __forceinline__ uint64_t mix64(uint64_t z);
+
+// ---- logistic regression with device batch sampling ------------------------
+// LogisticProblem::stochastic_gradient (problems.cpp:265-290) fed by
+// sample_batch (sync.cpp:153-179): one CTA per local worker.  Thread 0 draws
+// the batch from the worker's shard with the reference's SplitMix64 streams
+// (integer work: bit-exact indices), then the CTA walks the batch in order:
+// the products x_j * w_j in parallel, their sum sequentially from 0.0 (the
+// reference's dot order), and the per-feature accumulation -y*s*x_j in
+// parallel (each feature's sum keeps the reference's sample order).  Every
+// add/mul is an explicit _rn op; the only inexact step against the
+// reference is exp() in the sigmoid (CUDA's libdevice vs glibc, <= 1 ulp).
+
+__device__ __forceinline__ uint64_t stream_state_dev(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t it) {
+  uint64_t s = mix64(seed + 0x9e3779b97f4a7c15ULL);
+  s = mix64(s ^ purpose);
+  s = mix64(s ^ rank);
+  return mix64(s ^ it);
+}
+
+struct DevRng {  // Rng::next_u64 / uniform_below (rng.cpp:28-43)
+  uint64_t s;
+  __device__ __forceinline__ uint64_t next() {
+    s += 0x9e3779b97f4a7c15ULL;
+    return mix64(s);
+  }
+  __device__ __forceinline__ uint64_t below(uint64_t n) {
+    const uint64_t limit = ~0ULL - ~0ULL % n;
+    uint64_t v = next();
+    while (v >= limit) v = next();
+    return v % n;
+  }
+};
+
+constexpr uint64_t kBatchStream = 0xd6e8feb86659fd93ULL;       // rng.hpp:45
+constexpr uint64_t kEpochOrderStream = 0xe7037ed1a0b428dbULL;  // rng.hpp:47
+
+struct LogisticArgs {
+  const double* x;        // [M][d] row-major
+  const double* y;        // [M] labels in {-1, +1}
+  const int* shard;       // local workers' shards, concatenated
+  const int* shard_off;   // [P + 1]
+  int* order;             // [P][max_shard] cached epoch order (epoch sampling)
+  long* order_epoch;      // [P] epoch held in order (-1 = none)
+  int* batch;             // [P][B] the sampled indices
+  long max_shard;
+  long ld;                // row stride of w / g
+  int d, B, sampling;     // sampling: 0 replacement, 1 epoch
+  double l2;
+  uint64_t seed;
+  long t;
+  int first_rank;
+  unsigned long long* gerr;  // gradient failure latch: t << 32 | rank
+};
+
+__device__ __forceinline__ double softplus_dev(double z) {  // problems.cpp:338-341
+  return z > 0.0 ? __dadd_rn(z, log1p(exp(-z))) : log1p(exp(z));
+}
+
+// sample_batch (sync.cpp:153-179) for local worker k, into a.batch[k].
+__device__ void sample_batch_dev(const LogisticArgs& a, int k) {
+  const int rank = a.first_rank + k;
+  const int* sh = a.shard + a.shard_off[k];
+  const long size = a.shard_off[k + 1] - a.shard_off[k];
+  int* bt = a.batch + static_cast<long>(k) * a.B;
+  if (a.sampling == 0) {
+    DevRng r{stream_state_dev(a.seed, kBatchStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(a.t))};
+    for (int b = 0; b < a.B; ++b) bt[b] = sh[r.below(static_cast<uint64_t>(size))];
+    return;
+  }
+  int* ord = a.order + static_cast<long>(k) * a.max_shard;
+  long pos = a.t * a.B;
+  for (int b = 0; b < a.B; ++b, ++pos) {
+    const long epoch = pos / size;
+    if (a.order_epoch[k] != epoch) {  // epoch_order (problems.cpp:664-674)
+      for (long i = 0; i < size; ++i) ord[i] = sh[i];
+      DevRng r{stream_state_dev(a.seed, kEpochOrderStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(epoch))};
+      for (long i = size - 1; i > 0; --i) {
+        const long j = static_cast<long>(r.below(static_cast<uint64_t>(i + 1)));
+        const int tmp = ord[i];
+        ord[i] = ord[j];
+        ord[j] = tmp;
+      }
+      a.order_epoch[k] = epoch;
+    }
+    bt[b] = ord[pos % size];
+  }
+}
+
 template <typename T> struct SmallArgs {
   T* w;
   const T* g;
@@ -681,7 +775,91 @@ template <typename T> struct SmallArgs {
   double wd;
   StepConsts<T> c;      // alpha / awd overwritten per iteration
   unsigned long long* err;
+  int logistic;         // 1: each iteration first computes the logistic gradients (lg) into g
+  LogisticArgs lg;
 };
+
+constexpr int kSmallLogiMaxDim = 512;  // features per worker in the fused small-world logistic path
+
+// Logistic gradients of every worker at iteration t inside the one-CTA
+// small-world kernel: one warp per worker, lane j owning features j + 32q.
+// Same operation order as logistic_grad_kernel (and the reference): the
+// products in parallel, their sum sequentially on lane 0, the per-feature
+// accumulation in sample order.
+template <typename T>
+__device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
+  constexpr int Q = kSmallLogiMaxDim / 32;
+  __shared__ double prod[kThreads / 32][kSmallLogiMaxDim];
+  __shared__ double sval[kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  LogisticArgs L = a.lg;
+  L.t = t;
+  const int d = L.d;
+  for (int k = warp; k < a.nw; k += kThreads / 32) {
+    if (lane == 0) sample_batch_dev(L, k);
+    __syncwarp();
+    const T* wr = a.w + static_cast<long>(k) * a.ld;
+    double wreg[Q], acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = lane + 32 * q;
+      wreg[q] = j < d ? static_cast<double>(wr[j]) : 0.0;
+      acc[q] = 0.0;
+    }
+    const int* bt = L.batch + static_cast<long>(k) * L.B;
+    double loss = 0.0;
+    for (int b = 0; b < L.B; ++b) {
+      const int idx = bt[b];
+      const double* x = L.x + static_cast<long>(idx) * d;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j = lane + 32 * q;
+        if (j < d) prod[warp][j] = __dmul_rn(x[j], wreg[q]);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const double y = L.y[idx];
+        double z = 0.0;
+        for (int j = 0; j < d; ++j) z = __dadd_rn(z, prod[warp][j]);
+        const double nz = __dmul_rn(-y, z);
+        sval[warp] = __dmul_rn(-y, __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz))));
+        loss = __dadd_rn(loss, softplus_dev(nz));
+      }
+      __syncwarp();
+      const double ys = sval[warp];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int j = lane + 32 * q;
+        if (j < d) acc[q] = __dadd_rn(acc[q], __dmul_rn(ys, x[j]));
+      }
+    }
+    const double inv = __ddiv_rn(1.0, static_cast<double>(L.B));
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = lane + 32 * q;
+      if (j < d) {
+        double v = __dmul_rn(acc[q], inv);
+        if (L.l2 > 0.0) v = __dadd_rn(v, __dmul_rn(L.l2, wreg[q]));
+        bad = bad || !isfinite(v);
+        g[static_cast<long>(k) * a.ld + j] = static_cast<T>(v);
+      }
+    }
+    if (lane == 0) {
+      loss = __dmul_rn(loss, inv);
+      if (L.l2 > 0.0) {
+        double dd = 0.0;
+        for (int j = 0; j < d; ++j) dd = __dadd_rn(dd, __dmul_rn(static_cast<double>(wr[j]), static_cast<double>(wr[j])));
+        loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(0.5, L.l2), dd));
+      }
+      bad = bad || !isfinite(loss);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) {
+      atomicMin(L.gerr, (static_cast<unsigned long long>(t) << 32) | static_cast<unsigned int>(L.first_rank + k));
+    }
+    __syncwarp();
+  }
+}
 
 template <typename T, int OPT>
 __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T> a) {
@@ -692,6 +870,10 @@ __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T
     const long t = a.t0 + i;
     c.alpha = static_cast<T>(a.alpha[i]);
     c.awd = static_cast<T>(a.alpha[i] * a.wd);
+    if (a.logistic) {
+      small_logistic_grads(a, t, const_cast<T*>(a.g));
+      __syncthreads();
+    }
     if (a.bsp) {
       const T inv = static_cast<T>(1.0 / static_cast<double>(a.nw));
       for (long e = threadIdx.x; e < a.nvec; e += blockDim.x) {
@@ -1263,7 +1445,8 @@ struct PushFold {        // phase 2: one chunk of a slice this GPU owns
   const unsigned long long* flags;  // flag of (row 0, this chunk); rows are flag_ld apart
   long flag_ld;
   int S;                 // rows (= members)
-  int dst_beg;           // S member param-row pointers in the dst table
+  int dst_beg;           // member param-row pointers in the dst table
+  int n_dst;             // two-shot: S (every member, peer stores); one-shot: 1 (my member)
   int err_rank;          // members[0]
 };
 
@@ -1283,11 +1466,17 @@ template <typename T> struct PushArgs {
   unsigned long long epoch;
   unsigned long long* err;
   unsigned long long* timeout;
+  long stage_shift;      // one-shot: bytes to this launch's staging buffer (double-buffered), else 0
+  long flag_shift;       // one-shot: flags to this launch's flag set, else 0
   StepConsts<T> c;
   double bc1[kMaxLocal];
   double bc2[kMaxLocal];
 };
 
+// Two-shot (each slice owner folds and stores the mean to every member) or
+// one-shot (every member GPU receives every member's stepped row and folds
+// it for its own member; small rows: no remote stores into params, so the
+// next iteration needs no barrier).  Same kernel, different tables.
 template <typename T, int OPT>
 __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T> a) {
   constexpr int VN = Vec<T>::n;
@@ -1321,10 +1510,10 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
         const unsigned long long k = err_key(a.t, 0, it.rank);
         bad = k < bad ? k : bad;
       }
-      stv_cg(static_cast<T*>(it.dst) + (off - it.lo), x);
+      stv_cg(reinterpret_cast<T*>(static_cast<char*>(it.dst) + a.stage_shift) + (off - it.lo), x);
     }
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys(it.flag, a.epoch);
+    if (threadIdx.x == 0) st_release_sys(it.flag + a.flag_shift, a.epoch);
     __syncthreads();
   }
   // phase 2: ordered fold of owned chunks
@@ -1332,12 +1521,14 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
     if (threadIdx.x == 0) {
       fo = a.folds[u];
       ok_flag = 1;
-      for (int j = 0; j < fo.S && ok_flag; ++j) ok_flag = chain_wait(fo.flags + j * fo.flag_ld, a.epoch, a.timeout);
+      for (int j = 0; j < fo.S && ok_flag; ++j) {
+        ok_flag = chain_wait(fo.flags + a.flag_shift + j * fo.flag_ld, a.epoch, a.timeout);
+      }
     }
     __syncthreads();
     if (ok_flag) {
       const T inv = static_cast<T>(1.0 / static_cast<double>(fo.S));
-      const T* st = static_cast<const T*>(fo.stage);
+      const T* st = reinterpret_cast<const T*>(static_cast<const char*>(fo.stage) + a.stage_shift);
       for (long e = fo.lo / VN + threadIdx.x; e < fo.hi / VN; e += blockDim.x) {
         const long off = e * VN;
         const long so = off - fo.lo;
@@ -1357,7 +1548,7 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
           const unsigned long long k = err_key(a.t, 1, fo.err_rank);
           bad = k < bad ? k : bad;
         }
-        for (int q = 0; q < fo.S; ++q) stv_cg(a.dst[fo.dst_beg + q] + off, acc);
+        for (int q = 0; q < fo.n_dst; ++q) stv_cg(a.dst[fo.dst_beg + q] + off, acc);
       }
     }
     __syncthreads();
@@ -1520,93 +1711,6 @@ __global__ void broadcast_row_kernel(T* base, long ld, int rows, const T* src) {
   const long n = ld * rows;
   for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     base[i] = src[i % ld];
-  }
-}
-
-// ---- logistic regression with device batch sampling ------------------------
-// LogisticProblem::stochastic_gradient (problems.cpp:265-290) fed by
-// sample_batch (sync.cpp:153-179): one CTA per local worker.  Thread 0 draws
-// the batch from the worker's shard with the reference's SplitMix64 streams
-// (integer work: bit-exact indices), then the CTA walks the batch in order:
-// the products x_j * w_j in parallel, their sum sequentially from 0.0 (the
-// reference's dot order), and the per-feature accumulation -y*s*x_j in
-// parallel (each feature's sum keeps the reference's sample order).  Every
-// add/mul is an explicit _rn op; the only inexact step against the
-// reference is exp() in the sigmoid (CUDA's libdevice vs glibc, <= 1 ulp).
-
-__device__ __forceinline__ uint64_t stream_state_dev(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t it) {
-  uint64_t s = mix64(seed + 0x9e3779b97f4a7c15ULL);
-  s = mix64(s ^ purpose);
-  s = mix64(s ^ rank);
-  return mix64(s ^ it);
-}
-
-struct DevRng {  // Rng::next_u64 / uniform_below (rng.cpp:28-43)
-  uint64_t s;
-  __device__ __forceinline__ uint64_t next() {
-    s += 0x9e3779b97f4a7c15ULL;
-    return mix64(s);
-  }
-  __device__ __forceinline__ uint64_t below(uint64_t n) {
-    const uint64_t limit = ~0ULL - ~0ULL % n;
-    uint64_t v = next();
-    while (v >= limit) v = next();
-    return v % n;
-  }
-};
-
-constexpr uint64_t kBatchStream = 0xd6e8feb86659fd93ULL;       // rng.hpp:45
-constexpr uint64_t kEpochOrderStream = 0xe7037ed1a0b428dbULL;  // rng.hpp:47
-
-struct LogisticArgs {
-  const double* x;        // [M][d] row-major
-  const double* y;        // [M] labels in {-1, +1}
-  const int* shard;       // local workers' shards, concatenated
-  const int* shard_off;   // [P + 1]
-  int* order;             // [P][max_shard] cached epoch order (epoch sampling)
-  long* order_epoch;      // [P] epoch held in order (-1 = none)
-  int* batch;             // [P][B] the sampled indices
-  long max_shard;
-  long ld;                // row stride of w / g
-  int d, B, sampling;     // sampling: 0 replacement, 1 epoch
-  double l2;
-  uint64_t seed;
-  long t;
-  int first_rank;
-  unsigned long long* gerr;  // gradient failure latch: t << 32 | rank
-};
-
-__device__ __forceinline__ double softplus_dev(double z) {  // problems.cpp:338-341
-  return z > 0.0 ? __dadd_rn(z, log1p(exp(-z))) : log1p(exp(z));
-}
-
-// sample_batch (sync.cpp:153-179) for local worker k, into a.batch[k].
-__device__ void sample_batch_dev(const LogisticArgs& a, int k) {
-  const int rank = a.first_rank + k;
-  const int* sh = a.shard + a.shard_off[k];
-  const long size = a.shard_off[k + 1] - a.shard_off[k];
-  int* bt = a.batch + static_cast<long>(k) * a.B;
-  if (a.sampling == 0) {
-    DevRng r{stream_state_dev(a.seed, kBatchStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(a.t))};
-    for (int b = 0; b < a.B; ++b) bt[b] = sh[r.below(static_cast<uint64_t>(size))];
-    return;
-  }
-  int* ord = a.order + static_cast<long>(k) * a.max_shard;
-  long pos = a.t * a.B;
-  for (int b = 0; b < a.B; ++b, ++pos) {
-    const long epoch = pos / size;
-    if (a.order_epoch[k] != epoch) {  // epoch_order (problems.cpp:664-674)
-      for (long i = 0; i < size; ++i) ord[i] = sh[i];
-      DevRng r{stream_state_dev(a.seed, kEpochOrderStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(epoch))};
-      for (long i = size - 1; i > 0; --i) {
-        const long j = static_cast<long>(r.below(static_cast<uint64_t>(i + 1)));
-        const int tmp = ord[i];
-        ord[i] = ord[j];
-        ord[j] = tmp;
-      }
-      a.order_epoch[k] = epoch;
-    }
-    bt[b] = ord[pos % size];
   }
 }
 

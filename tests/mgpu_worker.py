@@ -115,7 +115,9 @@ def main():
     for case in CASES:
         if case[1] % G:
             continue
-        for path in (0, 2, 3):  # auto (fused push two-shot / chain by shape), chain forced, unfused pull two-shot
+        # auto (one-shot / fused push two-shot / chain by shape), chain forced,
+        # unfused pull two-shot, auto without one-shot
+        for path in (0, 2, 3, 4):
             ok = run_case(*case, rank, G, orc, path) and ok
     for case in (("ds", 8, 2, True, 2, 1001), ("bsp", 8, 8, False, 1, 777)):  # running-stats tail
         ok = run_case(*case, rank, G, orc, 0, sd=6) and ok

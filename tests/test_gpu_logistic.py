@@ -157,3 +157,22 @@ def test_logistic_setup_errors(cuda_device, c1_data):
         e.logistic_setup(x, y, L2, B, SamplingMode.EPOCH, RUN_SEED)
         with pytest.raises(ValueError, match="iteration must be >= 0"):
             e.logistic_gradients(-1)
+
+
+@pytest.mark.parametrize("kind,N,alpha,rank,what", [("ds", 2, 0.1, 2, "non-finite stochastic gradient"),
+                                                     ("ds", 2, 1e308, 0, "apply_step"),
+                                                     ("bsp", 4, 1e308, 2, "non-finite stochastic gradient")])
+def test_fused_small_world_divergence(cuda_device, c1_data, kind, N, alpha, rank, what):
+    """The one-CTA small-world path (dss_logistic_steps with n >= 2: sampling,
+    gradient, step and fold in one kernel) latches the same errors."""
+    x, y = c1_data
+    w = np.full((4, 20), 100.0)
+    w[2] = 1e200
+    if alpha < 1:
+        w[[0, 1, 3]] = 0.0
+    with engine(kind, 4, N) as e:
+        e.logistic_setup(x, y, L2, B, SamplingMode.REPLACEMENT, RUN_SEED)
+        e.upload_all(BUF_PARAMS, w)
+        with pytest.raises(DivergenceError) as ex:
+            e.logistic_steps(0, [alpha, alpha], check=True)
+        assert ex.value.rank == rank and ex.value.iteration == 0 and what in str(ex.value)
