@@ -1155,30 +1155,31 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
     auto cta_regs = [](int r) { return ((r + 7) / 8) * 8 * kThreads; };
     concurrent = DSS_CHAIN_B_CTAS_PER_SM * cta_regs(regs_b) + cta_regs(regs_a) <= 65536;
   }
+  if (concurrent && !c->side) {
+    ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+    ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
+    ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
+  }
+  if (concurrent) ck(cudaEventRecord(c->ev_fork, c->stream), "fork record");
+  if (cl.na > 0) {
+    // Kernel A is enqueued first: if the driver maps the side stream onto
+    // the same hardware queue, B simply runs after A (the sequential
+    // schedule) and can never block it.  When concurrent, A leaves
+    // DSS_CHAIN_B_CTAS_PER_SM slots per SM for B.
+    a.entries = cl.d_a;
+    a.n_entries = cl.na;
+    const long per_sm = concurrent ? long{DSS_CHAIN_CTAS_PER_SM - DSS_CHAIN_B_CTAS_PER_SM} : long{DSS_CHAIN_CTAS_PER_SM};
+    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units_a, c->sms * per_sm)), kThreads, 0,
+                                          c->stream>>>(a);
+    ck(cudaGetLastError(), "chain_partial_kernel launch");
+  }
   if (concurrent) {
-    // Kernel B only waits on flags released by kernel A (here or on other
-    // GPUs), never the reverse: it may run beside A.  Its few resident CTAs
-    // leave A room on every SM, so a spinning B can never starve A.
-    if (!c->side) {
-      ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
-      ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
-      ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
-    }
-    ck(cudaEventRecord(c->ev_fork, c->stream), "fork record");
+    // B waits only on flags released by kernel A (here or on other GPUs)
     ck(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork wait");
     chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units_b, c->sms * long{DSS_CHAIN_B_CTAS_PER_SM})),
                                  kThreads, 0, c->side>>>(b);
     ck(cudaGetLastError(), "chain_mean_kernel launch");
     ++c->launches;
-  }
-  if (cl.na > 0) {
-    a.entries = cl.d_a;
-    a.n_entries = cl.na;
-    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units_a, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
-                                          kThreads, 0, c->stream>>>(a);
-    ck(cudaGetLastError(), "chain_partial_kernel launch");
-  }
-  if (concurrent) {
     ck(cudaEventRecord(c->ev_join, c->side), "join record");
     ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join wait");
   } else if (cl.nb > 0) {
