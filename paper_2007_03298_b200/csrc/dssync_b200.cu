@@ -164,7 +164,10 @@ struct dss_ctx {
   std::vector<unsigned long long*> peer_push_flags;
   int push_occupancy = 0;
   // one-shot (small rows): double-buffered staging [2][P][G][d_pad] + flags [2][P][G][n_chunks]
-  bool oneshot = false;
+  // one-shot area after the two-shot staging: [2][P][G][d_pad] rows +
+  // [2][P][G][n_chunks] flags, double-buffered by one-shot launch count
+  bool oneshot[2] = {false, false};  // per schedule parity (same on every GPU)
+  long oneshot_base_elems = 0, oneshot_base_flags = 0;
   long oneshot_half_elems = 0, oneshot_half_flags = 0;
   unsigned long long oneshot_seq = 0;
   // dss_step_host pipeline
@@ -452,7 +455,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part);
 
 PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
   (void)t;
-  if (c->oneshot) return build_oneshot(c, part);
+  if (c->oneshot[t & 1]) return build_oneshot(c, part);
   PushLaunch pl;
   const int G = c->cfg.n_gpus;
   const int me = c->cfg.rank;
@@ -1268,8 +1271,8 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
     // alternate staging buffers: a GPU can only push launch n+2 after every
     // peer pushed launch n+1, i.e. after every peer finished folding launch n
     const long par = static_cast<long>(c->oneshot_seq++ & 1);
-    a.stage_shift = par * c->oneshot_half_elems * c->esz;
-    a.flag_shift = par * c->oneshot_half_flags;
+    a.stage_shift = (c->oneshot_base_elems + par * c->oneshot_half_elems) * c->esz;
+    a.flag_shift = c->oneshot_base_flags + par * c->oneshot_half_flags;
   }
   a.c = consts<T>(c, alpha);
   fill_bias(c, a);
@@ -1647,13 +1650,29 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         ps = std::max(ps, st);
         pf = std::max(pf, fl);
       }
-      c->oneshot = s.kind == DSS_DS_SYNC && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 &&
-                   c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
-      if (c->oneshot) {
+      // One-shot per schedule parity: every member GPU gathers every
+      // member's row.  Same NVLink bytes as two-shot for pairs (S = 2) and
+      // no barrier before the next iteration; for S > 2 only small rows.
+      for (long t = 0; t < 2; ++t) {
+        if (s.kind != DSS_DS_SYNC || !use_push(c.get()) || force_chain(c.get()) || cfg->path == 4) break;
+        const Partition part = make_partition(s, t);
+        bool ok = true;
+        for (int gi = 0; gi < part.n_groups(); ++gi) {
+          std::vector<int> gpus;
+          for (int q = 0; q < part.size(gi); ++q) gpus.push_back(part.group(gi)[q] / c->P);
+          const bool spans = gpus.front() != gpus.back();
+          const bool one_each = std::adjacent_find(gpus.begin(), gpus.end()) == gpus.end();
+          if (spans && one_each && part.size(gi) > 2 && c->d_pad * c->esz > DSS_ONESHOT_MAX_BYTES) ok = false;
+        }
+        c->oneshot[t] = ok;
+      }
+      if (c->oneshot[0] || c->oneshot[1]) {
+        c->oneshot_base_elems = ps;
+        c->oneshot_base_flags = pf;
         c->oneshot_half_elems = static_cast<long>(c->P) * cfg->n_gpus * c->d_pad;
         c->oneshot_half_flags = static_cast<long>(c->P) * cfg->n_gpus * c->chain_nchunks;
-        ps = std::max(ps, 2 * c->oneshot_half_elems);
-        pf = std::max(pf, 2 * c->oneshot_half_flags);
+        ps += 2 * c->oneshot_half_elems;
+        pf += 2 * c->oneshot_half_flags;
       }
       c->push_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(ps) * c->esz));
       c->push_flags = static_cast<unsigned long long*>(

@@ -53,9 +53,12 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #endif
 // 1: run the chain's mean pass (kernel B) concurrently with the partial
 // pass (kernel A) on a side stream, B with DSS_CHAIN_B_CTAS_PER_SM resident
-// CTAs per SM; 0: B after A on the context stream.
+// CTAs per SM; 0: B after A on the context stream.  Measured at 2 GPUs
+// (C2 / C3): concurrent 2534 / 369 iters/s (B=2), 2821 / 441 (B=4) vs
+// sequential 3126 / 480 -- A loses more from the slots it gives up than B
+// gains, so the default is sequential.
 #ifndef DSS_CHAIN_CONCURRENT
-#define DSS_CHAIN_CONCURRENT 1
+#define DSS_CHAIN_CONCURRENT 0
 #endif
 #ifndef DSS_CHAIN_B_CTAS_PER_SM
 #define DSS_CHAIN_B_CTAS_PER_SM 2
