@@ -94,11 +94,15 @@ struct ChainLaunch {
   int* d_dst_lr = nullptr;         // local row index of each destination
   int opt_mem = -1;                // fused step on the members (DS), kOptNone = fold only
   int opt_dst = -1;                // fused step of the destinations with the mean (BSP)
+  unsigned* d_order = nullptr;     // merged-kernel unit order (see chain_merged_kernel)
+  long n_order = 0;
 };
 
 struct PushLaunch {
   bool oneshot = false;
   int items = 0, folds = 0;
+  void** d_item_dst = nullptr;
+  unsigned long long** d_item_flag = nullptr;
   PushItem* d_items = nullptr;
   PushFold* d_folds = nullptr;
   void** d_dst = nullptr;
@@ -440,6 +444,26 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
   }
   cl.na = static_cast<int>(ea.size());
   cl.nb = static_cast<int>(eb.size());
+  if (DSS_CHAIN_MERGED && cl.na > 0 && cl.nb > 0) {
+    // slot s: the partial-pass units of chunk s, then the mean-pass units
+    // of chunk s - lag; lag ~ one resident round of CTAs
+    const long nch = c->chain_nchunks;
+    const long round = static_cast<long>(c->sms) * DSS_CHAIN_CTAS_PER_SM;
+    const long lag = std::max<long>(1, static_cast<long>(DSS_CHAIN_MERGE_LAG * round / (cl.na + cl.nb)));
+    std::vector<unsigned> order;
+    order.reserve(static_cast<size_t>(nch) * (cl.na + cl.nb));
+    for (long sl = 0; sl < nch + lag; ++sl) {
+      if (sl < nch) {
+        for (int e = 0; e < cl.na; ++e) order.push_back(static_cast<unsigned>(sl * cl.na + e));
+      }
+      if (sl >= lag) {
+        for (int e = 0; e < cl.nb; ++e) order.push_back(0x80000000u | static_cast<unsigned>((sl - lag) * cl.nb + e));
+      }
+    }
+    if (static_cast<long>(nch) * std::max(cl.na, cl.nb) >= 0x7fffffffL) throw std::invalid_argument("chain too long");
+    cl.n_order = static_cast<long>(order.size());
+    cl.d_order = upload_table(c, order);
+  }
   cl.d_a = upload_table(c, ea);
   cl.d_b = upload_table(c, eb);
   cl.d_src = upload_table(c, src);
@@ -469,6 +493,8 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
     throw std::logic_error("push: owner slot not found");
   };
   std::vector<PushItem> items;
+  std::vector<void*> item_dst;
+  std::vector<unsigned long long*> item_flag;
   std::vector<std::pair<long, long>> item_keys;  // (chunk-major, owner) order key, index
   std::vector<PushFold> folds;
   std::vector<void*> dst;
@@ -504,8 +530,10 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
         it.lr = my_member - c->first;
         it.lo = sl.lo + ch * CH;
         it.hi = std::min(sl.hi, it.lo + CH);
-        it.dst = stage + static_cast<size_t>(it.lo - sl.lo) * c->esz;
-        it.flag = flags + ch;
+        it.dst_beg = static_cast<int>(item_dst.size());
+        it.ndst = 1;
+        item_dst.push_back(stage + static_cast<size_t>(it.lo - sl.lo) * c->esz);
+        item_flag.push_back(flags + ch);
         it.rank = my_member;
         item_keys.push_back({ch * 64 + oo, static_cast<long>(items.size())});
         items.push_back(it);
@@ -540,6 +568,8 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
   items.swap(ordered);
   pl.items = static_cast<int>(items.size());
   pl.folds = static_cast<int>(folds.size());
+  pl.d_item_dst = upload_table(c, item_dst);
+  pl.d_item_flag = upload_table(c, item_flag);
   pl.d_items = upload_table(c, items);
   pl.d_folds = upload_table(c, folds);
   pl.d_dst = upload_table(c, dst);
@@ -559,7 +589,8 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   const long nch = c->chain_nchunks;
   const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, G, me, c->d_pad, force_chain(c));
   std::vector<PushItem> items;
-  std::vector<std::pair<long, long>> item_keys;
+  std::vector<void*> item_dst;
+  std::vector<unsigned long long*> item_flag;
   std::vector<PushFold> folds;
   std::vector<void*> dst;
   for (int gi : gp.spanning_groups) {
@@ -576,24 +607,25 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
       }
     }
     if (j < 0) continue;
-    for (int oo = 0; oo < m; ++oo) {
-      const int o = (oo + j) % m;  // every GPU starts at a different destination
-      const int gpu = mem[o] / c->P;
-      const long row = static_cast<long>(mem[o] - gpu * c->P) * G + j;
-      char* stage = static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpu)]) +
-                    static_cast<size_t>(row * c->d_pad) * c->esz;
-      unsigned long long* flags = c->peer_push_flags[static_cast<size_t>(gpu)] + row * nch;
-      for (long ch = 0; ch < nch; ++ch) {
-        PushItem it{};
-        it.lr = my_member - c->first;
-        it.lo = ch * CH;
-        it.hi = std::min(c->d_pad, it.lo + CH);
-        it.dst = stage + static_cast<size_t>(it.lo) * c->esz;
-        it.flag = flags + ch;
-        it.rank = my_member;
-        item_keys.push_back({ch * 64 + oo, static_cast<long>(items.size())});
-        items.push_back(it);
+    // one item per chunk of my member: stepped once, stored to all m
+    // stagings (every GPU starting at a different destination)
+    for (long ch = 0; ch < nch; ++ch) {
+      PushItem it{};
+      it.lr = my_member - c->first;
+      it.lo = ch * CH;
+      it.hi = std::min(c->d_pad, it.lo + CH);
+      it.dst_beg = static_cast<int>(item_dst.size());
+      it.ndst = m;
+      it.rank = my_member;
+      for (int oo = 0; oo < m; ++oo) {
+        const int o = (oo + j) % m;
+        const int gpu = mem[o] / c->P;
+        const long row = static_cast<long>(mem[o] - gpu * c->P) * G + j;
+        item_dst.push_back(static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpu)]) +
+                           static_cast<size_t>(row * c->d_pad + it.lo) * c->esz);
+        item_flag.push_back(c->peer_push_flags[static_cast<size_t>(gpu)] + row * nch + ch);
       }
+      items.push_back(it);
     }
     const long row0 = static_cast<long>(my_member - c->first) * G;
     const int dst_beg = static_cast<int>(dst.size());
@@ -613,13 +645,17 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
       folds.push_back(f);
     }
   }
-  std::stable_sort(item_keys.begin(), item_keys.end(),
-                   [](const std::pair<long, long>& x, const std::pair<long, long>& y) { return x.first < y.first; });
+  // chunk-major across this GPU's groups
   std::vector<PushItem> ordered;
   ordered.reserve(items.size());
-  for (const auto& k : item_keys) ordered.push_back(items[static_cast<size_t>(k.second)]);
+  const size_t ng = nch ? items.size() / static_cast<size_t>(nch) : 0;
+  for (long ch = 0; ch < nch; ++ch) {
+    for (size_t g = 0; g < ng; ++g) ordered.push_back(items[g * static_cast<size_t>(nch) + static_cast<size_t>(ch)]);
+  }
   pl.items = static_cast<int>(ordered.size());
   pl.folds = static_cast<int>(folds.size());
+  pl.d_item_dst = upload_table(c, item_dst);
+  pl.d_item_flag = upload_table(c, item_flag);
   pl.d_items = upload_table(c, ordered);
   pl.d_folds = upload_table(c, folds);
   pl.d_dst = upload_table(c, dst);
@@ -1158,6 +1194,25 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
     auto cta_regs = [](int r) { return ((r + 7) / 8) * 8 * kThreads; };
     concurrent = DSS_CHAIN_B_CTAS_PER_SM * cta_regs(regs_b) + cta_regs(regs_a) <= 65536;
   }
+  if (DSS_CHAIN_MERGED && cl.d_order) {
+    static int occ = -1;
+    if (occ < 0) {
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chain_merged_kernel<T, OPTM, OPTD>, kThreads, 0),
+         "chain occupancy");
+      occ = std::max(occ, 1);
+    }
+    a.entries = cl.d_a;
+    a.n_entries = cl.na;
+    a.entries_b = cl.d_b;
+    a.n_entries_b = cl.nb;
+    a.order = cl.d_order;
+    a.n_order = cl.n_order;
+    // fully resident: every position is visited in order by a live CTA
+    chain_merged_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(cl.n_order, static_cast<long>(c->sms) * occ)),
+                                         kThreads, 0, c->stream>>>(a);
+    ck(cudaGetLastError(), "chain_merged_kernel launch");
+    return;
+  }
   if (concurrent && !c->side) {
     ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
     ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
@@ -1254,6 +1309,8 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   PushArgs<T> a{};
   a.items = pl.d_items;
   a.n_items = pl.items;
+  a.item_dst = pl.d_item_dst;
+  a.item_flag = pl.d_item_flag;
   a.folds = pl.d_folds;
   a.n_folds = pl.folds;
   a.dst = reinterpret_cast<T* const*>(pl.d_dst);

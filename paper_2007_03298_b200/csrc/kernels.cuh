@@ -51,6 +51,15 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_ONESHOT_MAX_BYTES
 #define DSS_ONESHOT_MAX_BYTES (1L << 20)
 #endif
+// 1: both chain passes in one persistent kernel (chain_merged_kernel), the
+// mean-pass units DSS_CHAIN_MERGE_LAG resident rounds behind the partial
+// pass; 0: two kernels.
+#ifndef DSS_CHAIN_MERGED
+#define DSS_CHAIN_MERGED 1
+#endif
+#ifndef DSS_CHAIN_MERGE_LAG
+#define DSS_CHAIN_MERGE_LAG 1.0
+#endif
 // 1: run the chain's mean pass (kernel B) concurrently with the partial
 // pass (kernel A) on a side stream, B with DSS_CHAIN_B_CTAS_PER_SM resident
 // CTAs per SM; 0: B after A on the context stream.  Measured at 2 GPUs
@@ -758,6 +767,33 @@ __device__ void sample_batch_dev(const LogisticArgs& a, int k) {
   }
 }
 
+// Is the batch loss of checked_gradient (problems.cpp:277-287, sync.cpp:186)
+// finite?  Every term softplus(nz) <= max(nz, 0) + log 2, so when the
+// largest nz, the batch size and the l2 term keep the sum far below the
+// overflow threshold the loss is finite without evaluating log1p/exp on the
+// critical path.  Otherwise (exploding params only) the exact loss is
+// evaluated in the reference's order.
+template <typename T>
+__device__ bool logistic_loss_finite(const LogisticArgs& a, const int* bt, const T* wr, double max_nz, bool nan_nz) {
+  if (nan_nz) return false;
+  double dd = 0.0;
+  if (a.l2 > 0.0) {
+    for (int j = 0; j < a.d; ++j) dd = __dadd_rn(dd, __dmul_rn(static_cast<double>(wr[j]), static_cast<double>(wr[j])));
+  }
+  const double reg = __dmul_rn(__dmul_rn(0.5, a.l2), dd);
+  if (max_nz < 1e300 / static_cast<double>(a.B) && reg < 1e300) return true;
+  double loss = 0.0;
+  for (int b = 0; b < a.B; ++b) {
+    const double* x = a.x + static_cast<long>(bt[b]) * a.d;
+    double z = 0.0;
+    for (int j = 0; j < a.d; ++j) z = __dadd_rn(z, __dmul_rn(x[j], static_cast<double>(wr[j])));
+    loss = __dadd_rn(loss, softplus_dev(__dmul_rn(-a.y[bt[b]], z)));
+  }
+  loss = __dmul_rn(loss, __ddiv_rn(1.0, static_cast<double>(a.B)));
+  if (a.l2 > 0.0) loss = __dadd_rn(loss, reg);
+  return isfinite(loss);
+}
+
 template <typename T> struct SmallArgs {
   T* w;
   const T* g;
@@ -810,7 +846,8 @@ __device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
       acc[q] = 0.0;
     }
     const int* bt = L.batch + static_cast<long>(k) * L.B;
-    double loss = 0.0;
+    double max_nz = 0.0;
+    bool nan_nz = false;
     for (int b = 0; b < L.B; ++b) {
       const int idx = bt[b];
       const double* x = L.x + static_cast<long>(idx) * d;
@@ -826,7 +863,8 @@ __device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
         for (int j = 0; j < d; ++j) z = __dadd_rn(z, prod[warp][j]);
         const double nz = __dmul_rn(-y, z);
         sval[warp] = __dmul_rn(-y, __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz))));
-        loss = __dadd_rn(loss, softplus_dev(nz));
+        max_nz = fmax(max_nz, nz);
+        nan_nz = nan_nz || isnan(nz);
       }
       __syncwarp();
       const double ys = sval[warp];
@@ -848,15 +886,7 @@ __device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
         g[static_cast<long>(k) * a.ld + j] = static_cast<T>(v);
       }
     }
-    if (lane == 0) {
-      loss = __dmul_rn(loss, inv);
-      if (L.l2 > 0.0) {
-        double dd = 0.0;
-        for (int j = 0; j < d; ++j) dd = __dadd_rn(dd, __dmul_rn(static_cast<double>(wr[j]), static_cast<double>(wr[j])));
-        loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(0.5, L.l2), dd));
-      }
-      bad = bad || !isfinite(loss);
-    }
+    if (lane == 0) bad = bad || !logistic_loss_finite(L, bt, wr, max_nz, nan_nz);
     if (__any_sync(0xffffffffu, bad) && lane == 0) {
       atomicMin(L.gerr, (static_cast<unsigned long long>(t) << 32) | static_cast<unsigned int>(L.first_rank + k));
     }
@@ -1156,6 +1186,12 @@ template <typename T> struct ChainArgs {
   StepConsts<T> c;
   double bc1[kMaxLocal];
   double bc2[kMaxLocal];
+  // merged launch (chain_merged_kernel): kernel B's entries and the unit
+  // order, each unit = kind << 31 | chunk * n_entries(kind) + entry
+  const ChainEntry* entries_b;
+  int n_entries_b;
+  const unsigned* order;
+  long n_order;
 };
 
 __device__ __forceinline__ bool chain_wait(const unsigned long long* flag, unsigned long long epoch,
@@ -1270,109 +1306,123 @@ __device__ __forceinline__ void chain_deliver(const ChainArgs<T>& a, const Chain
 // once (w, g, state) and written once (state now, the mean later) while the
 // chunk's partial goes over NVLink.
 template <typename T, int OPTM, int OPTD>
-__global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs<T> a) {
+__device__ __forceinline__ void chain_unit_a(const ChainArgs<T>& a, const ChainEntry* entries, int n_entries, long u,
+                                             ChainEntry& en, int& ok_flag, unsigned long long& bad) {
   constexpr int VN = Vec<T>::n;
+  const long c = u / n_entries;
+  const int ei = static_cast<int>(u % n_entries);
+  if (threadIdx.x == 0) {
+    en = entries[ei];
+    ok_flag = 1;
+    if (en.stage > 0) ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
+  }
+  __syncthreads();
+  const long lo = c * a.chunk;
+  const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
+  const T inv = static_cast<T>(1.0 / static_cast<double>(en.m));
+  if (ok_flag) {
+    for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+      const long off = e * VN;
+      Pack<T> acc;
+      if constexpr (OPTM != kOptNone) {
+        // fused member step, members in load batches of up to 4, folded
+        // in ascending order straight from registers
+        int j = 0;
+        bool first = en.stage == 0;
+        if (!first) acc = ldv_cg(static_cast<const T*>(en.recv) + off);
+        while (j < en.run_cnt) {
+          const int nb = en.run_cnt - j >= 4 ? 4 : (en.run_cnt - j >= 2 ? 2 : 1);
+          Pack<T> gv[4], x[4];
+          const int* lrs = a.src_lr + en.run_beg + j;
+          for (int q = 0; q < nb; ++q) gv[q] = ldv(a.g + static_cast<long>(lrs[q]) * a.ld + off);
+          if (nb == 4) {
+            chain_step_batch<T, OPTM, 4>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
+          } else if (nb == 2) {
+            chain_step_batch<T, OPTM, 2>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
+          } else {
+            chain_step_batch<T, OPTM, 1>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
+          }
+          for (int q = 0; q < nb; ++q) {
+            if (first) {
+              acc = x[q];
+              first = false;
+            } else {
+#pragma unroll
+              for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x[q].v[l]);
+            }
+          }
+          j += nb;
+        }
+      } else {
+        int j0 = 0;
+        if (en.stage == 0) {
+          acc = ldv(a.src[en.run_beg] + off);
+          j0 = 1;
+        } else {
+          acc = ldv_cg(static_cast<const T*>(en.recv) + off);
+        }
+        for (int j = j0; j < en.run_cnt; ++j) {
+          const Pack<T> x = ldv(a.src[en.run_beg + j] + off);
+#pragma unroll
+          for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
+        }
+      }
+      if (!en.last) {
+        stv_cg(static_cast<T*>(en.send) + off, acc);
+      } else {
+        bool ok = true;
+#pragma unroll
+        for (int l = 0; l < VN; ++l) {
+          acc.v[l] = mul_(acc.v[l], inv);
+          ok = ok && finite_(acc.v[l]);
+        }
+        if (!ok) {
+          const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
+          bad = k < bad ? k : bad;
+        }
+        if (en.send) stv_cg(static_cast<T*>(en.send) + off, acc);
+        if constexpr (OPTD == kOptNone) {
+          chain_deliver<T, OPTD>(a, en, off, acc, bad);
+        } else {
+          stv(a.stage + off, acc);  // replicas step after the flag is out
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && en.send) {
+    if (DSS_CHAIN_FENCE) __threadfence_system();
+    st_release_sys(en.send_flags + c, a.epoch);
+  }
+  if constexpr (OPTD != kOptNone) {
+    // the next GPU already has this chunk: now step the local replicas
+    // with it, off the inter-GPU critical path
+    if (ok_flag && en.last) {
+      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+        const long off = e * VN;
+        chain_deliver<T, OPTD>(a, en, off, ldv(a.stage + off), bad);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Kernel A: the ordered partial pass.  Work unit = (chunk, entry), visited
+// chunk-major so every chain advances together.  A CTA only ever waits on a
+// flag written by the previous GPU's kernel A, which itself only waits on
+// GPUs before it: no cycle, no same-GPU dependency.  OPTM != none fuses the
+// members' optimizer step into the pass (DS): the stepped params are folded
+// straight from registers and never written back -- each member row is read
+// once (w, g, state) and written once (state now, the mean later) while the
+// chunk's partial goes over NVLink.
+template <typename T, int OPTM, int OPTD>
+__global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs<T> a) {
   __shared__ ChainEntry en;
   __shared__ int ok_flag;
   const long units = a.n_chunks * a.n_entries;
   unsigned long long bad = ~0ull;
   for (long u = blockIdx.x; u < units; u += gridDim.x) {
-    const long c = u / a.n_entries;
-    const int ei = static_cast<int>(u % a.n_entries);
-    if (threadIdx.x == 0) {
-      en = a.entries[ei];
-      ok_flag = 1;
-      if (en.stage > 0) ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
-    }
-    __syncthreads();
-    const long lo = c * a.chunk;
-    const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
-    const T inv = static_cast<T>(1.0 / static_cast<double>(en.m));
-    if (ok_flag) {
-      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
-        const long off = e * VN;
-        Pack<T> acc;
-        if constexpr (OPTM != kOptNone) {
-          // fused member step, members in load batches of up to 4, folded
-          // in ascending order straight from registers
-          int j = 0;
-          bool first = en.stage == 0;
-          if (!first) acc = ldv_cg(static_cast<const T*>(en.recv) + off);
-          while (j < en.run_cnt) {
-            const int nb = en.run_cnt - j >= 4 ? 4 : (en.run_cnt - j >= 2 ? 2 : 1);
-            Pack<T> gv[4], x[4];
-            const int* lrs = a.src_lr + en.run_beg + j;
-            for (int q = 0; q < nb; ++q) gv[q] = ldv(a.g + static_cast<long>(lrs[q]) * a.ld + off);
-            if (nb == 4) {
-              chain_step_batch<T, OPTM, 4>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
-            } else if (nb == 2) {
-              chain_step_batch<T, OPTM, 2>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
-            } else {
-              chain_step_batch<T, OPTM, 1>(a, a.src + en.run_beg + j, lrs, off, gv, x, bad, a.step_phase);
-            }
-            for (int q = 0; q < nb; ++q) {
-              if (first) {
-                acc = x[q];
-                first = false;
-              } else {
-#pragma unroll
-                for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x[q].v[l]);
-              }
-            }
-            j += nb;
-          }
-        } else {
-          int j0 = 0;
-          if (en.stage == 0) {
-            acc = ldv(a.src[en.run_beg] + off);
-            j0 = 1;
-          } else {
-            acc = ldv_cg(static_cast<const T*>(en.recv) + off);
-          }
-          for (int j = j0; j < en.run_cnt; ++j) {
-            const Pack<T> x = ldv(a.src[en.run_beg + j] + off);
-#pragma unroll
-            for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
-          }
-        }
-        if (!en.last) {
-          stv_cg(static_cast<T*>(en.send) + off, acc);
-        } else {
-          bool ok = true;
-#pragma unroll
-          for (int l = 0; l < VN; ++l) {
-            acc.v[l] = mul_(acc.v[l], inv);
-            ok = ok && finite_(acc.v[l]);
-          }
-          if (!ok) {
-            const unsigned long long k = err_key(a.t, en.err_phase, en.err_rank);
-            bad = k < bad ? k : bad;
-          }
-          if (en.send) stv_cg(static_cast<T*>(en.send) + off, acc);
-          if constexpr (OPTD == kOptNone) {
-            chain_deliver<T, OPTD>(a, en, off, acc, bad);
-          } else {
-            stv(a.stage + off, acc);  // replicas step after the flag is out
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && en.send) {
-      if (DSS_CHAIN_FENCE) __threadfence_system();
-      st_release_sys(en.send_flags + c, a.epoch);
-    }
-    if constexpr (OPTD != kOptNone) {
-      // the next GPU already has this chunk: now step the local replicas
-      // with it, off the inter-GPU critical path
-      if (ok_flag && en.last) {
-        for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
-          const long off = e * VN;
-          chain_deliver<T, OPTD>(a, en, off, ldv(a.stage + off), bad);
-        }
-      }
-    }
-    __syncthreads();
+    chain_unit_a<T, OPTM, OPTD>(a, a.entries, a.n_entries, u, en, ok_flag, bad);
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
@@ -1380,45 +1430,76 @@ __global__ void __launch_bounds__(kThreads) chain_partial_kernel(const ChainArgs
 // Kernel B: the mean pass g_{S-1} -> g_0 -> ... -> g_{S-2}: wait for the
 // chunk, deliver it on this GPU (store, or step the replicas: BSP), forward.
 template <typename T, int OPTD>
-__global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T> a) {
+__device__ __forceinline__ void chain_unit_b(const ChainArgs<T>& a, const ChainEntry* entries, int n_entries, long u,
+                                             ChainEntry& en, int& ok_flag, unsigned long long& bad) {
   constexpr int VN = Vec<T>::n;
+  const long c = u / n_entries;
+  const int ei = static_cast<int>(u % n_entries);
+  if (threadIdx.x == 0) {
+    en = entries[ei];
+    ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
+  }
+  __syncthreads();
+  const long lo = c * a.chunk;
+  const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
+  if (ok_flag) {
+    for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+      const long off = e * VN;
+      const Pack<T> mean = ldv_cg(static_cast<const T*>(en.recv) + off);
+      if (en.send) stv_cg(static_cast<T*>(en.send) + off, mean);
+      if constexpr (OPTD == kOptNone) chain_deliver<T, OPTD>(a, en, off, mean, bad);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && en.send) {
+    if (DSS_CHAIN_FENCE) __threadfence_system();
+    st_release_sys(en.send_flags + c, a.epoch);
+  }
+  if constexpr (OPTD != kOptNone) {
+    // forwarded: now the (HBM-heavy) replica step, off the critical path
+    if (ok_flag) {
+      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+        const long off = e * VN;
+        chain_deliver<T, OPTD>(a, en, off, ldv_cg(static_cast<const T*>(en.recv) + off), bad);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int OPTD>
+__global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T> a) {
   __shared__ ChainEntry en;
   __shared__ int ok_flag;
   const long units = a.n_chunks * a.n_entries;
   unsigned long long bad = ~0ull;
   for (long u = blockIdx.x; u < units; u += gridDim.x) {
-    const long c = u / a.n_entries;
-    const int ei = static_cast<int>(u % a.n_entries);
-    if (threadIdx.x == 0) {
-      en = a.entries[ei];
-      ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
+    chain_unit_b<T, OPTD>(a, a.entries, a.n_entries, u, en, ok_flag, bad);
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
+// Both passes in one persistent, fully resident kernel.  The host orders
+// the units so that B(c) comes `lag` chunks after A(c): a CTA that finishes
+// its partial-pass units moves on to mean-pass units whose chunks have had
+// time to come back, so the mean pass's HBM work overlaps the NVLink-bound
+// partial pass instead of following it.  A B unit only waits on A units at
+// earlier positions (here or on earlier GPUs), and A units never wait on B:
+// with every CTA resident and positions visited in order, the lowest
+// waiting position always has its producers running -- no deadlock.
+template <typename T, int OPTM, int OPTD>
+__global__ void __launch_bounds__(kThreads) chain_merged_kernel(const ChainArgs<T> a) {
+  __shared__ ChainEntry en;
+  __shared__ int ok_flag;
+  unsigned long long bad = ~0ull;
+  for (long p = blockIdx.x; p < a.n_order; p += gridDim.x) {
+    const unsigned w = a.order[p];
+    const long u = static_cast<long>(w & 0x7fffffffu);
+    if (w >> 31) {
+      chain_unit_b<T, OPTD>(a, a.entries_b, a.n_entries_b, u, en, ok_flag, bad);
+    } else {
+      chain_unit_a<T, OPTM, OPTD>(a, a.entries, a.n_entries, u, en, ok_flag, bad);
     }
-    __syncthreads();
-    const long lo = c * a.chunk;
-    const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
-    if (ok_flag) {
-      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
-        const long off = e * VN;
-        const Pack<T> mean = ldv_cg(static_cast<const T*>(en.recv) + off);
-        if (en.send) stv_cg(static_cast<T*>(en.send) + off, mean);
-        if constexpr (OPTD == kOptNone) chain_deliver<T, OPTD>(a, en, off, mean, bad);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && en.send) {
-      if (DSS_CHAIN_FENCE) __threadfence_system();
-      st_release_sys(en.send_flags + c, a.epoch);
-    }
-    if constexpr (OPTD != kOptNone) {
-      // forwarded: now the (HBM-heavy) replica step, off the critical path
-      if (ok_flag) {
-        for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
-          const long off = e * VN;
-          chain_deliver<T, OPTD>(a, en, off, ldv_cg(static_cast<const T*>(en.recv) + off), bad);
-        }
-      }
-    }
-    __syncthreads();
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
@@ -1434,11 +1515,10 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
 // The HBM step overlaps the NVLink push.  The grid is sized to be fully
 // resident, so every CTA finishes its phase-1 items before any CTA can spin
 // in phase 2 -- no CTA waits on work that cannot be scheduled.
-struct PushItem {        // phase 1: one chunk of my member, bound for one owner
+struct PushItem {        // phase 1: one chunk of my member, stepped once, pushed to ndst stagings
   int lr;                // my member's local row
   long lo, hi;           // element range
-  void* dst;             // owner's staging row j, positioned at element lo
-  unsigned long long* flag;  // owner's flag for (slice, j, chunk)
+  int dst_beg, ndst;     // destinations in the item tables: two-shot 1 (the slice owner), one-shot S
   int rank;              // member's global rank (error key)
 };
 struct PushFold {        // phase 2: one chunk of a slice this GPU owns
@@ -1456,6 +1536,8 @@ struct PushFold {        // phase 2: one chunk of a slice this GPU owns
 template <typename T> struct PushArgs {
   const PushItem* items;
   int n_items;
+  void* const* item_dst;                     // staging row j of a destination, positioned at the item's lo
+  unsigned long long* const* item_flag;      // its flag for (row j, chunk)
   const PushFold* folds;
   int n_folds;
   T* const* dst;         // member param rows (local or peer)
@@ -1513,10 +1595,13 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
         const unsigned long long k = err_key(a.t, 0, it.rank);
         bad = k < bad ? k : bad;
       }
-      stv_cg(reinterpret_cast<T*>(static_cast<char*>(it.dst) + a.stage_shift) + (off - it.lo), x);
+      for (int q = 0; q < it.ndst; ++q) {
+        stv_cg(reinterpret_cast<T*>(static_cast<char*>(a.item_dst[it.dst_beg + q]) + a.stage_shift) + (off - it.lo),
+               x);
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys(it.flag + a.flag_shift, a.epoch);
+    if (threadIdx.x < it.ndst) st_release_sys(a.item_flag[it.dst_beg + threadIdx.x] + a.flag_shift, a.epoch);
     __syncthreads();
   }
   // phase 2: ordered fold of owned chunks
@@ -1736,7 +1821,8 @@ __global__ void __launch_bounds__(128) logistic_grad_kernel(const LogisticArgs a
   }
   __syncthreads();
   const int* bt = a.batch + static_cast<long>(k) * a.B;
-  double loss = 0.0;  // thread 0 only
+  double max_nz = 0.0;  // thread 0 only
+  bool nan_nz = false;
   for (int b = 0; b < a.B; ++b) {
     const int idx = bt[b];
     const double* x = a.x + static_cast<long>(idx) * d;
@@ -1747,9 +1833,10 @@ __global__ void __launch_bounds__(128) logistic_grad_kernel(const LogisticArgs a
       double z = 0.0;
       for (int j = 0; j < d; ++j) z = __dadd_rn(z, prod[j]);
       const double nz = __dmul_rn(-y, z);
-      loss = __dadd_rn(loss, softplus_dev(nz));
       const double s = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz)));  // sigmoid (problems.cpp:337)
       sval[0] = __dmul_rn(-y, s);
+      max_nz = fmax(max_nz, nz);
+      nan_nz = nan_nz || isnan(nz);
     }
     __syncthreads();
     const double ys = sval[0];
@@ -1765,15 +1852,7 @@ __global__ void __launch_bounds__(128) logistic_grad_kernel(const LogisticArgs a
     gr[j] = static_cast<T>(v);
   }
   for (long j = d + threadIdx.x; j < a.ld; j += blockDim.x) gr[j] = T(0);
-  if (threadIdx.x == 0) {
-    loss = __dmul_rn(loss, inv);
-    if (a.l2 > 0.0) {
-      double dd = 0.0;
-      for (int j = 0; j < d; ++j) dd = __dadd_rn(dd, __dmul_rn(wd[j], wd[j]));
-      loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(0.5, a.l2), dd));
-    }
-    bad = bad || !isfinite(loss);
-  }
+  if (threadIdx.x == 0) bad = bad || !logistic_loss_finite(a, bt, wr, max_nz, nan_nz);
   // checked_gradient (sync.cpp:181-191): DivergenceError(rank, t)
   if (__syncthreads_or(bad) && threadIdx.x == 0) {
     atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.first_rank + k));
