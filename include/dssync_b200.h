@@ -108,10 +108,11 @@ typedef struct {
                            2 = (several GPUs) every spanning group uses the chain fold.
                            3 = (several GPUs) two-shot groups use the unfused pull fold
                            (step, barrier, fold) instead of the fused push kernel.
-                           4 = (several GPUs) as 0 but never one-shot: rows of at most
-                           1 MiB otherwise fold one-shot (every member GPU gathers every
-                           member row; no peer stores into params, no next-iteration
-                           barrier).
+                           4 = (several GPUs) as 0 but never one-shot.  Path 0 folds
+                           groups of one member per GPU one-shot (every member GPU
+                           gathers every member row; no peer stores into params, no
+                           next-iteration barrier) when the group is a pair or rows
+                           are at most 512 KiB.
                            Results are bit-identical on every path. */
   long stats_dim;       /* running_stats per worker (0 = none).  They travel with the
                            params (DS, sync_round) or the gradients (BSP) through the same

@@ -49,7 +49,7 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 // Rows up to this many bytes fold one-shot over NVLink (every member GPU
 // gathers every member's row) instead of two-shot.
 #ifndef DSS_ONESHOT_MAX_BYTES
-#define DSS_ONESHOT_MAX_BYTES (1L << 20)
+#define DSS_ONESHOT_MAX_BYTES (512L << 10)
 #endif
 // 1: both chain passes in one persistent kernel (chain_merged_kernel), the
 // mean-pass units DSS_CHAIN_MERGE_LAG resident rounds behind the partial
