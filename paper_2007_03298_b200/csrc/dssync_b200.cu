@@ -1700,12 +1700,18 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       c->chain_chunk = std::min<long>(c->d_pad, DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
-      long ps = 0, pf = 0;  // fused two-shot staging of this GPU's owned slices, worst parity
+      // Fused two-shot staging of the owned slices, worst parity and worst
+      // GPU: the one-shot area starts after it at the same offset on every
+      // GPU, because a pusher applies its own offset to the peer's buffer.
+      long ps = 0, pf = 0;
       for (long t = 0; t < (s.kind == DSS_DS_SYNC ? 2 : 1); ++t) {
-        long st = 0, fl = 0;
-        owned_layout(c.get(), make_partition(s, t), cfg->rank, c->chain_chunk, &st, &fl);
-        ps = std::max(ps, st);
-        pf = std::max(pf, fl);
+        const Partition part = make_partition(s, t);
+        for (int q = 0; q < cfg->n_gpus; ++q) {
+          long st = 0, fl = 0;
+          owned_layout(c.get(), part, q, c->chain_chunk, &st, &fl);
+          ps = std::max(ps, st);
+          pf = std::max(pf, fl);
+        }
       }
       // One-shot per schedule parity: every member GPU gathers every
       // member's row.  Same NVLink bytes as two-shot for pairs (S = 2) and

@@ -55,7 +55,7 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 // mean-pass units DSS_CHAIN_MERGE_LAG resident rounds behind the partial
 // pass; 0: two kernels.
 #ifndef DSS_CHAIN_MERGED
-#define DSS_CHAIN_MERGED 1
+#define DSS_CHAIN_MERGED 0
 #endif
 #ifndef DSS_CHAIN_MERGE_LAG
 #define DSS_CHAIN_MERGE_LAG 1.0
