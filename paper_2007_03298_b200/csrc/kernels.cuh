@@ -1568,10 +1568,15 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   __shared__ PushItem it;
   __shared__ PushFold fo;
   __shared__ int ok_flag;
+  __shared__ T* sdst[kMaxFold];
   unsigned long long bad = ~0ull;
   // phase 1: step + push
   for (int u = blockIdx.x; u < a.n_items; u += gridDim.x) {
     if (threadIdx.x == 0) it = a.items[u];
+    __syncthreads();
+    if (threadIdx.x < it.ndst) {
+      sdst[threadIdx.x] = reinterpret_cast<T*>(static_cast<char*>(a.item_dst[it.dst_beg + threadIdx.x]) + a.stage_shift);
+    }
     __syncthreads();
     const long r = static_cast<long>(it.lr) * a.ld;
     const T b1 = static_cast<T>(a.bc1[it.lr]);
@@ -1595,10 +1600,7 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
         const unsigned long long k = err_key(a.t, 0, it.rank);
         bad = k < bad ? k : bad;
       }
-      for (int q = 0; q < it.ndst; ++q) {
-        stv_cg(reinterpret_cast<T*>(static_cast<char*>(a.item_dst[it.dst_beg + q]) + a.stage_shift) + (off - it.lo),
-               x);
-      }
+      for (int q = 0; q < it.ndst; ++q) stv_cg(sdst[q] + (off - it.lo), x);
     }
     __syncthreads();
     if (threadIdx.x < it.ndst) st_release_sys(a.item_flag[it.dst_beg + threadIdx.x] + a.flag_shift, a.epoch);
