@@ -94,8 +94,6 @@ struct ChainLaunch {
   int* d_dst_lr = nullptr;         // local row index of each destination
   int opt_mem = -1;                // fused step on the members (DS), kOptNone = fold only
   int opt_dst = -1;                // fused step of the destinations with the mean (BSP)
-  unsigned* d_order = nullptr;     // merged-kernel unit order (see chain_merged_kernel)
-  long n_order = 0;
 };
 
 struct PushLaunch {
@@ -132,8 +130,6 @@ struct dss_ctx {
   int sms = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // chain kernel B, concurrent with kernel A
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   void* w = nullptr;
   void* g = nullptr;
@@ -444,26 +440,6 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
   }
   cl.na = static_cast<int>(ea.size());
   cl.nb = static_cast<int>(eb.size());
-  if (DSS_CHAIN_MERGED && cl.na > 0 && cl.nb > 0) {
-    // slot s: the partial-pass units of chunk s, then the mean-pass units
-    // of chunk s - lag; lag ~ one resident round of CTAs
-    const long nch = c->chain_nchunks;
-    const long round = static_cast<long>(c->sms) * DSS_CHAIN_CTAS_PER_SM;
-    const long lag = std::max<long>(1, static_cast<long>(DSS_CHAIN_MERGE_LAG * round / (cl.na + cl.nb)));
-    std::vector<unsigned> order;
-    order.reserve(static_cast<size_t>(nch) * (cl.na + cl.nb));
-    for (long sl = 0; sl < nch + lag; ++sl) {
-      if (sl < nch) {
-        for (int e = 0; e < cl.na; ++e) order.push_back(static_cast<unsigned>(sl * cl.na + e));
-      }
-      if (sl >= lag) {
-        for (int e = 0; e < cl.nb; ++e) order.push_back(0x80000000u | static_cast<unsigned>((sl - lag) * cl.nb + e));
-      }
-    }
-    if (static_cast<long>(nch) * std::max(cl.na, cl.nb) >= 0x7fffffffL) throw std::invalid_argument("chain too long");
-    cl.n_order = static_cast<long>(order.size());
-    cl.d_order = upload_table(c, order);
-  }
   cl.d_a = upload_table(c, ea);
   cl.d_b = upload_table(c, eb);
   cl.d_src = upload_table(c, src);
@@ -1171,80 +1147,28 @@ void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
 
 template <typename T, int OPTM, int OPTD>
 void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
-  ChainArgs<T> b = a;
-  b.entries = cl.d_b;
-  b.n_entries = cl.nb;
-  const long units_a = c->chain_nchunks * cl.na;
-  const long units_b = c->chain_nchunks * cl.nb;
-  TimedLaunch tl(c, DSS_KIND_CHAIN);  // spans both kernels; counts kernel A
-  if (cl.na == 0) --c->launches;
-  // Concurrency needs room for kernel A beside B's resident CTAs on every SM
-  // (otherwise spinning B CTAs could hold every slot A needs): only the
-  // light store-only B (DS), and only if the register files fit both.
-  bool concurrent = DSS_CHAIN_CONCURRENT && OPTD == kOptNone && cl.na > 0 && cl.nb > 0;
-  if (concurrent) {
-    static int regs_a = -1, regs_b = -1;
-    if (regs_a < 0) {
-      cudaFuncAttributes fa{}, fb{};
-      ck(cudaFuncGetAttributes(&fa, chain_partial_kernel<T, OPTM, OPTD>), "chain attrs");
-      ck(cudaFuncGetAttributes(&fb, chain_mean_kernel<T, OPTD>), "chain attrs");
-      regs_a = fa.numRegs;
-      regs_b = fb.numRegs;
-    }
-    auto cta_regs = [](int r) { return ((r + 7) / 8) * 8 * kThreads; };
-    concurrent = DSS_CHAIN_B_CTAS_PER_SM * cta_regs(regs_b) + cta_regs(regs_a) <= 65536;
-  }
-  if (DSS_CHAIN_MERGED && cl.d_order) {
-    static int occ = -1;
-    if (occ < 0) {
-      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chain_merged_kernel<T, OPTM, OPTD>, kThreads, 0),
-         "chain occupancy");
-      occ = std::max(occ, 1);
-    }
-    a.entries = cl.d_a;
-    a.n_entries = cl.na;
-    a.entries_b = cl.d_b;
-    a.n_entries_b = cl.nb;
-    a.order = cl.d_order;
-    a.n_order = cl.n_order;
-    // fully resident: every position is visited in order by a live CTA
-    chain_merged_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(cl.n_order, static_cast<long>(c->sms) * occ)),
-                                         kThreads, 0, c->stream>>>(a);
-    ck(cudaGetLastError(), "chain_merged_kernel launch");
-    return;
-  }
-  if (concurrent && !c->side) {
-    ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
-    ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
-    ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
-  }
-  if (concurrent) ck(cudaEventRecord(c->ev_fork, c->stream), "fork record");
+  // Kernel B follows kernel A on the stream.  Measured alternatives that
+  // lost at 2 GPUs (C2 / C3 iters/s against 3108 / 480 for this schedule):
+  // B concurrently on a side stream with A giving up CTA slots (2534 / 369),
+  // and both passes in one persistent kernel with lagged mean-pass units
+  // (2300 / stalled).
   if (cl.na > 0) {
-    // Kernel A is enqueued first: if the driver maps the side stream onto
-    // the same hardware queue, B simply runs after A (the sequential
-    // schedule) and can never block it.  When concurrent, A leaves
-    // DSS_CHAIN_B_CTAS_PER_SM slots per SM for B.
     a.entries = cl.d_a;
     a.n_entries = cl.na;
-    const long per_sm = concurrent ? long{DSS_CHAIN_CTAS_PER_SM - DSS_CHAIN_B_CTAS_PER_SM} : long{DSS_CHAIN_CTAS_PER_SM};
-    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units_a, c->sms * per_sm)), kThreads, 0,
-                                          c->stream>>>(a);
+    const long units = c->chain_nchunks * cl.na;
+    TimedLaunch tl(c, DSS_KIND_CHAIN);
+    chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                                          kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
   }
-  if (concurrent) {
-    // B waits only on flags released by kernel A (here or on other GPUs)
-    ck(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork wait");
-    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units_b, c->sms * long{DSS_CHAIN_B_CTAS_PER_SM})),
-                                 kThreads, 0, c->side>>>(b);
+  if (cl.nb > 0) {
+    a.entries = cl.d_b;
+    a.n_entries = cl.nb;
+    const long units = c->chain_nchunks * cl.nb;
+    TimedLaunch tl(c, DSS_KIND_CHAIN);
+    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
+                                 kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_mean_kernel launch");
-    ++c->launches;
-    ck(cudaEventRecord(c->ev_join, c->side), "join record");
-    ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join wait");
-  } else if (cl.nb > 0) {
-    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units_b, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
-                                 kThreads, 0, c->stream>>>(b);
-    ck(cudaGetLastError(), "chain_mean_kernel launch");
-    ++c->launches;
   }
 }
 
@@ -1778,10 +1702,6 @@ extern "C" int dss_destroy(dss_ctx* c) {
   if (c->copy_in) cudaStreamSynchronize(c->copy_in), cudaStreamDestroy(c->copy_in);
   if (c->copy_out) cudaStreamSynchronize(c->copy_out), cudaStreamDestroy(c->copy_out);
   for (cudaEvent_t e : {c->ev_in, c->ev_free, c->ev_snap, c->ev_out}) {
-    if (e) cudaEventDestroy(e);
-  }
-  if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
-  for (cudaEvent_t e : {c->ev_fork, c->ev_join}) {
     if (e) cudaEventDestroy(e);
   }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

@@ -51,27 +51,6 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_ONESHOT_MAX_BYTES
 #define DSS_ONESHOT_MAX_BYTES (512L << 10)
 #endif
-// 1: both chain passes in one persistent kernel (chain_merged_kernel), the
-// mean-pass units DSS_CHAIN_MERGE_LAG resident rounds behind the partial
-// pass; 0: two kernels.
-#ifndef DSS_CHAIN_MERGED
-#define DSS_CHAIN_MERGED 0
-#endif
-#ifndef DSS_CHAIN_MERGE_LAG
-#define DSS_CHAIN_MERGE_LAG 1.0
-#endif
-// 1: run the chain's mean pass (kernel B) concurrently with the partial
-// pass (kernel A) on a side stream, B with DSS_CHAIN_B_CTAS_PER_SM resident
-// CTAs per SM; 0: B after A on the context stream.  Measured at 2 GPUs
-// (C2 / C3): concurrent 2534 / 369 iters/s (B=2), 2821 / 441 (B=4) vs
-// sequential 3126 / 480 -- A loses more from the slots it gives up than B
-// gains, so the default is sequential.
-#ifndef DSS_CHAIN_CONCURRENT
-#define DSS_CHAIN_CONCURRENT 0
-#endif
-#ifndef DSS_CHAIN_B_CTAS_PER_SM
-#define DSS_CHAIN_B_CTAS_PER_SM 2
-#endif
 // 1: full system fence before each chunk's release flag; 0: rely on the
 // cumulativity of st.release.sys after the CTA barrier (lighter).
 #ifndef DSS_CHAIN_FENCE
@@ -1186,12 +1165,6 @@ template <typename T> struct ChainArgs {
   StepConsts<T> c;
   double bc1[kMaxLocal];
   double bc2[kMaxLocal];
-  // merged launch (chain_merged_kernel): kernel B's entries and the unit
-  // order, each unit = kind << 31 | chunk * n_entries(kind) + entry
-  const ChainEntry* entries_b;
-  int n_entries_b;
-  const unsigned* order;
-  long n_order;
 };
 
 __device__ __forceinline__ bool chain_wait(const unsigned long long* flag, unsigned long long epoch,
@@ -1475,31 +1448,6 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
   unsigned long long bad = ~0ull;
   for (long u = blockIdx.x; u < units; u += gridDim.x) {
     chain_unit_b<T, OPTD>(a, a.entries, a.n_entries, u, en, ok_flag, bad);
-  }
-  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
-}
-
-// Both passes in one persistent, fully resident kernel.  The host orders
-// the units so that B(c) comes `lag` chunks after A(c): a CTA that finishes
-// its partial-pass units moves on to mean-pass units whose chunks have had
-// time to come back, so the mean pass's HBM work overlaps the NVLink-bound
-// partial pass instead of following it.  A B unit only waits on A units at
-// earlier positions (here or on earlier GPUs), and A units never wait on B:
-// with every CTA resident and positions visited in order, the lowest
-// waiting position always has its producers running -- no deadlock.
-template <typename T, int OPTM, int OPTD>
-__global__ void __launch_bounds__(kThreads) chain_merged_kernel(const ChainArgs<T> a) {
-  __shared__ ChainEntry en;
-  __shared__ int ok_flag;
-  unsigned long long bad = ~0ull;
-  for (long p = blockIdx.x; p < a.n_order; p += gridDim.x) {
-    const unsigned w = a.order[p];
-    const long u = static_cast<long>(w & 0x7fffffffu);
-    if (w >> 31) {
-      chain_unit_b<T, OPTD>(a, a.entries_b, a.n_entries_b, u, en, ok_flag, bad);
-    } else {
-      chain_unit_a<T, OPTM, OPTD>(a, a.entries, a.n_entries, u, en, ok_flag, bad);
-    }
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
