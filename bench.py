@@ -512,10 +512,14 @@ def our_arm(args, cfg):
                 row.update(alg_bytes_per_step=nb_bytes[key]["fold_hbm"] + nb_bytes[key]["fold_nvlink"],
                            nvlink_bytes_per_step=nb_bytes[key]["fold_nvlink"],
                            nvlink_gbs=nb_bytes[key]["fold_nvlink"] / (ms_ / 1e3) / 1e9 if ms_ else None)
+            elif k == "chain_mean":
+                row.update(note="mean pass of the chain (rank 0); its NVLink bytes are counted under chain")
             elif k == "chain":
-                # rank-0 outbound NVLink bytes of its chain roles (per-direction link load)
+                # rank-0 outbound NVLink bytes of its chain roles (per-direction
+                # link load) over both passes' time
+                both = ms_ + r["kinds"].get("chain_mean", (0.0, 0))[0]
                 row.update(nvlink_bytes_per_step=nb_bytes[key]["chain_nvlink"],
-                           nvlink_gbs=nb_bytes[key]["chain_nvlink"] / (ms_ / 1e3) / 1e9 if ms_ else None)
+                           nvlink_gbs=nb_bytes[key]["chain_nvlink"] / (both / 1e3) / 1e9 if both else None)
             rows[k] = row
         return rows
 

@@ -335,8 +335,9 @@ enum {
   DSS_KIND_BSP = 2,      /* bsp_kernel: fused gradient fold + step */
   DSS_KIND_BARRIER = 3,  /* barrier_kernel: cross-GPU flag barrier */
   DSS_KIND_GRADIENT = 4, /* quad_grad_kernel: synthetic gradients */
-  DSS_KIND_CHAIN = 5,    /* chain_partial/mean_kernel: ordered chain fold over NVLink */
-  DSS_KIND_COUNT = 6
+  DSS_KIND_CHAIN = 5,    /* chain_partial_kernel: ordered chain fold, partial pass over NVLink */
+  DSS_KIND_CHAIN_MEAN = 6, /* chain_mean_kernel: the chain's mean pass */
+  DSS_KIND_COUNT = 7
 };
 int dss_kernel_times_by_kind(dss_ctx* ctx, double* total_ms, long* launches);
 /* gpu_launches: hot-path kernels launched since creation (all kinds). */

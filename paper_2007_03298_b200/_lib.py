@@ -20,7 +20,7 @@ DSS_F32, DSS_F64 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_STATS, BUF_STATS_OBS = range(6)
 SAMPLING_REPLACEMENT, SAMPLING_EPOCH = 0, 1  # dss_sampling
 IPC_BYTES = 576
-KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain"]
+KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain", "chain_mean"]
 
 
 class dss_hparams(C.Structure):

@@ -1165,7 +1165,7 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
     a.entries = cl.d_b;
     a.n_entries = cl.nb;
     const long units = c->chain_nchunks * cl.nb;
-    TimedLaunch tl(c, DSS_KIND_CHAIN);
+    TimedLaunch tl(c, DSS_KIND_CHAIN_MEAN);
     chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
                                  kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_mean_kernel launch");
@@ -2383,9 +2383,9 @@ P* logi_alloc(dss_ctx* c, size_t n) {
   return static_cast<P*>(p);
 }
 
-// 3 d doubles (w, products, accumulators) + the broadcast scalar
-size_t logistic_smem(long d) { return sizeof(double) * (3 * static_cast<size_t>(d) + 2); }
-constexpr long kLogisticMaxDim = 9000;
+// w as doubles [d] + the -y*s factors [batch]
+size_t logistic_smem(long d, long batch) { return sizeof(double) * static_cast<size_t>(d + batch); }
+constexpr long kLogisticMaxSmem = 200 * 1024;
 
 }  // namespace
 
@@ -2399,7 +2399,9 @@ extern "C" int dss_logistic_setup(dss_ctx* c, const double* x, const double* y, 
     if (sampling != DSS_SAMPLING_REPLACEMENT && sampling != DSS_SAMPLING_EPOCH) {
       throw std::invalid_argument("sampling must be replacement or epoch");
     }
-    if (c->d > kLogisticMaxDim) throw std::invalid_argument("logistic on the device supports dim <= 9000");
+    if (static_cast<long>(logistic_smem(c->d, batch_size)) > kLogisticMaxSmem) {
+      throw std::invalid_argument("logistic on the device supports (dim + batch_size) * 8 B <= 200 KiB");
+    }
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     ck(cudaStreamSynchronize(c->stream), "stream sync");
     free_logistic(c);
@@ -2430,11 +2432,11 @@ extern "C" int dss_logistic_setup(dss_ctx* c, const double* x, const double* y, 
        "shard upload");
     ck(cudaMemset(L.order_epoch, 0xff, sizeof(long) * c->P), "epoch init");  // -1
     ck(cudaMemset(L.batch, 0, sizeof(int) * c->P * batch_size), "batch init");
-    if (logistic_smem(c->d) > 48 * 1024) {
+    if (logistic_smem(c->d, batch_size) > 48 * 1024) {
       ck(cudaFuncSetAttribute(logistic_grad_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(logistic_smem(c->d))), "smem attr");
+                              static_cast<int>(logistic_smem(c->d, batch_size))), "smem attr");
       ck(cudaFuncSetAttribute(logistic_grad_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(logistic_smem(c->d))), "smem attr");
+                              static_cast<int>(logistic_smem(c->d, batch_size))), "smem attr");
     }
     L.max_shard = max_shard;
     L.M = M;
@@ -2476,10 +2478,10 @@ void launch_logistic(dss_ctx* c, long t) {
   const LogisticArgs a = logistic_args(c, t);
   TimedLaunch tl(c, DSS_KIND_GRADIENT);
   if (c->cfg.dtype == DSS_F64) {
-    logistic_grad_kernel<double><<<c->P, 128, logistic_smem(c->d), c->stream>>>(
+    logistic_grad_kernel<double><<<c->P, 128, logistic_smem(c->d, c->logi.B), c->stream>>>(
         a, static_cast<const double*>(c->w), static_cast<double*>(c->g));
   } else {
-    logistic_grad_kernel<float><<<c->P, 128, logistic_smem(c->d), c->stream>>>(
+    logistic_grad_kernel<float><<<c->P, 128, logistic_smem(c->d, c->logi.B), c->stream>>>(
         a, static_cast<const float*>(c->w), static_cast<float*>(c->g));
   }
   ck(cudaGetLastError(), "logistic_grad_kernel launch");
@@ -2501,7 +2503,7 @@ extern "C" int dss_logistic_gradients(dss_ctx* c, long t) {
 
 extern "C" int dss_logistic_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
   if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
-  if (small_path(c, n) && c->logi.ready && c->d <= kSmallLogiMaxDim) {
+  if (small_path(c, n) && c->logi.ready && c->d <= kSmallLogiMaxDim && c->logi.B <= kSmallLogiMaxBatch) {
     // the whole run in one CTA: sampling, gradient, step and group fold
     const int st = guard(c, [&]() -> int {
       if (t0 < 0) throw std::invalid_argument("iteration must be >= 0");

@@ -746,6 +746,42 @@ __device__ void sample_batch_dev(const LogisticArgs& a, int k) {
   }
 }
 
+// Replacement sampling (sync.cpp:160-166) with the draws spread over
+// threads: draw b of the stream is mix64(s0 + (b+1) * phi) unless an earlier
+// draw was rejected by uniform_below (probability size / 2^64 per draw), so
+// thread `lane` of `width` takes draws lane, lane + width, ...; if any draw
+// is rejected, thread 0 redoes the batch sequentially.  `sync` is the
+// barrier of the participating group (warp or block); bt is visible to the
+// group on return.  Epoch sampling stays on thread 0 (its per-epoch order is
+// one sequential shuffle, cached).
+template <typename Sync, typename Any>
+__device__ void sample_batch_par(const LogisticArgs& a, int k, int lane, int width, Sync sync, Any any) {
+  if (a.sampling != 0) {
+    if (lane == 0) sample_batch_dev(a, k);
+    sync();
+    return;
+  }
+  const int rank = a.first_rank + k;
+  const int* sh = a.shard + a.shard_off[k];
+  const uint64_t n = static_cast<uint64_t>(a.shard_off[k + 1] - a.shard_off[k]);
+  int* bt = a.batch + static_cast<long>(k) * a.B;
+  const uint64_t s0 = stream_state_dev(a.seed, kBatchStream, static_cast<uint64_t>(rank), static_cast<uint64_t>(a.t));
+  const uint64_t limit = ~0ULL - ~0ULL % n;
+  bool rejected = false;
+  for (int b = lane; b < a.B; b += width) {
+    const uint64_t v = mix64(s0 + static_cast<uint64_t>(b + 1) * 0x9e3779b97f4a7c15ULL);
+    if (v >= limit) {
+      rejected = true;
+    } else {
+      bt[b] = sh[v % n];
+    }
+  }
+  if (any(rejected)) {
+    if (lane == 0) sample_batch_dev(a, k);
+  }
+  sync();
+}
+
 // Is the batch loss of checked_gradient (problems.cpp:277-287, sync.cpp:186)
 // finite?  Every term softplus(nz) <= max(nz, 0) + log 2, so when the
 // largest nz, the batch size and the l2 term keep the sum far below the
@@ -797,70 +833,60 @@ template <typename T> struct SmallArgs {
   LogisticArgs lg;
 };
 
-constexpr int kSmallLogiMaxDim = 512;  // features per worker in the fused small-world logistic path
+constexpr int kSmallLogiMaxDim = 256;    // features per worker in the fused small-world logistic path
+constexpr int kSmallLogiMaxBatch = 256;  // batch size there
 
 // Logistic gradients of every worker at iteration t inside the one-CTA
-// small-world kernel: one warp per worker, lane j owning features j + 32q.
-// Same operation order as logistic_grad_kernel (and the reference): the
-// products in parallel, their sum sequentially on lane 0, the per-feature
-// accumulation in sample order.
+// small-world kernel: one warp per worker.  The reference walks the batch
+// example by example (problems.cpp:273-282), but an example's margin only
+// depends on w, so all margins are computed at once (lane b: z_b summed in
+// feature order) and then every feature's sum is taken in example order
+// (lane j): the same additions in the same order, with the critical path
+// d + B steps long instead of B * (d + sigmoid).
 template <typename T>
 __device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
   constexpr int Q = kSmallLogiMaxDim / 32;
-  __shared__ double prod[kThreads / 32][kSmallLogiMaxDim];
-  __shared__ double sval[kThreads / 32];
+  __shared__ double wsm[kThreads / 32][kSmallLogiMaxDim];
+  __shared__ double ysm[kThreads / 32][kSmallLogiMaxBatch];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   LogisticArgs L = a.lg;
   L.t = t;
   const int d = L.d;
   for (int k = warp; k < a.nw; k += kThreads / 32) {
-    if (lane == 0) sample_batch_dev(L, k);
-    __syncwarp();
+    sample_batch_par(L, k, lane, 32, [] { __syncwarp(); }, [](bool p) { return __any_sync(0xffffffffu, p); });
     const T* wr = a.w + static_cast<long>(k) * a.ld;
-    double wreg[Q], acc[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int j = lane + 32 * q;
-      wreg[q] = j < d ? static_cast<double>(wr[j]) : 0.0;
-      acc[q] = 0.0;
-    }
+    for (int j = lane; j < d; j += 32) wsm[warp][j] = static_cast<double>(wr[j]);
+    __syncwarp();
     const int* bt = L.batch + static_cast<long>(k) * L.B;
+    // every example's margin at once (lane b): z_b in the reference's
+    // feature order, then -y_b * sigmoid(-y_b z_b)
     double max_nz = 0.0;
     bool nan_nz = false;
-    for (int b = 0; b < L.B; ++b) {
+    for (int b = lane; b < L.B; b += 32) {
       const int idx = bt[b];
       const double* x = L.x + static_cast<long>(idx) * d;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const int j = lane + 32 * q;
-        if (j < d) prod[warp][j] = __dmul_rn(x[j], wreg[q]);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        const double y = L.y[idx];
-        double z = 0.0;
-        for (int j = 0; j < d; ++j) z = __dadd_rn(z, prod[warp][j]);
-        const double nz = __dmul_rn(-y, z);
-        sval[warp] = __dmul_rn(-y, __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz))));
-        max_nz = fmax(max_nz, nz);
-        nan_nz = nan_nz || isnan(nz);
-      }
-      __syncwarp();
-      const double ys = sval[warp];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const int j = lane + 32 * q;
-        if (j < d) acc[q] = __dadd_rn(acc[q], __dmul_rn(ys, x[j]));
-      }
+      double z = 0.0;
+      for (int j = 0; j < d; ++j) z = __dadd_rn(z, __dmul_rn(x[j], wsm[warp][j]));
+      const double y = L.y[idx];
+      const double nz = __dmul_rn(-y, z);
+      ysm[warp][b] = __dmul_rn(-y, __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz))));
+      max_nz = fmax(max_nz, nz);
+      nan_nz = nan_nz || isnan(nz);
     }
+    for (int off = 16; off > 0; off >>= 1) max_nz = fmax(max_nz, __shfl_xor_sync(0xffffffffu, max_nz, off));
+    nan_nz = __any_sync(0xffffffffu, nan_nz);
+    __syncwarp();
+    // then every feature (lane j): the gradient sum in example order
     const double inv = __ddiv_rn(1.0, static_cast<double>(L.B));
     bool bad = false;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int j = lane + 32 * q;
       if (j < d) {
-        double v = __dmul_rn(acc[q], inv);
-        if (L.l2 > 0.0) v = __dadd_rn(v, __dmul_rn(L.l2, wreg[q]));
+        double acc = 0.0;
+        for (int b = 0; b < L.B; ++b) acc = __dadd_rn(acc, __dmul_rn(ysm[warp][b], L.x[static_cast<long>(bt[b]) * d + j]));
+        double v = __dmul_rn(acc, inv);
+        if (L.l2 > 0.0) v = __dadd_rn(v, __dmul_rn(L.l2, wsm[warp][j]));
         bad = bad || !isfinite(v);
         g[static_cast<long>(k) * a.ld + j] = static_cast<T>(v);
       }
@@ -1752,57 +1778,63 @@ __global__ void broadcast_row_kernel(T* base, long ld, int rows, const T* src) {
   }
 }
 
-// dynamic shared memory: wd[d], prod[d], acc[d] (doubles) + 2 scalars
+// One CTA per local worker.  All margins first (thread b: z_b summed in the
+// reference's feature order, then -y_b * sigmoid(-y_b z_b)), then every
+// feature's gradient sum in example order (thread j): the reference's
+// additions in the reference's order (problems.cpp:273-289), with a
+// critical path of d + B steps.  Dynamic shared memory: w as doubles [d],
+// the -y*s factors [B], and a reduction scratch.
 template <typename T>
 __global__ void __launch_bounds__(128) logistic_grad_kernel(const LogisticArgs a, const T* __restrict__ w,
                                                             T* __restrict__ g) {
   extern __shared__ double sh[];
+  __shared__ double red_max[4];
+  __shared__ int red_nan;
   const int k = blockIdx.x;
   const int d = a.d;
   double* wd = sh;
-  double* prod = sh + d;
-  double* acc = sh + 2 * d;
-  double* sval = sh + 3 * d;  // [0] = -y*s of the current sample
+  double* ys = sh + d;
   const T* wr = w + static_cast<long>(k) * a.ld;
-  if (threadIdx.x == 0) sample_batch_dev(a, k);
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    wd[j] = static_cast<double>(wr[j]);
-    acc[j] = 0.0;
-  }
+  if (threadIdx.x == 0) red_nan = 0;
+  sample_batch_par(a, k, threadIdx.x, blockDim.x, [] { __syncthreads(); },
+                   [](bool p) { return __syncthreads_or(p) != 0; });
+  for (int j = threadIdx.x; j < d; j += blockDim.x) wd[j] = static_cast<double>(wr[j]);
   __syncthreads();
   const int* bt = a.batch + static_cast<long>(k) * a.B;
-  double max_nz = 0.0;  // thread 0 only
+  double max_nz = 0.0;
   bool nan_nz = false;
-  for (int b = 0; b < a.B; ++b) {
+  for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
     const int idx = bt[b];
     const double* x = a.x + static_cast<long>(idx) * d;
-    for (int j = threadIdx.x; j < d; j += blockDim.x) prod[j] = __dmul_rn(x[j], wd[j]);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double y = a.y[idx];
-      double z = 0.0;
-      for (int j = 0; j < d; ++j) z = __dadd_rn(z, prod[j]);
-      const double nz = __dmul_rn(-y, z);
-      const double s = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz)));  // sigmoid (problems.cpp:337)
-      sval[0] = __dmul_rn(-y, s);
-      max_nz = fmax(max_nz, nz);
-      nan_nz = nan_nz || isnan(nz);
-    }
-    __syncthreads();
-    const double ys = sval[0];
-    for (int j = threadIdx.x; j < d; j += blockDim.x) acc[j] = __dadd_rn(acc[j], __dmul_rn(ys, x[j]));
+    double z = 0.0;
+    for (int j = 0; j < d; ++j) z = __dadd_rn(z, __dmul_rn(x[j], wd[j]));
+    const double y = a.y[idx];
+    const double nz = __dmul_rn(-y, z);
+    ys[b] = __dmul_rn(-y, __ddiv_rn(1.0, __dadd_rn(1.0, exp(-nz))));  // sigmoid (problems.cpp:337)
+    max_nz = fmax(max_nz, nz);
+    nan_nz = nan_nz || isnan(nz);
   }
+  for (int off = 16; off > 0; off >>= 1) max_nz = fmax(max_nz, __shfl_xor_sync(0xffffffffu, max_nz, off));
+  if ((threadIdx.x & 31) == 0) red_max[threadIdx.x >> 5] = max_nz;
+  if (nan_nz) red_nan = 1;
+  __syncthreads();
   const double inv = __ddiv_rn(1.0, static_cast<double>(a.B));
   bool bad = false;
   T* gr = g + static_cast<long>(k) * a.ld;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    double v = __dmul_rn(acc[j], inv);
+    double acc = 0.0;
+    for (int b = 0; b < a.B; ++b) acc = __dadd_rn(acc, __dmul_rn(ys[b], a.x[static_cast<long>(bt[b]) * d + j]));
+    double v = __dmul_rn(acc, inv);
     if (a.l2 > 0.0) v = __dadd_rn(v, __dmul_rn(a.l2, wd[j]));
     bad = bad || !isfinite(v);
     gr[j] = static_cast<T>(v);
   }
   for (long j = d + threadIdx.x; j < a.ld; j += blockDim.x) gr[j] = T(0);
-  if (threadIdx.x == 0) bad = bad || !logistic_loss_finite(a, bt, wr, max_nz, nan_nz);
+  if (threadIdx.x == 0) {
+    double m = red_max[0];
+    for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) m = fmax(m, red_max[i]);
+    bad = bad || !logistic_loss_finite(a, bt, wr, m, red_nan != 0);
+  }
   // checked_gradient (sync.cpp:181-191): DivergenceError(rank, t)
   if (__syncthreads_or(bad) && threadIdx.x == 0) {
     atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.first_rank + k));
