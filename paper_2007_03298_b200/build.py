@@ -29,7 +29,7 @@ NVCC_FLAGS = [
     "-I" + INCLUDE, "-I" + CSRC,
 ]
 
-SOURCES = ["dssync_b200.cu", "schedule.cpp", "problems.cpp"]
+SOURCES = ["dssync_b200.cu", "engine.cu", "problems_abi.cu", "schedule.cpp", "problems.cpp"]
 
 
 def _nvcc() -> str:

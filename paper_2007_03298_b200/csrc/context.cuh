@@ -1,0 +1,399 @@
+// Host-side context of the C ABI (include/dssync_b200.h): the per-GPU
+// device state (struct dss_ctx), the launch tables built from the schedule,
+// and the helpers shared by the engine (engine.cu: plans, launches, the
+// iteration flow) and the entry points (dssync_b200.cu, problems_abi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "dssync_b200.h"
+#include "kernels.cuh"
+#include "problems.hpp"
+#include "schedule.hpp"
+
+namespace dssb {
+
+
+extern thread_local std::string g_last_global_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct PeerError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+inline uint64_t mix64_host(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// Rng::for_stream (rng.cpp:20-26): the state the stream starts from.
+inline uint64_t stream_state(uint64_t seed, uint64_t purpose, uint64_t rank, uint64_t iteration) {
+  uint64_t s = mix64_host(seed + 0x9e3779b97f4a7c15ULL);
+  s = mix64_host(s ^ purpose);
+  s = mix64_host(s ^ rank);
+  s = mix64_host(s ^ iteration);
+  return s;
+}
+
+constexpr uint64_t kDataGen = 0x9e3779b97f4a7c15ULL;        // rng.hpp:40
+constexpr uint64_t kInitParams = 0xbf58476d1ce4e5b9ULL;     // rng.hpp:41
+constexpr uint64_t kGradientNoise = 0xa0761d6478bd642fULL;  // rng.hpp:44
+
+inline const char* collective_name(int topology) {
+  switch (topology) {
+    case DSS_TREE: return "tree_allreduce_avg";
+    case DSS_PS: return "ps_allreduce_avg";
+    default: return "ring_allreduce_avg";
+  }
+}
+
+// Device CSR table of groups for one launch of ds_group_kernel.
+struct GroupLaunch {
+  int size = 0;     // uniform group size of this launch (0 = mixed)
+  int groups = 0;
+  int* d_members = nullptr;
+  int* d_offsets = nullptr;
+};
+
+struct FoldLaunch {
+  int entries = 0;
+  int uniform_m = 0;  // src count if uniform, else 0
+  long max_len = 0;   // longest slice (elements)
+  FoldEntry* d_entries = nullptr;
+  void** d_src = nullptr;
+  void** d_dst = nullptr;
+};
+
+struct ChainLaunch {
+  int na = 0, nb = 0;              // kernel A / kernel B entries on this GPU
+  ChainEntry* d_a = nullptr;
+  ChainEntry* d_b = nullptr;
+  void** d_src = nullptr;          // member rows
+  void** d_dst = nullptr;          // mean destinations
+  int* d_src_lr = nullptr;         // local row index of each member
+  int* d_dst_lr = nullptr;         // local row index of each destination
+  int opt_mem = -1;                // fused step on the members (DS), kOptNone = fold only
+  int opt_dst = -1;                // fused step of the destinations with the mean (BSP)
+};
+
+struct PushLaunch {
+  bool oneshot = false;
+  int items = 0, folds = 0;
+  void** d_item_dst = nullptr;
+  unsigned long long** d_item_flag = nullptr;
+  PushItem* d_items = nullptr;
+  PushFold* d_folds = nullptr;
+  void** d_dst = nullptr;
+};
+
+struct ParityPlan {
+  PushLaunch push;                     // fused two-shot (DS step, one member per GPU)
+  bool any_push = false;               // identical on every GPU
+  bool built = false;
+  bool any_spanning = false;  // identical on every GPU
+  bool any_twoshot = false;   // identical on every GPU
+  bool any_chain = false;     // identical on every GPU
+  std::vector<GroupLaunch> local;      // fused step+fold launches
+  GroupLaunch spanning_step;           // singleton in-place steps of spanning members
+  FoldLaunch fold;                     // owned two-shot slices
+  ChainLaunch chain;                   // ordered chain-fold groups
+};
+
+}  // namespace dssb
+
+struct dss_ctx {
+  dss_config cfg{};
+  int P = 0;            // local workers
+  int first = 0;        // first global rank here
+  long d = 0, d_pad = 0;
+  int esz = 4;
+  int sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+
+  void* w = nullptr;
+  void* g = nullptr;
+  void* m1 = nullptr;
+  void* m2 = nullptr;
+  void* mg = nullptr;     // mean gradient row (BSP over several GPUs)
+  void* stats = nullptr;      // [P][s_pad] running statistics
+  void* stats_obs = nullptr;  // [P][s_pad] batch observations
+  long s = 0, s_pad = 0;
+  std::vector<void*> peer_stats;
+  void* wstar = nullptr;  // quadratic optimum row
+  unsigned long long* d_err = nullptr;
+  unsigned long long* d_gerr = nullptr;  // gradient-producer failures: t << 32 | rank
+  unsigned long long* d_timeout = nullptr;
+  unsigned long long* flags = nullptr;  // [G] barrier words, written by peers
+  unsigned long long** d_peer_flags = nullptr;
+  unsigned long long* h_err = nullptr;  // pinned readback
+
+  // chain fold: receive rows [2 (partial, mean)][slots][d_pad] and their
+  // per-chunk epoch flags [2][slots][n_chunks], both peer-mapped
+  void* chain_buf = nullptr;
+  unsigned long long* chain_flags = nullptr;
+  int chain_slots = 0;
+  long chain_chunk = 0, chain_nchunks = 0;
+  unsigned long long chain_epoch = 0;
+  std::vector<void*> peer_chain_buf;
+  std::vector<unsigned long long*> peer_chain_flags;
+  // fused two-shot staging: each GPU's owned slices, S rows each, + flags
+  void* push_buf = nullptr;
+  unsigned long long* push_flags = nullptr;
+  std::vector<void*> peer_push_buf;
+  std::vector<unsigned long long*> peer_push_flags;
+  int push_occupancy = 0;
+  // one-shot (small rows): double-buffered staging [2][P][G][d_pad] + flags [2][P][G][n_chunks]
+  // one-shot area after the two-shot staging: [2][P][G][d_pad] rows +
+  // [2][P][G][n_chunks] flags, double-buffered by one-shot launch count
+  bool oneshot[2] = {false, false};  // per schedule parity (same on every GPU)
+  long oneshot_base_elems = 0, oneshot_base_flags = 0;
+  long oneshot_half_elems = 0, oneshot_half_flags = 0;
+  unsigned long long oneshot_seq = 0;
+  // dss_step_host pipeline
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_free = nullptr, ev_snap = nullptr, ev_out = nullptr;
+  void* snapshot = nullptr;
+  bool host_pipe = false;
+
+  std::vector<long> step_count;
+  std::vector<void*> peer_w, peer_g, peer_mg;
+  std::vector<unsigned long long*> peer_flag;
+  std::vector<void*> opened;  // IPC mappings to close
+  bool attached = false;
+  unsigned long long epoch = 0;
+  bool pending_remote = false;
+
+  dssb::ParityPlan step_plan[2];   // DS (or BSP at [0])
+  dssb::ParityPlan sync_plan[2];   // sync_round (no step)
+  dssb::ParityPlan mean_plan;      // ordered fold of every worker's params into mg (trace)
+  dssb::ParityPlan stats_plan[2];  // running-stats fold per parity (DS) / world group at [0] (BSP)
+  double* d_loss = nullptr;  // [P + 1] loss accumulators (trace)
+
+  // logistic problem on the device (dss_logistic_setup)
+  struct {
+    bool ready = false;
+    double* x = nullptr;       // [M][d]
+    double* y = nullptr;       // [M]
+    int* shard = nullptr;      // local shards, concatenated
+    int* shard_off = nullptr;  // [P + 1]
+    int* order = nullptr;      // [P][max_shard]
+    long* order_epoch = nullptr;
+    int* batch = nullptr;      // [P][B]
+    long max_shard = 0;
+    int M = 0, B = 0, sampling = 0;
+    double l2 = 0.0;
+    uint64_t seed = 0;
+    std::vector<void*> mem;
+  } logi;
+  dssb::GroupLaunch apply_launch;  // singleton groups of every local worker
+
+  // tiny-problem multi-iteration path (dss_steps)
+  int* d_small_members[2] = {nullptr, nullptr};
+  int* d_small_offsets[2] = {nullptr, nullptr};
+  int small_ngroups[2] = {0, 0};
+  double* d_small_buf = nullptr;  // [n] alphas, [n][P] bc1, [n][P] bc2
+  long small_cap = 0;
+  std::vector<double> h_small;
+
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+  std::vector<int> ev_kind;
+  double kind_ms[DSS_KIND_COUNT] = {};
+  long kind_n[DSS_KIND_COUNT] = {};
+  std::vector<cudaEvent_t> ev_pool;
+  long launches = 0;
+
+  int last_status = DSS_OK;
+  std::string last_error;
+  int last_rank = -1;
+  long last_iteration = -1;
+
+  std::vector<void*> allocations;
+};
+
+namespace dssb {
+
+inline int fail(dss_ctx* c, int status, const std::string& msg, int rank = -1, long it = -1) {
+  if (c) {
+    c->last_status = status;
+    c->last_error = msg;
+    c->last_rank = rank;
+    c->last_iteration = it;
+  }
+  g_last_global_error = msg;
+  return status;
+}
+
+template <typename F>
+int guard(dss_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    return fail(c, DSS_EINVAL, e.what());
+  } catch (const CudaError& e) {
+    return fail(c, DSS_ECUDA, e.what());
+  } catch (const PeerError& e) {
+    return fail(c, DSS_ENCCL, e.what());
+  } catch (const std::exception& e) {
+    return fail(c, DSS_ERUNTIME, e.what());
+  }
+}
+
+inline void* dalloc(dss_ctx* c, size_t bytes) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, bytes), "cudaMalloc");
+  ck(cudaMemsetAsync(p, 0, bytes, c->stream), "cudaMemset");
+  c->allocations.push_back(p);
+  return p;
+}
+
+template <typename T>
+T* upload_table(dss_ctx* c, const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = static_cast<T*>(dalloc(c, v.size() * sizeof(T)));
+  ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream),
+     "table upload");
+  ck(cudaStreamSynchronize(c->stream), "table upload sync");
+  return p;
+}
+
+inline bool multi(const dss_ctx* c) { return c->cfg.n_gpus > 1; }
+inline bool force_fold(const dss_ctx* c) { return c->cfg.path == 1 && !multi(c); }
+inline bool force_chain(const dss_ctx* c) { return c->cfg.path == 2 && multi(c); }
+inline bool use_push(const dss_ctx* c) { return multi(c) && c->cfg.path != 3; }  // path 3: unfused pull two-shot (A/B)
+
+struct OwnedSlot {
+  int group;
+  int S;
+  long lo, hi;
+  long stage_off;
+  long flag_off;
+  long nch;
+};
+
+struct RowGeom {
+  void* base;
+  long len;  // logical row length (dim or stats_dim)
+  long ld;   // padded row stride
+};
+
+// ---- launch helpers ---------------------------------------------------------
+
+struct TimedLaunch {
+  dss_ctx* c;
+  int kind;
+  cudaEvent_t b = nullptr, e = nullptr;
+  TimedLaunch(dss_ctx* cc, int k) : c(cc), kind(k) {
+    ++c->launches;
+    if (!c->timing) return;
+    for (cudaEvent_t* ev : {&b, &e}) {
+      if (!c->ev_pool.empty()) {
+        *ev = c->ev_pool.back();
+        c->ev_pool.pop_back();
+      } else {
+        ck(cudaEventCreate(ev), "cudaEventCreate");
+      }
+    }
+    ck(cudaEventRecord(b, c->stream), "cudaEventRecord");
+  }
+  ~TimedLaunch() {
+    if (!c->timing) return;
+    cudaEventRecord(e, c->stream);
+    c->ev_pending.emplace_back(b, e);
+    c->ev_kind.push_back(kind);
+  }
+};
+
+inline int grid_x(const dss_ctx* c, long nvec, int ys) {
+  const long want = static_cast<long>(c->sms) * (2048 / kThreads);
+  long gx = (want + ys - 1) / ys;
+  const long need = (nvec + kThreads - 1) / kThreads;
+  gx = std::min(gx, need);
+  return static_cast<int>(std::max(1L, std::min(gx, 65535L)));
+}
+
+template <typename T>
+StepConsts<T> consts(const dss_ctx* c, double alpha) {
+  const dss_hparams& h = c->cfg.hp;
+  StepConsts<T> k;
+  k.alpha = static_cast<T>(alpha);
+  k.wd = static_cast<T>(h.weight_decay);
+  k.mom = static_cast<T>(h.momentum);
+  k.b1 = static_cast<T>(h.beta1);
+  k.omb1 = static_cast<T>(1.0 - h.beta1);
+  k.b2 = static_cast<T>(h.beta2);
+  k.omb2 = static_cast<T>(1.0 - h.beta2);
+  k.eps = static_cast<T>(h.epsilon);
+  k.awd = static_cast<T>(alpha * h.weight_decay);
+  return k;
+}
+
+template <typename Args>
+void fill_bias(const dss_ctx* c, Args& a) {
+  const dss_hparams& h = c->cfg.hp;
+  for (int k = 0; k < c->P; ++k) {
+    const double t = static_cast<double>(c->step_count[static_cast<size_t>(k)] + 1);
+    a.bc1[k] = 1.0 - std::pow(h.beta1, t);  // optim.cpp:76-77
+    a.bc2[k] = 1.0 - std::pow(h.beta2, t);  // optim.cpp:78
+  }
+}
+
+// ---- engine (engine.cu) -----------------------------------------------------
+
+GroupLaunch make_group_launch(dss_ctx* c, const std::vector<std::vector<int>>& groups);
+std::vector<OwnedSlot> owned_layout(const dss_ctx* c, const Partition& part, int q, long chunk, long* stage_total,
+                                    long* flag_total);
+// All launch tables of the context (both schedule parities, sync rounds,
+// the trace mean, running stats); after dss_ipc_attach on several GPUs.
+void build_plans(dss_ctx* c);
+
+void launch_groups_any(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha, const void* g, long g_ld,
+                       int step_phase, int sync_phase = 1, void* rows = nullptr, long rows_ld = 0);
+void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t);
+void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha = 0.0);
+void launch_push_any(dss_ctx* c, const PushLaunch& pl, long t, double alpha);
+template <typename T>
+void launch_bsp(dss_ctx* c, long t, double alpha);
+
+// Cross-GPU flag barrier (no-op on one GPU).
+void barrier(dss_ctx* c);
+// Barrier if peers may still be writing into our rows.
+void quiesce(dss_ctx* c);
+void fold_stats(dss_ctx* c, long t, bool barrier_done);
+void bump_steps(dss_ctx* c);
+int check_impl(dss_ctx* c);
+int check_rank(dss_ctx* c, int rank, int* lr);
+RowGeom geom(dss_ctx* c, int buffer);
+
+// Tiny worlds (engine.cu): whole iterations in one CTA when every worker is
+// on this GPU and all rows fit 32 KB; logistic = 1 adds the device
+// gradient phase (problems_abi.cu).
+bool small_path(const dss_ctx* c, long n);
+template <typename T>
+void run_small(dss_ctx* c, long t0, long n, const double* alphas, bool logistic = false);
+
+// Logistic problem state on the device (problems_abi.cu).
+LogisticArgs logistic_args(dss_ctx* c, long t);
+void free_logistic(dss_ctx* c);
+
+}  // namespace dssb

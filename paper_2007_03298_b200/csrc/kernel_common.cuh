@@ -1,0 +1,191 @@
+// Shared pieces of the sm_100a kernels: tuning knobs, exact scalar ops,
+// 16-byte vectors, the optimizer step of one element (optim.cpp:46-98),
+// the divergence latch and the reference's SplitMix64 / Box-Muller stream.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dssb {
+
+constexpr int kThreads = 256;
+constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel params
+
+// Tuning knobs (compile-time; the defaults are the measured best, see
+// DESIGN.md).  Members whose loads are issued together before the first
+// state store, per optimizer, and the CTAs/SM the register cap targets.
+#ifndef DSS_CHUNK_MOMENTUM
+#define DSS_CHUNK_MOMENTUM 8
+#endif
+#ifndef DSS_CHUNK_ADAM
+#define DSS_CHUNK_ADAM 4
+#endif
+#ifndef DSS_MIN_BLOCKS
+#define DSS_MIN_BLOCKS 2
+#endif
+#ifndef DSS_MIN_BLOCKS_M8_MOMENTUM
+#define DSS_MIN_BLOCKS_M8_MOMENTUM 1
+#endif
+// Chain fold pipelining: elements per chunk (one flag each) and resident
+// CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
+// start one round after stage j instead of after the whole row.
+#ifndef DSS_CHAIN_CHUNK
+#define DSS_CHAIN_CHUNK 8192
+#endif
+#ifndef DSS_CHAIN_CTAS_PER_SM
+#define DSS_CHAIN_CTAS_PER_SM 8
+#endif
+// Rows up to this many bytes fold one-shot over NVLink (every member GPU
+// gathers every member's row) instead of two-shot.
+#ifndef DSS_ONESHOT_MAX_BYTES
+#define DSS_ONESHOT_MAX_BYTES (512L << 10)
+#endif
+// 1: full system fence before each chunk's release flag; 0: rely on the
+// cumulativity of st.release.sys after the CTA barrier (lighter).
+#ifndef DSS_CHAIN_FENCE
+#define DSS_CHAIN_FENCE 0
+#endif
+
+enum OptKind : int { kOptNone = -1, kSgd = 0, kMomentum = 1, kAdam = 2, kAdamW = 3 };
+
+// ---- exact scalar ops ------------------------------------------------------
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ bool finite_(float a) { return isfinite(a); }
+__device__ __forceinline__ bool finite_(double a) { return isfinite(a); }
+
+// ---- 16-byte vectors ---------------------------------------------------------
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  using type = float4;
+  static constexpr int n = 4;
+};
+template <> struct Vec<double> {
+  using type = double2;
+  static constexpr int n = 2;
+};
+
+template <typename T> struct Pack {
+  T v[Vec<T>::n];
+};
+
+// Streaming loads/stores (evict-first): every byte is touched once per
+// iteration and the working set is far larger than L2.
+template <typename T>
+__device__ __forceinline__ Pack<T> ldv(const T* p) {
+  Pack<T> r;
+  typename Vec<T>::type x = __ldcs(reinterpret_cast<const typename Vec<T>::type*>(p));
+  static_assert(sizeof(x) == sizeof(r), "pack");
+  *reinterpret_cast<typename Vec<T>::type*>(r.v) = x;
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void stv(T* p, const Pack<T>& r) {
+  __stcs(reinterpret_cast<typename Vec<T>::type*>(p),
+         *reinterpret_cast<const typename Vec<T>::type*>(r.v));
+}
+// Peer/remote rows: cache-global accesses (no L1 allocation); peer
+// addresses bypass the local L2 anyway.
+template <typename T>
+__device__ __forceinline__ Pack<T> ldv_cg(const T* p) {
+  Pack<T> r;
+  *reinterpret_cast<typename Vec<T>::type*>(r.v) =
+      __ldcg(reinterpret_cast<const typename Vec<T>::type*>(p));
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void stv_cg(T* p, const Pack<T>& r) {
+  __stcg(reinterpret_cast<typename Vec<T>::type*>(p),
+         *reinterpret_cast<const typename Vec<T>::type*>(r.v));
+}
+
+// ---- optimizer constants for one launch (rounded once from double) ---------
+template <typename T> struct StepConsts {
+  T alpha;   // a
+  T wd;      // weight_decay
+  T mom;     // momentum
+  T b1, omb1;  // beta1, 1 - beta1 (computed in double, optim.cpp:84)
+  T b2, omb2;  // beta2, 1 - beta2
+  T eps;
+  T awd;     // a * weight_decay (optim.cpp:89, left-to-right)
+};
+
+// apply_step for one element (optim.cpp:56-91).  Operator order is the
+// reference's, left to right:
+//   sgd:      ge = g + wd*w;               w' = w - a*ge
+//   momentum: ge = g + wd*w; b = mom*b + ge; w' = w - a*b
+//   adam(w):  ge = adam ? g + wd*w : g
+//             m = b1*m + (1-b1)*ge;  v = b2*v + ((1-b2)*ge)*ge
+//             w' = w - (a*(m/bc1)) / (sqrt(v/bc2) + eps);  adamw: w' -= (a*wd)*w
+template <typename T, int OPT>
+__device__ __forceinline__ T step_elem(T w, T g, T& m1, T& m2, const StepConsts<T>& c, T bc1, T bc2) {
+  if constexpr (OPT == kSgd) {
+    const T ge = add_(g, mul_(c.wd, w));
+    return sub_(w, mul_(c.alpha, ge));
+  } else if constexpr (OPT == kMomentum) {
+    const T ge = add_(g, mul_(c.wd, w));
+    m1 = add_(mul_(c.mom, m1), ge);
+    return sub_(w, mul_(c.alpha, m1));
+  } else {
+    const T ge = (OPT == kAdam) ? add_(g, mul_(c.wd, w)) : g;
+    m1 = add_(mul_(c.b1, m1), mul_(c.omb1, ge));
+    m2 = add_(mul_(c.b2, m2), mul_(mul_(c.omb2, ge), ge));
+    const T mhat = div_(m1, bc1);
+    const T vhat = div_(m2, bc2);
+    T out = sub_(w, div_(mul_(c.alpha, mhat), add_(sqrt_(vhat), c.eps)));
+    if constexpr (OPT == kAdamW) out = sub_(out, mul_(c.awd, w));
+    return out;
+  }
+}
+
+// ---- divergence latch ----------------------------------------------------
+// key = t << 34 | phase << 32 | rank; atomicMin keeps the earliest iteration,
+// then phase (DS: 0 local step before 1 group sync, sync.cpp:348-370; BSP:
+// 0 gradient collective before 1 step, sync.cpp:389-421), then lowest rank
+// (sync.cpp:126-128).
+__device__ __forceinline__ unsigned long long err_key(long t, int phase, int rank) {
+  return (static_cast<unsigned long long>(t) << 34) |
+         (static_cast<unsigned long long>(phase) << 32) | static_cast<unsigned int>(rank);
+}
+
+__device__ __forceinline__ void latch_error(unsigned long long* err, unsigned long long key) {
+  // warp-aggregate: one atomic per warp that saw a failure
+  const unsigned mask = __activemask();
+  unsigned long long k = key;
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(mask, k, off);
+    k = o < k ? o : k;
+  }
+  if ((threadIdx.x & 31) == (__ffs(mask) - 1) && k != ~0ull) atomicMin(err, k);
+}
+
+
+// ---- synthetic gradients: SplitMix64 + Box-Muller (rng.cpp:8-51) -----------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// i-th gaussian of the stream whose state after for_stream is s0: draws
+// 2i and 2i+1 (0-based), draw j = mix64(s0 + (j+1) * phi) (rng.cpp:28-31).
+__device__ __forceinline__ double gaussian_at(uint64_t s0, uint64_t i) {
+  const uint64_t phi = 0x9e3779b97f4a7c15ULL;
+  const uint64_t x = mix64(s0 + (2 * i + 1) * phi);
+  const uint64_t y = mix64(s0 + (2 * i + 2) * phi);
+  const double u1 = __dsub_rn(1.0, __dmul_rn(static_cast<double>(x >> 11), 0x1.0p-53));
+  const double u2 = __dmul_rn(static_cast<double>(y >> 11), 0x1.0p-53);
+  // sqrt(-2 log u1) * cos(2 pi u2), the argument rounded as (2.0*pi)*u2
+  return __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, log(u1))),
+                   cos(__dmul_rn(6.283185307179586232, u2)));
+}
+
+}  // namespace dssb

@@ -3,10 +3,12 @@ import re
 import subprocess
 import sys
 
-cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-fmad=false",
-       "-Xcompiler", "-fPIC", "-Iinclude", "-Ipaper_2007_03298_b200/csrc", "-Xptxas=-v", "-c",
-       "paper_2007_03298_b200/csrc/dssync_b200.cu", "-o", "/tmp/ptxas_report.o"]
-out = subprocess.run(cmd, capture_output=True, text=True).stderr
+out = ""
+for src in ("engine.cu", "dssync_b200.cu", "problems_abi.cu"):
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-fmad=false",
+           "-Xcompiler", "-fPIC", "-Iinclude", "-Ipaper_2007_03298_b200/csrc", "-Xptxas=-v", "-c",
+           "paper_2007_03298_b200/csrc/" + src, "-o", "/tmp/ptxas_report.o"]
+    out += subprocess.run(cmd, capture_output=True, text=True).stderr
 cur = None
 rows = []
 for line in out.splitlines():
