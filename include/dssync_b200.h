@@ -108,11 +108,12 @@ typedef struct {
                            2 = (several GPUs) every spanning group uses the chain fold.
                            3 = (several GPUs) two-shot groups use the unfused pull fold
                            (step, barrier, fold) instead of the fused push kernel.
-                           4 = (several GPUs) as 0 but never one-shot.  Path 0 folds
-                           groups of one member per GPU one-shot (every member GPU
-                           gathers every member row; no peer stores into params, no
-                           next-iteration barrier) when the group is a pair or rows
-                           are at most 512 KiB.
+                           4 = (several GPUs) as 0 but never one-shot.  Path 0 folds a
+                           schedule parity one-shot (every member GPU gathers every
+                           member row and folds it for its own members; no peer stores
+                           into params, no next-iteration barrier) when its spanning
+                           groups are pairs with one member per GPU, or rows are at
+                           most 512 KiB.
                            Results are bit-identical on every path. */
   long stats_dim;       /* running_stats per worker (0 = none).  They travel with the
                            params (DS, sync_round) or the gradients (BSP) through the same

@@ -203,26 +203,35 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         }
       }
       // One-shot per schedule parity: every member GPU gathers every
-      // member's row.  Same NVLink bytes as two-shot for pairs (S = 2) and
-      // no barrier before the next iteration; for S > 2 only small rows.
+      // member's row and folds it for its own members.  Pairs with one
+      // member per GPU move the same NVLink bytes as two-shot and skip the
+      // next iteration's barrier, so they go one-shot at any size; any
+      // other spanning group (larger, or several members per GPU: the
+      // chain) only for rows of at most DSS_ONESHOT_MAX_BYTES.
+      long rows = 0;
       for (long t = 0; t < 2; ++t) {
         if (s.kind != DSS_DS_SYNC || !use_push(c.get()) || force_chain(c.get()) || cfg->path == 4) break;
         const Partition part = make_partition(s, t);
+        const bool small = c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
         bool ok = true;
+        long rmax = 0;
         for (int gi = 0; gi < part.n_groups(); ++gi) {
           std::vector<int> gpus;
           for (int q = 0; q < part.size(gi); ++q) gpus.push_back(part.group(gi)[q] / c->P);
-          const bool spans = gpus.front() != gpus.back();
+          if (gpus.front() == gpus.back()) continue;  // local group
           const bool one_each = std::adjacent_find(gpus.begin(), gpus.end()) == gpus.end();
-          if (spans && one_each && part.size(gi) > 2 && c->d_pad * c->esz > DSS_ONESHOT_MAX_BYTES) ok = false;
+          if (!(one_each && part.size(gi) == 2) && !small) ok = false;
+          rmax = std::max<long>(rmax, part.size(gi));
         }
-        c->oneshot[t] = ok;
+        c->oneshot[t] = ok && rmax > 0;
+        if (c->oneshot[t]) rows = std::max(rows, rmax);
       }
       if (c->oneshot[0] || c->oneshot[1]) {
+        c->oneshot_rows = rows;
         c->oneshot_base_elems = ps;
         c->oneshot_base_flags = pf;
-        c->oneshot_half_elems = static_cast<long>(c->P) * cfg->n_gpus * c->d_pad;
-        c->oneshot_half_flags = static_cast<long>(c->P) * cfg->n_gpus * c->chain_nchunks;
+        c->oneshot_half_elems = static_cast<long>(c->P) * rows * c->d_pad;
+        c->oneshot_half_flags = static_cast<long>(c->P) * rows * c->chain_nchunks;
         ps += 2 * c->oneshot_half_elems;
         pf += 2 * c->oneshot_half_flags;
       }

@@ -270,10 +270,12 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
   return pl;
 }
 
-// One-shot tables of parity t for this GPU: my member's stepped row goes to
-// every member GPU's staging (row lr_o * G + j on GPU o, lr_o the member's
-// local row there, j my position in the group); every GPU folds all S rows
-// of its own member in ascending order and keeps the mean locally.
+// One-shot tables of parity t for this GPU.  Every member's stepped row
+// goes to every GPU of its group: row slot * R + q of GPU o's staging, with
+// slot = the local row there of the group's first member on o, q the
+// member's position in the group and R the largest group size.  Every GPU
+// then folds all m rows of each of its groups in member order and stores
+// the mean into its own members only.
 PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   PushLaunch pl;
   pl.oneshot = true;
@@ -281,49 +283,60 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   const int me = c->cfg.rank;
   const long CH = c->chain_chunk;
   const long nch = c->chain_nchunks;
-  const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, G, me, c->d_pad, force_chain(c));
+  const long R = c->oneshot_rows;
+  const GpuPlan gp = make_plan(part, c->cfg.strategy.world_size, G, me, c->d_pad, force_chain(c), true);
   std::vector<PushItem> items;
   std::vector<void*> item_dst;
   std::vector<unsigned long long*> item_flag;
   std::vector<PushFold> folds;
   std::vector<void*> dst;
   for (int gi : gp.spanning_groups) {
-    bool chain = false;
-    for (const ChainRole& r : gp.chain) chain = chain || r.group == gi;
-    if (chain) continue;
     const int* mem = part.group(gi);
     const int m = part.size(gi);
-    int j = -1, my_member = -1;
+    if (m > R) throw std::logic_error("one-shot: group larger than the staging rows");
+    std::vector<int> gpus, slot;  // distinct GPUs of the group and the group's slot on each
     for (int q = 0; q < m; ++q) {
-      if (mem[q] / c->P == me) {
-        j = q;
-        my_member = mem[q];
+      const int gpu = mem[q] / c->P;
+      if (gpus.empty() || gpus.back() != gpu) {
+        gpus.push_back(gpu);
+        slot.push_back(mem[q] - gpu * c->P);
       }
     }
+    const int S = static_cast<int>(gpus.size());
+    int j = -1;  // my position among the group's GPUs
+    for (int o = 0; o < S; ++o) j = gpus[static_cast<size_t>(o)] == me ? o : j;
     if (j < 0) continue;
-    // one item per chunk of my member: stepped once, stored to all m
-    // stagings (every GPU starting at a different destination)
-    for (long ch = 0; ch < nch; ++ch) {
-      PushItem it{};
-      it.lr = my_member - c->first;
-      it.lo = ch * CH;
-      it.hi = std::min(c->d_pad, it.lo + CH);
-      it.dst_beg = static_cast<int>(item_dst.size());
-      it.ndst = m;
-      it.rank = my_member;
-      for (int oo = 0; oo < m; ++oo) {
-        const int o = (oo + j) % m;
-        const int gpu = mem[o] / c->P;
-        const long row = static_cast<long>(mem[o] - gpu * c->P) * G + j;
-        item_dst.push_back(static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpu)]) +
-                           static_cast<size_t>(row * c->d_pad + it.lo) * c->esz);
-        item_flag.push_back(c->peer_push_flags[static_cast<size_t>(gpu)] + row * nch + ch);
-      }
-      items.push_back(it);
+    std::vector<int> mine;
+    for (int q = 0; q < m; ++q) {
+      if (mem[q] / c->P == me) mine.push_back(q);
     }
-    const long row0 = static_cast<long>(my_member - c->first) * G;
+    // one item per (local member, chunk): stepped once, stored to all S
+    // GPUs, every GPU starting at a different destination
+    for (int q : mine) {
+      for (long ch = 0; ch < nch; ++ch) {
+        PushItem it{};
+        it.lr = mem[q] - c->first;
+        it.lo = ch * CH;
+        it.hi = std::min(c->d_pad, it.lo + CH);
+        it.dst_beg = static_cast<int>(item_dst.size());
+        it.ndst = S;
+        it.rank = mem[q];
+        for (int oo = 0; oo < S; ++oo) {
+          const int o = (oo + j) % S;
+          const int gpu = gpus[static_cast<size_t>(o)];
+          const long row = static_cast<long>(slot[static_cast<size_t>(o)]) * R + q;
+          item_dst.push_back(static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpu)]) +
+                             static_cast<size_t>(row * c->d_pad + it.lo) * c->esz);
+          item_flag.push_back(c->peer_push_flags[static_cast<size_t>(gpu)] + row * nch + ch);
+        }
+        items.push_back(it);
+      }
+    }
+    const long row0 = static_cast<long>(slot[static_cast<size_t>(j)]) * R;
     const int dst_beg = static_cast<int>(dst.size());
-    dst.push_back(static_cast<char*>(c->w) + static_cast<size_t>(my_member - c->first) * c->d_pad * c->esz);
+    for (int q : mine) {
+      dst.push_back(static_cast<char*>(c->w) + static_cast<size_t>(mem[q] - c->first) * c->d_pad * c->esz);
+    }
     for (long ch = 0; ch < nch; ++ch) {
       PushFold f{};
       f.lo = ch * CH;
@@ -334,17 +347,17 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
       f.flag_ld = nch;
       f.S = m;
       f.dst_beg = dst_beg;
-      f.n_dst = 1;
+      f.n_dst = static_cast<int>(mine.size());
       f.err_rank = mem[0];
       folds.push_back(f);
     }
   }
-  // chunk-major across this GPU's groups
+  // chunk-major across this GPU's members
   std::vector<PushItem> ordered;
   ordered.reserve(items.size());
-  const size_t ng = nch ? items.size() / static_cast<size_t>(nch) : 0;
+  const size_t nm = nch ? items.size() / static_cast<size_t>(nch) : 0;
   for (long ch = 0; ch < nch; ++ch) {
-    for (size_t g = 0; g < ng; ++g) ordered.push_back(items[g * static_cast<size_t>(nch) + static_cast<size_t>(ch)]);
+    for (size_t g = 0; g < nm; ++g) ordered.push_back(items[g * static_cast<size_t>(nch) + static_cast<size_t>(ch)]);
   }
   pl.items = static_cast<int>(ordered.size());
   pl.folds = static_cast<int>(folds.size());
@@ -386,7 +399,8 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
       }
     }
   } else {
-    const GpuPlan gp = make_plan(part, s.world_size, G, multi(c) ? c->cfg.rank : 0, c->d_pad, force_chain(c));
+    const GpuPlan gp = make_plan(part, s.world_size, G, multi(c) ? c->cfg.rank : 0, c->d_pad, force_chain(c),
+                                 with_step && c->oneshot[t & 1]);
     pp.any_spanning = gp.any_spanning_globally;
     pp.any_twoshot = gp.any_twoshot_globally;
     pp.any_chain = gp.any_chain_globally;

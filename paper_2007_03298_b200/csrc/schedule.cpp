@@ -206,7 +206,8 @@ void slice_range(long d_pad, int s, int j, long* lo, long* hi) {
   *hi = c1 * kRowAlign;
 }
 
-GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad, bool force_chain) {
+GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad, bool force_chain,
+                  bool no_chain) {
   GpuPlan plan;
   const int per = world_size / n_gpus;
   std::vector<int> slots_used(static_cast<size_t>(n_gpus), 0);
@@ -229,7 +230,8 @@ GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, l
     }
     const bool spanning = gpus.size() > 1;
     if (spanning) plan.any_spanning_globally = true;
-    const bool chain = spanning && (force_chain || *std::max_element(count.begin(), count.end()) >= 2);
+    const bool chain =
+        spanning && !no_chain && (force_chain || *std::max_element(count.begin(), count.end()) >= 2);
     slot_of[static_cast<size_t>(g)].assign(static_cast<size_t>(n_gpus), -1);
     if (chain) {
       plan.any_chain_globally = true;

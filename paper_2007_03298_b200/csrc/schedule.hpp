@@ -91,9 +91,11 @@ struct GpuPlan {
 
 // force_chain: every spanning group takes the chain path (tests); otherwise
 // only groups with >= 2 members on some GPU (where the chain moves fewer
-// NVLink bytes than the two-shot).
+// NVLink bytes than the two-shot).  no_chain: no group takes the chain (a
+// one-shot parity: every spanning group is gathered whole by every member
+// GPU).
 GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad,
-                  bool force_chain = false);
+                  bool force_chain = false, bool no_chain = false);
 
 // [lo, hi) of the j-th of s near-equal chunk-aligned slices of [0, d_pad).
 void slice_range(long d_pad, int s, int j, long* lo, long* hi);
