@@ -105,6 +105,38 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0):
     return True
 
 
+def logistic_case(rank, G, sampling, kind):
+    """C1 end to end on G GPUs (device batch sampling + logistic gradient +
+    the step, f64) equals the same run with all workers on one GPU, bit for
+    bit: the schedule, the sampling streams and every fold are independent
+    of the packing."""
+    from paper_2007_03298_b200 import SamplingMode, logistic_dataset
+    W, N, T = 4, (2 if kind == "ds" else 4), 40
+    if W % G:
+        return True
+    x, y = logistic_dataset(11, 20, 2000)
+    alphas = 1.0 * 0.5 ** (np.arange(T) // 15)
+    s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING, WorldConfig(W, N))
+    e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 20, OptimizerHyperparams(), "f64", rank, rank, G)
+    attach(e)
+    e.logistic_setup(x, y, 0.05, 8, sampling, 1)
+    e.logistic_steps(0, alphas, check=True)
+    parts = [None] * G
+    dist.all_gather_object(parts, e.download_all(BUF_PARAMS))
+    e.close()
+    if rank != 0:
+        return True
+    with DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 20, OptimizerHyperparams(), "f64", 0) as one:
+        one.logistic_setup(x, y, 0.05, 8, sampling, 1)
+        for t in range(T):  # per-iteration launches (the one-CTA path has its own test)
+            one.logistic_gradients(t)
+            one.step(t, float(alphas[t]))
+        ref = one.download_all(BUF_PARAMS)
+    ok = np.array_equal(np.concatenate(parts), ref)
+    print(f"case logistic {kind} sampling={int(sampling)} G={G}: {'OK' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
 def main():
     rank = int(os.environ["RANK"])
     G = int(os.environ["WORLD_SIZE"])
@@ -121,6 +153,10 @@ def main():
             ok = run_case(*case, rank, G, orc, path) and ok
     for case in (("ds", 8, 2, True, 2, 1001), ("bsp", 8, 8, False, 1, 777)):  # running-stats tail
         ok = run_case(*case, rank, G, orc, 0, sd=6) and ok
+    from paper_2007_03298_b200 import SamplingMode
+    for kind in ("ds", "bsp"):
+        for sampling in (SamplingMode.REPLACEMENT, SamplingMode.EPOCH):
+            ok = logistic_case(rank, G, sampling, kind) and ok
     dist.barrier()
     if rank == 0:
         print("MGPU " + ("PASS" if ok else "FAIL"), flush=True)

@@ -176,3 +176,23 @@ def test_fused_small_world_divergence(cuda_device, c1_data, kind, N, alpha, rank
         with pytest.raises(DivergenceError) as ex:
             e.logistic_steps(0, [alpha, alpha], check=True)
         assert ex.value.rank == rank and ex.value.iteration == 0 and what in str(ex.value)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_one_cta_path_equals_per_launch_path(cuda_device, golden, c1_data, dtype):
+    """The one-CTA small-world kernel (dss_logistic_steps, n >= 2) and one
+    gradient launch + one step launch per iteration do the same additions
+    in the same order: identical bits."""
+    meta, a = golden
+    x, y = c1_data
+    for m in meta["c1"]:
+        alphas = a[f"{m['tag']}_alphas"][:120]
+        with engine(m["kind"], 4, m["N"], dtype) as e1, engine(m["kind"], 4, m["N"], dtype) as e2:
+            for e in (e1, e2):
+                e.logistic_setup(x, y, L2, B, sampling_of(m), RUN_SEED)
+            e1.logistic_steps(0, alphas, check=True)
+            for t, al in enumerate(alphas):
+                e2.logistic_gradients(t)
+                e2.step(t, float(al))
+            e2.check()
+            assert np.array_equal(e1.download_all(BUF_PARAMS), e2.download_all(BUF_PARAMS)), (m["tag"], dtype)
