@@ -97,6 +97,8 @@ struct ChainLaunch {
 
 struct PushLaunch {
   bool oneshot = false;
+  bool bsp = false;                // one-shot BSP: push gradients, fold, step the replicas
+  int* d_dst_lr = nullptr;         // BSP: local row of each dst
   int items = 0, folds = 0;
   void** d_item_dst = nullptr;
   unsigned long long** d_item_flag = nullptr;

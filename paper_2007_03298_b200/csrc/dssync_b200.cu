@@ -209,6 +209,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // other spanning group (larger, or several members per GPU: the
       // chain) only for rows of at most DSS_ONESHOT_MAX_BYTES.
       long rows = 0;
+      const bool small_rows = c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
+      if (s.kind == DSS_BSP && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 && small_rows &&
+          s.world_size <= kMaxFold) {
+        c->oneshot[0] = true;  // BSP: gather all W gradient rows (build_bsp_multi_plan)
+        rows = s.world_size;
+      }
       for (long t = 0; t < 2; ++t) {
         if (s.kind != DSS_DS_SYNC || !use_push(c.get()) || force_chain(c.get()) || cfg->path == 4) break;
         const Partition part = make_partition(s, t);
@@ -461,6 +467,17 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
       // Packed GPUs (P >= 2) use the ordered chain over the gradient rows
       // instead: every GPU forwards one partial row, not P rows.
       const ParityPlan& pp = c->step_plan[0];
+      if (pp.any_push) {
+        // one-shot: push the gradients, fold all W, step the replicas
+        quiesce(c);
+        launch_push_any(c, pp.push, t, alpha);
+        c->pending_remote = false;
+        fold_stats(c, t, false);
+        bump_steps(c);
+        if (out) *out = round_outcome(s, t, c->d + c->s);
+        if (check) return check_impl(c);
+        return DSS_OK;
+      }
       c->pending_remote = false;
       barrier(c);
       if (pp.any_twoshot) {

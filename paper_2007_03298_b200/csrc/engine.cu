@@ -290,6 +290,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   std::vector<unsigned long long*> item_flag;
   std::vector<PushFold> folds;
   std::vector<void*> dst;
+  std::vector<int> dst_lr;
   for (int gi : gp.spanning_groups) {
     const int* mem = part.group(gi);
     const int m = part.size(gi);
@@ -336,6 +337,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
     const int dst_beg = static_cast<int>(dst.size());
     for (int q : mine) {
       dst.push_back(static_cast<char*>(c->w) + static_cast<size_t>(mem[q] - c->first) * c->d_pad * c->esz);
+      dst_lr.push_back(mem[q] - c->first);
     }
     for (long ch = 0; ch < nch; ++ch) {
       PushFold f{};
@@ -366,6 +368,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   pl.d_items = upload_table(c, ordered);
   pl.d_folds = upload_table(c, folds);
   pl.d_dst = upload_table(c, dst);
+  pl.d_dst_lr = upload_table(c, dst_lr);
   return pl;
 }
 
@@ -493,6 +496,15 @@ ParityPlan build_bsp_multi_plan(dss_ctx* c) {
   const int G = c->cfg.n_gpus;
   const int W = c->cfg.strategy.world_size;
   const Partition part = make_partition(c->cfg.strategy, 0);  // one all-world group
+  if (c->oneshot[0]) {
+    // small rows: every GPU gathers all W gradient rows, folds them in rank
+    // order and steps its replicas (one kernel, no barrier)
+    pp.any_spanning = true;
+    pp.any_push = true;
+    pp.push = build_oneshot(c, part);
+    pp.push.bsp = true;
+    return pp;
+  }
   const GpuPlan gp = make_plan(part, W, G, c->cfg.rank, c->d_pad, force_chain(c));
   pp.any_spanning = true;
   pp.any_twoshot = gp.any_twoshot_globally;
@@ -911,6 +923,7 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   a.folds = pl.d_folds;
   a.n_folds = pl.folds;
   a.dst = reinterpret_cast<T* const*>(pl.d_dst);
+  a.dst_lr = pl.d_dst_lr;
   a.w = static_cast<T*>(c->w);
   a.g = static_cast<const T*>(c->g);
   a.m1 = static_cast<T*>(c->m1);
@@ -930,13 +943,14 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   }
   a.c = consts<T>(c, alpha);
   fill_bias(c, a);
+  auto kern = pl.bsp ? push_twoshot_kernel<T, OPT, true> : push_twoshot_kernel<T, OPT, false>;
   int occ = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, push_twoshot_kernel<T, OPT>, kThreads, 0), "occupancy");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0), "occupancy");
   // fully resident grid: phase-1 work can never wait behind spinning CTAs
   const long grid = std::max(1L, std::min<long>(static_cast<long>(std::max(occ, 1)) * c->sms,
                                                 std::max(pl.items, pl.folds)));
   TimedLaunch tl(c, DSS_KIND_FOLD);
-  push_twoshot_kernel<T, OPT><<<static_cast<int>(grid), kThreads, 0, c->stream>>>(a);
+  kern<<<static_cast<int>(grid), kThreads, 0, c->stream>>>(a);
   ck(cudaGetLastError(), "push_twoshot_kernel launch");
 }
 

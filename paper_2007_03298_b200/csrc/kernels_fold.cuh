@@ -506,6 +506,7 @@ template <typename T> struct PushArgs {
   const PushFold* folds;
   int n_folds;
   T* const* dst;         // member param rows (local or peer)
+  const int* dst_lr;     // BSP: local row of each dst (its optimizer state and bias corrections)
   T* w;
   const T* g;
   T* m1;
@@ -527,7 +528,10 @@ template <typename T> struct PushArgs {
 // one-shot (every member GPU receives every member's stepped row and folds
 // it for its own member; small rows: no remote stores into params, so the
 // next iteration needs no barrier).  Same kernel, different tables.
-template <typename T, int OPT>
+// BSP = true (one-shot over the world): phase 1 pushes the raw gradient
+// rows, phase 2 folds all W of them in rank order and steps every local
+// replica with the mean gradient (sync.cpp:389-421).
+template <typename T, int OPT, bool BSP = false>
 __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   __shared__ PushItem it;
@@ -548,6 +552,11 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
     const T b2 = static_cast<T>(a.bc2[it.lr]);
     for (long e = it.lo / VN + threadIdx.x; e < it.hi / VN; e += blockDim.x) {
       const long off = e * VN;
+      if constexpr (BSP) {
+        const Pack<T> gv = ldv(a.g + r + off);
+        for (int q = 0; q < it.ndst; ++q) stv_cg(sdst[q] + (off - it.lo), gv);
+        continue;
+      }
       Pack<T> x = ldv(a.w + r + off);
       const Pack<T> gv = ldv(a.g + r + off);
       Pack<T> s1, s2;
@@ -599,11 +608,37 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
           acc.v[l] = mul_(acc.v[l], inv);
           ok = ok && finite_(acc.v[l]);
         }
-        if (!ok) {
-          const unsigned long long k = err_key(a.t, 1, fo.err_rank);
+        if (!ok) {  // collective failure: members[0] (DS phase 1, BSP phase 0)
+          const unsigned long long k = err_key(a.t, BSP ? 0 : 1, fo.err_rank);
           bad = k < bad ? k : bad;
         }
-        for (int q = 0; q < fo.n_dst; ++q) stv_cg(a.dst[fo.dst_beg + q] + off, acc);
+        if constexpr (BSP) {
+          for (int q = 0; q < fo.n_dst; ++q) {  // every local replica steps with the mean gradient
+            const int lr = a.dst_lr[fo.dst_beg + q];
+            const long r = static_cast<long>(lr) * a.ld + off;
+            Pack<T> x = ldv(a.w + r);
+            Pack<T> s1, s2;
+            if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
+            if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+            const T b1 = static_cast<T>(a.bc1[lr]);
+            const T b2 = static_cast<T>(a.bc2[lr]);
+            bool oks = true;
+#pragma unroll
+            for (int l = 0; l < VN; ++l) {
+              x.v[l] = step_elem<T, OPT>(x.v[l], acc.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
+              oks = oks && finite_(x.v[l]);
+            }
+            stv(a.w + r, x);
+            if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
+            if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+            if (!oks) {
+              const unsigned long long k = err_key(a.t, 1, a.first_rank + lr);
+              bad = k < bad ? k : bad;
+            }
+          }
+        } else {
+          for (int q = 0; q < fo.n_dst; ++q) stv_cg(a.dst[fo.dst_beg + q] + off, acc);
+        }
       }
     }
     __syncthreads();
