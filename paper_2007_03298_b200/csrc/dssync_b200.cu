@@ -210,9 +210,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // chain) only for rows of at most DSS_ONESHOT_MAX_BYTES.
       long rows = 0;
       const bool small_rows = c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
+      // BSP: gather all W gradient rows (build_bsp_multi_plan).  Its one
+      // fold per chunk serialises W rows on one CTA, so only for small
+      // worlds: at 4 GPUs W=4 / 16 gain 2.4x / 1.9x at 1 KB rows, W=64 loses.
       if (s.kind == DSS_BSP && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 && small_rows &&
-          s.world_size <= kMaxFold) {
-        c->oneshot[0] = true;  // BSP: gather all W gradient rows (build_bsp_multi_plan)
+          s.world_size <= 16) {
+        c->oneshot[0] = true;
         rows = s.world_size;
       }
       for (long t = 0; t < 2; ++t) {
