@@ -26,6 +26,11 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_MIN_BLOCKS_M8_MOMENTUM
 #define DSS_MIN_BLOCKS_M8_MOMENTUM 1
 #endif
+// 1: while a group kernel steps one chunk of members, prefetch the next
+// chunk's rows into L2 (stateful optimizers with chunked member loads).
+#ifndef DSS_GROUP_PREFETCH
+#define DSS_GROUP_PREFETCH 1
+#endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.
@@ -86,6 +91,10 @@ __device__ __forceinline__ Pack<T> ldv(const T* p) {
   static_assert(sizeof(x) == sizeof(r), "pack");
   *reinterpret_cast<typename Vec<T>::type*>(r.v) = x;
   return r;
+}
+// L2 prefetch of one vector's cache line (no registers, no wait).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 template <typename T>
 __device__ __forceinline__ void stv(T* p, const Pack<T>& r) {

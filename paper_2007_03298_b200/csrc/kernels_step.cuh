@@ -85,6 +85,22 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
           if constexpr (OPT != kOptNone && OPT != kSgd) s1[q] = ldv(a.m1 + rj);
           if constexpr (OPT == kAdam || OPT == kAdamW) s2[q] = ldv(a.m2 + rj);
         }
+        if constexpr (DSS_GROUP_PREFETCH && CH < M) {
+          // the next chunk's members are fetched into L2 while this one steps
+          if (c0 + CH < M) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const int j = c0 + CH + q;
+              if (j < M) {
+                const long rj = static_cast<long>(lrow[j]) * a.ld + off;
+                prefetch_l2(a.w + rj);
+                if constexpr (OPT != kOptNone) prefetch_l2(a.g + static_cast<long>(lrow[j]) * a.g_ld + off);
+                if constexpr (OPT != kOptNone && OPT != kSgd) prefetch_l2(a.m1 + rj);
+                if constexpr (OPT == kAdam || OPT == kAdamW) prefetch_l2(a.m2 + rj);
+              }
+            }
+          }
+        }
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
           const int j = c0 + q;
