@@ -216,6 +216,7 @@ struct dss_ctx {
   int* d_small_offsets[2] = {nullptr, nullptr};
   int small_ngroups[2] = {0, 0};
   double* d_small_buf = nullptr;  // [n] alphas, [n][P] bc1, [n][P] bc2
+  unsigned* d_small_bar = nullptr;  // grid barrier of the persistent multi-CTA variant
   long small_cap = 0;
   std::vector<double> h_small;
 
@@ -389,10 +390,13 @@ int check_impl(dss_ctx* c);
 int check_rank(dss_ctx* c, int rank, int* lr);
 RowGeom geom(dss_ctx* c, int buffer);
 
-// Tiny worlds (engine.cu): whole iterations in one CTA when every worker is
-// on this GPU and all rows fit 32 KB; logistic = 1 adds the device
-// gradient phase (problems_abi.cu).
+// Small worlds (engine.cu): whole iterations in one launch when every
+// worker is on this GPU and all rows fit DSS_PERSIST_MAX_BYTES -- one CTA up
+// to 32 KB, else a resident grid with a barrier between iterations;
+// logistic = 1 (one CTA only) adds the device gradient phase
+// (problems_abi.cu).
 bool small_path(const dss_ctx* c, long n);
+long small_bytes(const dss_ctx* c);
 template <typename T>
 void run_small(dss_ctx* c, long t0, long n, const double* alphas, bool logistic = false);
 

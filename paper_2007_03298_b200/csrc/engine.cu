@@ -1127,16 +1127,27 @@ RowGeom geom(dss_ctx* c, int buffer) {
 // ---- tiny worlds: whole iterations in one CTA (dss_steps, dss_logistic_steps)
 
 // Worlds small enough that one CTA beats one launch per iteration.
+long small_bytes(const dss_ctx* c) { return static_cast<long>(c->P) * c->d_pad * c->esz; }
+
 bool small_path(const dss_ctx* c, long n) {
-  const long bytes = static_cast<long>(c->P) * c->d_pad * c->esz;
-  return !multi(c) && c->cfg.path == 0 && c->s == 0 && n >= 2 && bytes <= 32768 && c->P <= kMaxLocal;
+  return !multi(c) && c->cfg.path == 0 && c->s == 0 && n >= 2 && small_bytes(c) <= DSS_PERSIST_MAX_BYTES &&
+         c->P <= kMaxLocal;
 }
 
 template <typename T, int OPT>
-void launch_small_t(dss_ctx* c, const SmallArgs<T>& a) {
+void launch_small_t(dss_ctx* c, SmallArgs<T>& a, int grid) {
   TimedLaunch tl(c, c->cfg.strategy.kind == DSS_BSP ? DSS_KIND_BSP : DSS_KIND_GROUP);
-  small_steps_kernel<T, OPT><<<1, kThreads, 0, c->stream>>>(a);
-  ck(cudaGetLastError(), "small_steps_kernel launch");
+  if (grid == 1) {
+    small_steps_kernel<T, OPT><<<1, kThreads, 0, c->stream>>>(a);
+    ck(cudaGetLastError(), "small_steps_kernel launch");
+    return;
+  }
+  // persistent grid with a barrier between iterations: cooperative launch
+  // guarantees every CTA is resident
+  void* args[] = {&a};
+  ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(small_steps_kernel<T, OPT>), dim3(grid),
+                                 dim3(kThreads), args, 0, c->stream),
+     "small_steps_kernel cooperative launch");
 }
 
 template <typename T>
@@ -1197,11 +1208,24 @@ void run_small(dss_ctx* c, long t0, long n, const double* alphas, bool logistic)
     a.logistic = 1;
     a.lg = logistic_args(c, t0);
   }
+  // one CTA for tiny worlds (and the logistic phase, one warp per worker);
+  // above 32 KB a resident grid (up to two CTAs per SM), barrier between iterations
+  int grid = 1;
+  if (!logistic && small_bytes(c) > 32768) {
+    const long units = a.bsp ? a.nvec : std::max(a.ngroups[0], a.ngroups[1]) * a.nvec;
+    grid = static_cast<int>(std::min<long>(2L * c->sms, (units + kThreads - 1) / kThreads));
+    grid = std::max(grid, 1);
+  }
+  if (grid > 1) {
+    if (!c->d_small_bar) c->d_small_bar = static_cast<unsigned*>(dalloc(c, sizeof(unsigned)));
+    ck(cudaMemsetAsync(c->d_small_bar, 0, sizeof(unsigned), c->stream), "barrier reset");
+    a.bar = c->d_small_bar;
+  }
   switch (c->cfg.optimizer) {
-    case kSgd: launch_small_t<T, kSgd>(c, a); break;
-    case kMomentum: launch_small_t<T, kMomentum>(c, a); break;
-    case kAdam: launch_small_t<T, kAdam>(c, a); break;
-    case kAdamW: launch_small_t<T, kAdamW>(c, a); break;
+    case kSgd: launch_small_t<T, kSgd>(c, a, grid); break;
+    case kMomentum: launch_small_t<T, kMomentum>(c, a, grid); break;
+    case kAdam: launch_small_t<T, kAdam>(c, a, grid); break;
+    case kAdamW: launch_small_t<T, kAdamW>(c, a, grid); break;
     default: throw std::invalid_argument("unknown optimizer kind");
   }
   // the host table buffer is reused by the next call: wait for the copy

@@ -26,10 +26,11 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_MIN_BLOCKS_M8_MOMENTUM
 #define DSS_MIN_BLOCKS_M8_MOMENTUM 1
 #endif
-// 1: while a group kernel steps one chunk of members, prefetch the next
-// chunk's rows into L2 (stateful optimizers with chunked member loads).
-#ifndef DSS_GROUP_PREFETCH
-#define DSS_GROUP_PREFETCH 1
+// Single-GPU worlds of at most this many bytes per state array run a whole
+// dss_steps batch in one launch (a resident grid with a barrier between
+// iterations above 32 KB) instead of one launch per iteration.
+#ifndef DSS_PERSIST_MAX_BYTES
+#define DSS_PERSIST_MAX_BYTES (4L << 20)
 #endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
@@ -91,10 +92,6 @@ __device__ __forceinline__ Pack<T> ldv(const T* p) {
   static_assert(sizeof(x) == sizeof(r), "pack");
   *reinterpret_cast<typename Vec<T>::type*>(r.v) = x;
   return r;
-}
-// L2 prefetch of one vector's cache line (no registers, no wait).
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 template <typename T>
 __device__ __forceinline__ void stv(T* p, const Pack<T>& r) {

@@ -85,22 +85,6 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
           if constexpr (OPT != kOptNone && OPT != kSgd) s1[q] = ldv(a.m1 + rj);
           if constexpr (OPT == kAdam || OPT == kAdamW) s2[q] = ldv(a.m2 + rj);
         }
-        if constexpr (DSS_GROUP_PREFETCH && CH < M) {
-          // the next chunk's members are fetched into L2 while this one steps
-          if (c0 + CH < M) {
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-              const int j = c0 + CH + q;
-              if (j < M) {
-                const long rj = static_cast<long>(lrow[j]) * a.ld + off;
-                prefetch_l2(a.w + rj);
-                if constexpr (OPT != kOptNone) prefetch_l2(a.g + static_cast<long>(lrow[j]) * a.g_ld + off);
-                if constexpr (OPT != kOptNone && OPT != kSgd) prefetch_l2(a.m1 + rj);
-                if constexpr (OPT == kAdam || OPT == kAdamW) prefetch_l2(a.m2 + rj);
-              }
-            }
-          }
-        }
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
           const int j = c0 + q;
@@ -526,7 +510,24 @@ template <typename T> struct SmallArgs {
   unsigned long long* err;
   int logistic;         // 1: each iteration first computes the logistic gradients (lg) into g
   LogisticArgs lg;
+  unsigned* bar;        // grid barrier counter (zero at launch) when gridDim.x > 1
 };
+
+// Barrier across a fully resident grid: arrival count on a zeroed counter,
+// target = (iteration + 1) * gridDim.x.  The release fence publishes this
+// CTA's stores of the iteration before its arrival.
+__device__ __forceinline__ void small_grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
 
 constexpr int kSmallLogiMaxDim = 256;    // features per worker in the fused small-world logistic path
 constexpr int kSmallLogiMaxBatch = 256;  // batch size there
@@ -607,9 +608,11 @@ __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T
       small_logistic_grads(a, t, const_cast<T*>(a.g));
       __syncthreads();
     }
+    const long tid = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long nthreads = static_cast<long>(gridDim.x) * blockDim.x;
     if (a.bsp) {
       const T inv = static_cast<T>(1.0 / static_cast<double>(a.nw));
-      for (long e = threadIdx.x; e < a.nvec; e += blockDim.x) {
+      for (long e = tid; e < a.nvec; e += nthreads) {
         const long off = e * VN;
         Pack<T> gm = ldv(a.g + off);
         for (int k = 1; k < a.nw; ++k) {
@@ -655,7 +658,7 @@ __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T
       const int* members = a.members[p];
       const int* offsets = a.offsets[p];
       const long units = static_cast<long>(a.ngroups[p]) * a.nvec;
-      for (long u = threadIdx.x; u < units; u += blockDim.x) {
+      for (long u = tid; u < units; u += nthreads) {
         const int grp = static_cast<int>(u / a.nvec);
         const long off = (u % a.nvec) * VN;
         const int beg = offsets[grp];
@@ -706,7 +709,12 @@ __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T
         for (int j = 0; j < m; ++j) stv(a.w + static_cast<long>(members[beg + j]) * a.ld + off, acc);
       }
     }
-    __syncthreads();  // iteration t's rows are final before t+1 reads them
+    // iteration t's rows are final before t+1 reads them
+    if (gridDim.x == 1) {
+      __syncthreads();
+    } else {
+      small_grid_barrier(a.bar, static_cast<unsigned>(i + 1) * gridDim.x);
+    }
   }
   if (bad != ~0ull) atomicMin(a.err, bad);
 }

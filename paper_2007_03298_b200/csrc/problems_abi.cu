@@ -329,7 +329,8 @@ extern "C" int dss_logistic_gradients(dss_ctx* c, long t) {
 
 extern "C" int dss_logistic_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
   if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
-  if (small_path(c, n) && c->logi.ready && c->d <= kSmallLogiMaxDim && c->logi.B <= kSmallLogiMaxBatch) {
+  if (small_path(c, n) && small_bytes(c) <= 32768 && c->logi.ready && c->d <= kSmallLogiMaxDim &&
+      c->logi.B <= kSmallLogiMaxBatch) {
     // the whole run in one CTA: sampling, gradient, step and group fold
     const int st = guard(c, [&]() -> int {
       if (t0 < 0) throw std::invalid_argument("iteration must be >= 0");
