@@ -370,16 +370,24 @@ def test_c2_full_size_rows_vs_oracle(cuda_device, oracle):
         assert torch.max(torch.abs(after - before)).item() < 1e-6
 
 
-def test_batched_steps_equal_single_steps(cuda_device):
-    """dss_steps(t0, alphas) == the same iterations one dss_step at a time."""
+@pytest.mark.parametrize("kind,W,N,d,opt,dtype", [
+    ("ds", 16, 4, 3001, 3, "f32"),      # 192 KB per array: resident-grid multi-iteration kernel
+    ("ds", 16, 4, 40001, 1, "f64"),     # 5 MB: one launch per iteration
+    ("ds", 8, 2, 30001, 0, "f32"),      # rectangular C2 shape, 960 KB
+    ("bsp", 8, 8, 20001, 2, "f32"),     # BSP fold + step, 640 KB
+    ("bsp", 4, 4, 9001, 3, "f64"),
+])
+def test_batched_steps_equal_single_steps(cuda_device, kind, W, N, d, opt, dtype):
+    """dss_steps(t0, alphas) == the same iterations one dss_step at a time
+    (the batched path runs them in one launch up to 4 MB per array)."""
     rng = np.random.default_rng(9)
-    W, N, d = 16, 4, 3001
-    w = rng.standard_normal((W, d)).astype(np.float32)
-    g = rng.standard_normal((W, d)).astype(np.float32)
+    ft = np.float64 if dtype == "f64" else np.float32
+    w = rng.standard_normal((W, d)).astype(ft)
+    g = rng.standard_normal((W, d)).astype(ft)
     alphas = np.linspace(0.01, 0.05, 7)
     outs = []
     for batched in (False, True):
-        with engine_for("ds", W, N, 3, d, 0.01, "f32") as e:
+        with engine_for(kind, W, N, opt, d, 0.01, dtype, rect=(kind == "ds" and W != N * N)) as e:
             e.upload_all(BUF_PARAMS, w)
             e.upload_all(BUF_GRADS, g)
             if batched:
@@ -387,7 +395,7 @@ def test_batched_steps_equal_single_steps(cuda_device):
             else:
                 for t, a_t in enumerate(alphas):
                     e.step(t, float(a_t))
-            outs.append((e.download_all(BUF_PARAMS), e.step_count(5)))
+            outs.append((e.download_all(BUF_PARAMS), e.step_count(W - 1)))
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1] == len(alphas)
 
 
