@@ -1129,9 +1129,17 @@ RowGeom geom(dss_ctx* c, int buffer) {
 // Worlds small enough that one CTA beats one launch per iteration.
 long small_bytes(const dss_ctx* c) { return static_cast<long>(c->P) * c->d_pad * c->esz; }
 
+// One launch for the whole batch: always up to 32 KB per array (one CTA);
+// the resident grid up to DSS_PERSIST_MAX_BYTES only where its loops over
+// members / the BSP world stay short (measured: DS up to 16 workers, BSP
+// up to 4; beyond that one launch per iteration of the templated kernels
+// is faster).
 bool small_path(const dss_ctx* c, long n) {
-  return !multi(c) && c->cfg.path == 0 && c->s == 0 && n >= 2 && small_bytes(c) <= DSS_PERSIST_MAX_BYTES &&
-         c->P <= kMaxLocal;
+  if (multi(c) || c->cfg.path != 0 || c->s != 0 || n < 2 || c->P > kMaxLocal) return false;
+  const long bytes = small_bytes(c);
+  if (bytes <= 32768) return true;
+  const int max_workers = c->cfg.strategy.kind == DSS_BSP ? 4 : 16;
+  return bytes <= DSS_PERSIST_MAX_BYTES && c->P <= max_workers;
 }
 
 template <typename T, int OPT>

@@ -28,9 +28,11 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #endif
 // Single-GPU worlds of at most this many bytes per state array run a whole
 // dss_steps batch in one launch (a resident grid with a barrier between
-// iterations above 32 KB) instead of one launch per iteration.
+// iterations above 32 KB) instead of one launch per iteration.  Measured
+// against per-iteration launches: +40-100% for 4 workers at 16 KB-1 MB
+// total, +10-20% for 16 workers, a loss at 4 MB.
 #ifndef DSS_PERSIST_MAX_BYTES
-#define DSS_PERSIST_MAX_BYTES (4L << 20)
+#define DSS_PERSIST_MAX_BYTES (1L << 20)
 #endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
