@@ -372,6 +372,7 @@ def test_c2_full_size_rows_vs_oracle(cuda_device, oracle):
 
 @pytest.mark.parametrize("kind,W,N,d,opt,dtype", [
     ("ds", 16, 4, 3001, 3, "f32"),      # 192 KB per array: resident-grid multi-iteration kernel
+    ("ds", 4, 2, 50001, 1, "f32"),      # 800 KB: resident grid, momentum
     ("ds", 16, 4, 40001, 1, "f64"),     # 5 MB: one launch per iteration
     ("ds", 8, 2, 30001, 0, "f32"),      # rectangular C2 shape, 960 KB
     ("bsp", 8, 8, 20001, 2, "f32"),     # BSP fold + step, 640 KB
