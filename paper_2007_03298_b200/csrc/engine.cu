@@ -1151,7 +1151,13 @@ void launch_small_t(dss_ctx* c, SmallArgs<T>& a, int grid) {
     return;
   }
   // persistent grid with a barrier between iterations: cooperative launch
-  // guarantees every CTA is resident
+  // guarantees every CTA is resident (at most what fits the SMs)
+  static int occ = -1;
+  if (occ < 0) {
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, small_steps_kernel<T, OPT>, kThreads, 0), "occupancy");
+    occ = std::max(occ, 1);
+  }
+  grid = std::min(grid, occ * c->sms);
   void* args[] = {&a};
   ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(small_steps_kernel<T, OPT>), dim3(grid),
                                  dim3(kThreads), args, 0, c->stream),
