@@ -1138,7 +1138,7 @@ bool small_path(const dss_ctx* c, long n) {
   if (multi(c) || c->cfg.path != 0 || c->s != 0 || n < 2 || c->P > kMaxLocal) return false;
   const long bytes = small_bytes(c);
   if (bytes <= 32768) return true;
-  const int max_workers = c->cfg.strategy.kind == DSS_BSP ? 4 : 16;
+  const int max_workers = c->cfg.strategy.kind == DSS_BSP ? DSS_PERSIST_MAX_WORKERS_BSP : DSS_PERSIST_MAX_WORKERS_DS;
   return bytes <= DSS_PERSIST_MAX_BYTES && c->P <= max_workers;
 }
 

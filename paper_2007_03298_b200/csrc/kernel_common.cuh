@@ -34,6 +34,12 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_PERSIST_MAX_BYTES
 #define DSS_PERSIST_MAX_BYTES (1L << 20)
 #endif
+#ifndef DSS_PERSIST_MAX_WORKERS_DS
+#define DSS_PERSIST_MAX_WORKERS_DS 16
+#endif
+#ifndef DSS_PERSIST_MAX_WORKERS_BSP
+#define DSS_PERSIST_MAX_WORKERS_BSP 4
+#endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.
