@@ -686,45 +686,33 @@ __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T
         const int beg = offsets[grp];
         const int m = offsets[grp + 1] - beg;
         Pack<T> acc;
-        for (int j0 = 0; j0 < m; j0 += 4) {  // members in ascending order, loads of 4 in flight
-          Pack<T> xs[4], gs[4], s1[4], s2[4];
+        for (int j = 0; j < m; ++j) {
+          const int k = members[beg + j];
+          const long r = static_cast<long>(k) * a.ld + off;
+          Pack<T> x = ldv(a.w + r);
+          const Pack<T> gv = ldv(a.g + r);
+          Pack<T> s1, s2;
+          if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
+          const T b1 = static_cast<T>(a.bc1[static_cast<long>(i) * a.nw + k]);
+          const T b2 = static_cast<T>(a.bc2[static_cast<long>(i) * a.nw + k]);
+          bool ok = true;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (j0 + q < m) {
-              const long r = static_cast<long>(members[beg + j0 + q]) * a.ld + off;
-              xs[q] = ldv(a.w + r);
-              gs[q] = ldv(a.g + r);
-              if constexpr (OPT != kSgd) s1[q] = ldv(a.m1 + r);
-              if constexpr (OPT == kAdam || OPT == kAdamW) s2[q] = ldv(a.m2 + r);
-            }
+          for (int l = 0; l < VN; ++l) {
+            x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], c, b1, b2);
+            ok = ok && finite_(x.v[l]);
           }
+          if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
+          if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
+          if (!ok) {
+            const unsigned long long kk = err_key(t, 0, k);
+            bad = kk < bad ? kk : bad;
+          }
+          if (j == 0) {
+            acc = x;
+          } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int j = j0 + q;
-            if (j < m) {
-              const int k = members[beg + j];
-              const long r = static_cast<long>(k) * a.ld + off;
-              const T b1 = static_cast<T>(a.bc1[static_cast<long>(i) * a.nw + k]);
-              const T b2 = static_cast<T>(a.bc2[static_cast<long>(i) * a.nw + k]);
-              bool ok = true;
-#pragma unroll
-              for (int l = 0; l < VN; ++l) {
-                xs[q].v[l] = step_elem<T, OPT>(xs[q].v[l], gs[q].v[l], s1[q].v[l], s2[q].v[l], c, b1, b2);
-                ok = ok && finite_(xs[q].v[l]);
-              }
-              if constexpr (OPT != kSgd) stv(a.m1 + r, s1[q]);
-              if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2[q]);
-              if (!ok) {
-                const unsigned long long kk = err_key(t, 0, k);
-                bad = kk < bad ? kk : bad;
-              }
-              if (j == 0) {
-                acc = xs[q];
-              } else {
-#pragma unroll
-                for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], xs[q].v[l]);
-              }
-            }
+            for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
           }
         }
         if (m > 1) {
