@@ -1130,16 +1130,16 @@ RowGeom geom(dss_ctx* c, int buffer) {
 long small_bytes(const dss_ctx* c) { return static_cast<long>(c->P) * c->d_pad * c->esz; }
 
 // One launch for the whole batch: always up to 32 KB per array (one CTA);
-// the resident grid up to DSS_PERSIST_MAX_BYTES only where its loops over
-// members / the BSP world stay short (measured: DS up to 16 workers, BSP
-// up to 4; beyond that one launch per iteration of the templated kernels
-// is faster).
+// the resident grid where it beats one launch per iteration of the
+// templated kernels (measured sweep: up to 16 workers; DS up to 1 MB per
+// array, BSP up to 4 MB).
 bool small_path(const dss_ctx* c, long n) {
   if (multi(c) || c->cfg.path != 0 || c->s != 0 || n < 2 || c->P > kMaxLocal) return false;
   const long bytes = small_bytes(c);
   if (bytes <= 32768) return true;
-  const int max_workers = c->cfg.strategy.kind == DSS_BSP ? DSS_PERSIST_MAX_WORKERS_BSP : DSS_PERSIST_MAX_WORKERS_DS;
-  return bytes <= DSS_PERSIST_MAX_BYTES && c->P <= max_workers;
+  const bool bsp = c->cfg.strategy.kind == DSS_BSP;
+  const int max_workers = bsp ? DSS_PERSIST_MAX_WORKERS_BSP : DSS_PERSIST_MAX_WORKERS_DS;
+  return bytes <= (bsp ? DSS_PERSIST_MAX_BYTES_BSP : DSS_PERSIST_MAX_BYTES) && c->P <= max_workers;
 }
 
 template <typename T, int OPT>

@@ -34,11 +34,14 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_PERSIST_MAX_BYTES
 #define DSS_PERSIST_MAX_BYTES (1L << 20)
 #endif
+#ifndef DSS_PERSIST_MAX_BYTES_BSP
+#define DSS_PERSIST_MAX_BYTES_BSP (4L << 20)
+#endif
 #ifndef DSS_PERSIST_MAX_WORKERS_DS
 #define DSS_PERSIST_MAX_WORKERS_DS 16
 #endif
 #ifndef DSS_PERSIST_MAX_WORKERS_BSP
-#define DSS_PERSIST_MAX_WORKERS_BSP 4
+#define DSS_PERSIST_MAX_WORKERS_BSP 16
 #endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
