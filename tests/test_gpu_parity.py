@@ -230,6 +230,37 @@ def test_f32_bit_exact_vs_restatement(cuda_device, oracle, kind, W, N, rect, opt
                 assert np.array_equal(e.download_all(BUF_MOMENT2), m2)
 
 
+@pytest.mark.parametrize("kind,W,N", [("ds", 1, 1), ("bsp", 1, 1), ("ds", 4, 2), ("ds", 4, 4), ("bsp", 2, 2)])
+@pytest.mark.parametrize("d", [1, 3, 63, 64, 65, 257])
+def test_edge_shapes_vs_restatement(cuda_device, oracle, kind, W, N, d):
+    """Edge shapes: a single worker, a single full group, rows shorter than
+    one 16-B vector and around the 64-element padding; f32 AdamW with decay
+    (the most state) and SGD, batched and single steps, bit for bit."""
+    for opt in (0, 3):
+        rng = np.random.default_rng(d * 7 + W + opt)
+        wd = 0.01 if opt == 3 else 0.0
+        w = rng.standard_normal((W, d)).astype(np.float32)
+        m1, m2 = np.zeros_like(w), np.zeros_like(w)
+        steps = np.zeros(W, np.int64)
+        g = rng.standard_normal((W, d)).astype(np.float32)
+        alphas = [0.05, 0.02, 0.01]
+        with engine_for(kind, W, N, opt, d, wd, "f32") as e:
+            e.upload_all(BUF_PARAMS, w)
+            e.upload_all(BUF_GRADS, g)
+            e.steps(0, alphas, check=True)  # the one-launch batch
+            e.step(3, 0.01, check=True)     # and a single step
+            for t, alpha in enumerate(alphas + [0.01]):
+                if kind == "ds":
+                    rc = oracle.ds_step(W, N, t, opt, hparams(weight_decay=wd), alpha, steps, w, g.copy(), m1, m2)
+                else:
+                    rc = oracle.bsp_step(t, opt, hparams(weight_decay=wd), alpha, steps, w, g.copy(), m1, m2)
+                assert rc[0] == 0
+                steps += 1
+            assert np.array_equal(e.download_all(BUF_PARAMS), w), (kind, W, N, d, opt)
+            if opt:
+                assert np.array_equal(e.download_all(BUF_MOMENT2), m2)
+
+
 def test_f32_vs_f64_reference_tolerance(cuda_device, golden):
     """fp32 device params vs the fp64 reference on identical synthetic inputs.
     Tolerance (north star): max relative error <= 1e-6 with a magnitude floor
