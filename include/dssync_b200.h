@@ -217,7 +217,10 @@ int dss_step(dss_ctx* ctx, long t, double alpha, int check, dss_outcome* out);
 
 /* n consecutive iterations t0 .. t0+n-1 (alphas[i] for iteration t0+i) in
  * one call: the run_training loop body (sync.cpp:323-459, sync part) without
- * a host round trip per iteration. */
+ * a host round trip per iteration.  On one GPU, small worlds run the whole
+ * batch in one launch: one CTA up to 32 KB per array, a cooperative
+ * resident grid with a barrier between iterations up to 16 workers and
+ * 1 MB (DS) / 4 MB (BSP) per array.  Same bits as n dss_step calls. */
 int dss_steps(dss_ctx* ctx, long t0, long n, const double* alphas, int check, dss_outcome* last);
 
 /* One iteration fed from and returned to HOST memory, pipelined across
