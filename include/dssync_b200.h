@@ -309,6 +309,24 @@ int dss_logistic_setup(dss_ctx* ctx, const double* x, const double* y, int M, do
 int dss_logistic_gradients(dss_ctx* ctx, long t);
 /* n iterations of (dss_logistic_gradients(t), dss_step(t, alphas[i])). */
 int dss_logistic_steps(dss_ctx* ctx, long t0, long n, const double* alphas, int check, dss_outcome* last);
+/* ---- tiny MLP on the device (running statistics, acceptance.cpp:328-402) -- */
+/* TinyMlpProblem's data (problems.cpp:436-460) and initial_params
+ * (:466-476), host, bit-exact: x = M*d doubles, y = M targets; w = hidden*d
+ * + 2*hidden + 1 doubles ([W1 | b1 | w2 | b2]). */
+int dss_mlp_dataset(uint64_t seed, int d, int M, double* x, double* y);
+int dss_mlp_initial_params(uint64_t seed, int d, int hidden, double* w);
+/* Upload the MLP data and shard it as dss_logistic_setup does.  The context
+ * needs dim = hidden*d + 2*hidden + 1 and stats_dim = hidden. */
+int dss_mlp_setup(dss_ctx* ctx, const double* x, const double* y, int M, int d, int hidden, int batch_size,
+                  int sampling, uint64_t run_seed);
+/* Gradient rows (DSS_BUF_GRADS) and running-stat observations
+ * (DSS_BUF_STATS_OBS: the mean hidden pre-activations) of every local
+ * worker at iteration t (TinyMlpProblem::stochastic_gradient,
+ * problems.cpp:478-503, via checked_gradient).  Follow with
+ * dss_running_stats_update and dss_step, as run_training does. */
+int dss_mlp_gradients(dss_ctx* ctx, long t);
+/* TinyMlpProblem::full_loss (problems.cpp:516-526) of every local worker. */
+int dss_mlp_losses(dss_ctx* ctx, int exact, double* losses);
 /* Indices sampled by the last dss_logistic_gradients: [local_workers][batch]. */
 int dss_logistic_batch(dss_ctx* ctx, int* out);
 /* LogisticProblem::full_loss (problems.cpp:292-305) of every local worker:

@@ -184,7 +184,7 @@ class Reference:
         L.ref_make_shards.argtypes = [C.c_int, C.c_int, C.c_uint64, _P, _P] + E
         L.ref_epoch_order.argtypes = [_P, C.c_int, C.c_uint64, C.c_int, C.c_long, _P]
         L.ref_mlp_run.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double,
-                                                  _P, _P, _P, _P, _P, C.POINTER(C.c_int)] + E
+                                                  _P, _P, _P, _P, _P, _P, C.POINTER(C.c_int)] + E
         L.ref_bench_create.restype = _P
         L.ref_bench_create.argtypes = [C.c_int, C.c_long, C.c_int, _P, C.c_uint64]
         L.ref_bench_destroy.argtypes = [_P]
@@ -275,18 +275,23 @@ class Reference:
             return grads, params, bool(match.value), (tg, tl, ts, csv.value.decode())
         return grads, params, bool(match.value)
 
-    def mlp_run(self, kind, W, N, d_in, M, hidden, problem_seed, run_seed, batch, T, opt, hp, alpha):
+    def mlp_run(self, kind, W, N, d_in, M, hidden, problem_seed, run_seed, batch, T, opt, hp, alpha,
+                with_batches=False):
         dim = hidden * d_in + 2 * hidden + 1
         g = np.zeros((T, W, dim), _D)
         obs = np.zeros((T, W, hidden), _D)
         p = np.zeros((T, W, dim), _D)
         st = np.zeros((T, W, hidden), _D)
         w0 = np.zeros(dim, _D)
+        batches = np.zeros((T, W, batch), np.int32)
         match = C.c_int()
         rc = self.lib.ref_mlp_run(kind, W, N, d_in, M, hidden, problem_seed, run_seed, batch, T, opt, _ptr(hp), alpha,
-                                  _ptr(g), _ptr(obs), _ptr(p), _ptr(st), _ptr(w0), C.byref(match), *self._e())
+                                  _ptr(g), _ptr(obs), _ptr(p), _ptr(st), _ptr(w0), _ptr(batches), C.byref(match),
+                                  *self._e())
         if rc:
             raise RuntimeError(self.error())
+        if with_batches:
+            return g, obs, p, st, w0, batches, bool(match.value)
         return g, obs, p, st, w0, bool(match.value)
 
     def logistic_run(self, kind, W, N, d, M, l2, problem_seed, run_seed, batch, T, opt, hp, alpha0, factor, every,

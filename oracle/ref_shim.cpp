@@ -611,7 +611,8 @@ int ref_parse_config(const char* text, char* err, int errlen) {
 // and checked against run_training's final params and running_stats.
 int ref_mlp_run(int kind, int W, int N, int d_in, int M, int hidden, uint64_t problem_seed, uint64_t run_seed,
                 int batch, int T, int opt, const double* hp, double alpha, double* grads_out, double* obs_out,
-                double* params_out, double* stats_out, double* w0_out, int* matches, char* err, int errlen) {
+                double* params_out, double* stats_out, double* w0_out, int* batches_out, int* matches, char* err,
+                int errlen) {
   return guarded(err, errlen, nullptr, nullptr, [&] {
     DatasetSpec s;
     s.kind = "tiny-mlp";
@@ -649,6 +650,7 @@ int ref_mlp_run(int kind, int W, int N, int d_in, int M, int hidden, uint64_t pr
         Rng br = Rng::for_stream(run_seed, streams::kBatch, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
         std::vector<int> b(static_cast<size_t>(batch));
         for (auto& idx : b) idx = x.shard.indices[br.uniform_below(x.shard.indices.size())];
+        std::memcpy(batches_out + (static_cast<long>(t) * W + k) * batch, b.data(), sizeof(int) * static_cast<size_t>(batch));
         Rng noise = Rng::for_stream(run_seed, streams::kGradientNoise, static_cast<uint64_t>(k), static_cast<uint64_t>(t));
         smp[static_cast<size_t>(k)] = problem->stochastic_gradient(x.params, b, noise);
         std::memcpy(grads_out + (static_cast<long>(t) * W + k) * dim, smp[static_cast<size_t>(k)].grad.data(), sizeof(double) * static_cast<size_t>(dim));

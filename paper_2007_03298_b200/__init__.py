@@ -32,6 +32,8 @@ from .api import (  # noqa: F401
     is_square_mode,
     make_partition,
     make_shards,
+    mlp_dataset,
+    mlp_initial_params,
     quadratic_problem,
     round_outcome,
     sync_round,

@@ -89,6 +89,11 @@ SIGNATURES = {
     "dss_logistic_dataset": (C.c_int, [C.c_uint64, C.c_int, C.c_int, _P, _P]),
     "dss_quadratic_problem": (C.c_int, [C.c_uint64, C.c_int, C.c_double, _P, _P]),
     "dss_logistic_constants": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_double, _P, _P, _P]),
+    "dss_mlp_dataset": (C.c_int, [C.c_uint64, C.c_int, C.c_int, _P, _P]),
+    "dss_mlp_initial_params": (C.c_int, [C.c_uint64, C.c_int, C.c_int, _P]),
+    "dss_mlp_setup": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64]),
+    "dss_mlp_gradients": (C.c_int, [_P, C.c_long]),
+    "dss_mlp_losses": (C.c_int, [_P, C.c_int, _P]),
     "dss_make_shards": (C.c_int, [C.c_int, C.c_int, C.c_uint64, _P, _P]),
     "dss_epoch_order": (C.c_int, [_P, C.c_int, C.c_uint64, C.c_int, C.c_long, _P]),
     "dss_logistic_setup": (C.c_int, [_P, _P, _P, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64]),

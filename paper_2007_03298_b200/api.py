@@ -304,6 +304,21 @@ def logistic_constants(x, y, l2: float):
     return sm.value, fs.value, (w if l2 > 0.0 else None)
 
 
+def mlp_dataset(seed: int, d: int, M: int):
+    """TinyMlpProblem's data (problems.cpp:436-460), bit-exact: (x [M, d], y [M])."""
+    x = np.empty((M, d), dtype=np.float64)
+    y = np.empty(M, dtype=np.float64)
+    _check_global(L.load().dss_mlp_dataset(C.c_uint64(seed), d, M, x.ctypes.data, y.ctypes.data))
+    return x, y
+
+
+def mlp_initial_params(seed: int, d: int, hidden: int) -> np.ndarray:
+    """TinyMlpProblem::initial_params (problems.cpp:466-476), bit-exact."""
+    w = np.empty(hidden * d + 2 * hidden + 1, dtype=np.float64)
+    _check_global(L.load().dss_mlp_initial_params(C.c_uint64(seed), d, hidden, w.ctypes.data))
+    return w
+
+
 def make_shards(dataset_size: int, workers: int, seed: int) -> List[Shard]:  # problems.cpp:642-662
     idx = np.empty(max(dataset_size, 0), dtype=np.int32)
     off = np.empty(max(workers, 0) + 1, dtype=np.int32)
@@ -523,6 +538,26 @@ class DsSyncEngine:
         o = L.dss_outcome()
         self._ck(self.lib.dss_logistic_steps(self.h, t0, a.size, a.ctypes.data, 1 if check else 0, C.byref(o)))
         return SyncRoundOutcome(o.critical_path_steps, o.total_messages)
+
+    # -- tiny MLP on the device (running statistics) --
+    def mlp_setup(self, x, y, hidden: int, batch_size: int, sampling: int = SamplingMode.REPLACEMENT,
+                  run_seed: int = 1) -> None:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        if x.ndim != 2 or y.shape != (x.shape[0],):
+            raise ValueError("tiny-mlp: x must be [M, d] and y [M]")
+        self._ck(self.lib.dss_mlp_setup(self.h, x.ctypes.data, y.ctypes.data, x.shape[0], x.shape[1], hidden,
+                                        batch_size, int(sampling), C.c_uint64(run_seed)))
+        self._logistic_batch = batch_size
+
+    def mlp_gradients(self, t: int) -> None:
+        """Gradient rows and running-stat observations of every local worker."""
+        self._ck(self.lib.dss_mlp_gradients(self.h, t))
+
+    def mlp_losses(self, exact: bool = False) -> np.ndarray:
+        out = np.empty(self.local_workers, dtype=np.float64)
+        self._ck(self.lib.dss_mlp_losses(self.h, 1 if exact else 0, out.ctypes.data))
+        return out
 
     def logistic_batch(self) -> np.ndarray:
         out = np.empty((self.local_workers, self._logistic_batch), dtype=np.int32)

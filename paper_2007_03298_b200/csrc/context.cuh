@@ -205,10 +205,12 @@ struct dss_ctx {
     int* batch = nullptr;      // [P][B]
     long max_shard = 0;
     int M = 0, B = 0, sampling = 0;
+    int d_feat = 0;            // features per example (logistic: dim)
+    int hidden = 0;            // tiny MLP hidden units (0: logistic)
     double l2 = 0.0;
     uint64_t seed = 0;
     std::vector<void*> mem;
-  } logi;
+  } logi;                      // the dataset problem (logistic or tiny MLP)
   dssb::GroupLaunch apply_launch;  // singleton groups of every local worker
 
   // tiny-problem multi-iteration path (dss_steps)

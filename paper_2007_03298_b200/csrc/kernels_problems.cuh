@@ -43,9 +43,11 @@ struct DevRng {  // Rng::next_u64 / uniform_below (rng.cpp:28-43)
 constexpr uint64_t kBatchStream = 0xd6e8feb86659fd93ULL;       // rng.hpp:45
 constexpr uint64_t kEpochOrderStream = 0xe7037ed1a0b428dbULL;  // rng.hpp:47
 
+// A dataset problem on the device: logistic regression (hidden = 0) or
+// the tiny MLP (hidden units, running-stat observations into obs).
 struct LogisticArgs {
-  const double* x;        // [M][d] row-major
-  const double* y;        // [M] labels in {-1, +1}
+  const double* x;        // [M][d] row-major (d = features)
+  const double* y;        // [M] labels in {-1, +1} (logistic) / targets (MLP)
   const int* shard;       // local workers' shards, concatenated
   const int* shard_off;   // [P + 1]
   int* order;             // [P][max_shard] cached epoch order (epoch sampling)
@@ -59,6 +61,8 @@ struct LogisticArgs {
   long t;
   int first_rank;
   unsigned long long* gerr;  // gradient failure latch: t << 32 | rank
+  int hidden;             // MLP hidden units (0: logistic)
+  long obs_ld;            // MLP: row stride of the running-stat observation rows
 };
 
 __device__ __forceinline__ double softplus_dev(double z) {  // problems.cpp:338-341
@@ -398,6 +402,138 @@ __global__ void __launch_bounds__(kThreads) logistic_loss_kernel(const T* w, lon
     acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(0.5, l2), dd));
   }
   out[blockIdx.x] = acc;
+}
+
+// TinyMlpProblem::stochastic_gradient (problems.cpp:478-503) of local
+// worker blockIdx.x: one hidden tanh layer, scalar output, squared loss.
+// Params [W1 (h x d) | b1 (h) | w2 (h) | b2]; the observation is the mean
+// hidden pre-activation (the running-stats input, sync.cpp:193-201).  As
+// for the logistic kernel, every example's forward pass is computed first
+// (thread per (example, unit): z summed in the reference's feature order,
+// then thread per example: the output summed in unit order), then every
+// gradient element's sum over the examples is taken in example order --
+// the reference's additions in the reference's order.  Dynamic shared
+// memory: w as doubles [dim], z / tanh(z) / dz [B][h], err [B].
+template <typename T>
+__global__ void __launch_bounds__(128) mlp_grad_kernel(const LogisticArgs a, const T* __restrict__ w,
+                                                       T* __restrict__ g, T* __restrict__ obs) {
+  extern __shared__ double sh[];
+  const int k = blockIdx.x;
+  const int d = a.d, h = a.hidden, B = a.B;
+  const long dim = static_cast<long>(h) * d + 2 * h + 1;
+  double* wd = sh;
+  double* zs = wd + dim;
+  double* as = zs + static_cast<long>(B) * h;
+  double* dz = as + static_cast<long>(B) * h;
+  double* er = dz + static_cast<long>(B) * h;
+  const T* wr = w + static_cast<long>(k) * a.ld;
+  sample_batch_par(a, k, threadIdx.x, blockDim.x, [] { __syncthreads(); },
+                   [](bool p) { return __syncthreads_or(p) != 0; });
+  for (long e = threadIdx.x; e < dim; e += blockDim.x) wd[e] = static_cast<double>(wr[e]);
+  __syncthreads();
+  const int* bt = a.batch + static_cast<long>(k) * B;
+  const long hd = static_cast<long>(h) * d;
+  // forward, hidden layer: z_i = b1_i + sum_j W1_ij x_j (problems.cpp:550-556)
+  for (long u = threadIdx.x; u < static_cast<long>(B) * h; u += blockDim.x) {
+    const int b = static_cast<int>(u / h), i = static_cast<int>(u % h);
+    const double* x = a.x + static_cast<long>(bt[b]) * d;
+    double z = wd[hd + i];
+    for (int j = 0; j < d; ++j) z = __dadd_rn(z, __dmul_rn(wd[static_cast<long>(i) * d + j], x[j]));
+    zs[u] = z;
+    as[u] = tanh(z);
+  }
+  __syncthreads();
+  // output and error: out = b2 + sum_i w2_i a_i; err = out - y
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    double out = wd[hd + 2 * h];
+    for (int i = 0; i < h; ++i) out = __dadd_rn(out, __dmul_rn(wd[hd + h + i], as[static_cast<long>(b) * h + i]));
+    er[b] = __dsub_rn(out, a.y[bt[b]]);
+  }
+  __syncthreads();
+  // dz = err * w2_i * (1 - a_i^2)
+  for (long u = threadIdx.x; u < static_cast<long>(B) * h; u += blockDim.x) {
+    const int b = static_cast<int>(u / h), i = static_cast<int>(u % h);
+    dz[u] = __dmul_rn(__dmul_rn(er[b], wd[hd + h + i]), __dsub_rn(1.0, __dmul_rn(as[u], as[u])));
+  }
+  __syncthreads();
+  const double inv = __ddiv_rn(1.0, static_cast<double>(B));
+  bool bad = false;
+  T* gr = g + static_cast<long>(k) * a.ld;
+  for (long e = threadIdx.x; e < dim; e += blockDim.x) {
+    double acc = 0.0;
+    if (e < hd) {  // W1_ij += dz_i x_j
+      const int i = static_cast<int>(e / d), j = static_cast<int>(e % d);
+      for (int b = 0; b < B; ++b) {
+        acc = __dadd_rn(acc, __dmul_rn(dz[static_cast<long>(b) * h + i], a.x[static_cast<long>(bt[b]) * d + j]));
+      }
+    } else if (e < hd + h) {  // b1_i += dz_i
+      const int i = static_cast<int>(e - hd);
+      for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, dz[static_cast<long>(b) * h + i]);
+    } else if (e < hd + 2 * h) {  // w2_i += err a_i
+      const int i = static_cast<int>(e - hd - h);
+      for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, __dmul_rn(er[b], as[static_cast<long>(b) * h + i]));
+    } else {  // b2 += err
+      for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, er[b]);
+    }
+    const double v = __dmul_rn(acc, inv);
+    bad = bad || !isfinite(v);
+    gr[e] = static_cast<T>(v);
+  }
+  for (long e = dim + threadIdx.x; e < a.ld; e += blockDim.x) gr[e] = T(0);
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {  // observation: mean pre-activation
+    double acc = 0.0;
+    for (int b = 0; b < B; ++b) acc = __dadd_rn(acc, zs[static_cast<long>(b) * h + i]);
+    obs[static_cast<long>(k) * a.obs_ld + i] = static_cast<T>(__dmul_rn(acc, inv));
+  }
+  if (threadIdx.x == 0) {  // the batch loss, for checked_gradient (sync.cpp:186)
+    double loss = 0.0;
+    for (int b = 0; b < B; ++b) loss = __dadd_rn(loss, __dmul_rn(__dmul_rn(0.5, er[b]), er[b]));
+    bad = bad || !isfinite(__dmul_rn(loss, inv));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.first_rank + k));
+  }
+}
+
+// TinyMlpProblem::full_loss (problems.cpp:516-526) of local row blockIdx.x:
+// mean 0.5 * err^2 over the dataset.  exact = 1: one thread in the
+// reference's order; exact = 0: a parallel reduction over the examples.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) mlp_loss_kernel(const T* w, long ld, const double* x, const double* y,
+                                                            int d, int h, int M, int exact, double* out) {
+  __shared__ double part[kThreads / 32];
+  const T* wr = w + static_cast<long>(blockIdx.x) * ld;
+  const long hd = static_cast<long>(h) * d;
+  auto err_of = [&](int m) {
+    const double* xi = x + static_cast<long>(m) * d;
+    double o = static_cast<double>(wr[hd + 2 * h]);
+    for (int i = 0; i < h; ++i) {
+      double z = static_cast<double>(wr[hd + i]);
+      for (int j = 0; j < d; ++j) z = __dadd_rn(z, __dmul_rn(static_cast<double>(wr[static_cast<long>(i) * d + j]), xi[j]));
+      o = __dadd_rn(o, __dmul_rn(static_cast<double>(wr[hd + h + i]), tanh(z)));
+    }
+    return __dsub_rn(o, y[m]);
+  };
+  double acc = 0.0;
+  if (exact) {
+    if (threadIdx.x != 0) return;
+    for (int m = 0; m < M; ++m) {
+      const double e = err_of(m);
+      acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(0.5, e), e));
+    }
+  } else {
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+      const double e = err_of(m);
+      acc += 0.5 * e * e;
+    }
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    acc = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) acc += part[i];
+  }
+  out[blockIdx.x] = __ddiv_rn(acc, static_cast<double>(M));
 }
 
 }  // namespace dssb

@@ -255,6 +255,40 @@ LogisticConstants logistic_constants(const double* x, const double* y, int M, in
   throw std::runtime_error("logistic optimum solve did not reach tolerance 1e-12");
 }
 
+void mlp_dataset(uint64_t seed, int d, int M, std::vector<double>& x, std::vector<double>& y) {
+  if (d < 1) throw std::invalid_argument("problem.d must be >= 1 (got " + std::to_string(d) + ")");
+  if (M < 1) throw std::invalid_argument("tiny-mlp requires problem.M >= 1");
+  const size_t n = static_cast<size_t>(d);
+  HostRng rng = HostRng::for_stream(seed, kStreamDataGen, 0, 0);
+  std::vector<double> teacher = seeded_unit_vector(n, rng);
+  for (double& v : teacher) v *= 2.0;
+  x.assign(static_cast<size_t>(M) * n, 0.0);
+  y.assign(static_cast<size_t>(M), 0.0);
+  for (int i = 0; i < M; ++i) {
+    double z = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+      const double v = rng.gaussian();
+      x[static_cast<size_t>(i) * n + j] = v;
+      z += v * teacher[j];
+    }
+    y[static_cast<size_t>(i)] = std::sin(z);
+  }
+}
+
+void mlp_initial_params(uint64_t seed, int d_in, int hidden, std::vector<double>& w) {
+  if (hidden < 1 || hidden > 32) {
+    throw std::invalid_argument("problem.hidden must be in [1, 32] (got " + std::to_string(hidden) + ")");
+  }
+  const size_t d = static_cast<size_t>(d_in);
+  const size_t h = static_cast<size_t>(hidden);
+  HostRng rng = HostRng::for_stream(seed, kStreamInitParams, 0, 0);
+  w.assign(h * d + 2 * h + 1, 0.0);
+  const double s1 = 1.0 / std::sqrt(static_cast<double>(d));
+  for (size_t i = 0; i < h * d; ++i) w[i] = s1 * rng.gaussian();
+  const double s2 = 1.0 / std::sqrt(static_cast<double>(h));
+  for (size_t i = 0; i < h; ++i) w[h * d + h + i] = s2 * rng.gaussian();
+}
+
 void make_shards(int dataset_size, int workers, uint64_t seed, std::vector<int>& indices,
                  std::vector<int>& offsets) {
   if (workers < 1) throw std::invalid_argument("make_shards: workers must be >= 1");

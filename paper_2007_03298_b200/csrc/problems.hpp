@@ -10,6 +10,7 @@
 //   quadratic w*, w0   /root/reference/proj/src/problems.cpp:157-165
 //   logistic dataset   /root/reference/proj/src/problems.cpp:230-250
 //   logistic L, f*     /root/reference/proj/src/problems.cpp:18-82,292-416
+//   tiny-MLP data, w0  /root/reference/proj/src/problems.cpp:436-476
 //   make_shards        /root/reference/proj/src/problems.cpp:642-662
 //   epoch_order        /root/reference/proj/src/problems.cpp:664-674
 #pragma once
@@ -43,6 +44,13 @@ class HostRng {
 // Synthetic logistic data (problems.cpp:230-250): x is M x d row-major,
 // y in {-1, +1}.
 void logistic_dataset(uint64_t seed, int d, int M, std::vector<double>& x, std::vector<double>& y);
+
+// TinyMlpProblem's data and start (problems.cpp:436-476): x is M x d
+// gaussians, y = sin(x . teacher) with teacher = 2 * a seeded unit vector;
+// params [W1 (hidden x d) | b1 | w2 | b2] with W1, w2 seeded gaussians
+// scaled by 1/sqrt(d), 1/sqrt(hidden) and zero biases.
+void mlp_dataset(uint64_t seed, int d, int M, std::vector<double>& x, std::vector<double>& y);
+void mlp_initial_params(uint64_t seed, int d, int hidden, std::vector<double>& w);
 
 // LogisticProblem::finish_setup (problems.cpp:346-416): the smoothness
 // bound (power iteration on X^T X / 4M, + l2) and, for l2 > 0, the optimum

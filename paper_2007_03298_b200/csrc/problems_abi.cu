@@ -215,62 +215,105 @@ constexpr long kLogisticMaxSmem = 200 * 1024;
 
 }  // namespace dssb
 
+namespace {
+
+size_t mlp_smem(long dim, int batch, int hidden) {
+  return sizeof(double) * static_cast<size_t>(dim + 3L * batch * hidden + batch);
+}
+
+// Upload a dataset problem (x: M x d_feat, y: M) and shard it over the world
+// (make_shards(M, W, run_seed), sync.cpp:300); this GPU keeps its workers'
+// shards, the epoch-order cache and the batch rows.
+void dataset_setup(dss_ctx* c, const double* x, const double* y, int M, int d_feat, int hidden, double l2,
+                   int batch_size, int sampling, uint64_t run_seed) {
+  if (batch_size < 1) throw std::invalid_argument("batch_size must be >= 1");
+  if (sampling != DSS_SAMPLING_REPLACEMENT && sampling != DSS_SAMPLING_EPOCH) {
+    throw std::invalid_argument("sampling must be replacement or epoch");
+  }
+  ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+  ck(cudaStreamSynchronize(c->stream), "stream sync");
+  free_logistic(c);
+  std::vector<int> idx, off;
+  make_shards(M, c->cfg.strategy.world_size, run_seed, idx, off);
+  std::vector<int> local_off(static_cast<size_t>(c->P) + 1, 0);
+  long max_shard = 0;
+  for (int k = 0; k < c->P; ++k) {
+    const int n = off[static_cast<size_t>(c->first + k) + 1] - off[static_cast<size_t>(c->first + k)];
+    local_off[static_cast<size_t>(k) + 1] = local_off[static_cast<size_t>(k)] + n;
+    max_shard = std::max<long>(max_shard, n);
+  }
+  auto& L = c->logi;
+  const size_t xn = static_cast<size_t>(M) * d_feat;
+  L.x = logi_alloc<double>(c, xn);
+  L.y = logi_alloc<double>(c, static_cast<size_t>(M));
+  L.shard = logi_alloc<int>(c, static_cast<size_t>(local_off.back()));
+  L.shard_off = logi_alloc<int>(c, local_off.size());
+  L.order = logi_alloc<int>(c, static_cast<size_t>(c->P) * max_shard);
+  L.order_epoch = logi_alloc<long>(c, static_cast<size_t>(c->P));
+  L.batch = logi_alloc<int>(c, static_cast<size_t>(c->P) * batch_size);
+  ck(cudaMemcpy(L.x, x, sizeof(double) * xn, cudaMemcpyHostToDevice), "dataset x upload");
+  ck(cudaMemcpy(L.y, y, sizeof(double) * M, cudaMemcpyHostToDevice), "dataset y upload");
+  ck(cudaMemcpy(L.shard, idx.data() + off[static_cast<size_t>(c->first)], sizeof(int) * local_off.back(),
+                cudaMemcpyHostToDevice), "shard upload");
+  ck(cudaMemcpy(L.shard_off, local_off.data(), sizeof(int) * local_off.size(), cudaMemcpyHostToDevice),
+     "shard upload");
+  ck(cudaMemset(L.order_epoch, 0xff, sizeof(long) * c->P), "epoch init");  // -1
+  ck(cudaMemset(L.batch, 0, sizeof(int) * c->P * batch_size), "batch init");
+  L.max_shard = max_shard;
+  L.M = M;
+  L.B = batch_size;
+  L.sampling = sampling;
+  L.d_feat = d_feat;
+  L.hidden = hidden;
+  L.l2 = l2;
+  L.seed = run_seed;
+  L.ready = true;
+}
+
+template <typename K>
+void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+       "smem attr");
+  }
+}
+
+}  // namespace
+
 extern "C" int dss_logistic_setup(dss_ctx* c, const double* x, const double* y, int M, double l2, int batch_size,
                                   int sampling, uint64_t run_seed) {
   if (!c || !x || !y) return fail(c, DSS_EINVAL, "null argument");
   return guard(c, [&]() -> int {
     if (M < 1) throw std::invalid_argument("logistic requires problem.M >= 1");
     if (!(l2 >= 0.0)) throw std::invalid_argument("problem.mu must be >= 0");
-    if (batch_size < 1) throw std::invalid_argument("batch_size must be >= 1");
-    if (sampling != DSS_SAMPLING_REPLACEMENT && sampling != DSS_SAMPLING_EPOCH) {
-      throw std::invalid_argument("sampling must be replacement or epoch");
-    }
-    if (static_cast<long>(logistic_smem(c->d, batch_size)) > kLogisticMaxSmem) {
+    if (batch_size >= 1 && static_cast<long>(logistic_smem(c->d, batch_size)) > kLogisticMaxSmem) {
       throw std::invalid_argument("logistic on the device supports (dim + batch_size) * 8 B <= 200 KiB");
     }
-    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
-    ck(cudaStreamSynchronize(c->stream), "stream sync");
-    free_logistic(c);
-    // make_shards over the whole world (sync.cpp:300); keep this GPU's rows
-    std::vector<int> idx, off;
-    make_shards(M, c->cfg.strategy.world_size, run_seed, idx, off);
-    std::vector<int> local_off(static_cast<size_t>(c->P) + 1, 0);
-    long max_shard = 0;
-    for (int k = 0; k < c->P; ++k) {
-      const int n = off[static_cast<size_t>(c->first + k) + 1] - off[static_cast<size_t>(c->first + k)];
-      local_off[static_cast<size_t>(k) + 1] = local_off[static_cast<size_t>(k)] + n;
-      max_shard = std::max<long>(max_shard, n);
+    dataset_setup(c, x, y, M, static_cast<int>(c->d), 0, l2, batch_size, sampling, run_seed);
+    allow_smem(logistic_grad_kernel<double>, logistic_smem(c->d, batch_size));
+    allow_smem(logistic_grad_kernel<float>, logistic_smem(c->d, batch_size));
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_mlp_setup(dss_ctx* c, const double* x, const double* y, int M, int d_in, int hidden,
+                             int batch_size, int sampling, uint64_t run_seed) {
+  if (!c || !x || !y) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (M < 1) throw std::invalid_argument("tiny-mlp requires problem.M >= 1");
+    if (d_in < 1) throw std::invalid_argument("problem.d must be >= 1 (got " + std::to_string(d_in) + ")");
+    if (hidden < 1 || hidden > 32) {
+      throw std::invalid_argument("problem.hidden must be in [1, 32] (got " + std::to_string(hidden) + ")");
     }
-    auto& L = c->logi;
-    const size_t xn = static_cast<size_t>(M) * c->d;
-    L.x = logi_alloc<double>(c, xn);
-    L.y = logi_alloc<double>(c, static_cast<size_t>(M));
-    L.shard = logi_alloc<int>(c, static_cast<size_t>(local_off.back()));
-    L.shard_off = logi_alloc<int>(c, local_off.size());
-    L.order = logi_alloc<int>(c, static_cast<size_t>(c->P) * max_shard);
-    L.order_epoch = logi_alloc<long>(c, static_cast<size_t>(c->P));
-    L.batch = logi_alloc<int>(c, static_cast<size_t>(c->P) * batch_size);
-    ck(cudaMemcpy(L.x, x, sizeof(double) * xn, cudaMemcpyHostToDevice), "logistic x upload");
-    ck(cudaMemcpy(L.y, y, sizeof(double) * M, cudaMemcpyHostToDevice), "logistic y upload");
-    ck(cudaMemcpy(L.shard, idx.data() + off[static_cast<size_t>(c->first)], sizeof(int) * local_off.back(),
-                  cudaMemcpyHostToDevice), "shard upload");
-    ck(cudaMemcpy(L.shard_off, local_off.data(), sizeof(int) * local_off.size(), cudaMemcpyHostToDevice),
-       "shard upload");
-    ck(cudaMemset(L.order_epoch, 0xff, sizeof(long) * c->P), "epoch init");  // -1
-    ck(cudaMemset(L.batch, 0, sizeof(int) * c->P * batch_size), "batch init");
-    if (logistic_smem(c->d, batch_size) > 48 * 1024) {
-      ck(cudaFuncSetAttribute(logistic_grad_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(logistic_smem(c->d, batch_size))), "smem attr");
-      ck(cudaFuncSetAttribute(logistic_grad_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(logistic_smem(c->d, batch_size))), "smem attr");
+    const long dim = static_cast<long>(hidden) * d_in + 2 * hidden + 1;
+    if (c->d != dim) throw std::invalid_argument("tiny-mlp: the context dim must be hidden * d + 2 * hidden + 1");
+    if (c->s != hidden) throw std::invalid_argument("tiny-mlp: the context stats_dim must equal hidden");
+    if (batch_size >= 1 && static_cast<long>(mlp_smem(dim, batch_size, hidden)) > kLogisticMaxSmem) {
+      throw std::invalid_argument("tiny-mlp on the device supports (dim + 3 * batch * hidden + batch) * 8 B <= 200 KiB");
     }
-    L.max_shard = max_shard;
-    L.M = M;
-    L.B = batch_size;
-    L.sampling = sampling;
-    L.l2 = l2;
-    L.seed = run_seed;
-    L.ready = true;
+    dataset_setup(c, x, y, M, d_in, hidden, 0.0, batch_size, sampling, run_seed);
+    allow_smem(mlp_grad_kernel<double>, mlp_smem(dim, batch_size, hidden));
+    allow_smem(mlp_grad_kernel<float>, mlp_smem(dim, batch_size, hidden));
     return DSS_OK;
   });
 }
@@ -289,7 +332,9 @@ LogisticArgs logistic_args(dss_ctx* c, long t) {
   a.batch = L.batch;
   a.max_shard = L.max_shard;
   a.ld = c->d_pad;
-  a.d = static_cast<int>(c->d);
+  a.d = L.d_feat;
+  a.hidden = L.hidden;
+  a.obs_ld = c->s_pad;
   a.B = L.B;
   a.sampling = L.sampling;
   a.l2 = L.l2;
@@ -318,7 +363,7 @@ void launch_logistic(dss_ctx* c, long t) {
 extern "C" int dss_logistic_gradients(dss_ctx* c, long t) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
   return guard(c, [&]() -> int {
-    if (!c->logi.ready) throw std::invalid_argument("dss_logistic_setup has not been called");
+    if (!c->logi.ready || c->logi.hidden) throw std::invalid_argument("dss_logistic_setup has not been called");
     if (t < 0) throw std::invalid_argument("iteration must be >= 0");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
@@ -329,7 +374,7 @@ extern "C" int dss_logistic_gradients(dss_ctx* c, long t) {
 
 extern "C" int dss_logistic_steps(dss_ctx* c, long t0, long n, const double* alphas, int check, dss_outcome* last) {
   if (!c || (!alphas && n > 0)) return fail(c, DSS_EINVAL, "null argument");
-  if (small_path(c, n) && small_bytes(c) <= 32768 && c->logi.ready && c->d <= kSmallLogiMaxDim &&
+  if (small_path(c, n) && small_bytes(c) <= 32768 && c->logi.ready && !c->logi.hidden && c->d <= kSmallLogiMaxDim &&
       c->logi.B <= kSmallLogiMaxBatch) {
     // the whole run in one CTA: sampling, gradient, step and group fold
     const int st = guard(c, [&]() -> int {
@@ -361,6 +406,73 @@ extern "C" int dss_logistic_steps(dss_ctx* c, long t0, long n, const double* alp
   return DSS_OK;
 }
 
+extern "C" int dss_mlp_gradients(dss_ctx* c, long t) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    if (!c->logi.ready || !c->logi.hidden) throw std::invalid_argument("dss_mlp_setup has not been called");
+    if (t < 0) throw std::invalid_argument("iteration must be >= 0");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    const LogisticArgs a = logistic_args(c, t);
+    const size_t smem = mlp_smem(c->d, c->logi.B, c->logi.hidden);
+    TimedLaunch tl(c, DSS_KIND_GRADIENT);
+    if (c->cfg.dtype == DSS_F64) {
+      mlp_grad_kernel<double><<<c->P, 128, smem, c->stream>>>(a, static_cast<const double*>(c->w),
+                                                              static_cast<double*>(c->g),
+                                                              static_cast<double*>(c->stats_obs));
+    } else {
+      mlp_grad_kernel<float><<<c->P, 128, smem, c->stream>>>(a, static_cast<const float*>(c->w),
+                                                             static_cast<float*>(c->g),
+                                                             static_cast<float*>(c->stats_obs));
+    }
+    ck(cudaGetLastError(), "mlp_grad_kernel launch");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_mlp_losses(dss_ctx* c, int exact, double* losses) {
+  if (!c || !losses) return fail(c, DSS_EINVAL, "null argument");
+  return guard(c, [&]() -> int {
+    if (!c->logi.ready || !c->logi.hidden) throw std::invalid_argument("dss_mlp_setup has not been called");
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    quiesce(c);
+    if (!c->d_loss) c->d_loss = static_cast<double*>(dalloc(c, sizeof(double) * (c->P + 1)));
+    const auto& L = c->logi;
+    if (c->cfg.dtype == DSS_F64) {
+      mlp_loss_kernel<double><<<c->P, kThreads, 0, c->stream>>>(static_cast<const double*>(c->w), c->d_pad, L.x, L.y,
+                                                               L.d_feat, L.hidden, L.M, exact, c->d_loss);
+    } else {
+      mlp_loss_kernel<float><<<c->P, kThreads, 0, c->stream>>>(static_cast<const float*>(c->w), c->d_pad, L.x, L.y,
+                                                              L.d_feat, L.hidden, L.M, exact, c->d_loss);
+    }
+    ck(cudaGetLastError(), "mlp_loss_kernel launch");
+    ck(cudaMemcpyAsync(losses, c->d_loss, sizeof(double) * c->P, cudaMemcpyDeviceToHost, c->stream), "loss readback");
+    ck(cudaStreamSynchronize(c->stream), "loss sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_mlp_dataset(uint64_t seed, int d, int M, double* x, double* y) {
+  if (!x || !y) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    std::vector<double> hx, hy;
+    mlp_dataset(seed, d, M, hx, hy);
+    std::memcpy(x, hx.data(), sizeof(double) * hx.size());
+    std::memcpy(y, hy.data(), sizeof(double) * hy.size());
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_mlp_initial_params(uint64_t seed, int d, int hidden, double* w) {
+  if (!w) return fail(nullptr, DSS_EINVAL, "null argument");
+  return guard(nullptr, [&]() -> int {
+    std::vector<double> hw;
+    mlp_initial_params(seed, d, hidden, hw);
+    std::memcpy(w, hw.data(), sizeof(double) * hw.size());
+    return DSS_OK;
+  });
+}
+
 extern "C" int dss_logistic_batch(dss_ctx* c, int* out) {
   if (!c || !out) return fail(c, DSS_EINVAL, "null argument");
   return guard(c, [&]() -> int {
@@ -376,7 +488,7 @@ extern "C" int dss_logistic_batch(dss_ctx* c, int* out) {
 extern "C" int dss_logistic_losses(dss_ctx* c, int exact, double* losses) {
   if (!c || !losses) return fail(c, DSS_EINVAL, "null argument");
   return guard(c, [&]() -> int {
-    if (!c->logi.ready) throw std::invalid_argument("dss_logistic_setup has not been called");
+    if (!c->logi.ready || c->logi.hidden) throw std::invalid_argument("dss_logistic_setup has not been called");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
     if (!c->d_loss) c->d_loss = static_cast<double*>(dalloc(c, sizeof(double) * (c->P + 1)));

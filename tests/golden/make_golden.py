@@ -169,12 +169,14 @@ def mlp_stats(R: Reference) -> tuple[dict, dict]:
     arrs, meta = {}, []
     hp = R.hp_array()
     for kind, N in (("ds", 2), ("bsp", 4)):
-        g, obs, p, st, w0, match = R.mlp_run(1 if kind == "ds" else 0, 4, N, 4, 24, 6, 71, 5, 2, 8, 2, hp, 0.01)
+        g, obs, p, st, w0, bt, match = R.mlp_run(1 if kind == "ds" else 0, 4, N, 4, 24, 6, 71, 5, 2, 8, 2, hp, 0.01,
+                                                 with_batches=True)
         assert match, "mlp replay != run_training"
-        for name, arr in (("grads", g), ("obs", obs), ("params", p), ("stats", st)):
+        for name, arr in (("grads", g), ("obs", obs), ("params", p), ("stats", st), ("batches", bt)):
             arrs[f"mlp_{kind}_{name}"] = arr
         meta.append({"kind": kind, "W": 4, "N": N, "dim": g.shape[2], "stats_dim": obs.shape[2], "T": g.shape[0],
-                     "opt": "adam", "alpha": 0.01, "init": "tiny-mlp initial_params (seed 71)"})
+                     "opt": "adam", "alpha": 0.01, "init": "tiny-mlp initial_params (seed 71)",
+                     "problem": {"d": 4, "M": 24, "hidden": 6, "seed": 71}, "run_seed": 5, "batch": 2})
         arrs[f"mlp_{kind}_w0"] = w0
     return {"mlp": meta}, arrs
 

@@ -46,3 +46,12 @@ def test_setup_errors_match_reference():
         make_shards(3, 0, 1)
     with pytest.raises(ValueError, match="problem.M >= 1"):
         logistic_dataset(1, 3, 0)
+
+
+def test_mlp_initial_params_match_reference(golden):
+    """TinyMlpProblem::initial_params (problems.cpp:466-476), bit for bit."""
+    from paper_2007_03298_b200 import mlp_initial_params
+    meta, a = golden
+    for m in meta["mlp"]:
+        p = m["problem"]
+        assert np.array_equal(mlp_initial_params(p["seed"], p["d"], p["hidden"]), a[f"mlp_{m['kind']}_w0"])
