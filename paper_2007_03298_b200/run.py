@@ -23,7 +23,8 @@ Parity:
 - Logistic: the same holds for exp/log1p.
 
 Device path only: the anisotropic quadratic (problem.L != problem.mu, a
-dense d x d matvec) and the tiny-MLP are rejected with a clear message.
+dense d x d matvec) is rejected with a clear message.  The tiny MLP runs
+with its running statistics; its tanh is libdevice's (tolerance).
 """
 from __future__ import annotations
 
@@ -40,7 +41,7 @@ import numpy as np
 from . import _lib as L
 from ._lib import BUF_PARAMS
 from .api import (DivergenceError, DsSyncEngine, IterationTrace, StrategyKind, Topology,
-                  logistic_constants, logistic_dataset, quadratic_problem)
+                  logistic_constants, logistic_dataset, mlp_dataset, mlp_initial_params, quadratic_problem)
 from .config import ConfigError, RunConfig, load_run_config
 from .metrics import atomic_write_file, format_double, metrics_csv, summary_json
 
@@ -218,13 +219,46 @@ class Logistic(DeviceProblem):
         return losses, (None if self.has_optimum else float("nan"))
 
 
+class TinyMlp(DeviceProblem):
+    """TinyMlpProblem (problems.cpp:436-570): running statistics = the EMA
+    of the hidden pre-activations, folded with the params."""
+
+    kind = "tiny-mlp"
+    has_optimum = False
+    smoothness = float("nan")
+
+    def __init__(self, spec):
+        _check_common(spec)
+        if spec.M < 1:
+            raise ConfigError("tiny-mlp requires problem.M >= 1")
+        if spec.hidden < 1 or spec.hidden > 32:
+            raise ConfigError(f"problem.hidden must be in [1, 32] (got {spec.hidden})")
+        self.spec = spec
+        self.x, self.y = mlp_dataset(spec.seed, spec.d, spec.M)
+        self.dim = spec.hidden * spec.d + 2 * spec.hidden + 1
+        self.stats_dim = spec.hidden
+        self.mu = 0.0
+        self.w0 = mlp_initial_params(spec.seed, spec.d, spec.hidden)
+
+    def setup(self, engine, run_seed, cfg):
+        engine.broadcast_row(BUF_PARAMS, self.w0)
+        engine.mlp_setup(self.x, self.y, self.spec.hidden, cfg.batch_size, cfg.sampling, run_seed)
+
+    def gradients(self, engine, t, run_seed):
+        engine.mlp_gradients(t)
+        engine.running_stats_update()  # fold_running_stats (sync.cpp:193-201)
+
+    def losses(self, engine, with_mean=True):
+        return engine.mlp_losses(exact=True), float("nan")
+
+
 def make_device_problem(spec) -> DeviceProblem:  # problems.cpp:572-582
     if spec.kind == "quadratic":
         return Quadratic(spec)
     if spec.kind == "logistic":
         return Logistic(spec)
     if spec.kind == "tiny-mlp":
-        raise ConfigError("problem.kind tiny-mlp is not on the device path (a desk-scale verification model)")
+        return TinyMlp(spec)
     raise ConfigError("unknown problem.kind: " + spec.kind)
 
 
@@ -258,7 +292,7 @@ def run_training(problem: DeviceProblem, cfg: RunConfig, seed: int, device: int 
     if s.topology == Topology.PS:  # effective_bandwidth (sync.cpp:215-221)
         bw = cfg.cost.bandwidth * s.num_servers / W
     traces = []
-    with DsSyncEngine(s, cfg.optimizer, problem.dim, cfg.hp, dtype, device) as e:
+    with DsSyncEngine(s, cfg.optimizer, problem.dim, cfg.hp, dtype, device, stats_dim=problem.stats_dim) as e:
         problem.setup(e, seed, cfg)
         mean_engine = None
         if isinstance(problem, Logistic) and problem.has_optimum:

@@ -238,6 +238,14 @@ CLI_CONFIGS = [
     ("logistic_bsp", {"strategy": "bsp", "world_size": 4, "iterations": 40, "seeds": [2, 3], "batch_size": 8,
                       "problem": {"kind": "logistic", "d": 20, "M": 2000, "mu": 0.05, "seed": 11},
                       "lr": {"kind": "step-decay", "alpha": 1.0, "factor": 0.5, "every": 10}}, "tolerance"),
+    ("mlp_ds_adam", {"strategy": "ds-sync", "world_size": 4, "group_size": 2, "iterations": 30, "seeds": [2],
+                     "batch_size": 4, "problem": {"kind": "tiny-mlp", "d": 5, "M": 64, "hidden": 8, "seed": 3},
+                     "optimizer": {"kind": "adam"}, "lr": {"kind": "constant", "alpha": 0.01}}, "tolerance"),
+    ("mlp_bsp_epoch", {"strategy": "bsp", "world_size": 4, "iterations": 25, "seeds": [1, 4], "batch_size": 3,
+                       "sampling": "epoch",
+                       "problem": {"kind": "tiny-mlp", "d": 3, "M": 40, "hidden": 4, "seed": 9},
+                       "optimizer": {"kind": "sgd-momentum"}, "lr": {"kind": "step-decay", "alpha": 0.05,
+                                                                       "every": 10}}, "tolerance"),
     ("quad_diverges", {"strategy": "ds-sync", "world_size": 4, "iterations": 10,
                        "problem": {"kind": "quadratic", "d": 5, "mu": 1.0, "L": 1.0, "seed": 1},
                        "lr": {"kind": "constant", "alpha": 1e300}}, "error"),

@@ -23,7 +23,7 @@ def _rows(text):
     return list(csv.reader(io.StringIO(text)))
 
 
-@pytest.mark.parametrize("idx", range(7))
+@pytest.mark.parametrize("idx", range(9))
 def test_cli_matches_reference(cuda_device, golden, tmp_path, capsys, idx):
     meta, _ = golden
     r = meta["cli_runs"][idx]
