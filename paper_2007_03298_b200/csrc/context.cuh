@@ -131,8 +131,6 @@ struct dss_ctx {
   int sms = 148;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // chain mean pass beside the partial pass (DSS_CHAIN_CONCURRENT)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   void* w = nullptr;
   void* g = nullptr;

@@ -283,10 +283,6 @@ extern "C" int dss_destroy(dss_ctx* c) {
   for (cudaEvent_t e : {c->ev_in, c->ev_free, c->ev_snap, c->ev_out}) {
     if (e) cudaEventDestroy(e);
   }
-  if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
-  for (cudaEvent_t e : {c->ev_fork, c->ev_join}) {
-    if (e) cudaEventDestroy(e);
-  }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return DSS_OK;

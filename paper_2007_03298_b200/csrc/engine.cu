@@ -837,15 +837,6 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
   // B concurrently on a side stream with A giving up CTA slots (2534 / 369),
   // and both passes in one persistent kernel with lagged mean-pass units
   // (2300 / stalled).
-  const bool concurrent = DSS_CHAIN_CONCURRENT && OPTD == kOptNone && cl.na > 0 && cl.nb > 0;
-  if (concurrent) {
-    if (!c->side) {
-      ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
-      ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "fork event");
-      ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "join event");
-    }
-    ck(cudaEventRecord(c->ev_fork, c->stream), "fork record");  // B follows everything before A
-  }
   if (cl.na > 0) {
     a.entries = cl.d_a;
     a.n_entries = cl.na;
@@ -854,21 +845,6 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
     chain_partial_kernel<T, OPTM, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_CTAS_PER_SM})),
                                           kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
-  }
-  if (concurrent) {
-    // kernel A is already enqueued (a shared hardware queue serialises, it
-    // cannot deadlock); B's few CTAs take the slots A's first wave frees
-    a.entries = cl.d_b;
-    a.n_entries = cl.nb;
-    const long units = c->chain_nchunks * cl.nb;
-    TimedLaunch tl(c, DSS_KIND_CHAIN_MEAN);
-    ck(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork wait");
-    chain_mean_kernel<T, OPTD><<<static_cast<int>(std::min<long>(units, c->sms * long{DSS_CHAIN_B_CTAS_PER_SM})),
-                                 kThreads, 0, c->side>>>(a);
-    ck(cudaGetLastError(), "chain_mean_kernel launch");
-    ck(cudaEventRecord(c->ev_join, c->side), "join record");
-    ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join wait");
-    return;
   }
   if (cl.nb > 0) {
     a.entries = cl.d_b;

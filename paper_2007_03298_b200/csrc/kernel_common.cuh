@@ -43,16 +43,6 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_PERSIST_MAX_WORKERS_BSP
 #define DSS_PERSIST_MAX_WORKERS_BSP 16
 #endif
-// 1: the chain's mean pass (kernel B) runs on a side stream beside the
-// partial pass (kernel A, enqueued first so a shared hardware queue can
-// only serialise them), DSS_CHAIN_B_CTAS_PER_SM CTAs per SM, polling with
-// backoff.  0: B after A on the context stream.
-#ifndef DSS_CHAIN_CONCURRENT
-#define DSS_CHAIN_CONCURRENT 0
-#endif
-#ifndef DSS_CHAIN_B_CTAS_PER_SM
-#define DSS_CHAIN_B_CTAS_PER_SM 1
-#endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.

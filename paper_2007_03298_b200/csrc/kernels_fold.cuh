@@ -184,23 +184,16 @@ template <typename T> struct ChainArgs {
   double bc2[kMaxLocal];
 };
 
-// backoff: sleep between polls (doubling to ~1 us) -- for waiters that
-// may spin long beside running work (the concurrent mean pass).
 __device__ __forceinline__ bool chain_wait(const unsigned long long* flag, unsigned long long epoch,
-                                           unsigned long long* timeout, bool backoff = false) {
+                                           unsigned long long* timeout) {
   unsigned long long start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
-  unsigned ns = 32;
   while (ld_acquire_sys(flag) < epoch) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - start > 20000000000ull) {
       atomicExch(timeout, 1ull);
       return false;
-    }
-    if (backoff) {
-      __nanosleep(ns);
-      ns = ns < 1024 ? 2 * ns : ns;
     }
   }
   return true;
@@ -434,7 +427,7 @@ __device__ __forceinline__ void chain_unit_b(const ChainArgs<T>& a, const ChainE
   const int ei = static_cast<int>(u % n_entries);
   if (threadIdx.x == 0) {
     en = entries[ei];
-    ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout, DSS_CHAIN_CONCURRENT != 0) ? 1 : 0;
+    ok_flag = chain_wait(en.recv_flags + c, a.epoch, a.timeout) ? 1 : 0;
   }
   __syncthreads();
   const long lo = c * a.chunk;
