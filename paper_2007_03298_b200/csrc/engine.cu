@@ -99,9 +99,21 @@ unsigned long long* chain_flag(dss_ctx* c, unsigned long long* base, int region,
 
 // Chain-fold launch tables for this GPU's roles.  members of role i are
 // rows of `member_base` (local); its mean lands in dsts[i] (local rows).
+// inplace (a Partition, params rows): the mean travels straight into the
+// receiving GPU's first member row of the group instead of a receive row,
+// and the mean pass there copies it to the other members (one row write
+// less per group and GPU).
 ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* member_base,
                         const std::vector<std::vector<void*>>& dsts, int err_phase, int opt_mem = kOptNone,
-                        int opt_dst = kOptNone, const std::vector<std::vector<int>>& dst_lrs = {}) {
+                        int opt_dst = kOptNone, const std::vector<std::vector<int>>& dst_lrs = {},
+                        const Partition* inplace = nullptr) {
+  auto first_member_row = [&](int group, int gpu) -> void* {
+    const int* mem = inplace->group(group);
+    for (int q = 0; q < inplace->size(group); ++q) {
+      if (mem[q] / c->P == gpu) return row_ptr(c, c->peer_w, mem[q]);
+    }
+    throw std::logic_error("chain: receiver holds no member of the group");
+  };
   ChainLaunch cl;
   cl.opt_mem = opt_mem;
   cl.opt_dst = opt_dst;
@@ -134,7 +146,8 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
       a.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.next_gpu)], 0, r.next_slot);
       a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.next_gpu)], 0, r.next_slot);
     } else {
-      a.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+      a.send = inplace ? first_member_row(r.group, r.mean_next_gpu)
+                       : chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
       a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
     }
     a.err_rank = r.first_member;
@@ -144,10 +157,12 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
     if (r.stage <= r.S - 2) {
       ChainEntry b = a;
       b.last = 0;
-      b.recv = chain_row(c, c->chain_buf, 1, r.slot);
+      b.recv = inplace ? dsts[i][0] : chain_row(c, c->chain_buf, 1, r.slot);
+      b.dst_skip = inplace ? 1 : 0;
       b.recv_flags = chain_flag(c, c->chain_flags, 1, r.slot);
       if (r.stage < r.S - 2) {
-        b.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+        b.send = inplace ? first_member_row(r.group, r.mean_next_gpu)
+                         : chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
         b.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
       } else {
         b.send = nullptr;
@@ -433,7 +448,8 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
         lrs.push_back(l);
       }
       pp.chain = build_chain(c, gp.chain, c->w, dsts, s.kind == DSS_BSP ? 0 : 1,
-                             with_step ? c->cfg.optimizer : kOptNone, kOptNone, lrs);
+                             with_step ? c->cfg.optimizer : kOptNone, kOptNone, lrs,
+                             DSS_CHAIN_INPLACE && multi(c) ? &part : nullptr);
     }
   }
   if (force_fold(c)) pp.any_twoshot = pp.any_spanning;

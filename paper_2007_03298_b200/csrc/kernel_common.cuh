@@ -43,6 +43,11 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_PERSIST_MAX_WORKERS_BSP
 #define DSS_PERSIST_MAX_WORKERS_BSP 16
 #endif
+// 1: the chain's mean is sent straight into the receiving GPU's first
+// member row (DS steps and sync rounds), not into a receive row.
+#ifndef DSS_CHAIN_INPLACE
+#define DSS_CHAIN_INPLACE 1
+#endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.

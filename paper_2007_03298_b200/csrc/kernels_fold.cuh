@@ -154,6 +154,7 @@ struct ChainEntry {
   int err_rank;
   int err_phase;
   int m;              // group size (1/m)
+  int dst_skip;       // 1: the mean was received straight into dst[0] (in-place delivery)
 };
 
 template <typename T> struct ChainArgs {
@@ -270,7 +271,7 @@ template <typename T, int OPTD>
 __device__ __forceinline__ void chain_deliver(const ChainArgs<T>& a, const ChainEntry& en, long off,
                                               const Pack<T>& mean, unsigned long long& bad) {
   if constexpr (OPTD == kOptNone) {
-    for (int q = 0; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, mean);
+    for (int q = en.dst_skip; q < en.dst_cnt; ++q) stv(a.dst[en.dst_beg + q] + off, mean);
   } else {
     const Pack<T> gv[4] = {mean, mean, mean, mean};
     Pack<T> out[4];
