@@ -216,6 +216,32 @@ def cpu_baseline(cfg, seconds=12.0, sample_d=1 << 20):
                       f"(reference apply_step + ring_allreduce_avg), scaled by {ds_}/{d}"}
 
 
+def cpu_run_training_c1():
+    """The reference's own `dssync run` on config C1 (acceptance.cpp:239-258:
+    logistic d=20, M=2000, l2=0.05, batch 8, W=4 groups of 2, 300
+    iterations, step-decay lr), timed on the host: run_training with its
+    per-iteration trace (two full losses per worker)."""
+    import tempfile
+    from oracle.oracle import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        return None
+    cfg = {"strategy": "ds-sync", "world_size": 4, "group_size": 2, "iterations": 300, "batch_size": 8,
+           "seeds": [1], "problem": {"kind": "logistic", "d": 20, "M": 2000, "mu": 0.05, "seed": 11},
+           "lr": {"kind": "step-decay", "alpha": 1.0, "factor": 0.5, "every": 75}}
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "c1.json")
+        with open(path, "w") as f:
+            json.dump(cfg, f)
+        t0 = time.perf_counter()
+        rc, msg, _, _ = Reference().cmd_run(path, os.path.join(tmp, "out"))
+        el = time.perf_counter() - t0
+    if rc:
+        return None
+    return {"iters_s": 300 / el, "cores": 1,
+            "note": "the reference's `dssync run` on C1 (run_training lockstep, with its per-iteration trace), "
+                    "host, one thread"}
+
+
 # ---------------------------------------------------------------------------
 def step_bytes(cfg, G, rank, d_pad):
     """Algorithmic bytes one GPU moves per DS / BSP iteration, by kernel kind,
@@ -598,7 +624,9 @@ def our_arm(args, cfg):
         out["device_gradient_run"] = {
             "iters_s": 1000.0 / res["logistic"], "ms_per_step": res["logistic"],
             "note": "DS iterations with the logistic batch sampled and the gradient computed on the device "
-                    "(dss_logistic_steps: gradient kernel + fused step per iteration)"}
+                    "(dss_logistic_steps: one launch for the whole batch of iterations; no trace)"}
+        if not args.no_cpu_baseline:
+            out["device_gradient_run"]["cpu_reference_run_training"] = cpu_run_training_c1()
     if G == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(out))
