@@ -192,6 +192,7 @@ struct dss_ctx {
   dssb::ParityPlan mean_plan;      // ordered fold of every worker's params into mg (trace)
   dssb::ParityPlan stats_plan[2];  // running-stats fold per parity (DS) / world group at [0] (BSP)
   double* d_loss = nullptr;  // [P + 1] loss accumulators (trace)
+  void** d_loss_rows = nullptr;  // [P + 1] rows the trace losses read: local params, then mg
 
   // logistic problem on the device (dss_logistic_setup)
   struct {

@@ -49,7 +49,20 @@ extern "C" int dss_quadratic_init(dss_ctx* c, uint64_t problem_seed, double delt
     if (!(delta0 > 0.0)) throw std::invalid_argument("problem.delta0 must be > 0");
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     quiesce(c);
-    double *ws = nullptr, *u = nullptr, *ss = nullptr;
+    // scratch rows, freed on every exit (after the stream is drained)
+    struct Scratch {
+      double *ws = nullptr, *u = nullptr, *ss = nullptr;
+      cudaStream_t st;
+      ~Scratch() {
+        cudaStreamSynchronize(st);
+        cudaFree(ws);
+        cudaFree(u);
+        cudaFree(ss);
+      }
+    } sc{nullptr, nullptr, nullptr, c->stream};
+    double*& ws = sc.ws;
+    double*& u = sc.u;
+    double*& ss = sc.ss;
     ck(cudaMalloc(&ws, sizeof(double) * c->d), "cudaMalloc");
     ck(cudaMalloc(&u, sizeof(double) * c->d), "cudaMalloc");
     ck(cudaMalloc(&ss, sizeof(double)), "cudaMalloc");
@@ -75,9 +88,6 @@ extern "C" int dss_quadratic_init(dss_ctx* c, uint64_t problem_seed, double delt
     }
     ck(cudaGetLastError(), "init kernels");
     ck(cudaStreamSynchronize(c->stream), "init sync");
-    cudaFree(ws);
-    cudaFree(u);
-    cudaFree(ss);
     return DSS_OK;
   });
 }
@@ -101,10 +111,15 @@ extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, int exact, double* lo
     quiesce(c);
     if (!c->d_loss) c->d_loss = static_cast<double*>(dalloc(c, sizeof(double) * (c->P + 1)));
     const int rows = c->P + (suboptimality ? 1 : 0);
-    std::vector<void*> ptrs;
-    for (int k = 0; k < c->P; ++k) ptrs.push_back(static_cast<char*>(c->w) + static_cast<size_t>(k) * c->d_pad * c->esz);
-    if (suboptimality) ptrs.push_back(c->mg);  // after dss_global_mean
-    void** d_ptrs = upload_table(c, ptrs);
+    if (!c->d_loss_rows) {  // every local row, then the global-mean row (after dss_global_mean)
+      std::vector<void*> ptrs;
+      for (int k = 0; k < c->P; ++k) {
+        ptrs.push_back(static_cast<char*>(c->w) + static_cast<size_t>(k) * c->d_pad * c->esz);
+      }
+      ptrs.push_back(c->mg);
+      c->d_loss_rows = upload_table(c, ptrs);
+    }
+    void** d_ptrs = c->d_loss_rows;
     ck(cudaMemsetAsync(c->d_loss, 0, sizeof(double) * (c->P + 1), c->stream), "loss reset");
     dim3 grid(grid_x(c, c->d, rows), rows);
     if (exact) {
@@ -128,8 +143,6 @@ extern "C" int dss_quadratic_losses(dss_ctx* c, double mu, int exact, double* lo
     std::vector<double> h(static_cast<size_t>(rows));
     ck(cudaMemcpyAsync(h.data(), c->d_loss, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream), "loss readback");
     ck(cudaStreamSynchronize(c->stream), "loss sync");
-    cudaFree(d_ptrs);
-    c->allocations.erase(std::find(c->allocations.begin(), c->allocations.end(), static_cast<void*>(d_ptrs)));
     for (int k = 0; k < c->P; ++k) losses[k] = h[static_cast<size_t>(k)];
     if (suboptimality) *suboptimality = h[static_cast<size_t>(c->P)];
     return DSS_OK;
