@@ -37,6 +37,11 @@ CASES = [
 ]
 
 
+def device_of(rank):
+    """Process rank -> CUDA device (several ranks per device when oversubscribed)."""
+    return rank % torch.cuda.device_count()
+
+
 def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0):
     s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
                      WorldConfig(W, N), 1, rect)
@@ -45,7 +50,7 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0):
     rng = np.random.default_rng(1000 + W + opt)
     w = rng.standard_normal((W, d)).astype(np.float32)
     mine = local_slice(W, G, rank)
-    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", rank, rank, G, path=path, stats_dim=sd)
+    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G, path=path, stats_dim=sd)
     attach(e)
     e.upload_all(BUF_PARAMS, w[mine.start:mine.stop])
     rs = rng.standard_normal((W, sd)).astype(np.float32) if sd else None
@@ -117,7 +122,7 @@ def logistic_case(rank, G, sampling, kind):
     x, y = logistic_dataset(11, 20, 2000)
     alphas = 1.0 * 0.5 ** (np.arange(T) // 15)
     s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING, WorldConfig(W, N))
-    e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 20, OptimizerHyperparams(), "f64", rank, rank, G)
+    e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 20, OptimizerHyperparams(), "f64", device_of(rank), rank, G)
     attach(e)
     e.logistic_setup(x, y, 0.05, 8, sampling, 1)
     e.logistic_steps(0, alphas, check=True)
@@ -140,7 +145,7 @@ def logistic_case(rank, G, sampling, kind):
 def main():
     rank = int(os.environ["RANK"])
     G = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(rank)
+    torch.cuda.set_device(device_of(rank))
     dist.init_process_group("gloo")
     orc = Oracle()
     ok = True

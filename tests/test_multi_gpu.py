@@ -19,7 +19,11 @@ def _ngpus():
 
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_two_shot_nvlink_bit_exact(G):
-    if _ngpus() < G:
+    # DSS_TEST_OVERSUBSCRIBE=1 runs G processes over fewer GPUs (several
+    # contexts per device, peer access over IPC all the same): it checks the
+    # G-GPU plans, one-shot / push / chain tables and barriers for
+    # correctness when fewer GPUs are at hand.
+    if _ngpus() < G and not (os.environ.get("DSS_TEST_OVERSUBSCRIBE") and _ngpus() >= 1):
         pytest.skip(f"needs {G} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr=127.0.0.1", f"--master-port={29600 + G}", os.path.join(ROOT, "tests", "mgpu_worker.py")]
