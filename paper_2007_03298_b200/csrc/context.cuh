@@ -102,6 +102,7 @@ struct PushLaunch {
   int items = 0, folds = 0;
   void** d_item_dst = nullptr;
   unsigned long long** d_item_flag = nullptr;
+  int* d_item_gpu = nullptr;       // one-shot: destination GPU of each item_dst entry
   PushItem* d_items = nullptr;
   PushFold* d_folds = nullptr;
   void** d_dst = nullptr;
@@ -172,6 +173,8 @@ struct dss_ctx {
   long oneshot_base_elems = 0, oneshot_base_flags = 0;
   long oneshot_half_elems = 0, oneshot_half_flags = 0;
   long oneshot_rows = 0;  // staging rows per group slot: the largest group size
+  long oneshot_ack_off = 0;  // push_flags offset of the [G] acks (same on every GPU)
+  unsigned long long** d_oneshot_ack_peer = nullptr;  // [G] peers' ack arrays
   unsigned long long oneshot_seq = 0;
   // dss_step_host pipeline
   cudaStream_t copy_in = nullptr, copy_out = nullptr;

@@ -243,6 +243,8 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         c->oneshot_half_flags = static_cast<long>(c->P) * rows * c->chain_nchunks;
         ps += 2 * c->oneshot_half_elems;
         pf += 2 * c->oneshot_half_flags;
+        c->oneshot_ack_off = pf;  // [G] one-shot launches each peer has started
+        pf += cfg->n_gpus;
       }
       c->push_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(ps) * c->esz));
       c->push_flags = static_cast<unsigned long long*>(

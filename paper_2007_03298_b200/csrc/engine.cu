@@ -303,6 +303,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   std::vector<PushItem> items;
   std::vector<void*> item_dst;
   std::vector<unsigned long long*> item_flag;
+  std::vector<int> item_gpu;
   std::vector<PushFold> folds;
   std::vector<void*> dst;
   std::vector<int> dst_lr;
@@ -344,6 +345,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
           item_dst.push_back(static_cast<char*>(c->peer_push_buf[static_cast<size_t>(gpu)]) +
                              static_cast<size_t>(row * c->d_pad + it.lo) * c->esz);
           item_flag.push_back(c->peer_push_flags[static_cast<size_t>(gpu)] + row * nch + ch);
+          item_gpu.push_back(gpu);
         }
         items.push_back(it);
       }
@@ -384,6 +386,12 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
   pl.d_folds = upload_table(c, folds);
   pl.d_dst = upload_table(c, dst);
   pl.d_dst_lr = upload_table(c, dst_lr);
+  pl.d_item_gpu = upload_table(c, item_gpu);
+  if (!c->d_oneshot_ack_peer) {
+    std::vector<unsigned long long*> acks;
+    for (int q = 0; q < G; ++q) acks.push_back(c->peer_push_flags[static_cast<size_t>(q)] + c->oneshot_ack_off);
+    c->d_oneshot_ack_peer = upload_table(c, acks);
+  }
   return pl;
 }
 
@@ -956,6 +964,12 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
     const long par = static_cast<long>(c->oneshot_seq++ & 1);
     a.stage_shift = (c->oneshot_base_elems + par * c->oneshot_half_elems) * c->esz;
     a.flag_shift = c->oneshot_base_flags + par * c->oneshot_half_flags;
+    a.seq = c->oneshot_seq;  // 1, 2, ...: this launch's number
+    a.ack_peer = c->d_oneshot_ack_peer;
+    a.ack_mine = c->push_flags + c->oneshot_ack_off;
+    a.item_gpu = pl.d_item_gpu;
+    a.me = c->cfg.rank;
+    a.n_gpus = c->cfg.n_gpus;
   }
   a.c = consts<T>(c, alpha);
   fill_bias(c, a);

@@ -520,6 +520,16 @@ template <typename T> struct PushArgs {
   unsigned long long* timeout;
   long stage_shift;      // one-shot: bytes to this launch's staging buffer (double-buffered), else 0
   long flag_shift;       // one-shot: flags to this launch's flag set, else 0
+  // one-shot flow control: this is one-shot launch `seq` (1, 2, ...).  At
+  // the start every GPU records seq in each peer's acks[me]; a push into
+  // GPU q's buffer waits for acks[q] >= seq - 1 here, i.e. for q to have
+  // started launch seq - 1 and so finished launch seq - 2, the previous
+  // user of the same buffer (consecutive launches may have other peers).
+  unsigned long long seq; // 0: two-shot (no flow control)
+  unsigned long long* const* ack_peer;  // [G] each GPU's ack array
+  unsigned long long* ack_mine;         // [G] this GPU's ack array
+  const int* item_gpu;                  // destination GPU of each item_dst entry
+  int me, n_gpus;
   StepConsts<T> c;
   double bc1[kMaxLocal];
   double bc2[kMaxLocal];
@@ -540,12 +550,18 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   __shared__ int ok_flag;
   __shared__ T* sdst[kMaxFold];
   unsigned long long bad = ~0ull;
+  if (a.seq && blockIdx.x == 0 && threadIdx.x < a.n_gpus) {
+    st_release_sys(a.ack_peer[threadIdx.x] + a.me, a.seq);  // "I have started launch seq"
+  }
   // phase 1: step + push
   for (int u = blockIdx.x; u < a.n_items; u += gridDim.x) {
     if (threadIdx.x == 0) it = a.items[u];
     __syncthreads();
     if (threadIdx.x < it.ndst) {
       sdst[threadIdx.x] = reinterpret_cast<T*>(static_cast<char*>(a.item_dst[it.dst_beg + threadIdx.x]) + a.stage_shift);
+      if (a.seq > 1) {  // the destination is done with this buffer's previous launch
+        chain_wait(a.ack_mine + a.item_gpu[it.dst_beg + threadIdx.x], a.seq - 1, a.timeout);
+      }
     }
     __syncthreads();
     const long r = static_cast<long>(it.lr) * a.ld;
