@@ -166,9 +166,9 @@ struct dss_ctx {
   std::vector<unsigned long long*> peer_push_flags;
   int push_occupancy = 0;
   // one-shot (small rows): double-buffered staging [2][P][G][d_pad] + flags [2][P][G][n_chunks]
-  // one-shot area after the two-shot staging: [2][P][R][d_pad] rows +
-  // [2][P][R][n_chunks] flags (R = oneshot_rows), double-buffered by the
-  // one-shot launch count
+  // one-shot area after the two-shot staging: [B][P][R][d_pad] rows +
+  // [B][P][R][n_chunks] flags (R = oneshot_rows, B = DSS_ONESHOT_BUFFERS),
+  // rotated by the one-shot launch count
   bool oneshot[2] = {false, false};  // per schedule parity (same on every GPU)
   long oneshot_base_elems = 0, oneshot_base_flags = 0;
   long oneshot_half_elems = 0, oneshot_half_flags = 0;

@@ -241,8 +241,8 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         c->oneshot_base_flags = pf;
         c->oneshot_half_elems = static_cast<long>(c->P) * rows * c->d_pad;
         c->oneshot_half_flags = static_cast<long>(c->P) * rows * c->chain_nchunks;
-        ps += 2 * c->oneshot_half_elems;
-        pf += 2 * c->oneshot_half_flags;
+        ps += DSS_ONESHOT_BUFFERS * c->oneshot_half_elems;
+        pf += DSS_ONESHOT_BUFFERS * c->oneshot_half_flags;
         c->oneshot_ack_off = pf;  // [G] one-shot launches each peer has started
         pf += cfg->n_gpus;
       }

@@ -961,7 +961,7 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   if (pl.oneshot) {
     // alternate staging buffers: a GPU can only push launch n+2 after every
     // peer pushed launch n+1, i.e. after every peer finished folding launch n
-    const long par = static_cast<long>(c->oneshot_seq++ & 1);
+    const long par = static_cast<long>(c->oneshot_seq++ % DSS_ONESHOT_BUFFERS);
     a.stage_shift = (c->oneshot_base_elems + par * c->oneshot_half_elems) * c->esz;
     a.flag_shift = c->oneshot_base_flags + par * c->oneshot_half_flags;
     a.seq = c->oneshot_seq;  // 1, 2, ...: this launch's number

@@ -48,6 +48,12 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_CHAIN_INPLACE
 #define DSS_CHAIN_INPLACE 1
 #endif
+// One-shot staging buffers in rotation: a push into a peer waits until the
+// peer has started the launch DSS_ONESHOT_BUFFERS - 1 back, i.e. finished
+// the last launch that used the same buffer.
+#ifndef DSS_ONESHOT_BUFFERS
+#define DSS_ONESHOT_BUFFERS 3
+#endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.

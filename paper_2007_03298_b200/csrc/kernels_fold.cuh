@@ -520,11 +520,12 @@ template <typename T> struct PushArgs {
   unsigned long long* timeout;
   long stage_shift;      // one-shot: bytes to this launch's staging buffer (double-buffered), else 0
   long flag_shift;       // one-shot: flags to this launch's flag set, else 0
-  // one-shot flow control: this is one-shot launch `seq` (1, 2, ...).  At
-  // the start every GPU records seq in each peer's acks[me]; a push into
-  // GPU q's buffer waits for acks[q] >= seq - 1 here, i.e. for q to have
-  // started launch seq - 1 and so finished launch seq - 2, the previous
-  // user of the same buffer (consecutive launches may have other peers).
+  // one-shot flow control: this is one-shot launch `seq` (1, 2, ...) on
+  // buffer (seq - 1) % B, B = DSS_ONESHOT_BUFFERS.  At the start every GPU
+  // records seq in each peer's acks[me]; a push into GPU q's buffer waits
+  // for acks[q] >= seq - B + 1, i.e. for q to have started launch
+  // seq - B + 1 and so finished launch seq - B, the previous user of the
+  // same buffer (consecutive launches may have other peers).
   unsigned long long seq; // 0: two-shot (no flow control)
   unsigned long long* const* ack_peer;  // [G] each GPU's ack array
   unsigned long long* ack_mine;         // [G] this GPU's ack array
@@ -559,8 +560,8 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
     __syncthreads();
     if (threadIdx.x < it.ndst) {
       sdst[threadIdx.x] = reinterpret_cast<T*>(static_cast<char*>(a.item_dst[it.dst_beg + threadIdx.x]) + a.stage_shift);
-      if (a.seq > 1) {  // the destination is done with this buffer's previous launch
-        chain_wait(a.ack_mine + a.item_gpu[it.dst_beg + threadIdx.x], a.seq - 1, a.timeout);
+      if (a.seq >= DSS_ONESHOT_BUFFERS) {  // the destination is done with this buffer's previous launch
+        chain_wait(a.ack_mine + a.item_gpu[it.dst_beg + threadIdx.x], a.seq - DSS_ONESHOT_BUFFERS + 1, a.timeout);
       }
     }
     __syncthreads();
