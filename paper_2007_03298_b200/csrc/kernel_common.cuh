@@ -54,6 +54,9 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_ONESHOT_BUFFERS
 #define DSS_ONESHOT_BUFFERS 3
 #endif
+#ifndef DSS_ONESHOT_ACK_RELAXED
+#define DSS_ONESHOT_ACK_RELAXED 0
+#endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
 // start one round after stage j instead of after the whole row.

@@ -552,7 +552,14 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   __shared__ T* sdst[kMaxFold];
   unsigned long long bad = ~0ull;
   if (a.seq && blockIdx.x == 0 && threadIdx.x < a.n_gpus) {
-    st_release_sys(a.ack_peer[threadIdx.x] + a.me, a.seq);  // "I have started launch seq"
+    // "I have started launch seq".  The reads this releases (the folds of
+    // an earlier launch) finished at a kernel boundary, so a relaxed store
+    // suffices: a peer that sees it can only write after those reads.
+    if (DSS_ONESHOT_ACK_RELAXED) {
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a.ack_peer[threadIdx.x] + a.me), "l"(a.seq) : "memory");
+    } else {
+      st_release_sys(a.ack_peer[threadIdx.x] + a.me, a.seq);
+    }
   }
   // phase 1: step + push
   for (int u = blockIdx.x; u < a.n_items; u += gridDim.x) {
