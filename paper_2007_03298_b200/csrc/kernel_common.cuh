@@ -55,7 +55,7 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #define DSS_ONESHOT_BUFFERS 3
 #endif
 #ifndef DSS_ONESHOT_ACK_RELAXED
-#define DSS_ONESHOT_ACK_RELAXED 0
+#define DSS_ONESHOT_ACK_RELAXED 1
 #endif
 // Chain fold pipelining: elements per chunk (one flag each) and resident
 // CTAs per SM.  Small chunks and ~one round of CTAs per GPU let stage j+1
