@@ -165,7 +165,6 @@ struct dss_ctx {
   std::vector<void*> peer_push_buf;
   std::vector<unsigned long long*> peer_push_flags;
   int push_occupancy = 0;
-  // one-shot (small rows): double-buffered staging [2][P][G][d_pad] + flags [2][P][G][n_chunks]
   // one-shot area after the two-shot staging: [B][P][R][d_pad] rows +
   // [B][P][R][n_chunks] flags (R = oneshot_rows, B = DSS_ONESHOT_BUFFERS),
   // rotated by the one-shot launch count

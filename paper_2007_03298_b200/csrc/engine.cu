@@ -959,8 +959,8 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   a.err = c->d_err;
   a.timeout = c->d_timeout;
   if (pl.oneshot) {
-    // alternate staging buffers: a GPU can only push launch n+2 after every
-    // peer pushed launch n+1, i.e. after every peer finished folding launch n
+    // rotate the staging buffers; the kernel's acks keep a push from
+    // overwriting a buffer its destination still reads (see PushArgs::seq)
     const long par = static_cast<long>(c->oneshot_seq++ % DSS_ONESHOT_BUFFERS);
     a.stage_shift = (c->oneshot_base_elems + par * c->oneshot_half_elems) * c->esz;
     a.flag_shift = c->oneshot_base_flags + par * c->oneshot_half_flags;

@@ -518,7 +518,7 @@ template <typename T> struct PushArgs {
   unsigned long long epoch;
   unsigned long long* err;
   unsigned long long* timeout;
-  long stage_shift;      // one-shot: bytes to this launch's staging buffer (double-buffered), else 0
+  long stage_shift;      // one-shot: bytes to this launch's staging buffer (rotated), else 0
   long flag_shift;       // one-shot: flags to this launch's flag set, else 0
   // one-shot flow control: this is one-shot launch `seq` (1, 2, ...) on
   // buffer (seq - 1) % B, B = DSS_ONESHOT_BUFFERS.  At the start every GPU
