@@ -243,11 +243,13 @@ def cpu_run_training_c1():
 
 
 # ---------------------------------------------------------------------------
-def step_bytes(cfg, G, rank, d_pad):
+def step_bytes(cfg, G, rank, d_pad, path=0):
     """Algorithmic bytes one GPU moves per DS / BSP iteration, by kernel kind,
     averaged over the two schedule parities (block / comb iterations).
-      group: fused apply_step + fold (local groups) or in-place step
-             (members of spanning groups): d * bytes_per_elem per member
+      group: fused apply_step + fold of local groups, d * bytes_per_elem per
+             member (members of spanning groups are stepped inside the push /
+             one-shot / chain kernels; only the unfused pull path, path 3,
+             steps them in place with the group kernel)
       fold:  two-shot owner slice L over m members: reads m*L*4, writes m*L*4;
              the part touching other GPUs' rows crosses NVLink."""
     from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
@@ -273,8 +275,9 @@ def step_bytes(cfg, G, rank, d_pad):
             here = [m for m in g if m in mine]
             if not here:
                 continue
-            out["ds"]["group"] += 0.5 * len(here) * d * bpe
             gpus = sorted({m // P for m in g})
+            if len(gpus) == 1 or path == 3:
+                out["ds"]["group"] += 0.5 * len(here) * d * bpe
             if len(gpus) == 1:
                 continue
             if max(sum(1 for m in g if m // P == q) for q in gpus) >= 2:  # ordered chain
@@ -515,7 +518,7 @@ def our_arm(args, cfg):
         del e
     if G > 1:
         dist.barrier()
-    nb_bytes = step_bytes(cfg, G, rank, d_pad)
+    nb_bytes = step_bytes(cfg, G, rank, d_pad, args.path)
     if rank != 0:
         if G > 1:
             dist.destroy_process_group()
