@@ -1176,7 +1176,12 @@ template <typename T, int OPT>
 void launch_small_t(dss_ctx* c, SmallArgs<T>& a, int grid) {
   TimedLaunch tl(c, c->cfg.strategy.kind == DSS_BSP ? DSS_KIND_BSP : DSS_KIND_GROUP);
   if (grid == 1) {
-    small_steps_kernel<T, OPT><<<1, kThreads, 0, c->stream>>>(a);
+    const long units = a.bsp ? a.nvec : std::max(a.ngroups[0], a.ngroups[1]) * a.nvec;
+    if (DSS_SMALL_WIDE && !a.logistic && units > kThreads) {
+      small_steps_kernel<T, OPT, kSmallWide><<<1, kSmallWide, 0, c->stream>>>(a);
+    } else {
+      small_steps_kernel<T, OPT><<<1, kThreads, 0, c->stream>>>(a);
+    }
     ck(cudaGetLastError(), "small_steps_kernel launch");
     return;
   }

@@ -31,6 +31,13 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 // iterations above 32 KB) instead of one launch per iteration.  Measured
 // against per-iteration launches: +40-100% for 4 workers at 16 KB-1 MB
 // total, +10-20% for 16 workers, a loss at 4 MB.
+// One-CTA batches (<= 32 KB per array) with more element vectors than
+// kThreads run with kSmallWide threads: more member rows in flight.
+#ifndef DSS_SMALL_WIDE
+#define DSS_SMALL_WIDE 1
+#endif
+constexpr int kSmallWide = 512;
+
 #ifndef DSS_PERSIST_MAX_BYTES
 #define DSS_PERSIST_MAX_BYTES (1L << 20)
 #endif

@@ -595,18 +595,37 @@ __device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
   }
 }
 
-template <typename T, int OPT>
-__global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T> a) {
+// NT = kThreads for the logistic phase and the resident grid; a one-CTA
+// batch with more element vectors than kThreads runs wide (kSmallWide
+// threads) so more rows are in flight per member-ordered load round.
+template <typename T, int OPT, int NT = kThreads>
+__global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
   constexpr int VN = Vec<T>::n;
   unsigned long long bad = ~0ull;
   StepConsts<T> c = a.c;
+  // both parities' schedule tables in shared memory: the group -> member
+  // lookups are then not global-load rounds ahead of every row load
+  __shared__ int s_members[2][kMaxLocal];
+  __shared__ int s_offsets[2][kMaxLocal + 1];
+  if (!a.bsp) {
+    for (int p = 0; p < 2; ++p) {
+      for (int k = threadIdx.x; k < a.nw; k += blockDim.x) s_members[p][k] = a.members[p][k];
+      for (int k = threadIdx.x; k <= a.ngroups[p]; k += blockDim.x) s_offsets[p][k] = a.offsets[p][k];
+    }
+    __syncthreads();
+  }
+  double alpha_next = a.alpha[0];  // next iteration's step size, loaded one iteration ahead
   for (int i = 0; i < a.n; ++i) {
     const long t = a.t0 + i;
-    c.alpha = static_cast<T>(a.alpha[i]);
-    c.awd = static_cast<T>(a.alpha[i] * a.wd);
-    if (a.logistic) {
-      small_logistic_grads(a, t, const_cast<T*>(a.g));
-      __syncthreads();
+    const double alpha_i = alpha_next;
+    if (i + 1 < a.n) alpha_next = a.alpha[i + 1];
+    c.alpha = static_cast<T>(alpha_i);
+    c.awd = static_cast<T>(alpha_i * a.wd);
+    if constexpr (NT == kThreads) {
+      if (a.logistic) {
+        small_logistic_grads(a, t, const_cast<T*>(a.g));
+        __syncthreads();
+      }
     }
     const long tid = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long nthreads = static_cast<long>(gridDim.x) * blockDim.x;
@@ -677,8 +696,8 @@ __global__ void __launch_bounds__(kThreads) small_steps_kernel(const SmallArgs<T
       }
     } else {
       const int p = static_cast<int>(t & 1);
-      const int* members = a.members[p];
-      const int* offsets = a.offsets[p];
+      const int* members = s_members[p];
+      const int* offsets = s_offsets[p];
       const long units = static_cast<long>(a.ngroups[p]) * a.nvec;
       for (long u = tid; u < units; u += nthreads) {
         const int grp = static_cast<int>(u / a.nvec);

@@ -1,15 +1,9 @@
-# 1 GPU: resident-grid limits A/B after the load batching
-for v in base relax relax4m; do
-  if [ $v = base ]; then unset DSS_LIB_VARIANT; else export DSS_LIB_VARIANT=build/variants/libdssync_b200_$v.so; fi
-  timeout 600 python bench_sweep.py --max-mb 4 > gpurun_out/sweep_3a_$v.jsonl 2>gpurun_out/sweep_3a_$v.err; echo sweep_$v=$?
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_logistic.py -q > gpurun_out/pytest_3a.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_3a.log
+timeout 600 python bench_sweep.py --max-mb 1 --no-nccl > gpurun_out/sweep_3a.jsonl 2>gpurun_out/sweep_3a.err; echo sweep=$?
 python3 - <<'PY'
 import json
-rows = {}
-for v in ("base", "relax", "relax4m"):
-    for line in open(f"gpurun_out/sweep_3a_{v}.jsonl"):
-        try: d = json.loads(line)
-        except Exception: continue
-        rows.setdefault((d["N"], d["bytes_per_worker"]), {})[v] = (round(d["ds_iters_s"]), round(d["bsp_iters_s"]))
-for k in sorted(rows): print(k, rows[k])
+for line in open("gpurun_out/sweep_3a.jsonl"):
+    try: d = json.loads(line)
+    except Exception: continue
+    print(d["N"], d["bytes_per_worker"], round(d["ds_iters_s"]), round(d["bsp_iters_s"]))
 PY

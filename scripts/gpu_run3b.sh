@@ -1,11 +1,18 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_logistic.py -q > gpurun_out/pytest_3b.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_3b.log
-timeout 900 python bench_sweep.py > gpurun_out/sweep_3b_g1.jsonl 2>gpurun_out/sweep_3b.err; echo sweep=$?
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_logistic.py tests/test_gpu_mlp.py -q > gpurun_out/pytest_3c.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_3c.log
+for r in 1 2; do
+for v in narrow wide; do
+  if [ $v = narrow ]; then export DSS_LIB_VARIANT=$PWD/build/variants/libdssync_b200_narrow.so; else unset DSS_LIB_VARIANT; fi
+  timeout 300 python bench_sweep.py --max-mb 1 --no-nccl > gpurun_out/sweep_3c_${v}_$r.jsonl 2>gpurun_out/sweep_3c_${v}_$r.err; echo $v$r=$?
+done; done
 python3 - <<'PY'
 import json
-for line in open("gpurun_out/sweep_3b_g1.jsonl"):
-    try: d = json.loads(line)
-    except Exception: continue
-    if d["bytes_per_worker"] <= 1 << 22: print(d["N"], d["bytes_per_worker"], round(d["ds_iters_s"]), round(d["bsp_iters_s"]))
+rows = {}
+for v in ("narrow", "wide"):
+    for r in (1, 2):
+        for line in open(f"gpurun_out/sweep_3c_{v}_{r}.jsonl"):
+            try: d = json.loads(line)
+            except Exception: continue
+            rows.setdefault((d["N"], d["bytes_per_worker"]), {}).setdefault(v, []).append((round(d["ds_iters_s"]), round(d["bsp_iters_s"])))
+for k, x in sorted(rows.items()):
+    print(k, "narrow", x.get("narrow"), "wide", x.get("wide"))
 PY
-timeout 300 python bench.py --config c1 --steps 5000 --warmup 5 > gpurun_out/bench_c1_3b.log 2>&1; echo c1=$?; tail -1 gpurun_out/bench_c1_3b.log | python3 -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('value',d['value'],'bsp',d['bsp']['iters_s'],'e2e',d['e2e']['value'],'dev',d.get('device_gradient_run',{}).get('iters_s'))"
