@@ -500,3 +500,35 @@ def test_timing_and_launch_accounting(cuda_device):
             e.step(t, 0.01)
         tot, n, mx = e.kernel_times()
         assert n == 4 and e.launch_count - n0 == 4 and 0 < mx <= tot
+
+
+@pytest.mark.parametrize("kind,W,N,d,rect", [("ds", 8, 2, 300, True), ("ds", 9, 3, 700, False),
+                                             ("bsp", 4, 4, 1500, False)])
+@pytest.mark.parametrize("opt", [0, 3])
+def test_small_world_wide_cta(cuda_device, oracle, kind, W, N, d, rect, opt):
+    """The one-CTA batch kernel's 512-thread variant (more than 256 element
+    vectors per parity, still <= 32 KB per array): bit-exact vs the
+    restatement, f32 and f64."""
+    rng = np.random.default_rng(d + opt)
+    wd = 0.01 if opt == 3 else 0.0
+    for dtype, npt in (("f32", np.float32), ("f64", np.float64)):
+        w = rng.standard_normal((W, d)).astype(npt)
+        g = rng.standard_normal((W, d)).astype(npt)
+        alphas = np.array([0.05, 0.04, 0.03, 0.02, 0.01], dtype=np.float64)
+        with engine_for(kind, W, N, opt, d, wd, dtype, rect=rect) as e:
+            e.upload_all(BUF_PARAMS, w)
+            e.upload_all(BUF_GRADS, g)
+            e.steps(0, alphas, check=True)
+            got = e.download_all(BUF_PARAMS)
+        ref = w.copy()
+        m1, m2 = np.zeros_like(ref), np.zeros_like(ref)
+        steps = np.zeros(W, np.int64)
+        for i, a_i in enumerate(alphas):
+            if kind == "ds":
+                rc = oracle.ds_step(W, N, i, opt, hparams(weight_decay=wd), float(a_i), steps, ref, g, m1, m2,
+                                    rect=rect)
+            else:
+                rc = oracle.bsp_step(i, opt, hparams(weight_decay=wd), float(a_i), steps, ref, g, m1, m2)
+            assert rc[0] == 0
+            steps += 1
+        assert np.array_equal(got, ref), (dtype, kind, opt)
