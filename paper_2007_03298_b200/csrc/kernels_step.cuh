@@ -607,13 +607,22 @@ __global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
   // lookups are then not global-load rounds ahead of every row load
   __shared__ int s_members[2][kMaxLocal];
   __shared__ int s_offsets[2][kMaxLocal + 1];
+  __shared__ T s_inv[2][kMaxLocal];  // 1/m per group, the same value every unit computed before
   if (!a.bsp) {
     for (int p = 0; p < 2; ++p) {
       for (int k = threadIdx.x; k < a.nw; k += blockDim.x) s_members[p][k] = a.members[p][k];
       for (int k = threadIdx.x; k <= a.ngroups[p]; k += blockDim.x) s_offsets[p][k] = a.offsets[p][k];
+      for (int k = threadIdx.x; k < a.ngroups[p]; k += blockDim.x) {
+        s_inv[p][k] = static_cast<T>(1.0 / static_cast<double>(a.offsets[p][k + 1] - a.offsets[p][k]));
+      }
     }
     __syncthreads();
   }
+  // this thread's first (group, element vector) unit; later units advance by
+  // nthreads with a carry instead of a 64-bit divide per unit
+  const long tid0 = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int grp0 = a.bsp ? 0 : static_cast<int>(tid0 / a.nvec);
+  const long vec0 = a.bsp ? 0 : tid0 - static_cast<long>(grp0) * a.nvec;
   double alpha_next = a.alpha[0];  // next iteration's step size, loaded one iteration ahead
   for (int i = 0; i < a.n; ++i) {
     const long t = a.t0 + i;
@@ -698,10 +707,13 @@ __global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
       const int p = static_cast<int>(t & 1);
       const int* members = s_members[p];
       const int* offsets = s_offsets[p];
-      const long units = static_cast<long>(a.ngroups[p]) * a.nvec;
-      for (long u = tid; u < units; u += nthreads) {
-        const int grp = static_cast<int>(u / a.nvec);
-        const long off = (u % a.nvec) * VN;
+      const int ngroups = a.ngroups[p];
+      const long nvec = a.nvec;
+      const long units = static_cast<long>(ngroups) * nvec;
+      int grp = grp0;
+      long vec = vec0;
+      for (long u = tid; u < units;) {
+        const long off = vec * VN;
         const int beg = offsets[grp];
         const int m = offsets[grp + 1] - beg;
         Pack<T> acc;
@@ -735,7 +747,7 @@ __global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
           }
         }
         if (m > 1) {
-          const T inv = static_cast<T>(1.0 / static_cast<double>(m));
+          const T inv = s_inv[p][grp];
           bool ok = true;
 #pragma unroll
           for (int l = 0; l < VN; ++l) {
@@ -748,6 +760,19 @@ __global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
           }
         }
         for (int j = 0; j < m; ++j) stv(a.w + static_cast<long>(members[beg + j]) * a.ld + off, acc);
+        u += nthreads;
+        if (u >= units) break;
+        vec += nthreads;
+        if (vec >= nvec) {
+          if (vec < 2 * nvec) {
+            vec -= nvec;
+            ++grp;
+          } else {  // rows shorter than the thread count
+            const long q = vec / nvec;
+            grp += static_cast<int>(q);
+            vec -= q * nvec;
+          }
+        }
       }
     }
     // iteration t's rows are final before t+1 reads them
