@@ -1,7 +1,7 @@
 """DS-Sync sync-iteration benchmark (BASELINE.json metric) on 1..8 B200s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c1]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c4slice|c1]
+                    [--impl ours|reference] [--extras c3,c4slice,c2f64 | none]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
 A step is one DS-Sync iteration of the hot path over the config's worker
@@ -12,15 +12,23 @@ Default workload = BASELINE config C2 (W=8 workers, groups of 2 and 4,
 (W/N per GPU, so N=1 holds all 8; scaling is strong: total work fixed).
 BSP (ordered gradient fold + step) is measured on the same buffers.
 
+The headline line also carries keyed results for the other BASELINE
+configs that fit ("configs": C3, the C4 per-GPU slice and C2 in fp64 at
+N=1; C3 and, from 4 GPUs, full C4 at N>1), each with its own roofline and
+end-to-end number.
+
 Prints ONE JSON line (rank 0).  --impl reference times the reference's own
 CPU implementation (oracle/_ref = the unmodified reference sources) on the
-box's host cores instead.
+box's host cores at the full workload size, without loading the product
+library.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -34,7 +42,7 @@ sys.path.insert(0, ROOT)
 METRIC = "DS-Sync sync iters/s & effective GB/s vs BSP at 1/2/4/8 B200 (% of roofline)"
 
 # BASELINE configs.  bytes/elem: algorithmic HBM bytes per
-# worker-element per iteration (fp32): sgd 12, momentum 20, adam(w) 28.
+# worker-element per iteration (fp32; x2 for fp64): sgd 12, momentum 20, adam(w) 28.
 CONFIGS = {
     "c1": dict(W=4, N=2, rect=False, d=20, opt=0, alpha=0.05, wd=0.0, logistic=True,
                desc="C1: W=4, 2 groups of 2 shuffled every iteration, d=20 (logistic size), vanilla SGD"),
@@ -52,6 +60,7 @@ CONFIGS = {
 }
 BYTES_PER_ELEM = {0: 12, 1: 20, 2: 28, 3: 28}
 OPT_NAMES = ["vanilla-sgd", "sgd-momentum", "adam", "adamw"]
+NVLINK_PEAK = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
 def load_peaks():
@@ -61,6 +70,37 @@ def load_peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def config_dict(cfg, G):
+    """The `config` object, identical in both arms for the same --config/--gpus."""
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    P = W // G
+    return {"workload": cfg["desc"], "W": W, "N": N, "d": d, "optimizer": OPT_NAMES[cfg["opt"]],
+            "rectangular": cfg["rect"], "workers_per_gpu": P, "parallelism": f"dp{G} (W/G workers per GPU)",
+            "l2": (f"inputs larger than L2: {P * d * 4 / 1e6:.0f} MB per array per GPU" if P * d * 4 > 126e6
+                   else "inputs smaller than L2 (latency-bound config)")}
+
+
+def host_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    mem = None
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable"):
+                    mem = int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "mem_available_gb": round(mem / 1e9, 1) if mem else None}
 
 
 class ClockSampler:
@@ -90,9 +130,6 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append((time.time(), line.strip()))
 
-    def mark(self):
-        return time.time()
-
     def stop(self, t0, t1):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -116,104 +153,172 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def reference_arm(args, cfg):
-    """The reference's own CPU path: apply_step for every worker + each
-    group's ring_allreduce_avg (oracle/_ref = /root/reference/proj/src
-    compiled unmodified), all host threads, on a d-sample of the workload."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    from oracle.oracle import REF_SO, Reference
-    import ctypes as C
-    from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
+# The reference's CPU path (oracle/_ref: the unmodified reference sources
+# compiled by oracle/Makefile + oracle/ref_shim.cpp).  Nothing here loads the
+# product library.
+class RefBench:
+    """apply_step for every worker (threaded like run_training's Parallel
+    mode, sync.cpp:348-362) + each group's ring_allreduce_avg on the
+    concatenated payload, written back (sync.cpp:203-240, 364-370), on
+    resident fp64 WorkerStates (the reference is fp64-only)."""
 
+    def __init__(self, cfg, d, threads):
+        from oracle.oracle import Reference
+        self.R = R = Reference()
+        self.cfg, self.d, self.threads = cfg, d, threads
+        self.err = C.create_string_buffer(512)
+        hp = R.hp_array(weight_decay=cfg["wd"])
+        self.h = R.lib.ref_bench_create(cfg["W"], d, cfg["opt"], hp.ctypes.data, 1, threads)
+        self.tables = [self._table(p) for p in (0, 1)]
+
+    def _table(self, t):
+        W = self.cfg["W"]
+        m = np.zeros(W, np.int32)
+        o = np.zeros(W + 1, np.int32)
+        n = C.c_int()
+        rc = self.R.lib.ref_bench_partition(W, self.cfg["N"], int(self.cfg["rect"]), t, m.ctypes.data, o.ctypes.data,
+                                            C.byref(n), self.err, 512)
+        if rc:
+            raise RuntimeError(self.err.value.decode())
+        return m, o, n.value
+
+    def ds(self, t):
+        m, o, n = self.tables[t & 1]
+        rc = self.R.lib.ref_bench_ds_step(self.h, t, self.cfg["alpha"], m.ctypes.data, o.ctypes.data, n,
+                                          self.threads, self.err, 512)
+        if rc:
+            raise RuntimeError(self.err.value.decode())
+
+    def bsp(self, t):
+        rc = self.R.lib.ref_bench_bsp_step(self.h, t, self.cfg["alpha"], self.threads, self.err, 512)
+        if rc:
+            raise RuntimeError(self.err.value.decode())
+
+    def stock(self, t, N):
+        rc = self.R.lib.ref_bench_stock_step(self.h, N, t, self.cfg["alpha"], self.threads, self.err, 512)
+        if rc:
+            raise RuntimeError(self.err.value.decode())
+
+    def close(self):
+        if self.h:
+            self.R.lib.ref_bench_destroy(self.h)
+            self.h = None
+
+
+def ref_d(cfg):
+    """Largest d the host can hold for the reference bench: the full config
+    d unless memory forbids (C4 in fp64 needs ~700 GB)."""
+    nvec = 2 + {0: 0, 1: 1, 2: 2, 3: 2}[cfg["opt"]]
+    threads = os.cpu_count() or 1
+    # resident W x (params, grads, moments) + apply_step's copies in flight
+    per_elem = 8 * (cfg["W"] * nvec + min(threads, cfg["W"]) * (nvec - 1) + cfg["W"] // max(cfg["N"], 1) * 2)
+    avail = (host_info()["mem_available_gb"] or 32.0) * 1e9 * 0.6
+    return cfg["d"] if per_elem * cfg["d"] <= avail else int(avail // per_elem) // 64 * 64
+
+
+def time_ref(rb, fn, k0, K, budget_s=None):
+    """Per-iteration wall times of fn(t) for t = k0.. (all K, or until budget_s)."""
+    times = []
+    for t in range(k0, k0 + K):
+        t0 = time.perf_counter()
+        fn(t)
+        times.append(time.perf_counter() - t0)
+        if budget_s is not None and sum(times) > budget_s and len(times) >= 2:
+            break
+    return times
+
+
+def reference_arm(args, cfg):
+    """--impl reference: the reference's own CPU path at the full workload
+    size on every host core; rank 0 only (other ranks exit 0)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    from oracle.oracle import REF_SO
     if not os.path.exists(REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdssync_ref.so not built"}))
         return
-    R = Reference()
-    W, N, d = cfg["W"], cfg["N"], cfg["d"]
     threads = os.cpu_count() or 1
-    d_sample = min(d, args.ref_sample)
-    hp = R.hp_array(weight_decay=cfg["wd"])
-    h = R.lib.ref_bench_create(W, d_sample, cfg["opt"], hp.ctypes.data, 1)
-    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
-    tables = []
-    for p in (0, 1):
-        groups = make_partition(s, p).groups
-        members = np.array([x for g in groups for x in g], np.int32)
-        offsets = np.cumsum([0] + [len(g) for g in groups]).astype(np.int32)
-        tables.append((members, offsets, len(groups)))
-    err = C.create_string_buffer(512)
-
-    def ds(t):
-        m, o, n = tables[t & 1]
-        rc = R.lib.ref_bench_ds_step(h, t, cfg["alpha"], m.ctypes.data, o.ctypes.data, n, threads, err, 512)
-        assert rc == 0, err.value
-
-    for t in range(args.warmup):
-        ds(t)
-    t0 = time.perf_counter()
-    for t in range(args.warmup, args.warmup + args.steps):
-        ds(t)
-    dt = (time.perf_counter() - t0) / args.steps
-    # BSP on the same sample
-    tb0 = time.perf_counter()
-    nb = max(1, min(args.steps, 20))
-    for t in range(nb):
-        rc = R.lib.ref_bench_bsp_step(h, t, cfg["alpha"], threads, err, 512)
-        assert rc == 0, err.value
-    dtb = (time.perf_counter() - tb0) / nb
-    R.lib.ref_bench_destroy(h)
-    scale = d_sample / d  # per-element work: iters/s at full d = sample iters/s * d_sample / d
-    value = (1.0 / dt) * scale
-    sample = (f"W={W} workers x d={d_sample:,} fp64 (reference is fp64-only) of the d={d:,} workload, "
-              f"{args.steps} timed DS iterations; iters/s scaled by {d_sample}/{d}")
+    d = ref_d(cfg)
+    scaled = d != cfg["d"]
+    rb = RefBench(cfg, d, threads)
+    try:
+        for t in range(args.warmup):
+            rb.ds(t)
+        ts = time_ref(rb, rb.ds, args.warmup, args.steps)
+        ms = 1000.0 * sum(ts) / len(ts)
+        nb = min(args.steps, 5)
+        tb = time_ref(rb, rb.bsp, 0, nb)
+        ms_bsp = 1000.0 * sum(tb) / len(tb)
+    finally:
+        rb.close()
+    scale = d / cfg["d"]  # 1.0 unless the host cannot hold the workload
+    value = 1000.0 / ms * scale
+    sample = (f"the full workload: W={cfg['W']} workers x d={d:,} fp64 (the reference is fp64-only), "
+              f"{len(ts)} timed DS iterations after {args.warmup} warm-up, {threads} threads"
+              if not scaled else
+              f"size-scaled (host memory): W={cfg['W']} x d={d:,} of d={cfg['d']:,} fp64, {len(ts)} timed DS "
+              f"iterations, iters/s scaled by {d}/{cfg['d']}")
     out = {
         "metric": METRIC, "value": value, "unit": "iters/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "W": W, "N": N, "d": d, "optimizer": OPT_NAMES[cfg["opt"]],
-                   "rectangular": cfg["rect"]},
-        "effective_gbs": W * d * 4 / (1000.0 / value / 1e3) / 1e9,
-        "bsp": {"iters_s": (1.0 / dtb) * scale},
+        "steps": len(ts), "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter-addressed "
+        "reference Rng streams; fixed gradients, as in our arm)",
+        "config": config_dict(cfg, args.gpus),
+        "effective_gbs": cfg["W"] * cfg["d"] * 4 / (1.0 / value) / 1e9,
+        "bsp": {"iters_s": 1000.0 / ms_bsp * scale, "ms_per_step": ms_bsp / scale, "steps": nb},
         "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": host_info(),
+        "path": "oracle/_ref (unmodified /root/reference/proj/src): apply_step per worker on a thread pool + "
+                "ring_allreduce_avg per group (groups in parallel, run_training's Parallel mode)",
     }
+    if args.config == "c2" and not scaled:
+        out["stock_sync_round_legal_shape"] = stock_legal_shape(cfg, threads)
     print(json.dumps(out))
 
 
-def cpu_baseline(cfg, seconds=12.0, sample_d=1 << 20):
-    """cpu_baseline leg of our arm: the same reference CPU path, bounded."""
-    from oracle.oracle import REF_SO, Reference
-    import ctypes as C
-    from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
+def stock_legal_shape(cfg, threads, steps=3):
+    """The stock reference iteration on the nearest legal shape (C2's
+    rectangular W=8/N=2 is rejected by validate, schedule.cpp:8-24): W=4,
+    N=2 at the same d, apply_step on a thread pool + the reference's own
+    single-threaded sync_round (sync.cpp:268-282)."""
+    c = dict(cfg, W=4, N=2, rect=False)
+    rb = RefBench(c, cfg["d"], threads)
+    try:
+        rb.stock(0, 2)
+        ts = time_ref(rb, lambda t: rb.stock(t, 2), 1, steps)
+    finally:
+        rb.close()
+    ms = 1000.0 * sum(ts) / len(ts)
+    return {"iters_s": 1000.0 / ms, "ms_per_step": ms, "steps": len(ts),
+            "shape": f"W=4 workers, N=2 (legal square shape), d={cfg['d']:,} fp64, {OPT_NAMES[cfg['opt']]}",
+            "note": "stock sync_round + apply_step of the unmodified reference; labelled, not the headline shape"}
+
+
+def cpu_baseline(cfg, seconds=12.0):
+    """cpu_baseline leg of our arm: the same reference CPU path at the full
+    config d when the host can hold it (size-scaled and labelled otherwise),
+    bounded to ~`seconds` of DS iterations after one warm-up iteration."""
+    from oracle.oracle import REF_SO
     if not os.path.exists(REF_SO):
         return {"value": None, "unit": "iters/s", "cores": 0, "kind": "reference", "sample": "oracle/_ref missing"}
-    R = Reference()
-    W, N, d = cfg["W"], cfg["N"], cfg["d"]
     threads = os.cpu_count() or 1
-    ds_ = min(d, sample_d)
-    hp = R.hp_array(weight_decay=cfg["wd"])
-    h = R.lib.ref_bench_create(W, ds_, cfg["opt"], hp.ctypes.data, 1)
-    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
-    tabs = []
-    for p in (0, 1):
-        groups = make_partition(s, p).groups
-        tabs.append((np.array([x for g in groups for x in g], np.int32),
-                     np.cumsum([0] + [len(g) for g in groups]).astype(np.int32), len(groups)))
-    err = C.create_string_buffer(512)
-    n, t0 = 0, time.perf_counter()
-    while True:
-        m, o, ng = tabs[n & 1]
-        R.lib.ref_bench_ds_step(h, n, cfg["alpha"], m.ctypes.data, o.ctypes.data, ng, threads, err, 512)
-        n += 1
-        el = time.perf_counter() - t0
-        if el > seconds and n >= 2:
-            break
-    R.lib.ref_bench_destroy(h)
-    return {"value": n / el * ds_ / d, "unit": "iters/s", "cores": threads, "kind": "reference",
-            "sample": f"{n} DS iterations of W={W} x d={ds_:,} fp64 in {el:.1f} s on {threads} threads "
-                      f"(reference apply_step + ring_allreduce_avg), scaled by {ds_}/{d}"}
+    d = ref_d(cfg)
+    rb = RefBench(cfg, d, threads)
+    try:
+        rb.ds(0)
+        ts = time_ref(rb, rb.ds, 1, 1000, budget_s=seconds)
+    finally:
+        rb.close()
+    el = sum(ts)
+    value = len(ts) / el * d / cfg["d"]
+    if d == cfg["d"]:
+        sample = (f"{len(ts)} DS iterations of the full workload (W={cfg['W']} x d={d:,} fp64) in {el:.1f} s "
+                  f"on {threads} threads (reference apply_step + ring_allreduce_avg)")
+    else:
+        sample = (f"size-scaled (host memory): {len(ts)} DS iterations of W={cfg['W']} x d={d:,} fp64 in "
+                  f"{el:.1f} s on {threads} threads, iters/s scaled by {d}/{cfg['d']}")
+    return {"value": value, "unit": "iters/s", "cores": threads, "kind": "reference", "sample": sample}
 
 
 def cpu_run_training_c1():
@@ -243,18 +348,19 @@ def cpu_run_training_c1():
 
 
 # ---------------------------------------------------------------------------
-def step_bytes(cfg, G, rank, d_pad, path=0):
+def step_bytes(cfg, G, rank, d_pad, path=0, esz=4):
     """Algorithmic bytes one GPU moves per DS / BSP iteration, by kernel kind,
     averaged over the two schedule parities (block / comb iterations).
       group: fused apply_step + fold of local groups, d * bytes_per_elem per
              member (members of spanning groups are stepped inside the push /
              one-shot / chain kernels; only the unfused pull path, path 3,
              steps them in place with the group kernel)
-      fold:  two-shot owner slice L over m members: reads m*L*4, writes m*L*4;
-             the part touching other GPUs' rows crosses NVLink."""
+      fold:  two-shot owner slice L over m members: reads m*L*esz, writes
+             m*L*esz; the part touching other GPUs' rows crosses NVLink.
+      chain: rank-0 outbound rows of its chain roles (partial + mean)."""
     from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
     W, N, d = cfg["W"], cfg["N"], cfg["d"]
-    bpe = BYTES_PER_ELEM[cfg["opt"]]
+    bpe = BYTES_PER_ELEM[cfg["opt"]] * esz // 4
     P = W // G
     mine = set(range(rank * P, (rank + 1) * P))
     out = {"ds": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0},
@@ -266,8 +372,8 @@ def step_bytes(cfg, G, rank, d_pad, path=0):
         # partial row out unless last stage; mean row out if this GPU forwards
         # in the mean pass (last -> g0 -> ... -> g_{S-2})
         S, j = len(gpus), gpus.index(rank)
-        partial = d * 4 if j < S - 1 else 0
-        mean = d * 4 if (j == S - 1 or j < S - 2) else 0
+        partial = d * esz if j < S - 1 else 0
+        mean = d * esz if (j == S - 1 or j < S - 2) else 0
         return partial + mean
 
     for p in (0, 1):
@@ -285,8 +391,8 @@ def step_bytes(cfg, G, rank, d_pad, path=0):
                 continue
             S, j = len(gpus), gpus.index(rank)
             L = (chunks // S + (1 if j < chunks % S else 0)) * 64
-            out["ds"]["fold_hbm"] += 0.5 * 2 * len(here) * L * 4
-            out["ds"]["fold_nvlink"] += 0.5 * 2 * (len(g) - len(here)) * L * 4
+            out["ds"]["fold_hbm"] += 0.5 * 2 * len(here) * L * esz
+            out["ds"]["fold_nvlink"] += 0.5 * 2 * (len(g) - len(here)) * L * esz
     if G == 1:
         out["bsp"]["group"] = W * d * bpe
     elif P >= 2:
@@ -294,8 +400,8 @@ def step_bytes(cfg, G, rank, d_pad, path=0):
         out["bsp"]["group"] = P * d * bpe
     else:
         L = (chunks // G + (1 if rank < chunks % G else 0)) * 64
-        out["bsp"]["fold_hbm"] = (P + 1) * L * 4
-        out["bsp"]["fold_nvlink"] = ((W - P) + (G - 1)) * L * 4
+        out["bsp"]["fold_hbm"] = (P + 1) * L * esz
+        out["bsp"]["fold_nvlink"] = ((W - P) + (G - 1)) * L * esz
         out["bsp"]["group"] = P * d * bpe
     return out
 
@@ -306,7 +412,13 @@ class NcclBaseline:
     pre-sum of this GPU's member rows, one ncclAllReduce per distinct GPU set
     (torch.distributed.new_group -> ncclCommSplit), x 1/m, copy back.
     BSP: local pre-sum of the gradients, world ncclAllReduce, x 1/W, copy into
-    every local gradient row, our apply_step."""
+    every local gradient row, our apply_step.
+
+    Copy-free where the layout allows: the local rows are one strided view
+    of the engine's contiguous [P][row_stride] allocation, so the pre-sum is
+    a single reduction over that view and a group's members are written back
+    with one broadcast copy; a GPU holding exactly one member of every group
+    all-reduces its own row in place."""
 
     def __init__(self, e, cfg, G, rank):
         import torch
@@ -316,9 +428,10 @@ class NcclBaseline:
         self.e, self.cfg, self.G, self.rank = e, cfg, G, rank
         W, N, d = cfg["W"], cfg["N"], cfg["d"]
         P = W // G
-        self.first = rank * P
-        self.rows = {k: self._view(e, BUF_PARAMS, k, d) for k in range(self.first, self.first + P)}
-        self.grads = {k: self._view(e, BUF_GRADS, k, d) for k in range(self.first, self.first + P)}
+        self.P, self.first = P, rank * P
+        stride = e.row_stride
+        self.params = self._view(e, BUF_PARAMS, self.first, P, stride)[:, :d]
+        self.grads = self._view(e, BUF_GRADS, self.first, P, stride)[:, :d]
         s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
         self.plans = []
         comms = {}
@@ -332,73 +445,110 @@ class NcclBaseline:
                 if gpus not in comms:
                     comms[gpus] = dist.new_group(list(gpus)) if len(gpus) > 1 else None
                 if rank in gpus:
-                    plan.append((comms[gpus], len(gpus), groups))
+                    local = [self._rows([m - self.first for m in g if self.first <= m < self.first + P])
+                             for g in groups]
+                    plan.append((comms[gpus], groups, local))
             self.plans.append(plan)
+        self.acc = torch.empty(d, dtype=torch.float32, device="cuda")
         self.torch, self.dist = torch, dist
 
     @staticmethod
-    def _view(e, buf, rank, n):
+    def _rows(idx):
+        """A group's local member rows as a basic slice (a view, no gather):
+        blocks are consecutive rows, combs every N-th row."""
+        if len(idx) == 1:
+            return idx[0]
+        step = idx[1] - idx[0]
+        assert all(b - a == step for a, b in zip(idx, idx[1:])), idx
+        return slice(idx[0], idx[-1] + 1, step)
+
+    @staticmethod
+    def _view(e, buf, first, P, stride):
         import torch
 
         class _A:
             def __init__(self, ptr):
-                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                self.__cuda_array_interface__ = {"shape": (P, stride), "typestr": "<f4", "data": (ptr, False),
                                                  "version": 3}
-        return torch.as_tensor(_A(e.device_ptr(buf, rank)), device="cuda")
+        return torch.as_tensor(_A(e.device_ptr(buf, first)), device="cuda")
 
     def ds_step(self, t, alpha):
         torch, dist = self.torch, self.dist
         self.e.apply_step(alpha, check=False)
-        for comm, S, groups in self.plans[t & 1]:
-            local = [[m for m in g if m in self.rows] for g in groups]
-            sums = torch.stack([torch.stack([self.rows[m] for m in lg]).sum(0) for lg in local])
-            if comm is not None:
-                dist.all_reduce(sums, group=comm)
-            for lg, g, v in zip(local, groups, sums):
-                v.mul_(1.0 / len(g))
-                for m in lg:
-                    self.rows[m].copy_(v)
+        for comm, groups, local in self.plans[t & 1]:
+            for g, lg in zip(groups, local):
+                if isinstance(lg, int):  # one member here: all-reduce its row in place
+                    rows = self.params[lg]
+                else:  # several: one strided reduction into the accumulator
+                    torch.sum(self.params[lg], dim=0, out=self.acc)
+                    rows = self.acc
+                if comm is not None:
+                    dist.all_reduce(rows, group=comm)
+                rows.mul_(1.0 / len(g))
+                if not isinstance(lg, int):
+                    dst = self.params[lg]
+                    dst.copy_(rows.expand_as(dst))  # one broadcast copy into every local member
+        return None
 
     def bsp_step(self, t, alpha):
         torch, dist = self.torch, self.dist
-        acc = torch.stack(list(self.grads.values())).sum(0)
-        dist.all_reduce(acc)
-        acc.mul_(1.0 / self.cfg["W"])
-        for g in self.grads.values():
-            g.copy_(acc)
+        torch.sum(self.grads, dim=0, out=self.acc)
+        dist.all_reduce(self.acc)
+        self.acc.mul_(1.0 / self.cfg["W"])
+        self.grads.copy_(self.acc.expand_as(self.grads))
         self.e.apply_step(alpha, check=False)
 
 
-def our_arm(args, cfg):
+def dominant_roofline(kinds_rows, ms_step, peak, peak_kind, G):
+    """Roofline of the kernel with the most time in the step.  HBM kernels
+    (group / bsp) against the measured copy peak; cross-GPU kernels (fold =
+    push / pull two-shot and one-shot, chain = the ordered chain's partial +
+    mean passes) against the measured NVLink peer-copy peak per direction."""
+    cand = {}
+    for k, v in kinds_rows.items():
+        if k in ("group", "bsp") and v.get("alg_bytes_per_step"):
+            cand[k] = ("hbm", v["ms_per_step"], v["launches_per_step"], v["alg_bytes_per_step"])
+        elif k == "fold" and v.get("nvlink_bytes_per_step"):
+            cand[k] = ("nvlink", v["ms_per_step"], v["launches_per_step"], v["nvlink_bytes_per_step"])
+        elif k == "chain" and v.get("nvlink_bytes_per_step"):
+            both = v["ms_per_step"] + kinds_rows.get("chain_mean", {}).get("ms_per_step", 0.0)
+            cand[k] = ("nvlink", both, v["launches_per_step"], v["nvlink_bytes_per_step"])
+    if not cand:
+        return None
+    k, (bound, ms_, n_, b_) = max(cand.items(), key=lambda kv: kv[1][1])
+    per_ms, per_b = ms_ / n_, b_ / n_
+    ach = per_b / (per_ms / 1e3) / 1e9 if per_ms else None
+    names = {"group": "ds_group_kernel (fused apply_step + ordered fold + broadcast)",
+             "bsp": "bsp_kernel (fused ordered gradient fold + step)",
+             "fold": "push_twoshot / one-shot / fold_kernel (fused step + ordered fold over NVLink peers)",
+             "chain": "chain_partial_kernel + chain_mean_kernel (ordered chain fold with the step fused)"}
+    pk = peak if bound == "hbm" else NVLINK_PEAK
+    r = {"bound": bound, "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk if ach else None,
+         "traffic": None, "peak_kind": peak_kind if bound == "hbm" else
+         "measured NVLink peer copy per direction (B200_PROFILING.md); 900 GB/s nominal",
+         "kernel": names.get(k, k), "kind": k, "avg_launch_ms": per_ms, "alg_bytes_per_launch": per_b,
+         "share_of_step": ms_ / ms_step if ms_step else None}
+    if bound == "nvlink" and ach:
+        r["frac_of_nominal_900"] = ach / 900.0
+    return r
+
+
+def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False):
+    """DS + BSP iterations of one config on this rank's engine(s).  Returns
+    the per-rank measurements (times already max-over-ranks)."""
     import torch
     import torch.distributed as dist
-    from paper_2007_03298_b200 import (BUF_GRADS, BUF_PARAMS, DsSyncEngine, OptimizerHyperparams, OptimizerKind,
+    from paper_2007_03298_b200 import (BUF_GRADS, DsSyncEngine, OptimizerHyperparams, OptimizerKind,
                                        StrategyKind, SyncStrategy, Topology, WorldConfig)
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    G = args.gpus
-    if world != G:
-        raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if G > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     W, N, d = cfg["W"], cfg["N"], cfg["d"]
-    if W % G:
-        raise SystemExit(f"W={W} not divisible by {G} GPUs")
     P = W // G
-    d_pad = (d + 63) // 64 * 64
-    peak, peak_kind = load_peaks()
+    esz = 8 if dtype == "f64" else 4
     hp = OptimizerHyperparams(weight_decay=cfg["wd"])
-    # one dedicated stream for the engine, torch's events and NCCL plumbing
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
 
     def make(kind):
         s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W), 1,
                          cfg["rect"] and kind == StrategyKind.DS_SYNC)
-        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, "f32", local, rank, G, path=args.path)
+        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, dtype, local, rank, G, path=args.path)
         e.set_stream(stream.cuda_stream)
         if G > 1:
             from paper_2007_03298_b200.dist import attach
@@ -431,7 +581,7 @@ def our_arm(args, cfg):
         return max_over_ranks(a.elapsed_time(b)) / K
 
     res = {}
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local) if full else None
     for kind, name in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
         e = make(kind)
         l0 = e.launch_count
@@ -440,11 +590,11 @@ def our_arm(args, cfg):
         for t in range(args.warmup):
             step(t)
         e.check()
-        if name == "ds":
+        if clocks and name == "ds":
             clocks.start()
             tc0 = time.time()
         ms = timed(step, args.warmup, args.steps, batched=steps)
-        if name == "ds":
+        if clocks and name == "ds":
             res["clocks"] = clocks.stop(tc0, time.time())
         launches = (e.launch_count - l0) / (args.warmup + args.steps)
         # second pass: every hot kernel bracketed by events on its stream
@@ -455,42 +605,35 @@ def our_arm(args, cfg):
         e.check()
         res[name] = dict(ms=ms, kinds={k: (v[0] / args.steps, v[1] / args.steps) for k, v in kinds.items()},
                          launches_per_step=launches)
-        if name == "ds":
+        host_gb = (host_info()["mem_available_gb"] or 64.0) * 1e9
+        if name == "ds" and not args.no_e2e and 2 * P * d * esz * G > 0.5 * host_gb:
+            res["e2e_skipped"] = (f"pinned host buffers of {2 * P * d * esz * G / 1e9:.0f} GB across the ranks "
+                                  f"exceed half of the host's {host_gb / 1e9:.0f} GB")
+        elif name == "ds" and not args.no_e2e:
             # e2e through the C-ABI with host buffers: pinned H2D of every
-            # local worker's gradient, the step, D2H of every worker's params.
-            K2 = max(3, min(args.steps, args.e2e_steps if P * d * 4 > (1 << 20) else args.steps))
-            if P * d * 4 <= 2e9:
-                hg = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
-                hw = torch.empty((P, d), dtype=torch.float32, pin_memory=True)
-                e.download_all(BUF_GRADS, hg)
+            # local worker's gradient, the step, D2H of every worker's params
+            # (dss_step_host: copies on two copy streams, the D2H of step t
+            # overlapping the H2D of step t+1)
+            big = P * d * esz > (1 << 30)
+            K2 = max(3, min(args.steps, args.e2e_steps if big else args.steps))
+            if big:
+                K2 = min(K2, 5)
+            tdt = torch.float64 if dtype == "f64" else torch.float32
+            hg = torch.empty((P, d), dtype=tdt, pin_memory=True)
+            hw = torch.empty((P, d), dtype=tdt, pin_memory=True)
+            e.download_all(BUF_GRADS, hg)
 
-                def e2e(t):
-                    # dss_step_host: grads H2D on a copy stream, the step,
-                    # params D2H from a device snapshot on another copy
-                    # stream, overlapping the next iteration's H2D
-                    e.step_host(t, cfg["alpha"], hg, hw)
-            else:
-                # large rows: stream every worker row through one pinned
-                # staging row (same bytes per step, bounded host memory)
-                hrow = np.empty(d, dtype=np.float32)
-                hrow_t = torch.from_numpy(hrow).pin_memory()
-                first = rank * P
-
-                def e2e(t):
-                    for k in range(first, first + P):
-                        e._ck(e.lib.dss_upload(e.h, BUF_GRADS, k, hrow_t.data_ptr(), d))
-                    e.step(t, cfg["alpha"])
-                    for k in range(first, first + P):
-                        e._ck(e.lib.dss_download(e.h, BUF_PARAMS, k, hrow_t.data_ptr(), d))
             def e2e_run(k0, K):
                 for t in range(k0, k0 + K):
-                    e2e(t)
+                    e.step_host(t, cfg["alpha"], hg, hw)
                 e.host_sync()  # the last iteration's params are on the host
             t_e2e = args.warmup + 2 * args.steps
-            e2e_run(t_e2e, args.warmup)  # first call sets up the copy streams and the snapshot row
-            res["e2e_ms"] = timed(e2e, t_e2e + args.warmup, K2, batched=e2e_run)
+            e2e_run(t_e2e, 1 if big else args.warmup)  # sets up the copy streams and the snapshot rows
+            res["e2e_ms"] = timed(None, t_e2e + args.warmup, K2, batched=e2e_run)
+            res["e2e_steps"] = K2
             e.check()
-        if G > 1 and not args.no_nccl:
+            del hg, hw
+        if G > 1 and with_nccl:
             nb = NcclBaseline(e, cfg, G, rank)
             fn = (lambda t: nb.ds_step(t, cfg["alpha"])) if name == "ds" else (lambda t: nb.bsp_step(t, cfg["alpha"]))
             for t in range(3):
@@ -500,33 +643,19 @@ def our_arm(args, cfg):
         e.close()
         del e
         torch.cuda.synchronize()
+    d_pad = (d + 63) // 64 * 64
+    res["bytes"] = step_bytes(cfg, G, rank, d_pad, args.path, esz)
+    return res
 
-    if cfg.get("logistic") and G == 1:
-        # C1 end to end on the device: batch sampling + logistic gradient
-        # (fp64 inside, f32 rows) + the DS step, nothing from the host but
-        # the learning rates (acceptance.cpp:239-258 data: d=20, M=2000)
-        from paper_2007_03298_b200 import logistic_dataset
-        x, y = logistic_dataset(11, d, 2000)
-        e = make(StrategyKind.DS_SYNC)
-        e.logistic_setup(x, y, 0.05, 8, 0, 1)
-        alphas = np.full(args.steps, cfg["alpha"])
-        e.logistic_steps(0, alphas[:args.warmup])
-        ms = timed(None, args.warmup, args.steps, batched=lambda k0, K: e.logistic_steps(k0, alphas[:K]))
-        e.check()
-        res["logistic"] = ms
-        e.close()
-        del e
-    if G > 1:
-        dist.barrier()
-    nb_bytes = step_bytes(cfg, G, rank, d_pad, args.path)
-    if rank != 0:
-        if G > 1:
-            dist.destroy_process_group()
-        return
 
+def summarize(args, cfg, dtype, G, res, peak, peak_kind):
+    """The result object of one config (rank 0)."""
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    P = W // G
+    esz = 8 if dtype == "f64" else 4
     ds, bsp = res["ds"], res["bsp"]
-    ipsec = 1000.0 / ds["ms"]
-    bpe = BYTES_PER_ELEM[cfg["opt"]]
+    nb_bytes = res["bytes"]
+    bpe = BYTES_PER_ELEM[cfg["opt"]] * esz // 4
 
     def kernel_rows(r, key):
         rows = {}
@@ -544,8 +673,6 @@ def our_arm(args, cfg):
             elif k == "chain_mean":
                 row.update(note="mean pass of the chain (rank 0); its NVLink bytes are counted under chain")
             elif k == "chain":
-                # rank-0 outbound NVLink bytes of its chain roles (per-direction
-                # link load) over both passes' time
                 both = ms_ + r["kinds"].get("chain_mean", (0.0, 0))[0]
                 row.update(nvlink_bytes_per_step=nb_bytes[key]["chain_nvlink"],
                            nvlink_gbs=nb_bytes[key]["chain_nvlink"] / (both / 1e3) / 1e9 if both else None)
@@ -553,106 +680,177 @@ def our_arm(args, cfg):
         return rows
 
     ds_k = kernel_rows(ds, "ds")
-    # HBM roofline: the HBM-bound kernel with the most time (at N > 1 the
-    # cross-GPU fold kernels are reported against NVLink in "nvlink")
-    hbm_k = {k: v for k, v in ds_k.items() if v.get("alg_bytes_per_step") and k in ("group", "bsp")} or ds_k
-    dom = max(hbm_k.items(), key=lambda kv: kv[1]["ms_per_step"])
-    # dominant kernel: its algorithmic bytes per launch / its mean launch time
-    dk, dv = dom
-    per_launch_ms = dv["ms_per_step"] / dv["launches_per_step"]
-    per_launch_bytes = dv.get("alg_bytes_per_step", 0.0) / dv["launches_per_step"]
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms else None
+    roof = dominant_roofline(ds_k, ds["ms"], peak, peak_kind, G)
+    # the HBM kernel is always reported too (at N > 1 it may not dominate)
+    hbm = dominant_roofline({k: v for k, v in ds_k.items() if k in ("group", "bsp")}, ds["ms"], peak, peak_kind, G)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and roof:
         try:
-            tr = json.load(open(prof)).get(f"{args.config}_g{G}")
-            traffic = tr["bytes_per_launch"] if tr else None
+            tr = json.load(open(prof)).get(f"{cfg.get('key', args.config)}{'_f64' if esz == 8 else ''}_g{G}")
+            if tr and tr.get("kind", "group") == roof.get("kind"):
+                traffic = tr["bytes_per_launch"]
         except Exception:
             traffic = None
+    if roof:
+        roof["traffic"] = traffic
+        if roof["bound"] == "hbm" and roof["achieved"] and roof["achieved"] > peak:
+            roof["note"] = (f"above the copy peak: the group kernel reads 2+ bytes per byte written (the peak "
+                            f"is a 1:1 copy); {P * d * esz / 1e6:.0f} MB per array per GPU against 126 MB of L2")
     out = {
-        "metric": METRIC,
-        "value": ipsec,
-        "unit": "iters/s",
-        "n_gpus": G,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ds["ms"],
-        "higher_is_better": True,
-        "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic: isotropic-quadratic gradients (SplitMix64/Box-Muller, seeds 7/1), device-resident",
-        "config": {"workload": cfg["desc"], "W": W, "N": N, "d": d, "optimizer": OPT_NAMES[cfg["opt"]],
-                   "rectangular": cfg["rect"], "workers_per_gpu": P, "parallelism": f"dp{G} (W/G workers per GPU)",
-                   "fold_path": {0: "auto", 2: "chain"}.get(args.path, args.path),
-                   "l2": f"inputs larger than L2: {P * d * 4 / 1e6:.0f} MB per array per GPU"
-                         if P * d * 4 > 126e6 else "inputs smaller than L2 (latency-bound config)"},
-        "effective_gbs": W * d * 4 / (ds["ms"] / 1e3) / 1e9,
-        "hbm_gbs_algorithmic": W * d * bpe / (ds["ms"] / 1e3) / 1e9,
+        "value": 1000.0 / ds["ms"], "unit": "iters/s", "ms_per_step": ds["ms"], "dtype": dtype,
+        "config": config_dict(cfg, G),
+        "effective_gbs": W * d * esz / (ds["ms"] / 1e3) / 1e9,
+        "hbm_gbs_algorithmic": W * d * bpe / G / (ds["ms"] / 1e3) / 1e9,
         "bsp": {"iters_s": 1000.0 / bsp["ms"], "ms_per_step": bsp["ms"],
-                "effective_gbs": W * d * 4 / (bsp["ms"] / 1e3) / 1e9, "ds_speedup_over_bsp": bsp["ms"] / ds["ms"],
+                "effective_gbs": W * d * esz / (bsp["ms"] / 1e3) / 1e9, "ds_speedup_over_bsp": bsp["ms"] / ds["ms"],
                 "kernels": kernel_rows(bsp, "bsp")},
         "kernels": ds_k,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": {"group": "ds_group_kernel (fused apply_step + ordered fold + broadcast)",
-                                "fold": "fold_kernel (two-shot ordered fold over NVLink peers)",
-                                "bsp": "bsp_kernel", "barrier": "barrier_kernel"}.get(dk, dk),
-                     "avg_launch_ms": per_launch_ms, "alg_bytes_per_launch": per_launch_bytes,
-                     "share_of_step": dv["ms_per_step"] / ds["ms"] if ds["ms"] else None},
+        "roofline": roof,
         "gpu_launches": int(round(ds["launches_per_step"] * args.steps)),
-        "clocks": res.get("clocks"),
-        "e2e": {"value": 1000.0 / res["e2e_ms"], "unit": "iters/s", "h2d_bytes_per_step": P * d * 4 * G,
-                "d2h_bytes_per_step": P * d * 4 * G,
-                "path": "C-ABI dss_step_host: pinned grads H2D + step + params D2H every step (copies on two "
-                        "copy streams, D2H of step t overlapping H2D of step t+1)" if P * d * 4 <= 2e9 else
-                        "C-ABI dss_upload/dss_step/dss_download per row through one pinned staging row"},
     }
-    if achieved and peak and achieved > peak:
-        # the peak is a 1:1 read:write copy; the group kernel's mix is
-        # read-heavy (SGD 2:1), and at N > 1 a GPU's rows are a small multiple
-        # of L2, so some of the previous launch's stores are still L2 hits
-        out["roofline"]["note"] = (f"above the copy peak: the group kernel reads 2+ bytes per byte written "
-                                   f"(the peak is a 1:1 copy); {P * d * 4 / 1e6:.0f} MB per array per GPU "
-                                   f"against 126 MB of L2")
-    for kk, note in (("fold", "rank-0 two-shot kernel: remote reads + remote writes per owned slice (= per-direction "
-                               "link bytes in a symmetric fold) / kernel time"),
-                     ("chain", "rank-0 chain kernels: outbound partial + mean rows of its chain roles / kernel time "
-                               "(includes the fused optimizer step)")):
-        if kk in ds_k and ds_k[kk].get("nvlink_gbs"):
-            out.setdefault("nvlink", {"achieved": ds_k[kk]["nvlink_gbs"], "peak": 770.0, "unit": "GB/s",
-                                      "frac": ds_k[kk]["nvlink_gbs"] / 770.0, "kernel": kk,
-                                      "peak_kind": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
-                                      "note": note})
-    if G > 1 and "nccl_ds" in res:
+    if hbm and roof and hbm.get("kind") != roof.get("kind"):
+        out["roofline_hbm_kernel"] = hbm
+    if "e2e_ms" in res:
+        out["e2e"] = {"value": 1000.0 / res["e2e_ms"], "unit": "iters/s", "h2d_bytes_per_step": P * d * esz * G,
+                      "d2h_bytes_per_step": P * d * esz * G, "steps": res["e2e_steps"],
+                      "path": "C-ABI dss_step_host: pinned grads H2D + step + params D2H every step (copies on two "
+                              "copy streams, D2H of step t overlapping H2D of step t+1)"}
+    elif "e2e_skipped" in res:
+        out["e2e"] = {"value": None, "unit": "iters/s", "skipped": res["e2e_skipped"]}
+    if "nccl_ds" in res:
         out["nccl_baselines"] = {
             "ds_split_allreduce": {"iters_s": 1000.0 / res["nccl_ds"], "ms_per_step": res["nccl_ds"]},
             "bsp_world_allreduce": {"iters_s": 1000.0 / res["nccl_bsp"], "ms_per_step": res["nccl_bsp"]},
             "note": "torch.distributed NCCL (ncclCommSplit sub-communicators); tolerance-parity only"}
-    if "logistic" in res:
+    return out
+
+
+def extras_for(args, G):
+    if args.extras == "none":
+        return []
+    if args.extras != "auto":
+        return [x for x in args.extras.split(",") if x]
+    if args.config != "c2":
+        return []
+    return ["c3", "c4slice", "c2f64"] if G == 1 else (["c3", "c4"] if G >= 4 else ["c3"])
+
+
+def our_arm(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    G = args.gpus
+    if world != G:
+        raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if cfg["W"] % G:
+        raise SystemExit(f"W={cfg['W']} not divisible by {G} GPUs")
+    peak, peak_kind = load_peaks()
+    # one dedicated stream for the engine, torch's events and NCCL plumbing
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+
+    res = measure(args, cfg, "f32", G, rank, local, stream, full=True, with_nccl=not args.no_nccl)
+    logistic_ms = None
+    if cfg.get("logistic") and G == 1:
+        logistic_ms = logistic_run(args, cfg, local, stream)
+    extra_res = {}
+    for name in extras_for(args, G):
+        key, dtype = (name[:-3], "f64") if name.endswith("f64") else (name, "f32")
+        c = dict(CONFIGS[key], key=key)
+        if c["W"] % G:
+            continue
+        extra_res[name] = (c, dtype, measure(args, c, dtype, G, rank, local, stream, full=False))
+    if G > 1:
+        dist.barrier()
+    if rank != 0:
+        if G > 1:
+            dist.destroy_process_group()
+        return
+
+    head = summarize(args, dict(cfg, key=args.config), "f32", G, res, peak, peak_kind)
+    out = {"metric": METRIC, "value": head["value"], "unit": "iters/s", "n_gpus": G, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic: isotropic-quadratic gradients (SplitMix64/Box-Muller, seeds 7/1), device-resident",
+           "config": head["config"]}
+    if args.path:
+        out["fold_path"] = {2: "chain forced for every spanning group", 3: "unfused pull two-shot"}.get(
+            args.path, args.path)
+    for k in ("effective_gbs", "hbm_gbs_algorithmic", "bsp", "kernels", "roofline", "roofline_hbm_kernel",
+              "gpu_launches", "e2e", "nccl_baselines"):
+        if k in head:
+            out[k] = head[k]
+    out["clocks"] = res.get("clocks")
+    if logistic_ms is not None:
         out["device_gradient_run"] = {
-            "iters_s": 1000.0 / res["logistic"], "ms_per_step": res["logistic"],
+            "iters_s": 1000.0 / logistic_ms, "ms_per_step": logistic_ms,
             "note": "DS iterations with the logistic batch sampled and the gradient computed on the device "
                     "(dss_logistic_steps: one launch for the whole batch of iterations; no trace)"}
         if not args.no_cpu_baseline:
             out["device_gradient_run"]["cpu_reference_run_training"] = cpu_run_training_c1()
+    if extra_res:
+        out["configs"] = {}
+        for name, (c, dtype, r) in extra_res.items():
+            s = summarize(args, c, dtype, G, r, peak, peak_kind)
+            if G == 1 and not args.no_cpu_baseline and dtype == "f32":
+                s["cpu_baseline"] = cpu_baseline(c, seconds=8.0)
+            out["configs"][name] = s
+            out["gpu_launches"] += s["gpu_launches"]
     if G == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg)
+        if "configs" in out and "c2f64" in out["configs"]:
+            out["configs"]["c2f64"]["cpu_baseline"] = dict(out["cpu_baseline"], note="same reference run as the "
+                                                           "headline: the reference is fp64")
+        out["host"] = host_info()
     print(json.dumps(out))
     if G > 1:
         dist.destroy_process_group()
 
 
+def logistic_run(args, cfg, local, stream):
+    """C1 end to end on the device: batch sampling + logistic gradient (fp64
+    inside, f32 rows) + the DS step, nothing from the host but the learning
+    rates (acceptance.cpp:239-258 data: d=20, M=2000)."""
+    import torch
+    from paper_2007_03298_b200 import (DsSyncEngine, OptimizerHyperparams, OptimizerKind, StrategyKind,
+                                       SyncStrategy, Topology, WorldConfig, logistic_dataset)
+    W, N, d = cfg["W"], cfg["N"], cfg["d"]
+    x, y = logistic_dataset(11, d, 2000)
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N))
+    e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, OptimizerHyperparams(), "f32", local)
+    e.set_stream(stream.cuda_stream)
+    e.logistic_setup(x, y, 0.05, 8, 0, 1)
+    alphas = np.full(args.steps, cfg["alpha"])
+    e.logistic_steps(0, alphas[:args.warmup])
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    e.logistic_steps(args.warmup, alphas)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e.check()
+    e.close()
+    return a.elapsed_time(b) / args.steps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=1 << 19)
+    ap.add_argument("--extras", default="auto",
+                    help="comma list of extra configs (c3, c4, c4slice, c2f64, ...), 'auto' or 'none'")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--d", type=int, default=None, help="override the config's d (profiling runs)")

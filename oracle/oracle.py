@@ -186,7 +186,11 @@ class Reference:
         L.ref_mlp_run.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, _P, C.c_double,
                                                   _P, _P, _P, _P, _P, _P, C.POINTER(C.c_int)] + E
         L.ref_bench_create.restype = _P
-        L.ref_bench_create.argtypes = [C.c_int, C.c_long, C.c_int, _P, C.c_uint64]
+        L.ref_bench_create.argtypes = [C.c_int, C.c_long, C.c_int, _P, C.c_uint64, C.c_int]
+        L.ref_bench_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_long, _P, _P, C.POINTER(C.c_int)] + E
+        L.ref_bench_stock_step.argtypes = [_P, C.c_int, C.c_long, C.c_double, C.c_int] + E
+        L.ref_bench_bytes.restype = C.c_long
+        L.ref_bench_bytes.argtypes = [_P]
         L.ref_bench_destroy.argtypes = [_P]
         L.ref_bench_ds_step.argtypes = [_P, C.c_long, C.c_double, _P, _P, C.c_int, C.c_int] + E
         L.ref_bench_bsp_step.argtypes = [_P, C.c_long, C.c_double, C.c_int] + E

@@ -8,6 +8,7 @@
 // (namespace dssync): make_partition, group_of, check_mixing, validate,
 // apply_step, sync_round, run_training, ring/tree/ps_allreduce_avg,
 // make_problem, make_shards, Rng.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -707,22 +708,31 @@ struct RefBench {
   long d = 0;
 };
 
-void* ref_bench_create(int W, long d, int opt, const double* hp, uint64_t seed) {
+void* ref_bench_create(int W, long d, int opt, const double* hp, uint64_t seed, int threads) {
+  // Synthetic O(1) inputs from counter-addressed reference Rng streams, so
+  // they can be generated on every host thread: the common start w0 in
+  // 1M-element chunks, each worker's gradient from its own stream.
   auto* b = new RefBench;
   b->d = d;
   b->ws.resize(static_cast<size_t>(W));
   b->grads.resize(static_cast<size_t>(W));
-  Rng r(seed);
+  const long chunk = 1L << 20;
   ParamVector w0(static_cast<size_t>(d));
-  for (auto& x : w0) x = r.gaussian();
-  for (int k = 0; k < W; ++k) {
-    b->ws[static_cast<size_t>(k)].rank = k;
-    b->ws[static_cast<size_t>(k)].params = w0;
-    b->ws[static_cast<size_t>(k)].opt = make_opt(opt, hp, 0.0);
+  parallel_for(static_cast<size_t>((d + chunk - 1) / chunk), threads, [&](size_t c) {
+    Rng r = Rng::for_stream(seed, streams::kInitParams, c, 0);
+    const long hi = std::min(d, static_cast<long>(c + 1) * chunk);
+    for (long i = static_cast<long>(c) * chunk; i < hi; ++i) w0[static_cast<size_t>(i)] = r.gaussian();
+  });
+  parallel_for(static_cast<size_t>(W), threads, [&](size_t k) {
+    WorkerState& x = b->ws[k];
+    x.rank = static_cast<int>(k);
+    x.params = w0;
+    x.opt = make_opt(opt, hp, 0.0);
+    Rng r = Rng::for_stream(seed, streams::kGradientNoise, k, 0);
     ParamVector g(static_cast<size_t>(d));
-    for (auto& x : g) x = 0.01 * r.gaussian();
-    b->grads[static_cast<size_t>(k)] = std::move(g);
-  }
+    for (auto& v : g) v = 0.01 * r.gaussian();
+    b->grads[k] = std::move(g);
+  });
   return b;
 }
 
@@ -758,6 +768,63 @@ int ref_bench_bsp_step(void* h, long t, double alpha, int threads, char* err, in
     AllReduceResult red = ring_allreduce_avg(members, b->grads);
     parallel_for(b->ws.size(), threads, [&](size_t k) { local_step(b->ws[k], red.values[k], alpha, t); });
   });
+}
+
+// The group table the reference bench arm uses, built without the product
+// library.  Legal shapes (W = N*N or N = W) come from the reference's own
+// make_partition (schedule.cpp:31-54).  The rectangular C2/C3 shapes
+// (W = N*K) are rejected by the reference's validate (schedule.cpp:8-24);
+// for them this applies the builder's documented extension of
+// schedule.cpp:49, g(x) = t even ? x / N : x % N, which reduces to the
+// reference's rule when K = N.  Returns 1 for shapes neither rule covers.
+int ref_bench_partition(int W, int N, int rect, long t, int* members, int* offsets, int* n_groups, char* err,
+                        int errlen) {
+  bool legal = true;
+  try {
+    validate(WorldConfig{W, N});
+  } catch (const std::invalid_argument&) {
+    legal = false;
+  }
+  if (legal) return ref_make_partition(W, N, t, members, offsets, n_groups, err, errlen);
+  if (!rect || N <= 0 || W % N != 0 || t < 0) {
+    put(err, errlen, "ref_bench_partition: shape is neither legal nor rectangular");
+    return 1;
+  }
+  const int K = W / N;
+  const int ng = (t % 2 == 0) ? K : N;
+  int pos = 0;
+  offsets[0] = 0;
+  for (int g = 0; g < ng; ++g) {
+    for (int x = 0; x < W; ++x) {
+      if (((t % 2 == 0) ? x / N : x % N) == g) members[pos++] = x;
+    }
+    offsets[g + 1] = pos;
+  }
+  *n_groups = ng;
+  return 0;
+}
+
+// The stock reference iteration on a legal shape: apply_step for every
+// worker (threaded, like run_training's Parallel mode, sync.cpp:348-362)
+// followed by the reference's own sync_round (sync.cpp:268-282), which
+// syncs the groups one after another on the calling thread.
+int ref_bench_stock_step(void* h, int N, long t, double alpha, int threads, char* err, int errlen) {
+  auto* b = static_cast<RefBench*>(h);
+  return guarded(err, errlen, nullptr, nullptr, [&] {
+    parallel_for(b->ws.size(), threads, [&](size_t k) { local_step(b->ws[k], b->grads[k], alpha, t); });
+    sync_round(b->ws, make_strategy(1, 0, static_cast<int>(b->ws.size()), N, 1), t);
+  });
+}
+
+// Host memory the bench holds (params + grads + optimizer moments), bytes.
+long ref_bench_bytes(void* h) {
+  auto* b = static_cast<RefBench*>(h);
+  long n = 0;
+  for (size_t k = 0; k < b->ws.size(); ++k) {
+    n += static_cast<long>(b->ws[k].params.size() + b->grads[k].size() + b->ws[k].opt.first_moment.size() +
+                           b->ws[k].opt.second_moment.size());
+  }
+  return n * static_cast<long>(sizeof(double));
 }
 
 }  // extern "C"

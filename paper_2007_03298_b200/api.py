@@ -176,7 +176,8 @@ def iteration_trace(engine: "DsSyncEngine", t: int, outcome: SyncRoundOutcome, m
     for x in losses:  # sync.cpp:582-584: ascending sum, then a division
         acc += float(x)
     W = engine.strategy.world.world_size
-    payload = data_size if data_size > 0.0 else 8.0 * engine.dim  # sync.cpp:314-318
+    # sync.cpp:314-318: the default payload is params ++ running stats, 8 B each
+    payload = data_size if data_size > 0.0 else 8.0 * (engine.dim + engine.stats_dim)
     bw = bandwidth
     if engine.strategy.topology == Topology.PS:  # effective_bandwidth (sync.cpp:215-221)
         bw = bandwidth * engine.strategy.num_servers / W
@@ -402,6 +403,28 @@ class DsSyncEngine:
     def _arr(self, x) -> np.ndarray:
         return np.ascontiguousarray(x, dtype=self.dtype)
 
+    def _host_ptr(self, x, shape, what: str) -> int:
+        """Address of a host buffer the library reads or writes in full.
+        The C side copies prod(shape) elements of the engine's dtype, so the
+        buffer must be exactly that: right shape, right dtype, C-contiguous."""
+        if isinstance(x, np.ndarray):
+            ok = x.shape == tuple(shape) and x.dtype == self.dtype and x.flags["C_CONTIGUOUS"]
+            got = f"{x.dtype}{list(x.shape)}"
+            ptr = x.ctypes.data
+        elif hasattr(x, "data_ptr"):  # torch tensor (pinned host memory makes copies asynchronous)
+            import torch
+            want = torch.float64 if self.dtype == np.float64 else torch.float32
+            ok = (tuple(x.shape) == tuple(shape) and x.dtype == want and x.is_contiguous()
+                  and x.device.type == "cpu")
+            got = f"{x.dtype}{list(x.shape)} on {x.device}"
+            ptr = x.data_ptr()
+        else:
+            raise TypeError(f"{what}: expected a numpy array or a torch tensor")
+        if not ok:
+            raise ValueError(f"{what}: need a C-contiguous host {np.dtype(self.dtype).name}{list(shape)} "
+                             f"buffer, got {got}")
+        return ptr
+
     def upload(self, buffer: int, rank: int, host) -> None:
         a = self._arr(host)
         self._ck(self.lib.dss_upload(self.h, buffer, rank, a.ctypes.data, a.size))
@@ -417,24 +440,23 @@ class DsSyncEngine:
 
     def upload_all(self, buffer: int, host) -> None:
         """host: [local_workers, row length] (pinned memory makes this asynchronous)."""
+        shape = (self.local_workers, self._len(buffer))
         if isinstance(host, np.ndarray):
-            a = self._arr(host)
-            assert a.shape == (self.local_workers, self._len(buffer))
-            self._keep = a
-            ptr = a.ctypes.data
-        else:  # any object exposing data_ptr() (e.g. a pinned torch tensor)
-            ptr = host.data_ptr()
-        self._ck(self.lib.dss_upload_all(self.h, buffer, ptr))
+            host = self._arr(host)
+            self._keep = host  # the copy may still be in flight when this returns
+        self._ck(self.lib.dss_upload_all(self.h, buffer, self._host_ptr(host, shape, "upload_all")))
 
     def download_all(self, buffer: int, out=None) -> np.ndarray:
+        shape = (self.local_workers, self._len(buffer))
         if out is None:
-            out = np.empty((self.local_workers, self._len(buffer)), dtype=self.dtype)
-        ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
-        self._ck(self.lib.dss_download_all(self.h, buffer, ptr))
+            out = np.empty(shape, dtype=self.dtype)
+        self._ck(self.lib.dss_download_all(self.h, buffer, self._host_ptr(out, shape, "download_all")))
         return out
 
     def broadcast_row(self, buffer: int, row) -> None:
         a = self._arr(row)
+        if a.shape != (self._len(buffer),):
+            raise ValueError(f"broadcast_row: need a row of {self._len(buffer)} elements, got shape {a.shape}")
         self._ck(self.lib.dss_broadcast_row(self.h, buffer, a.ctypes.data))
 
     def device_ptr(self, buffer: int, rank: int) -> int:
@@ -473,8 +495,9 @@ class DsSyncEngine:
         """dss_step_host: one iteration fed from / returned to pinned host
         buffers ([local_workers, dim]), copies pipelined across calls; the
         previous call's host_params are complete when this returns."""
-        gp = host_grads.ctypes.data if isinstance(host_grads, np.ndarray) else host_grads.data_ptr()
-        pp = host_params.ctypes.data if isinstance(host_params, np.ndarray) else host_params.data_ptr()
+        shape = (self.local_workers, self.dim)
+        gp = self._host_ptr(host_grads, shape, "step_host grads")
+        pp = self._host_ptr(host_params, shape, "step_host params")
         self._ck(self.lib.dss_step_host(self.h, t, alpha, C.c_void_p(gp), C.c_void_p(pp)))
 
     def host_sync(self) -> None:
