@@ -26,6 +26,9 @@ constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel param
 #ifndef DSS_MIN_BLOCKS_M8_MOMENTUM
 #define DSS_MIN_BLOCKS_M8_MOMENTUM 1
 #endif
+#ifndef DSS_MIN_BLOCKS_M8_ADAM
+#define DSS_MIN_BLOCKS_M8_ADAM DSS_MIN_BLOCKS
+#endif
 // Single-GPU worlds of at most this many bytes per state array run a whole
 // dss_steps batch in one launch (a resident grid with a barrier between
 // iterations above 32 KB) instead of one launch per iteration.  Measured
@@ -182,6 +185,19 @@ __device__ __forceinline__ T step_elem(T w, T g, T& m1, T& m2, const StepConsts<
     if constexpr (OPT == kAdamW) out = sub_(out, mul_(c.awd, w));
     return out;
   }
+}
+
+// apply_step over one 16-B vector of one worker (optim.cpp:56-91 per
+// element).  A branch-free fp32 Adam sequence (the intrinsics' fast paths
+// spelled out, one range flag per vector, exact fallback) was built, proven
+// bit-identical on the device and measured slower: C4-slice DS 6030 vs 6123
+// GB/s, BSP 5305 vs 5617 (profiles/r02/adamw_ab.jsonl).
+template <typename T, int OPT>
+__device__ __forceinline__ void step_pack(Pack<T>& x, const Pack<T>& g, Pack<T>& m1, Pack<T>& m2,
+                                          const StepConsts<T>& c, T bc1, T bc2) {
+  constexpr int VN = Vec<T>::n;
+#pragma unroll
+  for (int l = 0; l < VN; ++l) x.v[l] = step_elem<T, OPT>(x.v[l], g.v[l], m1.v[l], m2.v[l], c, bc1, bc2);
 }
 
 // ---- divergence latch ----------------------------------------------------

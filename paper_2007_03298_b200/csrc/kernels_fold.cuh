@@ -213,12 +213,10 @@ __device__ __forceinline__ Pack<T> chain_step(const ChainArgs<T>& a, T* wrow, in
   if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
   const T b1 = static_cast<T>(a.bc1[lr]);
   const T b2 = static_cast<T>(a.bc2[lr]);
+  step_pack<T, OPT>(x, gv, s1, s2, a.c, b1, b2);
   bool ok = true;
 #pragma unroll
-  for (int l = 0; l < VN; ++l) {
-    x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
-    ok = ok && finite_(x.v[l]);
-  }
+  for (int l = 0; l < VN; ++l) ok = ok && finite_(x.v[l]);
   if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
   if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
   if (!ok) {
@@ -248,12 +246,10 @@ __device__ __forceinline__ void chain_step_batch(const ChainArgs<T>& a, T* const
     const long r = static_cast<long>(lr[q]) * a.ld + off;
     const T b1 = static_cast<T>(a.bc1[lr[q]]);
     const T b2 = static_cast<T>(a.bc2[lr[q]]);
+    step_pack<T, OPT>(x[q], gv[q], s1[q], s2[q], a.c, b1, b2);
     bool ok = true;
 #pragma unroll
-    for (int l = 0; l < VN; ++l) {
-      x[q].v[l] = step_elem<T, OPT>(x[q].v[l], gv[q].v[l], s1[q].v[l], s2[q].v[l], a.c, b1, b2);
-      ok = ok && finite_(x[q].v[l]);
-    }
+    for (int l = 0; l < VN; ++l) ok = ok && finite_(x[q].v[l]);
     if constexpr (OPT != kSgd) stv(a.m1 + r, s1[q]);
     if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2[q]);
     if (!ok) {
@@ -587,12 +583,10 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
       Pack<T> s1, s2;
       if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r + off);
       if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r + off);
+      step_pack<T, OPT>(x, gv, s1, s2, a.c, b1, b2);
       bool ok = true;
 #pragma unroll
-      for (int l = 0; l < VN; ++l) {
-        x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
-        ok = ok && finite_(x.v[l]);
-      }
+      for (int l = 0; l < VN; ++l) ok = ok && finite_(x.v[l]);
       if constexpr (OPT != kSgd) stv(a.m1 + r + off, s1);
       if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r + off, s2);
       if (!ok) {
@@ -647,12 +641,10 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
             if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
             const T b1 = static_cast<T>(a.bc1[lr]);
             const T b2 = static_cast<T>(a.bc2[lr]);
+            step_pack<T, OPT>(x, acc, s1, s2, a.c, b1, b2);
             bool oks = true;
 #pragma unroll
-            for (int l = 0; l < VN; ++l) {
-              x.v[l] = step_elem<T, OPT>(x.v[l], acc.v[l], s1.v[l], s2.v[l], a.c, b1, b2);
-              oks = oks && finite_(x.v[l]);
-            }
+            for (int l = 0; l < VN; ++l) oks = oks && finite_(x.v[l]);
             stv(a.w + r, x);
             if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
             if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);

@@ -35,7 +35,9 @@ template <typename T> struct GroupArgs {
 // member: each element of every array is read once and written once.
 template <int OPT, int M>
 constexpr int group_min_blocks() {
-  return (OPT == kMomentum && M == 8) ? DSS_MIN_BLOCKS_M8_MOMENTUM : DSS_MIN_BLOCKS;
+  return (OPT == kMomentum && M == 8)                    ? DSS_MIN_BLOCKS_M8_MOMENTUM
+         : ((OPT == kAdam || OPT == kAdamW) && M == 8) ? DSS_MIN_BLOCKS_M8_ADAM
+                                                        : DSS_MIN_BLOCKS;
 }
 
 template <typename T, int OPT, int M>
@@ -95,12 +97,10 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
               b1j = static_cast<T>(a.bc1[lrow[j]]);
               b2j = static_cast<T>(a.bc2[lrow[j]]);
             }
+            step_pack<T, OPT>(xs[q], gs[q], s1[q], s2[q], a.c, b1j, b2j);
             bool ok = true;
 #pragma unroll
-            for (int l = 0; l < VN; ++l) {
-              xs[q].v[l] = step_elem<T, OPT>(xs[q].v[l], gs[q].v[l], s1[q].v[l], s2[q].v[l], a.c, b1j, b2j);
-              ok = ok && finite_(xs[q].v[l]);
-            }
+            for (int l = 0; l < VN; ++l) ok = ok && finite_(xs[q].v[l]);
             if constexpr (OPT != kSgd) stv(a.m1 + rj, s1[q]);
             if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj, s2[q]);
             if (!ok) {
@@ -132,12 +132,10 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
           Pack<T> s1, s2;
           if constexpr (OPT != kSgd) s1 = ldv(a.m1 + rj + off);
           if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + rj + off);
+          step_pack<T, OPT>(x, gv, s1, s2, a.c, b1j, b2j);
           bool ok = true;
 #pragma unroll
-          for (int l = 0; l < VN; ++l) {
-            x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], a.c, b1j, b2j);
-            ok = ok && finite_(x.v[l]);
-          }
+          for (int l = 0; l < VN; ++l) ok = ok && finite_(x.v[l]);
           if constexpr (OPT != kSgd) stv(a.m1 + rj + off, s1);
           if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj + off, s2);
           if (!ok) {
@@ -422,12 +420,10 @@ __global__ void __launch_bounds__(kThreads, DSS_MIN_BLOCKS) bsp_kernel(const Bsp
       const long r = static_cast<long>(k) * a.ld + off;
       const T b1 = static_cast<T>(a.bc1[k]);
       const T b2 = static_cast<T>(a.bc2[k]);
+      step_pack<T, OPT>(x, gm, m1v, m2v, a.c, b1, b2);
       bool ok = true;
 #pragma unroll
-      for (int l = 0; l < VN; ++l) {
-        x.v[l] = step_elem<T, OPT>(x.v[l], gm.v[l], m1v.v[l], m2v.v[l], a.c, b1, b2);
-        ok = ok && finite_(x.v[l]);
-      }
+      for (int l = 0; l < VN; ++l) ok = ok && finite_(x.v[l]);
       stv(a.w + r, x);
       if constexpr (OPT != kSgd) stv(a.m1 + r, m1v);
       if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, m2v);
@@ -438,19 +434,24 @@ __global__ void __launch_bounds__(kThreads, DSS_MIN_BLOCKS) bsp_kernel(const Bsp
     };
     if constexpr (WT > 0) {
 #pragma unroll
-      for (int k = 0; k < WT; ++k) {
-        Pack<T> x, m1v, m2v;
-        if (k < BCH) {
-          x = xs[k];
-          m1v = s1[k];
-          m2v = s2[k];
-        } else {
-          const long r = static_cast<long>(k) * a.ld + off;
-          x = ldv(a.w + r);
-          if constexpr (OPT != kSgd) m1v = ldv(a.m1 + r);
-          if constexpr (OPT == kAdam || OPT == kAdamW) m2v = ldv(a.m2 + r);
+      for (int k = 0; k < BCH; ++k) step_store(k, xs[k], s1[k], s2[k]);
+      // the remaining workers in chunks of BCH: a chunk's params and state
+      // are all in flight before its first store
+#pragma unroll
+      for (int k0 = BCH; k0 < WT; k0 += BCH) {
+#pragma unroll
+        for (int q = 0; q < BCH; ++q) {
+          if (k0 + q < WT) {
+            const long r = static_cast<long>(k0 + q) * a.ld + off;
+            xs[q] = ldv(a.w + r);
+            if constexpr (OPT != kSgd) s1[q] = ldv(a.m1 + r);
+            if constexpr (OPT == kAdam || OPT == kAdamW) s2[q] = ldv(a.m2 + r);
+          }
         }
-        step_store(k, x, m1v, m2v);
+#pragma unroll
+        for (int q = 0; q < BCH; ++q) {
+          if (k0 + q < WT) step_store(k0 + q, xs[q], s1[q], s2[q]);
+        }
       }
     } else {
       // any W: workers in batches of 4 whose loads are all in flight before
@@ -686,12 +687,10 @@ __global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
               const long r = static_cast<long>(k) * a.ld + off;
               const T b1 = static_cast<T>(a.bc1[static_cast<long>(i) * a.nw + k]);
               const T b2 = static_cast<T>(a.bc2[static_cast<long>(i) * a.nw + k]);
+              step_pack<T, OPT>(xs[q], gm, s1[q], s2[q], c, b1, b2);
               bool ok = true;
 #pragma unroll
-              for (int l = 0; l < VN; ++l) {
-                xs[q].v[l] = step_elem<T, OPT>(xs[q].v[l], gm.v[l], s1[q].v[l], s2[q].v[l], c, b1, b2);
-                ok = ok && finite_(xs[q].v[l]);
-              }
+              for (int l = 0; l < VN; ++l) ok = ok && finite_(xs[q].v[l]);
               stv(a.w + r, xs[q]);
               if constexpr (OPT != kSgd) stv(a.m1 + r, s1[q]);
               if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2[q]);
@@ -727,12 +726,10 @@ __global__ void __launch_bounds__(NT) small_steps_kernel(const SmallArgs<T> a) {
           if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
           const T b1 = static_cast<T>(a.bc1[static_cast<long>(i) * a.nw + k]);
           const T b2 = static_cast<T>(a.bc2[static_cast<long>(i) * a.nw + k]);
+          step_pack<T, OPT>(x, gv, s1, s2, c, b1, b2);
           bool ok = true;
 #pragma unroll
-          for (int l = 0; l < VN; ++l) {
-            x.v[l] = step_elem<T, OPT>(x.v[l], gv.v[l], s1.v[l], s2.v[l], c, b1, b2);
-            ok = ok && finite_(x.v[l]);
-          }
+          for (int l = 0; l < VN; ++l) ok = ok && finite_(x.v[l]);
           if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
           if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
           if (!ok) {

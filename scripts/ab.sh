@@ -1,0 +1,7 @@
+#!/bin/bash
+# A/B of library variants: scripts/ab.sh "<variant.so|base> ..." "<config ...>"
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"; mkdir -p gpurun_out
+for round in 1 2; do for v in $1; do
+  timeout 600 python profiles/tools/group_kernel_ab.py $v $2
+done; done > gpurun_out/ab.jsonl 2>&1
+cat gpurun_out/ab.jsonl
