@@ -256,7 +256,12 @@ int dss_quadratic_gradients(dss_ctx* ctx, long t, uint64_t seed, double mu, doub
 
 /* w* = gaussians of stream (problem_seed, kDataGen, 1, 0) (problems.cpp:157-159)
  * and every worker's params = w* + sqrt(delta0) * u, u the normalised
- * gaussian vector of stream (problem_seed, kInitParams, 0, 0) (problems.cpp:161-165). */
+ * gaussian vector of stream (problem_seed, kInitParams, 0, 0) (problems.cpp:161-165).
+ * Device-generated at full size: tolerance-level parity with the reference
+ * (the Box-Muller log/cos are libdevice's, and |u|^2 is a fixed-order tree
+ * sum rather than the reference's sequential loop), but deterministic: the
+ * same call gives the same bits on every run and every rank.  The bit-exact
+ * host generator is dss_quadratic_problem. */
 int dss_quadratic_init(dss_ctx* ctx, uint64_t problem_seed, double delta0);
 /* Upload an explicit optimum w* (dim elements of the context dtype). */
 int dss_set_optimum(dss_ctx* ctx, const void* host, long n);
@@ -281,7 +286,7 @@ int dss_quadratic_losses(dss_ctx* ctx, double mu, int exact, double* losses, dou
 int dss_logistic_dataset(uint64_t seed, int d, int M, double* x, double* y);
 /* QuadraticProblem's optimum and start for A = mu*I (problems.cpp:157-165),
  * host, bit-exact: wstar, w0 = d doubles each (cf. dss_quadratic_init, the
- * device-side generator of the same rows for huge d). */
+ * device-side generator of these rows for huge d, equal within tolerance). */
 int dss_quadratic_problem(uint64_t seed, int d, double delta0, double* wstar, double* w0);
 /* LogisticProblem::finish_setup (problems.cpp:346-416), host, bit-exact:
  * the smoothness bound (power iteration on X^T X / 4M, + l2) and, when
@@ -367,9 +372,12 @@ long dss_launch_count(const dss_ctx* ctx);
 
 /* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
 /* CUDA IPC handles of this GPU's params, grads, mean-gradient, barrier-flag,
- * chain-row, chain-flag, running-stats, push-staging and push-flag buffers:
- * DSS_IPC_BYTES bytes written to out. */
-#define DSS_IPC_BYTES 576
+ * chain-row, chain-flag, running-stats, push-staging and push-flag buffers
+ * (9 x 64 B), then a 160-B layout fingerprint (dtype, dims, world,
+ * optimizer, path, chain and one-shot geometry): DSS_IPC_BYTES bytes
+ * written to out.  dss_ipc_attach fails with DSS_EINVAL when any rank's
+ * fingerprint differs from this context's. */
+#define DSS_IPC_BYTES 736
 int dss_ipc_export(dss_ctx* ctx, void* out);
 /* Map every GPU's exported handles (n_gpus * DSS_IPC_BYTES bytes, rank
  * order, own entry ignored).  Must be called on every rank before the first

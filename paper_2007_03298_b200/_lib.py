@@ -19,7 +19,7 @@ DSS_OK, DSS_EINVAL, DSS_EDIVERGED, DSS_ECUDA, DSS_ENCCL, DSS_ERUNTIME = range(6)
 DSS_F32, DSS_F64 = 0, 1
 BUF_PARAMS, BUF_GRADS, BUF_MOMENT1, BUF_MOMENT2, BUF_STATS, BUF_STATS_OBS = range(6)
 SAMPLING_REPLACEMENT, SAMPLING_EPOCH = 0, 1  # dss_sampling
-IPC_BYTES = 576
+IPC_BYTES = 736
 KIND_NAMES = ["group", "fold", "bsp", "barrier", "gradient", "chain", "chain_mean"]
 
 

@@ -786,6 +786,23 @@ extern "C" long dss_launch_count(const dss_ctx* c) { return c ? c->launches : -1
 
 // ------------------------------- multi-GPU -----------------------------------
 
+// Layout fingerprint exported beside the IPC handles: peers index each
+// other's buffers with their own geometry (row stride, chain slots, one-shot
+// offsets, ...), so every rank must have been created with the same
+// configuration.  Attach rejects a peer whose fingerprint differs.
+namespace {
+constexpr int kFingerprintWords = 20;
+void fingerprint(const dss_ctx* c, long long* f) {
+  const long long v[kFingerprintWords] = {
+      0x4453535942323030LL,  // "DSSYB200"
+      c->cfg.dtype, c->cfg.optimizer, c->cfg.strategy.kind, c->cfg.strategy.topology,
+      c->cfg.strategy.world_size, c->cfg.strategy.group_size, c->cfg.strategy.rectangular,
+      c->cfg.n_gpus, c->P, c->d, c->d_pad, c->s, c->chain_slots, c->chain_chunk,
+      c->oneshot_base_elems, c->oneshot_half_elems, c->oneshot_rows, c->oneshot_ack_off, c->cfg.path};
+  std::memcpy(f, v, sizeof(v));
+}
+}  // namespace
+
 extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
   if (!c || !out) return fail(c, DSS_EINVAL, "null argument");
   return guard(c, [&]() -> int {
@@ -803,6 +820,8 @@ extern "C" int dss_ipc_export(dss_ctx* c, void* out) {
     ck(cudaIpcGetMemHandle(&h[7], c->push_buf), "cudaIpcGetMemHandle(push staging)");
     ck(cudaIpcGetMemHandle(&h[8], c->push_flags), "cudaIpcGetMemHandle(push flags)");
     std::memcpy(out, h, sizeof(h));
+    static_assert(sizeof(h) + kFingerprintWords * sizeof(long long) == DSS_IPC_BYTES, "DSS_IPC_BYTES");
+    fingerprint(c, reinterpret_cast<long long*>(static_cast<char*>(out) + sizeof(h)));
     return DSS_OK;
   });
 }
@@ -823,8 +842,19 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
     c->peer_stats.assign(static_cast<size_t>(G), nullptr);
     c->peer_push_buf.assign(static_cast<size_t>(G), nullptr);
     c->peer_push_flags.assign(static_cast<size_t>(G), nullptr);
-    const auto* h = static_cast<const cudaIpcMemHandle_t*>(all);
+    long long mine[kFingerprintWords];
+    fingerprint(c, mine);
     for (int r = 0; r < G; ++r) {
+      const char* blob = static_cast<const char*>(all) + static_cast<size_t>(r) * DSS_IPC_BYTES;
+      if (std::memcmp(blob + 9 * sizeof(cudaIpcMemHandle_t), mine, sizeof(mine)) != 0) {
+        throw std::invalid_argument("dss_ipc_attach: rank " + std::to_string(r) +
+                                    " was created with a different configuration (dtype, dims, world, "
+                                    "optimizer or path) than rank " + std::to_string(c->cfg.rank));
+      }
+    }
+    for (int r = 0; r < G; ++r) {
+      const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(static_cast<const char*>(all) +
+                                                                  static_cast<size_t>(r) * DSS_IPC_BYTES);
       if (r == c->cfg.rank) {
         c->peer_w[static_cast<size_t>(r)] = c->w;
         c->peer_g[static_cast<size_t>(r)] = c->g;
@@ -839,7 +869,7 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
       }
       void* p[9];
       for (int b = 0; b < 9; ++b) {
-        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[r * 9 + b], cudaIpcMemLazyEnablePeerAccess);
+        cudaError_t e = cudaIpcOpenMemHandle(&p[b], h[b], cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
           throw PeerError("cudaIpcOpenMemHandle(rank " + std::to_string(r) + "): " + cudaGetErrorString(e));
         }

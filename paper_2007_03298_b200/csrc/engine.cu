@@ -974,14 +974,22 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   a.c = consts<T>(c, alpha);
   fill_bias(c, a);
   auto kern = pl.bsp ? push_twoshot_kernel<T, OPT, true> : push_twoshot_kernel<T, OPT, false>;
-  int occ = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0), "occupancy");
-  // fully resident grid: phase-1 work can never wait behind spinning CTAs
-  const long grid = std::max(1L, std::min<long>(static_cast<long>(std::max(occ, 1)) * c->sms,
-                                                std::max(pl.items, pl.folds)));
+  // Phase-2 CTAs spin on flags that phase-1 CTAs of this and other GPUs
+  // release, so every CTA must be resident at once: a cooperative launch
+  // guarantees it (or fails the launch) whatever else shares the GPU.  The
+  // occupancy query runs once per instantiation.
+  static int occ[2] = {-1, -1};
+  int& o = occ[pl.bsp ? 1 : 0];
+  if (o < 0) {
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0), "occupancy");
+    o = std::max(o, 1);
+  }
+  const long grid = std::max(1L, std::min<long>(static_cast<long>(o) * c->sms, std::max(pl.items, pl.folds)));
   TimedLaunch tl(c, DSS_KIND_FOLD);
-  kern<<<static_cast<int>(grid), kThreads, 0, c->stream>>>(a);
-  ck(cudaGetLastError(), "push_twoshot_kernel launch");
+  void* args[] = {&a};
+  ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(grid)),
+                                 dim3(kThreads), args, 0, c->stream),
+     "push_twoshot_kernel cooperative launch");
 }
 
 template <typename T>

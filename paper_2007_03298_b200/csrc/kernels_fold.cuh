@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   __shared__ PushFold fo;
   __shared__ int ok_flag;
   __shared__ T* sdst[kMaxFold];
+  __shared__ unsigned long long sok;  // bit q: destination q may be written (its flow-control wait succeeded)
   unsigned long long bad = ~0ull;
   if (a.seq && blockIdx.x == 0 && threadIdx.x < a.n_gpus) {
     // "I have started launch seq".  The reads this releases (the folds of
@@ -559,15 +560,22 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   }
   // phase 1: step + push
   for (int u = blockIdx.x; u < a.n_items; u += gridDim.x) {
-    if (threadIdx.x == 0) it = a.items[u];
+    if (threadIdx.x == 0) {
+      it = a.items[u];
+      sok = ~0ull;
+    }
     __syncthreads();
     if (threadIdx.x < it.ndst) {
       sdst[threadIdx.x] = reinterpret_cast<T*>(static_cast<char*>(a.item_dst[it.dst_beg + threadIdx.x]) + a.stage_shift);
-      if (a.seq >= DSS_ONESHOT_BUFFERS) {  // the destination is done with this buffer's previous launch
-        chain_wait(a.ack_mine + a.item_gpu[it.dst_beg + threadIdx.x], a.seq - DSS_ONESHOT_BUFFERS + 1, a.timeout);
+      // the destination must be done with this buffer's previous launch; on
+      // a timeout (latched) nothing is pushed into a buffer it may still read
+      if (a.seq >= DSS_ONESHOT_BUFFERS &&
+          !chain_wait(a.ack_mine + a.item_gpu[it.dst_beg + threadIdx.x], a.seq - DSS_ONESHOT_BUFFERS + 1, a.timeout)) {
+        atomicAnd(&sok, ~(1ull << threadIdx.x));
       }
     }
     __syncthreads();
+    const unsigned long long dst_ok = sok;
     const long r = static_cast<long>(it.lr) * a.ld;
     const T b1 = static_cast<T>(a.bc1[it.lr]);
     const T b2 = static_cast<T>(a.bc2[it.lr]);
@@ -575,7 +583,9 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
       const long off = e * VN;
       if constexpr (BSP) {
         const Pack<T> gv = ldv(a.g + r + off);
-        for (int q = 0; q < it.ndst; ++q) stv_cg(sdst[q] + (off - it.lo), gv);
+        for (int q = 0; q < it.ndst; ++q) {
+          if ((dst_ok >> q) & 1) stv_cg(sdst[q] + (off - it.lo), gv);
+        }
         continue;
       }
       Pack<T> x = ldv(a.w + r + off);
@@ -593,10 +603,14 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
         const unsigned long long k = err_key(a.t, 0, it.rank);
         bad = k < bad ? k : bad;
       }
-      for (int q = 0; q < it.ndst; ++q) stv_cg(sdst[q] + (off - it.lo), x);
+      for (int q = 0; q < it.ndst; ++q) {
+        if ((dst_ok >> q) & 1) stv_cg(sdst[q] + (off - it.lo), x);
+      }
     }
     __syncthreads();
-    if (threadIdx.x < it.ndst) st_release_sys(a.item_flag[it.dst_beg + threadIdx.x] + a.flag_shift, a.epoch);
+    if (threadIdx.x < it.ndst && ((dst_ok >> threadIdx.x) & 1)) {
+      st_release_sys(a.item_flag[it.dst_beg + threadIdx.x] + a.flag_shift, a.epoch);
+    }
     __syncthreads();
   }
   // phase 2: ordered fold of owned chunks

@@ -206,21 +206,31 @@ static __global__ void gaussian_fill_kernel(double* out, long d, uint64_t s0) {
   }
 }
 
-static __global__ void sumsq_kernel(const double* x, long d, double* out) {
+// Sum of squares in a fixed order: per thread a strided sum, a warp
+// butterfly, the warps in order into partial[blockIdx.x]; sumsq_finish adds
+// the block partials in block order.  The same grid always gives the same
+// bits (every rank of a multi-GPU run computes the same start row).
+static __global__ void sumsq_kernel(const double* x, long d, double* partial) {
   __shared__ double part[kThreads / 32];
   double acc = 0.0;
   const long stride = static_cast<long>(gridDim.x) * blockDim.x;
   for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < d; i += stride) {
-    acc += x[i] * x[i];
+    acc = __dadd_rn(acc, __dmul_rn(x[i], x[i]));
   }
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < kThreads / 32; ++i) s += part[i];
-    atomicAdd(out, s);
+    for (int i = 0; i < kThreads / 32; ++i) s = __dadd_rn(s, part[i]);
+    partial[blockIdx.x] = s;
   }
+}
+
+static __global__ void sumsq_finish(const double* partial, int n, double* out) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, partial[i]);
+  *out = s;
 }
 
 // w*_T = T(w*), row_T = T(w* + r * (u / |u|)) (problems.cpp:106-113,161-165)

@@ -65,12 +65,12 @@ extern "C" int dss_quadratic_init(dss_ctx* c, uint64_t problem_seed, double delt
     double*& ss = sc.ss;
     ck(cudaMalloc(&ws, sizeof(double) * c->d), "cudaMalloc");
     ck(cudaMalloc(&u, sizeof(double) * c->d), "cudaMalloc");
-    ck(cudaMalloc(&ss, sizeof(double)), "cudaMalloc");
-    ck(cudaMemsetAsync(ss, 0, sizeof(double), c->stream), "memset");
     const int gx = grid_x(c, c->d, 1);
+    ck(cudaMalloc(&ss, sizeof(double) * (1 + static_cast<size_t>(gx))), "cudaMalloc");
     gaussian_fill_kernel<<<gx, kThreads, 0, c->stream>>>(ws, c->d, stream_state(problem_seed, kDataGen, 1, 0));
     gaussian_fill_kernel<<<gx, kThreads, 0, c->stream>>>(u, c->d, stream_state(problem_seed, kInitParams, 0, 0));
-    sumsq_kernel<<<gx, kThreads, 0, c->stream>>>(u, c->d, ss);
+    sumsq_kernel<<<gx, kThreads, 0, c->stream>>>(u, c->d, ss + 1);
+    sumsq_finish<<<1, 1, 0, c->stream>>>(ss + 1, gx, ss);
     const double r = std::sqrt(delta0);
     const int gp = grid_x(c, c->d_pad, 1);
     if (c->cfg.dtype == DSS_F64) {

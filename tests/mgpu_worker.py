@@ -142,13 +142,29 @@ def logistic_case(rank, G, sampling, kind):
     return ok
 
 
+def fingerprint_case(rank, G):
+    """Ranks created with different geometry (here: a different d per rank)
+    must refuse to map each other's buffers (dss_ipc_attach fingerprint)."""
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(8, 2), 1, True)
+    e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 1000 + rank, OptimizerHyperparams(), "f32", device_of(rank), rank, G)
+    try:
+        attach(e)
+        ok = False
+    except ValueError as ex:
+        ok = "different configuration" in str(ex)
+    e.close()
+    if rank == 0:
+        print(f"case fingerprint mismatch G={G}: {'OK' if ok else 'MISSED'}", flush=True)
+    return ok
+
+
 def main():
     rank = int(os.environ["RANK"])
     G = int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(device_of(rank))
     dist.init_process_group("gloo")
     orc = Oracle()
-    ok = True
+    ok = fingerprint_case(rank, G)
     for case in CASES:
         if case[1] % G:
             continue

@@ -61,3 +61,71 @@ def test_null_handles_are_rejected():
     assert lib.dss_step(None, 0, 0.1, 0, None) == L.DSS_EINVAL
     assert lib.dss_check(None) == L.DSS_EINVAL
     assert lib.dss_destroy(None) == L.DSS_OK
+
+
+def _fake_engine(dtype, P, d):
+    """A DsSyncEngine shell (no device context) to exercise the host-side
+    argument checks that run before any C call."""
+    import numpy as np
+
+    from paper_2007_03298_b200 import DsSyncEngine
+    e = DsSyncEngine.__new__(DsSyncEngine)
+    e.dtype, e.local_workers, e.dim, e.stats_dim = dtype, P, d, 0
+    e.h = None
+
+    class _NoCalls:  # any C call reached means a check was skipped
+        def __getattr__(self, name):
+            def call(*a):
+                raise AssertionError(f"{name} called with an unchecked buffer")
+            return call
+    e.lib = _NoCalls()
+    return e
+
+
+def test_host_buffer_checks_reject_mismatched_buffers():
+    """step_host / upload_all / download_all hand raw pointers to C calls
+    that copy local_workers * dim elements: wrong shape, dtype or layout
+    must raise ValueError before any copy (not an assert)."""
+    import numpy as np
+    import torch
+    e = _fake_engine(np.float64, 2, 5)
+    good = np.zeros((2, 5))
+    assert e._host_ptr(good, (2, 5), "x") == good.ctypes.data
+    for bad in (np.zeros((2, 5), np.float32), np.zeros((2, 4)), np.zeros((5, 2)).T, np.zeros(10)):
+        with pytest.raises(ValueError):
+            e._host_ptr(bad, (2, 5), "x")
+    t = torch.zeros((2, 5), dtype=torch.float64)
+    assert e._host_ptr(t, (2, 5), "x") == t.data_ptr()
+    for bad in (torch.zeros((2, 5)), torch.zeros((5, 2), dtype=torch.float64).t(), torch.zeros((2, 6), dtype=torch.float64)):
+        with pytest.raises(ValueError):
+            e._host_ptr(bad, (2, 5), "x")
+    with pytest.raises(TypeError):
+        e._host_ptr([[0.0] * 5] * 2, (2, 5), "x")
+    with pytest.raises(ValueError):
+        e.step_host(0, 0.1, np.zeros((2, 5), np.float32), good)
+    with pytest.raises(ValueError):
+        e.download_all(0, np.zeros((3, 5)))
+    with pytest.raises(ValueError):
+        e.broadcast_row(0, np.zeros(4))
+
+
+def test_iteration_trace_payload_counts_running_stats():
+    """simulated_comm_time uses payload_bytes = 8 * (dim + stats_dim)
+    (sync.cpp:314-318)."""
+    import numpy as np
+
+    from paper_2007_03298_b200 import SyncRoundOutcome, SyncStrategy, StrategyKind, Topology, WorldConfig
+    from paper_2007_03298_b200.api import iteration_trace
+
+    class Fake:
+        dim, stats_dim = 10, 3
+        strategy = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(4, 2))
+
+        def global_mean(self):
+            return np.zeros(10)
+
+        def quadratic_losses(self, mu, exact=False):
+            return np.ones(4), 0.0
+
+    tr = iteration_trace(Fake(), 0, SyncRoundOutcome(3, 6), 1.0, bandwidth=2.0)
+    assert tr.simulated_comm_time == 3 * 8.0 * 13 / 2.0
