@@ -29,7 +29,7 @@ def build(ref: bool = True) -> None:
     """Build the oracle (and, when the reference sources are present, _ref)."""
     targets = [ORACLE_SO]
     if ref and os.path.isdir(REF_SRC):
-        targets += ["ref", "reftests", "acceptance"]
+        targets += ["ref", "reftests", "acceptance", "shimbench"]
     subprocess.run(["make", "-s", "-C", HERE, *targets], check=True)
 
 

@@ -1,25 +1,36 @@
 // Device-backed replacements of the reference's hot-path functions, built
 // over the C-ABI (include/dssync_b200.h):
 //
-//   dssync::apply_step      (include/dssync/optim.hpp:51-52)
-//   dssync::sync_round      (include/dssync/sync.hpp:128-129)
-//   dssync::make_partition  (include/dssync/schedule.hpp:37)
+//   dssync::apply_step          (include/dssync/optim.hpp:51-52)
+//   dssync::sync_round          (include/dssync/sync.hpp:128-129)
+//   dssync::make_partition      (include/dssync/schedule.hpp:37)
+//   dssync::ring/tree/ps_allreduce_avg  (include/dssync/comm.hpp:79-97) --
+//       the collective seam run_training's sync_one_group calls
+//       (sync.cpp:225-240 via run_collective, :143-151)
 //
-// Linked ahead of the reference objects (whose copies of these three
-// symbols are weakened with objcopy by oracle/Makefile), the reference's
-// own unit tests and run_training then execute their optimizer steps and
-// group averages on the B200.  This is the shim INTEGRATION.md describes.
+// Linked ahead of the reference objects (whose copies of the first three are
+// weakened with objcopy, and whose collectives are renamed to ref_*_allreduce_avg
+// so argument errors and single-member calls still take the reference's own
+// code), the reference's unit tests, acceptance suite and run_training then
+// execute their optimizer steps and group averages on the B200.  This is the
+// shim INTEGRATION.md describes.
+//
+// Contexts are cached per calling thread (each with its own stream), so
+// run_training's Parallel mode keeps its workers' steps concurrent instead of
+// serialising on one context.  A collective uploads the m member rows in one
+// copy and downloads one row: every member of a group gets identical bits.
 //
 // Test infrastructure: compiled against the reference headers, so it is
 // built only where /root/reference exists and travels as a binary.
 #include <cmath>
 #include <map>
-#include <mutex>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <tuple>
 #include <vector>
 
+#include "dssync/comm.hpp"
 #include "dssync/errors.hpp"
 #include "dssync/optim.hpp"
 #include "dssync/schedule.hpp"
@@ -30,7 +41,6 @@ namespace dssync {
 
 namespace {
 
-std::mutex g_mu;  // contexts are not thread-safe; Parallel-mode callers serialize here
 
 [[noreturn]] void throw_from(dss_ctx* c, int st) {
   char buf[1024] = {0};
@@ -49,7 +59,7 @@ std::mutex g_mu;  // contexts are not thread-safe; Parallel-mode callers seriali
 using Key = std::tuple<int, int, int, int, int, int, long, double, double, double, double, double>;
 
 dss_ctx* cached(const dss_config& cfg) {
-  static std::map<Key, dss_ctx*> cache;
+  thread_local std::map<Key, dss_ctx*> cache;  // a context is driven by one host thread
   const Key k{cfg.strategy.kind, cfg.strategy.topology, cfg.strategy.world_size, cfg.strategy.group_size,
               cfg.strategy.num_servers, cfg.optimizer, cfg.dim, cfg.hp.momentum, cfg.hp.beta1, cfg.hp.beta2,
               cfg.hp.epsilon, cfg.hp.weight_decay};
@@ -85,7 +95,6 @@ StepResult apply_step(const OptimizerState& state, const ParamVector& params, co
   r.state.step_count = state.step_count + 1;
   if (n == 0) return r;
 
-  std::lock_guard<std::mutex> lock(g_mu);
   dss_config cfg{};
   cfg.strategy = {DSS_DS_SYNC, DSS_RING, 1, 1, 1, 0};
   cfg.optimizer = static_cast<int>(state.kind);
@@ -142,7 +151,6 @@ SyncRoundOutcome sync_round(std::vector<WorkerState>& workers, const SyncStrateg
       throw std::invalid_argument("collective vectors must all have the same length");
     }
   }
-  std::lock_guard<std::mutex> lock(g_mu);
   dss_config cfg{};
   cfg.strategy = {static_cast<int>(strategy.kind), static_cast<int>(strategy.topology), strategy.world.world_size,
                   strategy.world.group_size, strategy.num_servers, 0};
@@ -151,13 +159,14 @@ SyncRoundOutcome sync_round(std::vector<WorkerState>& workers, const SyncStrateg
   cfg.dim = static_cast<long>(dim);
   cfg.n_gpus = 1;
   dss_ctx* c = cached(cfg);
-  std::vector<double> row(dim);
-  for (size_t k = 0; k < workers.size(); ++k) {  // concat_payload (sync.cpp:203-207)
-    std::copy(workers[k].params.begin(), workers[k].params.end(), row.begin());
-    std::copy(workers[k].running_stats.begin(), workers[k].running_stats.end(),
-              row.begin() + static_cast<long>(workers[k].params.size()));
-    if (int st = dss_upload(c, DSS_BUF_PARAMS, static_cast<int>(k), row.data(), cfg.dim)) throw_from(c, st);
+  thread_local std::vector<double> rows;  // concat_payload (sync.cpp:203-207) of every worker, one upload
+  rows.resize(workers.size() * dim);
+  for (size_t k = 0; k < workers.size(); ++k) {
+    double* r = rows.data() + k * dim;
+    std::copy(workers[k].params.begin(), workers[k].params.end(), r);
+    std::copy(workers[k].running_stats.begin(), workers[k].running_stats.end(), r + workers[k].params.size());
   }
+  if (int st = dss_upload_all(c, DSS_BUF_PARAMS, rows.data())) throw_from(c, st);
   dss_outcome o{};
   int st = dss_sync_round(c, t, /*check=*/1, &o);
   if (st) {
@@ -174,13 +183,92 @@ SyncRoundOutcome sync_round(std::vector<WorkerState>& workers, const SyncStrateg
     }
     throw_from(c, st);
   }
+  if (int st2 = dss_download_all(c, DSS_BUF_PARAMS, rows.data())) throw_from(c, st2);
   for (size_t k = 0; k < workers.size(); ++k) {  // split_payload (sync.cpp:209-213)
-    dss_download(c, DSS_BUF_PARAMS, static_cast<int>(k), row.data(), cfg.dim);
+    const double* r = rows.data() + k * dim;
     const size_t d = workers[k].params.size();
-    workers[k].params.assign(row.begin(), row.begin() + static_cast<long>(d));
-    workers[k].running_stats.assign(row.begin() + static_cast<long>(d), row.end());
+    workers[k].params.assign(r, r + d);
+    workers[k].running_stats.assign(r + d, r + dim);
   }
   return {o.critical_path_steps, o.total_messages};
+}
+
+// ---- the collective seam (comm.hpp:79-97) ----------------------------------
+// The reference's own collectives, renamed in comm.o by oracle/Makefile.
+AllReduceResult ref_ring_allreduce_avg(std::span<const int> members, std::span<const ParamVector> inputs);
+AllReduceResult ref_tree_allreduce_avg(std::span<const int> members, std::span<const ParamVector> inputs);
+AllReduceResult ref_ps_allreduce_avg(std::span<const int> members, std::span<const ParamVector> inputs,
+                                     int num_servers);
+
+namespace {
+
+bool device_collective_applies(std::span<const int> members, std::span<const ParamVector> inputs, int topology,
+                               int servers) {
+  // everything the reference rejects (check_collective_args, comm.cpp:56-72;
+  // tree needs 2^k members, ps a server) and a lone member (a copy, no
+  // steps) stay on the reference's code, with its exact errors
+  const size_t m = members.size();
+  if (m < 2 || inputs.size() != m || inputs[0].empty()) return false;
+  for (size_t i = 1; i < m; ++i) {
+    if (members[i] <= members[i - 1] || inputs[i].size() != inputs[0].size()) return false;
+  }
+  if (topology == DSS_TREE && (m & (m - 1)) != 0) return false;
+  if (topology == DSS_PS && servers < 1) return false;
+  return true;
+}
+
+// mean_of(inputs) (param.cpp:42-53) on the device: the m rows are one
+// all-member group (BSP-shaped sync round over m workers), folded in member
+// order and scaled by 1/m; every member receives those bits.
+AllReduceResult device_allreduce(std::span<const ParamVector> inputs, int topology, int servers, const char* name) {
+  const size_t m = inputs.size();
+  const size_t dim = inputs[0].size();
+  dss_config cfg{};
+  cfg.strategy = {DSS_BSP, topology, static_cast<int>(m), static_cast<int>(m), servers, 0};
+  cfg.optimizer = DSS_VANILLA_SGD;
+  cfg.dtype = DSS_F64;
+  cfg.dim = static_cast<long>(dim);
+  cfg.n_gpus = 1;
+  dss_ctx* c = cached(cfg);
+  thread_local std::vector<double> rows;
+  rows.resize(m * dim);
+  for (size_t k = 0; k < m; ++k) std::copy(inputs[k].begin(), inputs[k].end(), rows.data() + k * dim);
+  if (int st = dss_upload_all(c, DSS_BUF_PARAMS, rows.data())) throw_from(c, st);
+  dss_outcome o{};
+  int st = dss_sync_round(c, 0, /*check=*/1, &o);
+  if (st == DSS_EDIVERGED) {
+    dss_clear_error(c);
+    throw std::runtime_error(std::string(name) + ": non-finite value in result");  // require_finite (param.cpp:27-32)
+  }
+  if (st) throw_from(c, st);
+  AllReduceResult out;
+  out.values.resize(m);
+  out.values[0].resize(dim);
+  if (int st2 = dss_download(c, DSS_BUF_PARAMS, 0, out.values[0].data(), static_cast<long>(dim))) throw_from(c, st2);
+  for (size_t k = 1; k < m; ++k) out.values[k] = out.values[0];
+  out.steps.serial_steps = o.critical_path_steps;
+  out.steps.total_messages = o.total_messages;
+  return out;
+}
+
+}  // namespace
+
+AllReduceResult ring_allreduce_avg(std::span<const int> members, std::span<const ParamVector> inputs) {
+  if (!device_collective_applies(members, inputs, DSS_RING, 1)) return ref_ring_allreduce_avg(members, inputs);
+  return device_allreduce(inputs, DSS_RING, 1, "ring_allreduce_avg");
+}
+
+AllReduceResult tree_allreduce_avg(std::span<const int> members, std::span<const ParamVector> inputs) {
+  if (!device_collective_applies(members, inputs, DSS_TREE, 1)) return ref_tree_allreduce_avg(members, inputs);
+  return device_allreduce(inputs, DSS_TREE, 1, "tree_allreduce_avg");
+}
+
+AllReduceResult ps_allreduce_avg(std::span<const int> members, std::span<const ParamVector> inputs,
+                                 int num_servers) {
+  if (!device_collective_applies(members, inputs, DSS_PS, num_servers)) {
+    return ref_ps_allreduce_avg(members, inputs, num_servers);
+  }
+  return device_allreduce(inputs, DSS_PS, num_servers, "ps_allreduce_avg");
 }
 
 }  // namespace dssync

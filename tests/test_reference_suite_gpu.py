@@ -1,7 +1,8 @@
 """The reference's OWN test suites (proj/tests/*.cpp and acceptance.cpp, unmodified), compiled
-with tests/cpp/doctest.h and linked so that dssync::apply_step, sync_round
-and make_partition run on the B200 through the C-ABI (tests/cpp/b200_shim.cpp;
-oracle/Makefile target `reftests`).  Every other reference function, incl.
+with tests/cpp/doctest.h and linked so that dssync::apply_step, sync_round,
+make_partition and the ring/tree/ps collectives run on the B200 through the
+C-ABI (tests/cpp/b200_shim.cpp; oracle/Makefile targets `reftests`,
+`acceptance`, `shimbench`).  Every other reference function, incl.
 run_training, is the reference's own code calling into the device path."""
 import os
 import subprocess
@@ -51,3 +52,30 @@ def test_reference_acceptance_on_b200():
     sync_round and make_partition served by the B200 library."""
     p = _run(ACC_B200)
     assert p.returncode == 0 and "all 12 criteria passed" in p.stdout
+
+
+SHIM_PURE = os.path.join(ROOT, "oracle", "_ref", "shim_bench")
+SHIM_B200 = os.path.join(ROOT, "oracle", "_ref", "shim_bench_b200")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["lockstep", "parallel"])
+def test_run_training_through_the_shim_is_bit_identical(tmp_path, mode):
+    """run_training (DS, W=16 / N=4, momentum, isotropic quadratic, 12
+    iterations) linked with the B200 shim ends with the same params, bit for
+    bit, as the pure reference build."""
+    import json
+
+    import numpy as np
+    for p in (SHIM_PURE, SHIM_B200):
+        if not os.path.exists(p):
+            pytest.skip(f"{p} not built (make -C oracle shimbench)")
+    out = {}
+    for tag, exe in (("ref", SHIM_PURE), ("b200", SHIM_B200)):
+        f = str(tmp_path / f"{tag}.bin")
+        r = subprocess.run([exe, "20001", "12", "16", "4", mode, f], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[tag] = (json.loads(r.stdout.strip().splitlines()[-1]), np.fromfile(f))
+    assert out["ref"][1].size == 16 * 20001
+    assert np.array_equal(out["ref"][1], out["b200"][1])
+    assert out["ref"][0]["final_suboptimality"] == out["b200"][0]["final_suboptimality"]
