@@ -348,7 +348,16 @@ def cpu_run_training_c1():
 
 
 # ---------------------------------------------------------------------------
-def step_bytes(cfg, G, rank, d_pad, path=0, esz=4):
+def gpu_map(cfg, G, placement):
+    """gpu_of / row_of of every global rank for the DS engines (dss_placement)."""
+    from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig
+    from paper_2007_03298_b200 import placement as place
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(cfg["W"], cfg["N"]), 1, cfg["rect"])
+    gpu, row, tiling = place(s, G, placement)
+    return gpu, row, tiling
+
+
+def step_bytes(cfg, G, rank, d_pad, path=0, esz=4, placement=0):
     """Algorithmic bytes one GPU moves per DS / BSP iteration, by kernel kind,
     averaged over the two schedule parities (block / comb iterations).
       group: fused apply_step + fold of local groups, d * bytes_per_elem per
@@ -362,7 +371,8 @@ def step_bytes(cfg, G, rank, d_pad, path=0, esz=4):
     W, N, d = cfg["W"], cfg["N"], cfg["d"]
     bpe = BYTES_PER_ELEM[cfg["opt"]] * esz // 4
     P = W // G
-    mine = set(range(rank * P, (rank + 1) * P))
+    gpu_of = gpu_map(cfg, G, placement)[0]
+    mine = {k for k in range(W) if gpu_of[k] == rank}
     out = {"ds": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0},
            "bsp": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0}}
     s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
@@ -381,12 +391,12 @@ def step_bytes(cfg, G, rank, d_pad, path=0, esz=4):
             here = [m for m in g if m in mine]
             if not here:
                 continue
-            gpus = sorted({m // P for m in g})
+            gpus = sorted({gpu_of[m] for m in g})
             if len(gpus) == 1 or path == 3:
                 out["ds"]["group"] += 0.5 * len(here) * d * bpe
             if len(gpus) == 1:
                 continue
-            if max(sum(1 for m in g if m // P == q) for q in gpus) >= 2:  # ordered chain
+            if max(sum(1 for m in g if gpu_of[m] == q) for q in gpus) >= 2:  # ordered chain
                 out["ds"]["chain_nvlink"] += 0.5 * chain_out(gpus)
                 continue
             S, j = len(gpus), gpus.index(rank)
@@ -420,7 +430,7 @@ class NcclBaseline:
     with one broadcast copy; a GPU holding exactly one member of every group
     all-reduces its own row in place."""
 
-    def __init__(self, e, cfg, G, rank):
+    def __init__(self, e, cfg, G, rank, placement=0):
         import torch
         import torch.distributed as dist
         from paper_2007_03298_b200 import (BUF_GRADS, BUF_PARAMS, StrategyKind, SyncStrategy, Topology,
@@ -428,25 +438,26 @@ class NcclBaseline:
         self.e, self.cfg, self.G, self.rank = e, cfg, G, rank
         W, N, d = cfg["W"], cfg["N"], cfg["d"]
         P = W // G
-        self.P, self.first = P, rank * P
+        self.P = P
+        gpu_of, row_of, _ = gpu_map(cfg, G, placement)
+        first = e.local_ranks[0]  # local row 0
         stride = e.row_stride
-        self.params = self._view(e, BUF_PARAMS, self.first, P, stride)[:, :d]
-        self.grads = self._view(e, BUF_GRADS, self.first, P, stride)[:, :d]
+        self.params = self._view(e, BUF_PARAMS, first, P, stride)[:, :d]
+        self.grads = self._view(e, BUF_GRADS, first, P, stride)[:, :d]
         s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
         self.plans = []
         comms = {}
         for p in (0, 1):
             by_set = {}
             for g in make_partition(s, p).groups:
-                gpus = tuple(sorted({m // P for m in g}))
+                gpus = tuple(sorted({gpu_of[m] for m in g}))
                 by_set.setdefault(gpus, []).append(g)
             plan = []
             for gpus, groups in sorted(by_set.items()):
                 if gpus not in comms:
                     comms[gpus] = dist.new_group(list(gpus)) if len(gpus) > 1 else None
                 if rank in gpus:
-                    local = [self._rows([m - self.first for m in g if self.first <= m < self.first + P])
-                             for g in groups]
+                    local = [self._rows([row_of[m] for m in g if gpu_of[m] == rank]) for g in groups]
                     plan.append((comms[gpus], groups, local))
             self.plans.append(plan)
         self.acc = torch.empty(d, dtype=torch.float32, device="cuda")
@@ -548,7 +559,8 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False
     def make(kind):
         s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W), 1,
                          cfg["rect"] and kind == StrategyKind.DS_SYNC)
-        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, dtype, local, rank, G, path=args.path)
+        e = DsSyncEngine(s, OptimizerKind(cfg["opt"]), d, hp, dtype, local, rank, G, path=args.path,
+                         placement=args.placement if kind == StrategyKind.DS_SYNC else 0)
         e.set_stream(stream.cuda_stream)
         if G > 1:
             from paper_2007_03298_b200.dist import attach
@@ -634,7 +646,7 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False
             e.check()
             del hg, hw
         if G > 1 and with_nccl:
-            nb = NcclBaseline(e, cfg, G, rank)
+            nb = NcclBaseline(e, cfg, G, rank, args.placement if name == "ds" else 0)
             fn = (lambda t: nb.ds_step(t, cfg["alpha"])) if name == "ds" else (lambda t: nb.bsp_step(t, cfg["alpha"]))
             for t in range(3):
                 fn(t)
@@ -644,7 +656,7 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False
         del e
         torch.cuda.synchronize()
     d_pad = (d + 63) // 64 * 64
-    res["bytes"] = step_bytes(cfg, G, rank, d_pad, args.path, esz)
+    res["bytes"] = step_bytes(cfg, G, rank, d_pad, args.path, esz, args.placement)
     return res
 
 
@@ -780,6 +792,9 @@ def our_arm(args, cfg):
            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic: isotropic-quadratic gradients (SplitMix64/Box-Muller, seeds 7/1), device-resident",
            "config": head["config"]}
+    if G > 1:
+        out["placement"] = {"mode": ["contiguous", "tiled"][args.placement],
+                            "tiling_gr_gc": list(gpu_map(cfg, G, args.placement)[2])}
     if args.path:
         out["fold_path"] = {2: "chain forced for every spanning group", 3: "unfused pull two-shot"}.get(
             args.path, args.path)
@@ -855,6 +870,8 @@ def main():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--d", type=int, default=None, help="override the config's d (profiling runs)")
     ap.add_argument("--path", type=int, default=0, help="fold path: 0 auto, 2 chain for every spanning group")
+    ap.add_argument("--placement", type=int, default=0,
+                    help="DS worker placement over the GPUs: 0 contiguous, 1 tiled (dss_config.placement)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -119,6 +119,14 @@ typedef struct {
                            params (DS, sync_round) or the gradients (BSP) through the same
                            ordered group fold, without an optimizer step
                            (sync.cpp:203-213, 386-411). */
+  int placement;        /* worker placement over the GPUs (DS-Sync, n_gpus > 1):
+                           0 = contiguous packing, gpu(k) = k / (W/G).
+                           1 = tiled: the K x N (block x comb) grid of W = N*K workers is
+                           cut into gr x gc tiles, one per GPU, so blocks span gc GPUs
+                           and combs gr GPUs; (gr, gc) minimises the cross-GPU rows of
+                           the busier schedule parity (dss_placement).  Groups, fold
+                           order and results are unchanged; only which GPU holds which
+                           worker.  Ignored (contiguous) for BSP and single-group worlds. */
 } dss_config;
 
 typedef struct dss_ctx dss_ctx;
@@ -151,6 +159,12 @@ int dss_check_mixing(const dss_strategy* s, long t);
  * ring 2m-1 / 2m-1, tree 3log2m / m*log2m + 2(m-1), ps 2m / 2*m*min(P, dim)). */
 int dss_round_outcome(const dss_strategy* s, long t, long payload_dim, dss_outcome* out);
 
+/* Worker placement: gpu_of[k] and row_of[k] (the local row on that GPU) for
+ * every global rank k of a context created with this strategy, n_gpus and
+ * placement mode (dss_config.placement); *gr / *gc receive the tiling
+ * (0, 0 for contiguous packing).  Host only. */
+int dss_placement(const dss_strategy* s, int n_gpus, int placement, int* gpu_of, int* row_of, int* gr, int* gc);
+
 /* Multi-GPU plan for (strategy, t, n_gpus, rank): how many groups this GPU
  * folds locally, how many span GPUs, and the [lo, hi) element slice this GPU
  * owns in each spanning group (two-shot ownership).  Host-only, for tests. */
@@ -176,6 +190,11 @@ int dss_set_stream(dss_ctx* ctx, void* cuda_stream);
 
 /* First global rank hosted here and how many (P = W / n_gpus). */
 int dss_local_workers(const dss_ctx* ctx, int* first_rank, int* count);
+/* Global ranks of this GPU's workers in local-row order (count entries): the
+ * row order of dss_upload_all / dss_download_all.  Contiguous packing gives
+ * first_rank, first_rank + 1, ...; with the tiled placement first_rank is -1
+ * and the ranks come from here. */
+int dss_local_ranks(const dss_ctx* ctx, int* ranks);
 
 /* Padded row length in elements (multiple of 64) and element size in bytes. */
 long dss_row_stride(const dss_ctx* ctx);
@@ -369,6 +388,15 @@ enum {
 int dss_kernel_times_by_kind(dss_ctx* ctx, double* total_ms, long* launches);
 /* gpu_launches: hot-path kernels launched since creation (all kinds). */
 long dss_launch_count(const dss_ctx* ctx);
+
+/* ---- diagnostics ---- */
+/* With DSS_GUARD_BYTES=n in the environment at dss_create, every device
+ * allocation of the context carries n bytes (rounded up to 256) of 0xA5 on
+ * both sides.  dss_check_guards synchronizes the context's stream and
+ * counts overwritten guard bytes (*corrupted; DSS_ERUNTIME when nonzero):
+ * an out-of-bounds-write check that needs no compute-sanitizer.  Without
+ * the variable it checks nothing and returns DSS_OK. */
+int dss_check_guards(dss_ctx* ctx, long* corrupted);
 
 /* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
 /* CUDA IPC handles of this GPU's params, grads, mean-gradient, barrier-flag,

@@ -34,6 +34,7 @@ from .api import (  # noqa: F401
     make_shards,
     mlp_dataset,
     mlp_initial_params,
+    placement,
     quadratic_problem,
     round_outcome,
     sync_round,

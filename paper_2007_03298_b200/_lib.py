@@ -40,7 +40,7 @@ class dss_outcome(C.Structure):
 class dss_config(C.Structure):
     _fields_ = [("strategy", dss_strategy), ("optimizer", C.c_int), ("hp", dss_hparams),
                 ("dtype", C.c_int), ("dim", C.c_long), ("device", C.c_int), ("rank", C.c_int),
-                ("n_gpus", C.c_int), ("path", C.c_int), ("stats_dim", C.c_long)]
+                ("n_gpus", C.c_int), ("path", C.c_int), ("stats_dim", C.c_long), ("placement", C.c_int)]
 
 
 class dss_plan_summary(C.Structure):
@@ -64,6 +64,9 @@ SIGNATURES = {
     "dss_destroy": (C.c_int, [_P]),
     "dss_set_stream": (C.c_int, [_P, _P]),
     "dss_local_workers": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "dss_local_ranks": (C.c_int, [_P, _P]),
+    "dss_placement": (C.c_int, [C.POINTER(dss_strategy), C.c_int, C.c_int, _P, _P, C.POINTER(C.c_int),
+                                C.POINTER(C.c_int)]),
     "dss_row_stride": (C.c_long, [_P]),
     "dss_elem_size": (C.c_int, [_P]),
     "dss_device_ptr": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_P)]),
@@ -112,6 +115,7 @@ SIGNATURES = {
     "dss_ipc_export": (C.c_int, [_P, _P]),
     "dss_ipc_attach": (C.c_int, [_P, _P]),
     "dss_barrier": (C.c_int, [_P]),
+    "dss_check_guards": (C.c_int, [_P, C.POINTER(C.c_long)]),
 }
 
 _lib = None

@@ -256,6 +256,19 @@ def check_mixing(cfg, t: int) -> bool:  # schedule.cpp:67-90
     return r == 1
 
 
+def placement(strategy: SyncStrategy, n_gpus: int, mode: int = 1):
+    """Worker placement of a context (dss_placement): (gpu_of, row_of, (gr, gc))
+    for every global rank; (0, 0) is contiguous packing."""
+    s = _c_strategy(strategy)
+    W = strategy.world.world_size
+    gpu = np.zeros(W, dtype=np.int32)
+    row = np.zeros(W, dtype=np.int32)
+    gr, gc = C.c_int(), C.c_int()
+    _check_global(L.load().dss_placement(C.byref(s), n_gpus, mode, gpu.ctypes.data, row.ctypes.data, C.byref(gr),
+                                         C.byref(gc)))
+    return gpu.tolist(), row.tolist(), (gr.value, gc.value)
+
+
 def round_outcome(strategy: SyncStrategy, t: int, payload_dim: int) -> SyncRoundOutcome:
     s = _c_strategy(strategy)
     o = L.dss_outcome()
@@ -344,7 +357,7 @@ class DsSyncEngine:
 
     def __init__(self, strategy: SyncStrategy, optimizer: OptimizerKind, dim: int,
                  hp: Optional[OptimizerHyperparams] = None, dtype: str = "f32", device: int = 0,
-                 rank: int = 0, n_gpus: int = 1, path: int = 0, stats_dim: int = 0):
+                 rank: int = 0, n_gpus: int = 1, path: int = 0, stats_dim: int = 0, placement: int = 0):
         hp = hp or OptimizerHyperparams()
         self.lib = L.load()
         self.strategy = strategy
@@ -362,6 +375,7 @@ class DsSyncEngine:
         cfg.n_gpus = n_gpus
         cfg.path = path
         cfg.stats_dim = stats_dim
+        cfg.placement = placement
         self.stats_dim = int(stats_dim)
         h = C.c_void_p()
         st = self.lib.dss_create(C.byref(cfg), C.byref(h))
@@ -371,6 +385,10 @@ class DsSyncEngine:
         first, count = C.c_int(), C.c_int()
         self.lib.dss_local_workers(self.h, C.byref(first), C.byref(count))
         self.first_rank, self.local_workers = first.value, count.value
+        ranks = np.zeros(max(count.value, 1), dtype=np.int32)
+        self.lib.dss_local_ranks(self.h, ranks.ctypes.data)
+        # global ranks of the local rows: the row order of upload_all / download_all
+        self.local_ranks = ranks[:count.value].tolist()
         self.n_gpus = n_gpus
         self.rank = rank
 
@@ -595,6 +613,12 @@ class DsSyncEngine:
 
     def check(self) -> None:
         self._ck(self.lib.dss_check(self.h))
+
+    def check_guards(self) -> int:
+        """Overwritten guard-band bytes (DSS_GUARD_BYTES debug mode); raises if any."""
+        n = C.c_long()
+        self._ck(self.lib.dss_check_guards(self.h, C.byref(n)))
+        return n.value
 
     def clear_error(self) -> None:
         self._ck(self.lib.dss_clear_error(self.h))

@@ -126,7 +126,14 @@ struct ParityPlan {
 struct dss_ctx {
   dss_config cfg{};
   int P = 0;            // local workers
-  int first = 0;        // first global rank here
+  int first = 0;        // first SLOT here (slot = gpu * P + local row)
+  // worker placement: slot of every global rank and its inverse (identity for
+  // contiguous packing); every plan and kernel table works in slots, error
+  // keys carry global ranks (rank_of: local row -> global rank on the device)
+  std::vector<int> slot_of, rank_of_slot;
+  bool placed = false;
+  int tile_gr = 0, tile_gc = 0;
+  int* d_rank_of = nullptr;
   long d = 0, d_pad = 0;
   int esz = 4;
   int sms = 148;
@@ -239,6 +246,11 @@ struct dss_ctx {
   long last_iteration = -1;
 
   std::vector<void*> allocations;
+  // guard bands (DSS_GUARD_BYTES, debug): every device allocation gets
+  // `guard` bytes of 0xA5 on both sides, checked by dss_check_guards --
+  // an out-of-bounds-write detector where compute-sanitizer is unavailable
+  long guard = 0;
+  std::vector<std::pair<char*, size_t>> guarded;  // (user pointer, user bytes)
 };
 
 namespace dssb {
@@ -269,12 +281,21 @@ int guard(dss_ctx* c, F&& f) {
   }
 }
 
+constexpr unsigned char kGuardByte = 0xA5;
+
 inline void* dalloc(dss_ctx* c, size_t bytes) {
   void* p = nullptr;
-  ck(cudaMalloc(&p, bytes), "cudaMalloc");
-  ck(cudaMemsetAsync(p, 0, bytes, c->stream), "cudaMemset");
+  const size_t g = static_cast<size_t>(c->guard);
+  ck(cudaMalloc(&p, bytes + 2 * g), "cudaMalloc");
   c->allocations.push_back(p);
-  return p;
+  char* user = static_cast<char*>(p) + g;
+  if (g) {
+    ck(cudaMemsetAsync(p, kGuardByte, g, c->stream), "guard");
+    ck(cudaMemsetAsync(user + bytes, kGuardByte, g, c->stream), "guard");
+    c->guarded.push_back({user, bytes});
+  }
+  ck(cudaMemsetAsync(user, 0, bytes, c->stream), "cudaMemset");
+  return user;
 }
 
 template <typename T>
@@ -288,6 +309,14 @@ T* upload_table(dss_ctx* c, const std::vector<T>& v) {
 }
 
 inline bool multi(const dss_ctx* c) { return c->cfg.n_gpus > 1; }
+
+// The schedule of iteration t in slot space (see dss_ctx::slot_of).
+inline Partition part_at(const dss_ctx* c, long t) {
+  Partition p = make_partition(c->cfg.strategy, t);
+  return c->placed ? to_slots(p, c->slot_of) : p;
+}
+// Global rank of a slot (error keys and DivergenceError carry global ranks).
+inline int grank(const dss_ctx* c, int slot) { return c->rank_of_slot[static_cast<size_t>(slot)]; }
 inline bool force_fold(const dss_ctx* c) { return c->cfg.path == 1 && !multi(c); }
 inline bool force_chain(const dss_ctx* c) { return c->cfg.path == 2 && multi(c); }
 inline bool use_push(const dss_ctx* c) { return multi(c) && c->cfg.path != 3; }  // path 3: unfused pull two-shot (A/B)

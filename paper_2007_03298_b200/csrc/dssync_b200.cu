@@ -131,6 +131,18 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       throw std::invalid_argument("at most " + std::to_string(kMaxLocal) + " workers per GPU");
     }
     c->first = cfg->rank * c->P;
+    {
+      const Tiling tl = (cfg->placement == 1 && cfg->n_gpus > 1) ? choose_tiling(s, cfg->n_gpus) : Tiling{};
+      c->slot_of = placement_slots(s, cfg->n_gpus, tl);
+      c->rank_of_slot.assign(c->slot_of.size(), 0);
+      for (size_t k = 0; k < c->slot_of.size(); ++k) {
+        c->rank_of_slot[static_cast<size_t>(c->slot_of[k])] = static_cast<int>(k);
+        c->placed = c->placed || c->slot_of[k] != static_cast<int>(k);
+      }
+      c->tile_gr = c->placed ? tl.gr : 0;
+      c->tile_gc = c->placed ? tl.gc : 0;
+    }
+    if (cfg->placement < 0 || cfg->placement > 1) throw std::invalid_argument("placement must be 0 or 1");
     c->d = cfg->dim;
     c->d_pad = pad_dim(cfg->dim);
     c->esz = cfg->dtype == DSS_F64 ? 8 : 4;
@@ -141,6 +153,10 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     if (cfg->device < 0 || cfg->device >= ndev) throw CudaError("no CUDA device " + std::to_string(cfg->device));
     ck(cudaSetDevice(cfg->device), "cudaSetDevice");
     ck(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, cfg->device), "sm count");
+    if (const char* gb = std::getenv("DSS_GUARD_BYTES")) {  // debug: guard bands around every allocation
+      const long v = std::atol(gb);
+      c->guard = v > 0 ? (v + 255) / 256 * 256 : 0;
+    }
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own_stream;
 
@@ -167,6 +183,11 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         dalloc(c.get(), sizeof(unsigned long long) * static_cast<size_t>(std::max(cfg->n_gpus, 32))));
     ck(cudaMallocHost(&c->h_err, sizeof(unsigned long long)), "cudaMallocHost");
 
+    {
+      std::vector<int> rk(static_cast<size_t>(c->P));
+      for (int l = 0; l < c->P; ++l) rk[static_cast<size_t>(l)] = c->rank_of_slot[static_cast<size_t>(c->first + l)];
+      c->d_rank_of = upload_table(c.get(), rk);
+    }
     std::vector<std::vector<int>> singles;
     for (int k = 0; k < c->P; ++k) singles.push_back({c->first + k});
     c->apply_launch = make_group_launch(c.get(), singles);
@@ -175,7 +196,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // plan is global, so every GPU computes the same slot count)
       int slots = 0;
       for (long t = 0; t < (s.kind == DSS_DS_SYNC ? 2 : 1); ++t) {
-        const GpuPlan gp = make_plan(make_partition(s, t), s.world_size, cfg->n_gpus, cfg->rank, c->d_pad,
+        const GpuPlan gp = make_plan(part_at(c.get(), t), s.world_size, cfg->n_gpus, cfg->rank, c->d_pad,
                                      force_chain(c.get()));
         slots = std::max(slots, gp.max_chain_slots);
       }
@@ -183,8 +204,10 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       world.kind = DSS_BSP;
       world.group_size = s.world_size;
       world.rectangular = 0;
-      slots = std::max(slots, make_plan(make_partition(world, 0), s.world_size, cfg->n_gpus, cfg->rank, c->d_pad,
-                                        force_chain(c.get())).max_chain_slots);
+      if (!c->placed) {  // placed worlds fold the global mean two-shot (build_mean_plan)
+        slots = std::max(slots, make_plan(make_partition(world, 0), s.world_size, cfg->n_gpus, cfg->rank, c->d_pad,
+                                          force_chain(c.get())).max_chain_slots);
+      }
       c->chain_slots = slots;
       c->chain_chunk = std::min<long>(c->d_pad, DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
@@ -194,7 +217,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // GPU, because a pusher applies its own offset to the peer's buffer.
       long ps = 0, pf = 0;
       for (long t = 0; t < (s.kind == DSS_DS_SYNC ? 2 : 1); ++t) {
-        const Partition part = make_partition(s, t);
+        const Partition part = part_at(c.get(), t);
         for (int q = 0; q < cfg->n_gpus; ++q) {
           long st = 0, fl = 0;
           owned_layout(c.get(), part, q, c->chain_chunk, &st, &fl);
@@ -220,7 +243,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       }
       for (long t = 0; t < 2; ++t) {
         if (s.kind != DSS_DS_SYNC || !use_push(c.get()) || force_chain(c.get()) || cfg->path == 4) break;
-        const Partition part = make_partition(s, t);
+        const Partition part = part_at(c.get(), t);
         const bool small = c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
         bool ok = true;
         long rmax = 0;
@@ -302,9 +325,34 @@ extern "C" int dss_set_stream(dss_ctx* c, void* s) {
 
 extern "C" int dss_local_workers(const dss_ctx* c, int* first_rank, int* count) {
   if (!c || !first_rank || !count) return DSS_EINVAL;
-  *first_rank = c->first;
+  *first_rank = c->placed ? -1 : c->first;
   *count = c->P;
   return DSS_OK;
+}
+
+extern "C" int dss_local_ranks(const dss_ctx* c, int* ranks) {
+  if (!c || !ranks) return DSS_EINVAL;
+  for (int l = 0; l < c->P; ++l) ranks[l] = c->rank_of_slot[static_cast<size_t>(c->first + l)];
+  return DSS_OK;
+}
+
+extern "C" int dss_placement(const dss_strategy* s, int n_gpus, int placement, int* gpu_of, int* row_of, int* gr,
+                             int* gc) {
+  if (!s || n_gpus < 1 || s->world_size < 1 || s->world_size % n_gpus) {
+    return fail(nullptr, DSS_EINVAL, "dss_placement: world_size must be a multiple of n_gpus");
+  }
+  return guard(nullptr, [&]() -> int {
+    const Tiling tl = (placement == 1 && n_gpus > 1) ? choose_tiling(*s, n_gpus) : Tiling{};
+    const std::vector<int> slot = placement_slots(*s, n_gpus, tl);
+    const int P = s->world_size / n_gpus;
+    for (size_t k = 0; k < slot.size(); ++k) {
+      if (gpu_of) gpu_of[k] = slot[k] / P;
+      if (row_of) row_of[k] = slot[k] % P;
+    }
+    if (gr) *gr = tl.gr;
+    if (gc) *gc = tl.gc;
+    return DSS_OK;
+  });
 }
 
 extern "C" long dss_row_stride(const dss_ctx* c) { return c ? c->d_pad : -1; }
@@ -414,8 +462,10 @@ extern "C" int dss_set_step_count(dss_ctx* c, int rank, long step_count) {
 }
 
 extern "C" long dss_get_step_count(const dss_ctx* c, int rank) {
-  if (!c || rank < c->first || rank >= c->first + c->P) return -1;
-  return c->step_count[static_cast<size_t>(rank - c->first)];
+  if (!c || rank < 0 || rank >= static_cast<int>(c->slot_of.size())) return -1;
+  const int slot = c->slot_of[static_cast<size_t>(rank)];
+  if (slot < c->first || slot >= c->first + c->P) return -1;
+  return c->step_count[static_cast<size_t>(slot - c->first)];
 }
 
 // ------------------------------- hot path ------------------------------------
@@ -798,7 +848,8 @@ void fingerprint(const dss_ctx* c, long long* f) {
       c->cfg.dtype, c->cfg.optimizer, c->cfg.strategy.kind, c->cfg.strategy.topology,
       c->cfg.strategy.world_size, c->cfg.strategy.group_size, c->cfg.strategy.rectangular,
       c->cfg.n_gpus, c->P, c->d, c->d_pad, c->s, c->chain_slots, c->chain_chunk,
-      c->oneshot_base_elems, c->oneshot_half_elems, c->oneshot_rows, c->oneshot_ack_off, c->cfg.path};
+      c->oneshot_base_elems, c->oneshot_half_elems, c->oneshot_rows, c->oneshot_ack_off,
+      c->cfg.path * 1000003LL + c->guard + (static_cast<long long>(c->tile_gr * 64 + c->tile_gc) << 40)};
   std::memcpy(f, v, sizeof(v));
 }
 }  // namespace
@@ -875,6 +926,7 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
         }
         c->opened.push_back(p[b]);
       }
+      for (int b = 0; b < 9; ++b) p[b] = static_cast<char*>(p[b]) + c->guard;  // guard bands: user region
       c->peer_w[static_cast<size_t>(r)] = p[0];
       c->peer_g[static_cast<size_t>(r)] = p[1];
       c->peer_mg[static_cast<size_t>(r)] = p[2];
@@ -891,6 +943,34 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
     barrier(c);
     ck(cudaStreamSynchronize(c->stream), "attach sync");
     return check_impl(c) == DSS_OK ? DSS_OK : c->last_status;
+  });
+}
+
+extern "C" int dss_check_guards(dss_ctx* c, long* corrupted) {
+  if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  return guard(c, [&]() -> int {
+    ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(c->stream), "guard sync");
+    long bad = 0, first = -1;
+    std::vector<unsigned char> h(static_cast<size_t>(c->guard));
+    for (size_t i = 0; i < c->guarded.size(); ++i) {
+      const auto& gb = c->guarded[i];
+      for (const char* band : {gb.first - c->guard, gb.first + gb.second}) {
+        ck(cudaMemcpy(h.data(), band, h.size(), cudaMemcpyDeviceToHost), "guard readback");
+        for (unsigned char v : h) {
+          if (v != kGuardByte) {
+            ++bad;
+            if (first < 0) first = static_cast<long>(i);
+          }
+        }
+      }
+    }
+    if (corrupted) *corrupted = bad;
+    if (bad) {
+      return fail(c, DSS_ERUNTIME, "guard bands overwritten: " + std::to_string(bad) + " bytes (first in allocation " +
+                                       std::to_string(first) + " of " + std::to_string(c->guarded.size()) + ")");
+    }
+    return DSS_OK;
   });
 }
 

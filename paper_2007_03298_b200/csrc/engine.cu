@@ -150,7 +150,7 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
                        : chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
       a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
     }
-    a.err_rank = r.first_member;
+    a.err_rank = grank(c, r.first_member);
     a.err_phase = err_phase;
     a.m = r.m;
     ea.push_back(a);
@@ -243,7 +243,7 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
         it.ndst = 1;
         item_dst.push_back(stage + static_cast<size_t>(it.lo - sl.lo) * c->esz);
         item_flag.push_back(flags + ch);
-        it.rank = my_member;
+        it.rank = grank(c, my_member);
         item_keys.push_back({ch * 64 + oo, static_cast<long>(items.size())});
         items.push_back(it);
       }
@@ -263,7 +263,7 @@ PushLaunch build_push(dss_ctx* c, const Partition& part, long t) {
       f.S = S;
       f.dst_beg = dst_beg;
       f.n_dst = m;
-      f.err_rank = mem[0];
+      f.err_rank = grank(c, mem[0]);
       folds.push_back(f);
     }
   }
@@ -337,7 +337,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
         it.hi = std::min(c->d_pad, it.lo + CH);
         it.dst_beg = static_cast<int>(item_dst.size());
         it.ndst = S;
-        it.rank = mem[q];
+        it.rank = grank(c, mem[q]);
         for (int oo = 0; oo < S; ++oo) {
           const int o = (oo + j) % S;
           const int gpu = gpus[static_cast<size_t>(o)];
@@ -367,7 +367,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
       f.S = m;
       f.dst_beg = dst_beg;
       f.n_dst = static_cast<int>(mine.size());
-      f.err_rank = mem[0];
+      f.err_rank = grank(c, mem[0]);
       folds.push_back(f);
     }
   }
@@ -400,7 +400,7 @@ PushLaunch build_oneshot(dss_ctx* c, const Partition& part) {
 ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
   ParityPlan pp;
   const dss_strategy& s = c->cfg.strategy;
-  const Partition part = make_partition(s, t);
+  const Partition part = part_at(c, t);
   const int G = multi(c) ? c->cfg.n_gpus : 1;
   std::vector<std::vector<int>> local, span_members;
   std::vector<Slice> owned;
@@ -492,7 +492,7 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
       e.dst_cnt = m;
       e.lo = sl.lo;
       e.hi = sl.hi;
-      e.err_rank = mem[0];
+      e.err_rank = grank(c, mem[0]);
       e.err_phase = s.kind == DSS_BSP ? 0 : 1;
       if (m > kMaxFold) throw std::invalid_argument("group spans more members than the fold kernel holds (64)");
       for (int j = 0; j < m; ++j) {
@@ -609,6 +609,35 @@ ParityPlan build_mean_plan(dss_ctx* c) {
     return pp;
   }
   const int G = c->cfg.n_gpus;
+  if (c->placed) {
+    // tiled placement: rank order visits the GPUs several times, so the
+    // ordered chain does not apply; GPU j folds slice j of all W rows (peer
+    // loads in rank order) into every GPU's mean row
+    pp.any_spanning = pp.any_twoshot = true;
+    long lo = 0, hi = 0;
+    slice_range(c->d_pad, G, c->cfg.rank, &lo, &hi);
+    if (hi > lo) {
+      if (W > kMaxFold) throw std::invalid_argument("global mean supports at most 64 workers");
+      FoldEntry e{};
+      std::vector<void*> src, dst;
+      e.src_cnt = W;
+      e.dst_cnt = G;
+      e.lo = lo;
+      e.hi = hi;
+      e.err_rank = 0;
+      e.err_phase = 1;
+      for (int k = 0; k < W; ++k) src.push_back(row_ptr(c, c->peer_w, c->slot_of[static_cast<size_t>(k)]));
+      for (int q = 0; q < G; ++q) dst.push_back(c->peer_mg[static_cast<size_t>(q)]);
+      pp.fold.entries = 1;
+      pp.fold.uniform_m = W;
+      pp.fold.max_len = hi - lo;
+      pp.fold.d_entries = upload_table(c, std::vector<FoldEntry>{e});
+      pp.fold.d_src = upload_table(c, src);
+      pp.fold.d_dst = upload_table(c, dst);
+    }
+    pp.built = true;
+    return pp;
+  }
   const GpuPlan gp = make_plan(part, W, G, c->cfg.rank, c->d_pad, force_chain(c));
   pp.any_spanning = true;
   pp.any_twoshot = gp.any_twoshot_globally;
@@ -680,7 +709,7 @@ ParityPlan build_stats_plan(dss_ctx* c, const Partition& part) {
     e.dst_cnt = m;
     e.lo = lo;
     e.hi = hi;
-    e.err_rank = c->cfg.strategy.kind == DSS_BSP ? 0 : mem[0];
+    e.err_rank = c->cfg.strategy.kind == DSS_BSP ? 0 : grank(c, mem[0]);
     e.err_phase = c->cfg.strategy.kind == DSS_BSP ? 0 : 1;
     for (int j = 0; j < m; ++j) {
       const int gpu = mem[j] / c->P;
@@ -711,7 +740,7 @@ ParityPlan build_stats_plan(dss_ctx* c, const Partition& part) {
 void build_stats_plans(dss_ctx* c) {
   if (c->s == 0) return;
   const dss_strategy& s = c->cfg.strategy;
-  for (int p = 0; p < (s.kind == DSS_DS_SYNC ? 2 : 1); ++p) c->stats_plan[p] = build_stats_plan(c, make_partition(s, p));
+  for (int p = 0; p < (s.kind == DSS_DS_SYNC ? 2 : 1); ++p) c->stats_plan[p] = build_stats_plan(c, part_at(c, p));
 }
 
 void build_plans(dss_ctx* c) {
@@ -793,6 +822,7 @@ void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double al
   a.g_ld = g_ld;
   a.nvec = a.ld / Vec<T>::n;
   a.first_rank = c->first;
+  a.rank_of = c->d_rank_of;
   a.members = gl.d_members;
   a.offsets = gl.d_offsets;
   a.step_phase = step_phase;
@@ -915,6 +945,7 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
   a.m2 = static_cast<T*>(c->m2);
   a.ld = c->d_pad;
   a.first_rank = c->first;
+  a.rank_of = c->d_rank_of;
   a.step_phase = c->cfg.strategy.kind == DSS_BSP ? 1 : 0;
   a.c = consts<T>(c, alpha);
   fill_bias(c, a);
@@ -954,6 +985,7 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   a.m2 = static_cast<T*>(c->m2);
   a.ld = c->d_pad;
   a.first_rank = c->first;
+  a.rank_of = c->d_rank_of;
   a.t = t;
   a.epoch = c->chain_epoch;
   a.err = c->d_err;
@@ -1136,10 +1168,11 @@ int check_impl(dss_ctx* c) {
 }
 
 int check_rank(dss_ctx* c, int rank, int* lr) {
-  if (rank < c->first || rank >= c->first + c->P) {
+  const int slot = rank >= 0 && rank < static_cast<int>(c->slot_of.size()) ? c->slot_of[static_cast<size_t>(rank)] : -1;
+  if (slot < c->first || slot >= c->first + c->P) {
     throw std::invalid_argument("rank " + std::to_string(rank) + " is not hosted on this GPU");
   }
-  *lr = rank - c->first;
+  *lr = slot - c->first;
   return DSS_OK;
 }
 
@@ -1213,7 +1246,7 @@ void run_small(dss_ctx* c, long t0, long n, const double* alphas, bool logistic)
   const dss_strategy& s = c->cfg.strategy;
   if (!c->d_small_members[0]) {  // schedule tables of both parities, once
     for (int p = 0; p < 2; ++p) {
-      const Partition part = make_partition(s, p);
+      const Partition part = part_at(c, p);
       c->d_small_members[p] = upload_table(c, part.members);
       c->d_small_offsets[p] = upload_table(c, part.offsets);
       c->small_ngroups[p] = part.n_groups();

@@ -179,6 +179,7 @@ template <typename T> struct ChainArgs {
   T* m2;
   long ld;
   int first_rank;
+  const int* rank_of;  // local row -> global rank (error keys)
   int step_phase;
   StepConsts<T> c;
   double bc1[kMaxLocal];
@@ -220,7 +221,7 @@ __device__ __forceinline__ Pack<T> chain_step(const ChainArgs<T>& a, T* wrow, in
   if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
   if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
   if (!ok) {
-    const unsigned long long k = err_key(a.t, phase, a.first_rank + lr);
+    const unsigned long long k = err_key(a.t, phase, a.rank_of[lr]);
     bad = k < bad ? k : bad;
   }
   return x;
@@ -253,7 +254,7 @@ __device__ __forceinline__ void chain_step_batch(const ChainArgs<T>& a, T* const
     if constexpr (OPT != kSgd) stv(a.m1 + r, s1[q]);
     if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2[q]);
     if (!ok) {
-      const unsigned long long k = err_key(a.t, phase, a.first_rank + lr[q]);
+      const unsigned long long k = err_key(a.t, phase, a.rank_of[lr[q]]);
       bad = k < bad ? k : bad;
     }
     out[q] = x[q];
@@ -510,6 +511,7 @@ template <typename T> struct PushArgs {
   T* m2;
   long ld;
   int first_rank;
+  const int* rank_of;  // local row -> global rank (error keys)
   long t;
   unsigned long long epoch;
   unsigned long long* err;
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
             if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
             if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
             if (!oks) {
-              const unsigned long long k = err_key(a.t, 1, a.first_rank + lr);
+              const unsigned long long k = err_key(a.t, 1, a.rank_of[lr]);
               bad = k < bad ? k : bad;
             }
           }

@@ -59,7 +59,7 @@ struct LogisticArgs {
   double l2;
   uint64_t seed;
   long t;
-  int first_rank;
+  const int* rank_of;     // local row -> global rank (RNG streams, shards, error keys)
   unsigned long long* gerr;  // gradient failure latch: t << 32 | rank
   int hidden;             // MLP hidden units (0: logistic)
   long obs_ld;            // MLP: row stride of the running-stat observation rows
@@ -71,7 +71,7 @@ __device__ __forceinline__ double softplus_dev(double z) {  // problems.cpp:338-
 
 // sample_batch (sync.cpp:153-179) for local worker k, into a.batch[k].
 __device__ inline void sample_batch_dev(const LogisticArgs& a, int k) {
-  const int rank = a.first_rank + k;
+  const int rank = a.rank_of[k];
   const int* sh = a.shard + a.shard_off[k];
   const long size = a.shard_off[k + 1] - a.shard_off[k];
   int* bt = a.batch + static_cast<long>(k) * a.B;
@@ -114,7 +114,7 @@ __device__ void sample_batch_par(const LogisticArgs& a, int k, int lane, int wid
     sync();
     return;
   }
-  const int rank = a.first_rank + k;
+  const int rank = a.rank_of[k];
   const int* sh = a.shard + a.shard_off[k];
   const uint64_t n = static_cast<uint64_t>(a.shard_off[k + 1] - a.shard_off[k]);
   int* bt = a.batch + static_cast<long>(k) * a.B;
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(128) logistic_grad_kernel(const LogisticArgs a
   }
   // checked_gradient (sync.cpp:181-191): DivergenceError(rank, t)
   if (__syncthreads_or(bad) && threadIdx.x == 0) {
-    atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.first_rank + k));
+    atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.rank_of[k]));
   }
 }
 
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(128) mlp_grad_kernel(const LogisticArgs a, con
     bad = bad || !isfinite(__dmul_rn(loss, inv));
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) {
-    atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.first_rank + k));
+    atomicMin(a.gerr, (static_cast<unsigned long long>(a.t) << 32) | static_cast<unsigned int>(a.rank_of[k]));
   }
 }
 

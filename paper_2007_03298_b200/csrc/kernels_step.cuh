@@ -17,8 +17,9 @@ template <typename T> struct GroupArgs {
   long ld;
   long g_ld;
   long nvec;      // vectors per row to process
-  int first_rank;
-  const int* members;  // CSR over the groups of this launch (global ranks)
+  int first_rank;       // first slot on this GPU: local row = member slot - first_rank
+  const int* rank_of;   // local row -> global rank (error keys)
+  const int* members;  // CSR over the groups of this launch (slots; = global ranks for contiguous packing)
   const int* offsets;
   int step_phase;      // error phase for a failed local step
   int sync_phase;      // error phase for a failed group mean
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
   constexpr int VN = Vec<T>::n;
   const int beg = a.offsets[blockIdx.y];
   const int m = M > 0 ? M : a.offsets[blockIdx.y + 1] - beg;
-  const int lead = a.members[beg];
+  const int lead = a.rank_of[a.members[beg] - a.first_rank];  // members[0]: a failed group mean's rank
   // 1.0 / m in double, rounded once to T (param.cpp:49 / comm.cpp:107)
   const T inv = static_cast<T>(1.0 / static_cast<double>(m));
   unsigned long long bad = ~0ull;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
             if constexpr (OPT != kSgd) stv(a.m1 + rj, s1[q]);
             if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj, s2[q]);
             if (!ok) {
-              const unsigned long long k = err_key(a.t, a.step_phase, lrow[j] + a.first_rank);
+              const unsigned long long k = err_key(a.t, a.step_phase, a.rank_of[lrow[j]]);
               bad = k < bad ? k : bad;
             }
           }
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
           if constexpr (OPT != kSgd) stv(a.m1 + rj + off, s1);
           if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rj + off, s2);
           if (!ok) {
-            const unsigned long long k = err_key(a.t, a.step_phase, rk);
+            const unsigned long long k = err_key(a.t, a.step_phase, a.rank_of[lr]);
             bad = k < bad ? k : bad;
           }
         }
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) ds_group_bulk_kernel(const G
     return;
   }
   // consumers: thread x owns element e0 + x of every tile
-  const int lead = a.members[beg];
+  const int lead = a.rank_of[a.members[beg] - a.first_rank];
   const T inv = static_cast<T>(1.0 / static_cast<double>(M));
   int lr[M];
   T b1[M], b2[M];
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) ds_group_bulk_kernel(const G
         if constexpr (A >= 3) __stcs(a.m1 + gi, s1);
         if constexpr (A >= 4) __stcs(a.m2 + gi, s2);
         if (!finite_(w)) {
-          const unsigned long long k = err_key(a.t, a.step_phase, a.first_rank + lr[j]);
+          const unsigned long long k = err_key(a.t, a.step_phase, a.rank_of[lr[j]]);
           bad = k < bad ? k : bad;
         }
         acc = j == 0 ? w : add_(acc, w);
@@ -590,7 +591,7 @@ __device__ void small_logistic_grads(const SmallArgs<T>& a, long t, T* g) {
     }
     if (lane == 0) bad = bad || !logistic_loss_finite(L, bt, wr, max_nz, nan_nz);
     if (__any_sync(0xffffffffu, bad) && lane == 0) {
-      atomicMin(L.gerr, (static_cast<unsigned long long>(t) << 32) | static_cast<unsigned int>(L.first_rank + k));
+      atomicMin(L.gerr, (static_cast<unsigned long long>(t) << 32) | static_cast<unsigned int>(L.rank_of[k]));
     }
     __syncwarp();
   }

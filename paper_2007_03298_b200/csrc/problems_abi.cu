@@ -27,7 +27,8 @@ extern "C" int dss_quadratic_gradients(dss_ctx* c, long t, uint64_t seed, double
       a.mu = mu;
       a.scale = scale;
       for (int k = 0; k < c->P; ++k) {
-        a.s0[k] = stream_state(seed, kGradientNoise, static_cast<uint64_t>(c->first + k), static_cast<uint64_t>(t));
+        a.s0[k] = stream_state(seed, kGradientNoise, static_cast<uint64_t>(grank(c, c->first + k)),
+                               static_cast<uint64_t>(t));
       }
       dim3 grid(grid_x(c, c->d_pad, c->P), c->P);
       TimedLaunch tl(c, DSS_KIND_GRADIENT);
@@ -209,7 +210,13 @@ extern "C" int dss_epoch_order(const int* shard, int size, uint64_t seed, int ra
 namespace dssb {
 
 void free_logistic(dss_ctx* c) {
-  for (void* p : c->logi.mem) cudaFree(p);
+  for (void* p : c->logi.mem) {
+    char* user = static_cast<char*>(p) + c->guard;
+    c->guarded.erase(std::remove_if(c->guarded.begin(), c->guarded.end(),
+                                    [&](const std::pair<char*, size_t>& gb) { return gb.first == user; }),
+                     c->guarded.end());
+    cudaFree(p);
+  }
   c->logi.mem.clear();
   c->logi.ready = false;
 }
@@ -217,9 +224,16 @@ void free_logistic(dss_ctx* c) {
 template <typename P>
 P* logi_alloc(dss_ctx* c, size_t n) {
   void* p = nullptr;
-  ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(P)), "cudaMalloc");
+  const size_t g = static_cast<size_t>(c->guard), bytes = std::max<size_t>(n, 1) * sizeof(P);
+  ck(cudaMalloc(&p, bytes + 2 * g), "cudaMalloc");
   c->logi.mem.push_back(p);
-  return static_cast<P*>(p);
+  char* user = static_cast<char*>(p) + g;
+  if (g) {  // guard bands, as dalloc (checked by dss_check_guards)
+    ck(cudaMemset(p, kGuardByte, g), "guard");
+    ck(cudaMemset(user + bytes, kGuardByte, g), "guard");
+    c->guarded.push_back({user, bytes});
+  }
+  return reinterpret_cast<P*>(user);
 }
 
 // w as doubles [d] + the -y*s factors [batch]
@@ -248,10 +262,13 @@ void dataset_setup(dss_ctx* c, const double* x, const double* y, int M, int d_fe
   free_logistic(c);
   std::vector<int> idx, off;
   make_shards(M, c->cfg.strategy.world_size, run_seed, idx, off);
-  std::vector<int> local_off(static_cast<size_t>(c->P) + 1, 0);
+  // this GPU's workers' shards in local-row order (their global ranks need not be contiguous)
+  std::vector<int> local_off(static_cast<size_t>(c->P) + 1, 0), local_idx;
   long max_shard = 0;
   for (int k = 0; k < c->P; ++k) {
-    const int n = off[static_cast<size_t>(c->first + k) + 1] - off[static_cast<size_t>(c->first + k)];
+    const size_t r = static_cast<size_t>(grank(c, c->first + k));
+    local_idx.insert(local_idx.end(), idx.begin() + off[r], idx.begin() + off[r + 1]);
+    const int n = off[r + 1] - off[r];
     local_off[static_cast<size_t>(k) + 1] = local_off[static_cast<size_t>(k)] + n;
     max_shard = std::max<long>(max_shard, n);
   }
@@ -266,8 +283,7 @@ void dataset_setup(dss_ctx* c, const double* x, const double* y, int M, int d_fe
   L.batch = logi_alloc<int>(c, static_cast<size_t>(c->P) * batch_size);
   ck(cudaMemcpy(L.x, x, sizeof(double) * xn, cudaMemcpyHostToDevice), "dataset x upload");
   ck(cudaMemcpy(L.y, y, sizeof(double) * M, cudaMemcpyHostToDevice), "dataset y upload");
-  ck(cudaMemcpy(L.shard, idx.data() + off[static_cast<size_t>(c->first)], sizeof(int) * local_off.back(),
-                cudaMemcpyHostToDevice), "shard upload");
+  ck(cudaMemcpy(L.shard, local_idx.data(), sizeof(int) * local_off.back(), cudaMemcpyHostToDevice), "shard upload");
   ck(cudaMemcpy(L.shard_off, local_off.data(), sizeof(int) * local_off.size(), cudaMemcpyHostToDevice),
      "shard upload");
   ck(cudaMemset(L.order_epoch, 0xff, sizeof(long) * c->P), "epoch init");  // -1
@@ -353,7 +369,7 @@ LogisticArgs logistic_args(dss_ctx* c, long t) {
   a.l2 = L.l2;
   a.seed = L.seed;
   a.t = t;
-  a.first_rank = c->first;
+  a.rank_of = c->d_rank_of;
   a.gerr = c->d_gerr;
   return a;
 }

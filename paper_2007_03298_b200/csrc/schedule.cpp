@@ -206,6 +206,51 @@ void slice_range(long d_pad, int s, int j, long* lo, long* hi) {
   *hi = c1 * kRowAlign;
 }
 
+Tiling choose_tiling(const dss_strategy& s, int G) {
+  Tiling best;
+  const int W = s.world_size, N = s.group_size;
+  if (s.kind != DSS_DS_SYNC || G <= 1 || N <= 0 || W == N || W % N != 0) return best;
+  const int K = W / N;
+  long best_busy = -1, best_total = -1;
+  for (int gr = G; gr >= 1; --gr) {  // larger gr first: ties keep whole blocks on a GPU
+    if (G % gr) continue;
+    const int gc = G / gr;
+    if (K % gr || N % gc) continue;
+    const long even = static_cast<long>(K) * (gc - 1);  // K blocks, each over gc GPUs
+    const long odd = static_cast<long>(N) * (gr - 1);   // N combs, each over gr GPUs
+    const long busy = std::max(even, odd), total = even + odd;
+    if (best_busy < 0 || busy < best_busy || (busy == best_busy && total < best_total)) {
+      best = {gr, gc};
+      best_busy = busy;
+      best_total = total;
+    }
+  }
+  return best;
+}
+
+std::vector<int> placement_slots(const dss_strategy& s, int G, const Tiling& t) {
+  const int W = s.world_size;
+  std::vector<int> slot(static_cast<size_t>(W));
+  if (t.gr == 0) {
+    for (int k = 0; k < W; ++k) slot[static_cast<size_t>(k)] = k;
+    return slot;
+  }
+  const int N = s.group_size, K = W / N, P = W / G;
+  const int Kt = K / t.gr, Nt = N / t.gc;
+  for (int k = 0; k < W; ++k) {
+    const int b = k / N, c = k % N;
+    const int gpu = (b / Kt) * t.gc + c / Nt;
+    slot[static_cast<size_t>(k)] = gpu * P + (b % Kt) * Nt + c % Nt;
+  }
+  return slot;
+}
+
+Partition to_slots(const Partition& part, const std::vector<int>& slot_of) {
+  Partition out = part;
+  for (int& m : out.members) m = slot_of[static_cast<size_t>(m)];
+  return out;
+}
+
 GpuPlan make_plan(const Partition& part, int world_size, int n_gpus, int rank, long d_pad, bool force_chain,
                   bool no_chain) {
   GpuPlan plan;

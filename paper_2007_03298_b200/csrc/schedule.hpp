@@ -89,6 +89,26 @@ struct GpuPlan {
   int max_chain_slots = 0;           // over all GPUs: receive slots needed
 };
 
+// ---------------------------------------------------------------------------
+// Worker placement over G GPUs.  Slot v = gpu * P + local row.  Contiguous
+// packing is slot(k) = k.  The tiled placement (DS-Sync only, W = N * K:
+// block b = k / N, comb c = k % N, a K x N grid) cuts the grid into
+// gr x gc tiles of (K/gr) x (N/gc) workers, one tile per GPU, local rows in
+// ascending rank order.  Every block then spans gc GPUs and every comb gr
+// GPUs, each GPU's members of a group forming one contiguous run of the
+// ascending fold order (what the chain fold needs).  choose_tiling picks the
+// (gr, gc) with the fewest cross-GPU row transfers in the busier parity
+// (sum over groups of 2 (S - 1) rows), then the fewest overall.
+struct Tiling {
+  int gr = 0, gc = 0;  // 0: contiguous packing
+};
+Tiling choose_tiling(const dss_strategy& s, int n_gpus);
+// slot_of[k] for every global rank k (identity for contiguous packing).
+std::vector<int> placement_slots(const dss_strategy& s, int n_gpus, const Tiling& t);
+// The partition with every member replaced by its slot (member order, i.e.
+// the ascending-rank fold order, kept).
+Partition to_slots(const Partition& part, const std::vector<int>& slot_of);
+
 // force_chain: every spanning group takes the chain path (tests); otherwise
 // only groups with >= 2 members on some GPU (where the chain moves fewer
 // NVLink bytes than the two-shot).  no_chain: no group takes the chain (a

@@ -31,7 +31,7 @@ case "$task" in
     echo "mgpu rc=$?"; tail -c 600 gpurun_out/bench_g$n.err ;;
   mtests)
     n=$1; shift
-    timeout 1500 python -m pytest tests/test_multi_gpu.py -m gpu -x -q "$@" > gpurun_out/mgpu_tests_g$n.log 2>&1
+    timeout 1500 python -m pytest tests/test_multi_gpu.py -m gpu -x -q -s "$@" > gpurun_out/mgpu_tests_g$n.log 2>&1
     echo "mtests rc=$?"; tail -5 gpurun_out/mgpu_tests_g$n.log ;;
   ncu)
     re=$1; shift

@@ -42,29 +42,32 @@ def device_of(rank):
     return rank % torch.cuda.device_count()
 
 
-def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0):
+def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0, placement=0):
     s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
                      WorldConfig(W, N), 1, rect)
     wd = 0.01 if opt in (1, 3) else 0.0
     hp = OptimizerHyperparams(weight_decay=wd)
     rng = np.random.default_rng(1000 + W + opt)
     w = rng.standard_normal((W, d)).astype(np.float32)
-    mine = local_slice(W, G, rank)
-    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G, path=path, stats_dim=sd)
+    e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G, path=path, stats_dim=sd,
+                     placement=placement)
+    mine = e.local_ranks  # this GPU's workers in local-row order (contiguous unless placed)
+    if not placement:
+        assert mine == list(local_slice(W, G, rank))
     attach(e)
-    e.upload_all(BUF_PARAMS, w[mine.start:mine.stop])
+    e.upload_all(BUF_PARAMS, w[mine])
     rs = rng.standard_normal((W, sd)).astype(np.float32) if sd else None
     if sd:
-        e.upload_all(BUF_STATS, rs[mine.start:mine.stop])
+        e.upload_all(BUF_STATS, rs[mine])
     m1, m2 = np.zeros_like(w), np.zeros_like(w)
     steps = np.zeros(W, np.int64)
     alpha = 0.05 if opt < 2 else 0.01
     for t in range(5):
         g = rng.standard_normal((W, d)).astype(np.float32)
-        e.upload_all(BUF_GRADS, g[mine.start:mine.stop])
+        e.upload_all(BUF_GRADS, g[mine])
         if sd:  # fold_running_stats EMA, then the stats ride the step's fold
             obs = rng.standard_normal((W, sd)).astype(np.float32)
-            e.upload_all(BUF_STATS_OBS, obs[mine.start:mine.stop])
+            e.upload_all(BUF_STATS_OBS, obs[mine])
             e.running_stats_update()
             rs = (np.float32(0.9) * rs + np.float32(0.1) * obs).astype(np.float32)
             if kind == "ds":
@@ -92,18 +95,20 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0):
     got = e.download_all(BUF_PARAMS)
     got_m1 = e.download_all(BUF_MOMENT1) if opt >= 1 else None
     got_rs = e.download_all(BUF_STATS) if sd else None
+    e.check_guards()  # DSS_GUARD_BYTES runs: no kernel wrote outside its buffers (raises otherwise)
     parts = [None] * G
-    dist.all_gather_object(parts, (got, got_m1, got_rs))
+    dist.all_gather_object(parts, (mine, got, got_m1, got_rs))
     e.close()
     if rank == 0:
-        full = np.concatenate([p[0] for p in parts])
+        order = np.argsort(np.concatenate([p[0] for p in parts]))  # rows back into rank order
+        full = np.concatenate([p[1] for p in parts])[order]
         ok = np.array_equal(full, w)
         if opt >= 1:
-            ok = ok and np.array_equal(np.concatenate([p[1] for p in parts]), m1)
+            ok = ok and np.array_equal(np.concatenate([p[2] for p in parts])[order], m1)
         if sd:
-            ok = ok and np.array_equal(np.concatenate([p[2] for p in parts]), rs)
+            ok = ok and np.array_equal(np.concatenate([p[3] for p in parts])[order], rs)
         diff = float(np.abs(full - w).max())
-        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d} path={path} stats={sd}: "
+        print(f"case {kind} W={W} N={N} rect={rect} opt={opt} d={d} path={path} stats={sd} placement={placement}: "
               f"{'OK' if ok else 'MISMATCH'} maxdiff={diff}",
               flush=True)
         return ok
@@ -142,6 +147,43 @@ def logistic_case(rank, G, sampling, kind):
     return ok
 
 
+def placed_logistic_case(rank, G):
+    """C1-style logistic run (device sampling from the workers' shards, f64)
+    over a placed 16-worker world equals the same run on one GPU: shards,
+    batch streams and gradient noise follow the global rank, not the row."""
+    from paper_2007_03298_b200 import SamplingMode, logistic_dataset
+    W, N, T = 16, 4, 12
+    if W % G:
+        return True
+    x, y = logistic_dataset(11, 20, 2000)
+    alphas = np.full(T, 0.5)
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N))
+    e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 20, OptimizerHyperparams(), "f64", device_of(rank), rank, G,
+                     placement=1)
+    attach(e)
+    e.logistic_setup(x, y, 0.05, 8, SamplingMode.EPOCH, 1)
+    for t in range(T):
+        e.logistic_gradients(t)
+        e.step(t, float(alphas[t]))
+    e.check()
+    parts = [None] * G
+    dist.all_gather_object(parts, (e.local_ranks, e.download_all(BUF_PARAMS)))
+    e.close()
+    if rank != 0:
+        return True
+    order = np.argsort(np.concatenate([p[0] for p in parts]))
+    got = np.concatenate([p[1] for p in parts])[order]
+    with DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 20, OptimizerHyperparams(), "f64", 0) as one:
+        one.logistic_setup(x, y, 0.05, 8, SamplingMode.EPOCH, 1)
+        for t in range(T):
+            one.logistic_gradients(t)
+            one.step(t, float(alphas[t]))
+        ref = one.download_all(BUF_PARAMS)
+    ok = np.array_equal(got, ref)
+    print(f"case placed logistic W=16 G={G}: {'OK' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
 def fingerprint_case(rank, G):
     """Ranks created with different geometry (here: a different d per rank)
     must refuse to map each other's buffers (dss_ipc_attach fingerprint)."""
@@ -174,6 +216,16 @@ def main():
             ok = run_case(*case, rank, G, orc, path) and ok
     for case in (("ds", 8, 2, True, 2, 1001), ("bsp", 8, 8, False, 1, 777)):  # running-stats tail
         ok = run_case(*case, rank, G, orc, 0, sd=6) and ok
+    # tiled placement (blocks over gc GPUs, combs over gr): every DS shape whose
+    # grid tiles differently from contiguous packing at this G, every path
+    for case in CASES:
+        if case[0] != "ds" or case[1] % G:
+            continue
+        for path in (0, 2, 3, 4):
+            ok = run_case(*case, rank, G, orc, path, placement=1) and ok
+    ok = run_case("ds", 32, 4, True, 2, 1001, rank, G, orc, 0, sd=6, placement=1) and ok
+    for kind in ("ds",):
+        ok = placed_logistic_case(rank, G) and ok
     from paper_2007_03298_b200 import SamplingMode
     for kind in ("ds", "bsp"):
         for sampling in (SamplingMode.REPLACEMENT, SamplingMode.EPOCH):

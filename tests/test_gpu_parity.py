@@ -532,3 +532,49 @@ def test_small_world_wide_cta(cuda_device, oracle, kind, W, N, d, rect, opt):
             assert rc[0] == 0
             steps += 1
         assert np.array_equal(got, ref), (dtype, kind, opt)
+
+
+def test_guard_bands_see_no_out_of_bounds_writes(cuda_device):
+    """compute-sanitizer is closed on this pool: the library's guard bands
+    (DSS_GUARD_BYTES) frame every device allocation, and a workload touching
+    every single-GPU kernel must leave all of them intact."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DSS_GUARD_BYTES=str(1 << 20))
+    p = subprocess.run([sys.executable, os.path.join(root, "profiles", "tools", "sanitize_run.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert "SANITIZE-RUN OK" in p.stdout and "guard bands on, 0 bytes overwritten" in p.stdout, p.stdout
+
+
+def test_guard_bands_catch_a_stray_write(cuda_device):
+    """The detector itself: a write just past a row buffer is reported."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2007_03298_b200 import *
+s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(4, 2))
+e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, 1000, None, "f32", 0)
+assert e.check_guards() == 0
+class A:
+    def __init__(self, p):
+        self.__cuda_array_interface__ = {"shape": (4,), "typestr": "<f4", "data": (p, False), "version": 3}
+end = e.device_ptr(BUF_PARAMS, 3) + 4 * e.row_stride  # one past the last row of the params buffer
+torch.as_tensor(A(end), device="cuda").fill_(1.0)
+torch.cuda.synchronize()
+try:
+    e.check_guards()
+    print("MISSED")
+except RuntimeError as ex:
+    print("CAUGHT", ex)
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DSS_GUARD_BYTES="4096")
+    p = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "CAUGHT guard bands overwritten: 16 bytes" in p.stdout, p.stdout

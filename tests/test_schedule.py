@@ -182,3 +182,52 @@ def test_multi_gpu_plan_covers_every_element_once(W, N, rect, G):
             assert len(ivs) <= len(gpus)
         assert n_chain == want_chain
         assert n_local == sum(1 for g in part.groups if len({m // per for m in g}) == 1)
+
+
+@pytest.mark.parametrize("W,N,rect", [(8, 2, True), (32, 4, True), (64, 8, False), (16, 4, False), (36, 6, False),
+                                      (4, 2, False), (128, 8, True)])
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_tiled_placement_properties(W, N, rect, G):
+    """dss_placement (the tiled worker placement): a bijection onto G GPUs x
+    W/G rows, local rows ascending by rank, and every group's members on a
+    GPU forming one contiguous run of its ascending (fold) order -- what the
+    ordered chain needs.  It never moves more rows across GPUs than
+    contiguous packing in the busier parity."""
+    from paper_2007_03298_b200 import (SyncStrategy, StrategyKind, Topology, WorldConfig, make_partition,
+                                       placement)
+    if W % G:
+        pytest.skip("W not a multiple of G")
+    s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, rect)
+    P = W // G
+    gpu, row, (gr, gc) = placement(s, G, 1)
+    assert sorted(zip(gpu, row)) == [(q, r) for q in range(G) for r in range(P)]
+    for q in range(G):
+        mine = [k for k in range(W) if gpu[k] == q]
+        assert [row[k] for k in mine] == list(range(P))
+    busy = {}
+    for mode, gmap in (("tiled", gpu), ("contiguous", [k // P for k in range(W)])):
+        b = 0
+        for t in (0, 1):
+            cross = 0
+            for grp in make_partition(s, t).groups:
+                seq = [gmap[m] for m in grp]
+                runs = [seq[0]] + [y for x, y in zip(seq, seq[1:]) if y != x]
+                assert len(runs) == len(set(runs)), (mode, grp, seq)
+                cross += len(set(seq)) - 1
+            b = max(b, cross)
+        busy[mode] = b
+    assert busy["tiled"] <= busy["contiguous"]
+    if (gr, gc) == (0, 0):
+        assert gpu == [k // P for k in range(W)]
+
+
+def test_tiled_placement_choices():
+    """C3 / C4 at 4 GPUs tile 2 x 2 (blocks and combs each over 2 GPUs);
+    at 2 GPUs contiguous packing is already best."""
+    from paper_2007_03298_b200 import SyncStrategy, StrategyKind, Topology, WorldConfig, placement
+    c3 = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(32, 4), 1, True)
+    c4 = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(64, 8))
+    assert placement(c3, 4)[2] == (2, 2) and placement(c4, 4)[2] == (2, 2)
+    assert placement(c3, 2)[2] == (2, 1) and placement(c4, 8)[2] in ((4, 2), (2, 4))
+    bsp = SyncStrategy(StrategyKind.BSP, Topology.RING, WorldConfig(32, 32))
+    assert placement(bsp, 4)[2] == (0, 0)
