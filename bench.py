@@ -793,7 +793,7 @@ def our_arm(args, cfg):
            "data": "synthetic: isotropic-quadratic gradients (SplitMix64/Box-Muller, seeds 7/1), device-resident",
            "config": head["config"]}
     if G > 1:
-        out["placement"] = {"mode": ["contiguous", "tiled"][args.placement],
+        out["placement"] = {"mode": ["contiguous", "tiled", "auto"][args.placement],
                             "tiling_gr_gc": list(gpu_map(cfg, G, args.placement)[2])}
     if args.path:
         out["fold_path"] = {2: "chain forced for every spanning group", 3: "unfused pull two-shot"}.get(
@@ -870,8 +870,8 @@ def main():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--d", type=int, default=None, help="override the config's d (profiling runs)")
     ap.add_argument("--path", type=int, default=0, help="fold path: 0 auto, 2 chain for every spanning group")
-    ap.add_argument("--placement", type=int, default=0,
-                    help="DS worker placement over the GPUs: 0 contiguous, 1 tiled (dss_config.placement)")
+    ap.add_argument("--placement", type=int, default=2,
+                    help="DS worker placement over the GPUs: 0 contiguous, 1 tiled, 2 auto (dss_config.placement)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -126,7 +126,10 @@ typedef struct {
                            and combs gr GPUs; (gr, gc) minimises the cross-GPU rows of
                            the busier schedule parity (dss_placement).  Groups, fold
                            order and results are unchanged; only which GPU holds which
-                           worker.  Ignored (contiguous) for BSP and single-group worlds. */
+                           worker.  Ignored (contiguous) for BSP and single-group worlds.
+                           2 = auto: the tiling where contiguous packing would leave an
+                           ordered chain >= 3 GPUs deep (C3 / C4 on 4 GPUs), else
+                           contiguous. */
 } dss_config;
 
 typedef struct dss_ctx dss_ctx;

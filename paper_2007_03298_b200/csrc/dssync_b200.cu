@@ -132,7 +132,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     }
     c->first = cfg->rank * c->P;
     {
-      const Tiling tl = (cfg->placement == 1 && cfg->n_gpus > 1) ? choose_tiling(s, cfg->n_gpus) : Tiling{};
+      const Tiling tl = choose_placement(s, cfg->n_gpus, cfg->placement);
       c->slot_of = placement_slots(s, cfg->n_gpus, tl);
       c->rank_of_slot.assign(c->slot_of.size(), 0);
       for (size_t k = 0; k < c->slot_of.size(); ++k) {
@@ -142,7 +142,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       c->tile_gr = c->placed ? tl.gr : 0;
       c->tile_gc = c->placed ? tl.gc : 0;
     }
-    if (cfg->placement < 0 || cfg->placement > 1) throw std::invalid_argument("placement must be 0 or 1");
+    if (cfg->placement < 0 || cfg->placement > 2) throw std::invalid_argument("placement must be 0, 1 or 2");
     c->d = cfg->dim;
     c->d_pad = pad_dim(cfg->dim);
     c->esz = cfg->dtype == DSS_F64 ? 8 : 4;
@@ -342,7 +342,8 @@ extern "C" int dss_placement(const dss_strategy* s, int n_gpus, int placement, i
     return fail(nullptr, DSS_EINVAL, "dss_placement: world_size must be a multiple of n_gpus");
   }
   return guard(nullptr, [&]() -> int {
-    const Tiling tl = (placement == 1 && n_gpus > 1) ? choose_tiling(*s, n_gpus) : Tiling{};
+    if (placement < 0 || placement > 2) throw std::invalid_argument("placement must be 0, 1 or 2");
+    const Tiling tl = choose_placement(*s, n_gpus, placement);
     const std::vector<int> slot = placement_slots(*s, n_gpus, tl);
     const int P = s->world_size / n_gpus;
     for (size_t k = 0; k < slot.size(); ++k) {

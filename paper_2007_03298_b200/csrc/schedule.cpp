@@ -228,6 +228,28 @@ Tiling choose_tiling(const dss_strategy& s, int G) {
   return best;
 }
 
+Tiling choose_placement(const dss_strategy& s, int G, int mode) {
+  if (mode == 0 || G <= 1) return Tiling{};
+  if (mode == 1) return choose_tiling(s, G);
+  // auto: is there a deep chain under contiguous packing?
+  const int W = s.world_size, P = W / G;
+  bool deep_chain = false;
+  for (long t = 0; t < 2 && !deep_chain && s.kind == DSS_DS_SYNC; ++t) {
+    const Partition part = make_partition(s, t);
+    for (int g = 0; g < part.n_groups() && !deep_chain; ++g) {
+      std::vector<int> per(static_cast<size_t>(G), 0);
+      for (int j = 0; j < part.size(g); ++j) ++per[static_cast<size_t>(part.group(g)[j] / P)];
+      int span = 0, most = 0;
+      for (int x : per) {
+        span += x > 0;
+        most = std::max(most, x);
+      }
+      deep_chain = span >= 3 && most >= 2;
+    }
+  }
+  return deep_chain ? choose_tiling(s, G) : Tiling{};
+}
+
 std::vector<int> placement_slots(const dss_strategy& s, int G, const Tiling& t) {
   const int W = s.world_size;
   std::vector<int> slot(static_cast<size_t>(W));

@@ -103,6 +103,13 @@ struct Tiling {
   int gr = 0, gc = 0;  // 0: contiguous packing
 };
 Tiling choose_tiling(const dss_strategy& s, int n_gpus);
+// placement mode 2 (auto): the tiling only where contiguous packing leaves an
+// ordered chain three or more GPUs deep (a group with several members on a
+// GPU that spans >= 3 GPUs: C3 / C4 on 4 GPUs); contiguous packing otherwise
+// (its one-member-per-GPU groups take the push two-shot, which measured
+// faster than the chains a tiling would create: C2 on 4 GPUs 3501 vs 3103
+// iters/s, profiles/r02/placement_ab_g4.jsonl).
+Tiling choose_placement(const dss_strategy& s, int n_gpus, int mode);
 // slot_of[k] for every global rank k (identity for contiguous packing).
 std::vector<int> placement_slots(const dss_strategy& s, int n_gpus, const Tiling& t);
 // The partition with every member replaced by its slot (member order, i.e.

@@ -231,3 +231,16 @@ def test_tiled_placement_choices():
     assert placement(c3, 2)[2] == (2, 1) and placement(c4, 8)[2] in ((4, 2), (2, 4))
     bsp = SyncStrategy(StrategyKind.BSP, Topology.RING, WorldConfig(32, 32))
     assert placement(bsp, 4)[2] == (0, 0)
+
+
+def test_auto_placement_tiles_only_deep_chains():
+    """placement=2: C3 / C4 on 4 GPUs (contiguous combs would chain over 4
+    GPUs, 2 members each) are tiled; C2 on 4 GPUs (quads one member per GPU:
+    push two-shot) and everything on 2 GPUs stay contiguous."""
+    from paper_2007_03298_b200 import SyncStrategy, StrategyKind, Topology, WorldConfig, placement
+    c2 = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(8, 2), 1, True)
+    c3 = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(32, 4), 1, True)
+    c4 = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(64, 8))
+    assert placement(c3, 4, 2)[2] == (2, 2) and placement(c4, 4, 2)[2] == (2, 2)
+    assert placement(c2, 4, 2)[2] == (0, 0) and placement(c3, 2, 2)[2] == (0, 0)
+    assert placement(c4, 8, 2)[2] == (0, 0) and placement(c3, 8, 2)[2] == (0, 0)
