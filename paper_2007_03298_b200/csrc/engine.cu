@@ -890,7 +890,10 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
   // lost at 2 GPUs (C2 / C3 iters/s against 3108 / 480 for this schedule):
   // B concurrently on a side stream with A giving up CTA slots (2534 / 369),
   // and both passes in one persistent kernel with lagged mean-pass units
-  // (2300 / stalled).
+  // (2300 / stalled).  Round 2: both passes in one cooperative kernel, every
+  // CTA taking its partial-pass units then its mean-pass units (no lag):
+  // bit-exact but slower everywhere -- C2 @2 GPUs 3200 -> 2790, C3 @4 (tiled)
+  // 744 -> 572, C4 @4 32.1 -> 21.3 (profiles/r02/chain_fused_ab_g*.jsonl).
   if (cl.na > 0) {
     a.entries = cl.d_a;
     a.n_entries = cl.na;
