@@ -7,8 +7,9 @@ DS-Sync vs our bit-exact BSP vs an NCCL BSP all-reduce baseline.
 
 One JSON line per (N, bytes, G) on rank 0.  `ds_iters_s` / `bsp_iters_s`
 run through the C-ABI (dss_steps, device-resident rows);
-`nccl_bsp_iters_s` (G > 1) = local pre-sum + torch.distributed NCCL world
-all-reduce + x1/W + our apply_step.  Effective GB/s = W * d * 4 / t.
+`nccl_bsp_iters_s` (G > 1) = local pre-sum (one strided reduction) +
+torch.distributed NCCL world all-reduce + x1/W + our apply_step.  DS engines
+use the auto worker placement (--placement).  Effective GB/s = W * d * 4 / t.
 """
 from __future__ import annotations
 
@@ -33,6 +34,7 @@ def main():
     ap.add_argument("--mem-gb", type=float, default=150.0, help="per-GPU cap for the worker arrays")
     ap.add_argument("--path", type=int, default=0, help="fold path (0 auto; 4 auto without one-shot)")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--placement", type=int, default=2, help="DS placement: 0 contiguous, 1 tiled, 2 auto")
     args = ap.parse_args()
 
     import torch
@@ -83,10 +85,11 @@ def main():
                 continue
             K = int(max(5, min(2000, 4e9 / (P * nbytes * 3 + 1))))
             row = {"N": N, "W": W, "bytes_per_worker": nbytes, "d": d, "n_gpus": G, "steps": K, "opt": args.opt,
-                   "path": args.path}
+                   "path": args.path, "placement": args.placement}
             for kind, key in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
                 s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W))
-                e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, d, None, "f32", local, rank, G, path=args.path)
+                e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, d, None, "f32", local, rank, G, path=args.path,
+                                 placement=args.placement if kind == StrategyKind.DS_SYNC else 0)
                 e.set_stream(stream.cuda_stream)
                 if G > 1:
                     from paper_2007_03298_b200.dist import attach
@@ -104,22 +107,22 @@ def main():
                 row[key + "_iters_s"] = 1000.0 / ms
                 row[key + "_eff_gbs"] = W * d * 4 / (ms / 1e3) / 1e9
                 if key == "bsp" and G > 1 and not args.no_nccl:
-                    grads = []
-                    for k in range(rank * P, (rank + 1) * P):
-                        ptr = e.device_ptr(BUF_GRADS, k)
+                    # the local gradient rows as one strided view of the engine's
+                    # contiguous [P][row_stride] buffer: no gather copies
+                    ptr, stride = e.device_ptr(BUF_GRADS, e.local_ranks[0]), e.row_stride
 
-                        class _A:
-                            __cuda_array_interface__ = {"shape": (d,), "typestr": "<f4", "data": (ptr, False),
-                                                        "version": 3}
-                        grads.append(torch.as_tensor(_A(), device="cuda"))
+                    class _A:
+                        __cuda_array_interface__ = {"shape": (P, stride), "typestr": "<f4", "data": (ptr, False),
+                                                    "version": 3}
+                    grads = torch.as_tensor(_A(), device="cuda")[:, :d]
+                    acc = torch.empty(d, dtype=torch.float32, device="cuda")
 
                     def nccl(K):
                         for _ in range(K):
-                            acc = torch.stack(grads).sum(0)
+                            torch.sum(grads, dim=0, out=acc)
                             dist.all_reduce(acc)
                             acc.mul_(1.0 / W)
-                            for gr in grads:
-                                gr.copy_(acc)
+                            grads.copy_(acc.expand_as(grads))
                             e.apply_step(0.01, check=False)
                     nccl(3)
                     ms = timed(nccl, K)
