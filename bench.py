@@ -1,6 +1,6 @@
 """DS-Sync sync-iteration benchmark (BASELINE.json metric) on 1..8 B200s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c4slice|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c4slice|c2sq|c1]
                     [--impl ours|reference] [--extras c3,c4slice,c2f64 | none]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
@@ -13,9 +13,9 @@ Default workload = BASELINE config C2 (W=8 workers, groups of 2 and 4,
 BSP (ordered gradient fold + step) is measured on the same buffers.
 
 The headline line also carries keyed results for the other BASELINE
-configs that fit ("configs": C3, the C4 per-GPU slice and C2 in fp64 at
-N=1; C3 and, from 4 GPUs, full C4 at N>1), each with its own roofline and
-end-to-end number.
+configs that fit ("configs": C3, the C4 per-GPU slice, C2 in fp64 and C2's
+size on the legal square shape W=16/N=4 at N=1; C3 and, from 4 GPUs, full
+C4 at N>1), each with its own roofline and end-to-end number.
 
 Prints ONE JSON line (rank 0).  --impl reference times the reference's own
 CPU implementation (oracle/_ref = the unmodified reference sources) on the
@@ -54,6 +54,11 @@ CONFIGS = {
                     "(WideResNet-28-10 size), SGD-momentum 0.9 wd=1e-4"),
     "c4": dict(W=64, N=8, rect=False, d=340_000_000, opt=3, alpha=3e-5, wd=0.01,
                desc="C4: W=64 virtual workers, groups of 8, d=340,000,000 fp32 (BERT-large size), AdamW"),
+    # C2's buffer size on a shape the reference itself accepts (W = N^2):
+    # every group index of this line is pinned by the reference's make_partition
+    "c2sq": dict(W=16, N=4, rect=False, d=25_000_000, opt=0, alpha=0.05, wd=0.0,
+                 desc="C2 size on a legal square shape: W=16 workers, groups of 4 (blocks / combs), d=25,000,000 "
+                      "fp32, vanilla SGD alpha=0.05"),
     # one GPU's share of C4's block iteration: 8 workers, one group of 8, AdamW
     "c4slice": dict(W=8, N=8, rect=False, d=340_000_000, opt=3, alpha=3e-5, wd=0.01,
                     desc="C4 per-GPU slice: 8 workers in one group of 8, d=340,000,000 fp32, AdamW"),
@@ -745,7 +750,7 @@ def extras_for(args, G):
         return [x for x in args.extras.split(",") if x]
     if args.config != "c2":
         return []
-    return ["c3", "c4slice", "c2f64"] if G == 1 else (["c3", "c4"] if G >= 4 else ["c3"])
+    return ["c3", "c4slice", "c2f64", "c2sq"] if G == 1 else (["c3", "c4"] if G >= 4 else ["c3"])
 
 
 def our_arm(args, cfg):

@@ -48,7 +48,7 @@ def test_reference_partition_rule_matches_the_product_schedule():
 
     import bench
     from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig, make_partition
-    for name in ("c1", "c2", "c3", "c4", "c4slice"):
+    for name in ("c1", "c2", "c3", "c4", "c4slice", "c2sq"):
         c = bench.CONFIGS[name]
         rb = bench.RefBench(dict(c, d=64), 64, 1)
         try:
