@@ -351,8 +351,11 @@ def epoch_order(shard: Shard, seed: int, rank: int, epoch: int) -> List[int]:  #
 class DsSyncEngine:
     """Device-resident DS-Sync / BSP workers on one GPU (one context).
 
-    Workers ``first_rank .. first_rank + local_workers - 1`` live in HBM as
-    worker-major rows.  ``step`` runs one fused iteration on the device.
+    This GPU's workers live in HBM as worker-major rows, in the order of
+    ``local_ranks`` (``first_rank .. first_rank + local_workers - 1`` under
+    contiguous packing; any subset of ranks under the tiled ``placement``,
+    where ``first_rank`` is -1).  ``step`` runs one fused iteration on the
+    device.
     """
 
     def __init__(self, strategy: SyncStrategy, optimizer: OptimizerKind, dim: int,

@@ -1,5 +1,5 @@
 """Host-side multi-GPU logic over a real gloo process group on CPU
-(world_size 2 and 4): IPC handle exchange/attach plumbing, and every rank's
+(world_size 2, 4 and 8): IPC handle exchange/attach plumbing, and every rank's
 two-shot plan agreeing with every other's (each element of each spanning
 group owned exactly once, ownership identical from every rank's view)."""
 import os
@@ -78,6 +78,20 @@ def _worker(rank, world, port, q):
                     for x, y in zip(ivs, ivs[1:]):
                         assert x[1] == y[0]
                 results[(W, N, t)] = (len(by_group), tuple(chains))
+        # every rank derives the same worker placement (dss_placement is
+        # host-side and deterministic), for every mode and DS shape
+        from paper_2007_03298_b200 import placement
+        for (W, N, rect) in [(8, 2, True), (32, 4, True), (64, 8, False), (16, 4, False)]:
+            if W % world:
+                continue
+            st = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, rect)
+            for mode in (0, 1, 2):
+                mine = placement(st, world, mode)
+                allp = [None] * world
+                dist.all_gather_object(allp, mine)
+                assert all(p == allp[0] for p in allp), (W, N, mode)
+                gpu, row, _ = mine
+                assert sorted(zip(gpu, row)) == [(g, r) for g in range(world) for r in range(W // world)]
         q.put((rank, "ok", results))
     except Exception as ex:  # pragma: no cover - reported to the parent
         q.put((rank, repr(ex), None))
@@ -85,7 +99,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_gloo_plan_and_handle_exchange(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
