@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+
+#include <nvtx3/nvToolsExt.h>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -338,11 +340,34 @@ struct RowGeom {
 
 // ---- launch helpers ---------------------------------------------------------
 
+// NVTX ranges (header-only NVTX3: a no-op unless a tool is attached) around
+// every hot launch, named by kernel kind, and around each API iteration, so
+// an nsys / ncu timeline shows the DS-Sync phases.  DSS_NVTX=0 removes them.
+#ifndef DSS_NVTX
+#define DSS_NVTX 1
+#endif
+inline const char* kind_name(int k) {
+  static const char* names[DSS_KIND_COUNT] = {"dss:group", "dss:fold", "dss:bsp", "dss:barrier",
+                                              "dss:gradient", "dss:chain", "dss:chain_mean"};
+  return k >= 0 && k < DSS_KIND_COUNT ? names[k] : "dss:?";
+}
+struct NvtxRange {
+  explicit NvtxRange(const char* name) {
+    if (DSS_NVTX) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (DSS_NVTX) nvtxRangePop();
+  }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct TimedLaunch {
   dss_ctx* c;
   int kind;
   cudaEvent_t b = nullptr, e = nullptr;
-  TimedLaunch(dss_ctx* cc, int k) : c(cc), kind(k) {
+  NvtxRange range;
+  TimedLaunch(dss_ctx* cc, int k) : c(cc), kind(k), range(kind_name(k)) {
     ++c->launches;
     if (!c->timing) return;
     for (cudaEvent_t* ev : {&b, &e}) {

@@ -473,6 +473,7 @@ extern "C" long dss_get_step_count(const dss_ctx* c, int rank) {
 
 extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome* out) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  NvtxRange range(c->cfg.strategy.kind == DSS_DS_SYNC ? "dss_step ds-sync" : "dss_step bsp");
   return guard(c, [&]() -> int {
     if (t < 0) throw std::invalid_argument("iteration must be >= 0");
     // run_training (sync.cpp:324-328) / check_step_args (optim.cpp:33-35)
