@@ -189,6 +189,10 @@ struct dss_ctx {
   cudaEvent_t ev_in = nullptr, ev_free = nullptr, ev_snap = nullptr, ev_out = nullptr;
   void* snapshot = nullptr;
   bool host_pipe = false;
+  // element-chunked host pipeline (one GPU, all groups local): per chunk,
+  // H2D of the gradients, the step of that element range, D2H of the params
+  // overlap across chunks and iterations
+  std::vector<cudaEvent_t> hc_in, hc_step, hc_out;
 
   std::vector<long> step_count;
   std::vector<void*> peer_w, peer_g, peer_mg;
@@ -432,7 +436,8 @@ std::vector<OwnedSlot> owned_layout(const dss_ctx* c, const Partition& part, int
 void build_plans(dss_ctx* c);
 
 void launch_groups_any(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha, const void* g, long g_ld,
-                       int step_phase, int sync_phase = 1, void* rows = nullptr, long rows_ld = 0);
+                       int step_phase, int sync_phase = 1, void* rows = nullptr, long rows_ld = 0, long lo = 0,
+                       long n = -1);
 void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t);
 void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha = 0.0);
 void launch_push_any(dss_ctx* c, const PushLaunch& pl, long t, double alpha);

@@ -464,32 +464,42 @@ def test_small_world_multi_iteration_kernel(cuda_device, oracle, kind, W, N, opt
         assert np.array_equal(got, ref), (dtype, kind, opt)
 
 
-def test_step_host_pipeline(cuda_device, oracle):
+@pytest.mark.parametrize("W,N,rect,opt,dtype,d", [(8, 2, True, 1, "f32", 50_021), (4, 2, False, 3, "f64", 9_000),
+                                                   (16, 4, False, 0, "f32", 70_001), (8, 8, False, 2, "f32", 777)])
+def test_step_host_pipeline(cuda_device, oracle, W, N, rect, opt, dtype, d):
     """dss_step_host: grads fed from host, params returned to host every
-    iteration with the copies pipelined across calls.  Iteration t's params
-    are complete once call t+1 (or host_sync) returns; every one is bit-exact
-    vs the oracle."""
+    iteration with the copies pipelined across calls (element-chunked on one
+    GPU: each chunk's copy-in, step and copy-out overlap).  Iteration t's
+    params are complete once call t+1 (or host_sync) returns; every one is
+    bit-exact vs the oracle, and a plain dss_step right after the pipeline
+    sees the same state."""
     import torch
     rng = np.random.default_rng(12)
-    W, N, d, T = 8, 2, 50_021, 6
-    w = rng.standard_normal((W, d)).astype(np.float32)
-    grads = [rng.standard_normal((W, d)).astype(np.float32) for _ in range(T)]
+    T = 6
+    ft = np.float64 if dtype == "f64" else np.float32
+    tt = torch.float64 if dtype == "f64" else torch.float32
+    w = rng.standard_normal((W, d)).astype(ft)
+    grads = [rng.standard_normal((W, d)).astype(ft) for _ in range(T + 1)]
     hg = [torch.from_numpy(g).pin_memory() for g in grads]
-    hp = [torch.empty((W, d), dtype=torch.float32).pin_memory() for _ in range(T)]
-    with engine_for("ds", W, N, 1, d, 1e-4, "f32", rect=True) as e:
+    hp = [torch.empty((W, d), dtype=tt).pin_memory() for _ in range(T)]
+    with engine_for("ds", W, N, opt, d, 1e-4, dtype, rect=rect) as e:
         e.upload_all(BUF_PARAMS, w)
         for t in range(T):
             e.step_host(t, 0.05, hg[t], hp[t])
-            if t >= 1:  # the previous iteration's params have landed
-                pass
+        e.upload_all(BUF_GRADS, grads[T])  # ordered after the pipeline's last copies
+        e.step(T, 0.05)
+        last = e.download_all(BUF_PARAMS)
         e.host_sync()
     ref = w.copy()
-    m1 = np.zeros_like(ref)
+    m1 = np.zeros_like(ref) if opt else None
+    m2 = np.zeros_like(ref) if opt >= 2 else None
     steps = np.zeros(W, np.int64)
-    for t in range(T):
-        oracle.ds_step(W, N, t, 1, hparams(weight_decay=1e-4), 0.05, steps, ref, grads[t], m1, None, True)
+    for t in range(T + 1):
+        oracle.ds_step(W, N, t, opt, hparams(weight_decay=1e-4), 0.05, steps, ref, grads[t], m1, m2, rect)
         steps += 1
-        assert np.array_equal(hp[t].numpy(), ref), t
+        if t < T:
+            assert np.array_equal(hp[t].numpy(), ref), t
+    assert np.array_equal(last, ref)
 
 
 def test_timing_and_launch_accounting(cuda_device):
