@@ -250,11 +250,7 @@ int dss_steps(dss_ctx* ctx, long t0, long n, const double* alphas, int check, ds
  * stream, the iteration runs, and the resulting params are snapshotted on
  * the device and copied out to host_params ([local_workers][dim], pinned) on
  * a second copy stream -- so iteration t's copy-out overlaps iteration t+1's
- * copy-in.  On one GPU with every group local (no running statistics) the
- * iteration is additionally split into element chunks (the step is
- * elementwise), so each chunk's copy-in, step and copy-out overlap the
- * neighbouring chunks' and no snapshot is needed.
- * host_params of iteration t is complete once the next
+ * copy-in.  host_params of iteration t is complete once the next
  * dss_step_host or dss_host_sync returns; host_grads may be reused as soon
  * as the next call returns.  Collective on several GPUs (like dss_step). */
 int dss_step_host(dss_ctx* ctx, long t, double alpha, const void* host_grads, void* host_params);

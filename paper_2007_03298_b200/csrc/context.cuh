@@ -189,10 +189,6 @@ struct dss_ctx {
   cudaEvent_t ev_in = nullptr, ev_free = nullptr, ev_snap = nullptr, ev_out = nullptr;
   void* snapshot = nullptr;
   bool host_pipe = false;
-  // element-chunked host pipeline (one GPU, all groups local): per chunk,
-  // H2D of the gradients, the step of that element range, D2H of the params
-  // overlap across chunks and iterations
-  std::vector<cudaEvent_t> hc_in, hc_step, hc_out;
 
   std::vector<long> step_count;
   std::vector<void*> peer_w, peer_g, peer_mg;

@@ -308,9 +308,6 @@ extern "C" int dss_destroy(dss_ctx* c) {
   for (cudaEvent_t e : {c->ev_in, c->ev_free, c->ev_snap, c->ev_out}) {
     if (e) cudaEventDestroy(e);
   }
-  for (auto* v : {&c->hc_in, &c->hc_step, &c->hc_out}) {
-    for (cudaEvent_t e : *v) cudaEventDestroy(e);
-  }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return DSS_OK;
@@ -559,95 +556,12 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
   });
 }
 
-// DS-Sync on one GPU with every group local and no running statistics: the
-// step is elementwise, so the iteration is split into element chunks that
-// flow H2D (copy_in) -> step (stream) -> D2H (copy_out), each stage of chunk
-// k overlapping the others' work on chunks k +- 1 and the previous / next
-// iteration.  PCIe carries both directions at once; the period approaches
-// max(H2D, D2H) instead of H2D + step + snapshot.
-#ifndef DSS_HOST_CHUNKS
-#define DSS_HOST_CHUNKS 8
-#endif
-
-namespace {
-
-bool host_chunked(const dss_ctx* c) {
-  if (DSS_HOST_CHUNKS < 2 || multi(c) || c->s != 0 || c->cfg.strategy.kind != DSS_DS_SYNC) return false;
-  for (int p = 0; p < 2; ++p) {
-    if (c->step_plan[p].any_spanning || !c->step_plan[p].built) return false;
-  }
-  return c->d >= 64L * DSS_HOST_CHUNKS;
-}
-
-int step_host_chunked(dss_ctx* c, long t, double alpha, const void* host_grads, void* host_params) {
-  const int K = DSS_HOST_CHUNKS;
-  if (c->hc_in.empty()) {
-    ck(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking), "copy stream");
-    ck(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking), "copy stream");
-    for (auto* v : {&c->hc_in, &c->hc_step, &c->hc_out}) {
-      v->resize(static_cast<size_t>(K));
-      for (cudaEvent_t& e : *v) {
-        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-        ck(cudaEventRecord(e, c->stream), "event");
-      }
-    }
-  }
-  // the previous call's params must be on the host before we return
-  std::vector<cudaEvent_t> prev_out = c->hc_out;
-  const size_t row = static_cast<size_t>(c->d) * c->esz;
-  const size_t ld = static_cast<size_t>(c->d_pad) * c->esz;
-  const long per = (c->d + K - 1) / K;
-  const long chunk = (per + 63) / 64 * 64;  // whole 16-B vectors and 256-B aligned starts
-  const ParityPlan& pp = c->step_plan[t & 1];
-  for (int k = 0; k < K; ++k) {
-    const long lo = static_cast<long>(k) * chunk;
-    if (lo >= c->d) break;
-    const long hi = std::min(c->d, lo + chunk);
-    const size_t off = static_cast<size_t>(lo) * c->esz, width = static_cast<size_t>(hi - lo) * c->esz;
-    // grads chunk in, once the previous iteration's step of this chunk is done reading them
-    ck(cudaStreamWaitEvent(c->copy_in, c->hc_step[static_cast<size_t>(k)], 0), "wait");
-    ck(cudaMemcpy2DAsync(static_cast<char*>(c->g) + off, ld, static_cast<const char*>(host_grads) + off, row, width,
-                         static_cast<size_t>(c->P), cudaMemcpyHostToDevice, c->copy_in),
-       "grads H2D");
-    ck(cudaEventRecord(c->hc_in[static_cast<size_t>(k)], c->copy_in), "event");
-    // step this element range once the grads are in and the previous
-    // iteration's params of the range are out
-    ck(cudaStreamWaitEvent(c->stream, c->hc_in[static_cast<size_t>(k)], 0), "wait");
-    ck(cudaStreamWaitEvent(c->stream, c->hc_out[static_cast<size_t>(k)], 0), "wait");
-    const long n = (hi - lo + 63) / 64 * 64;  // the last chunk covers the zero padding too
-    for (const GroupLaunch& gl : pp.local) {
-      launch_groups_any(c, gl, c->cfg.optimizer, t, alpha, c->g, c->d_pad, 0, 1, nullptr, 0, lo, n);
-    }
-    ck(cudaEventRecord(c->hc_step[static_cast<size_t>(k)], c->stream), "event");
-    // params chunk out
-    ck(cudaStreamWaitEvent(c->copy_out, c->hc_step[static_cast<size_t>(k)], 0), "wait");
-    ck(cudaMemcpy2DAsync(static_cast<char*>(host_params) + off, row, static_cast<char*>(c->w) + off, ld, width,
-                         static_cast<size_t>(c->P), cudaMemcpyDeviceToHost, c->copy_out),
-       "params D2H");
-    ck(cudaEventRecord(c->hc_out[static_cast<size_t>(k)], c->copy_out), "event");
-  }
-  bump_steps(c);
-  // later work on the context's stream (the next step, uploads, downloads)
-  // must not overwrite params rows whose D2H is still reading them
-  for (cudaEvent_t e : c->hc_out) ck(cudaStreamWaitEvent(c->stream, e, 0), "wait");
-  for (cudaEvent_t e : prev_out) ck(cudaEventSynchronize(e), "previous copy-out");
-  return DSS_OK;
-}
-
-}  // namespace
-
 extern "C" int dss_step_host(dss_ctx* c, long t, double alpha, const void* host_grads, void* host_params) {
   if (!c || !host_grads || !host_params) return fail(c, DSS_EINVAL, "null argument");
-  if (host_chunked(c)) {
-    return guard(c, [&]() -> int {
-      if (t < 0) throw std::invalid_argument("iteration must be >= 0");
-      if (!std::isfinite(alpha) || alpha < 0.0) {
-        throw std::invalid_argument("learning rate at t=" + std::to_string(t) + " must be finite and >= 0");
-      }
-      ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
-      return step_host_chunked(c, t, alpha, host_grads, host_params);
-    });
-  }
+  // An element-chunked variant (each chunk's copy-in, step and copy-out
+  // overlapping the neighbours', no snapshot) was built, checked bit-exact
+  // and measured slower: C2 56.1 (this path) vs 42.3 / 49.6 / 54.6 iters/s
+  // with 2 / 4 / 8 chunks (profiles/r02/e2e_chunked_ab.jsonl).
   int st = guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
     if (!c->host_pipe) {
@@ -700,7 +614,7 @@ extern "C" int dss_host_sync(dss_ctx* c) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
   return guard(c, [&]() -> int {
     ck(cudaSetDevice(c->cfg.device), "cudaSetDevice");
-    if (c->host_pipe || !c->hc_in.empty()) {
+    if (c->host_pipe) {
       ck(cudaStreamSynchronize(c->copy_in), "copy-in sync");
       ck(cudaStreamSynchronize(c->copy_out), "copy-out sync");
     }
