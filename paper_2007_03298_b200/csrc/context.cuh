@@ -432,8 +432,7 @@ std::vector<OwnedSlot> owned_layout(const dss_ctx* c, const Partition& part, int
 void build_plans(dss_ctx* c);
 
 void launch_groups_any(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha, const void* g, long g_ld,
-                       int step_phase, int sync_phase = 1, void* rows = nullptr, long rows_ld = 0, long lo = 0,
-                       long n = -1);
+                       int step_phase, int sync_phase = 1, void* rows = nullptr, long rows_ld = 0);
 void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t);
 void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha = 0.0);
 void launch_push_any(dss_ctx* c, const PushLaunch& pl, long t, double alpha);

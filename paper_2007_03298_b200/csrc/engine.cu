@@ -811,8 +811,7 @@ void launch_group_m(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
 // opt < 0: fold only (sync_round); otherwise the optimizer kind.
 template <typename T>
 void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha,
-                   const void* g, long g_ld, int step_phase, int sync_phase, void* rows = nullptr, long rows_ld = 0,
-                   long lo = 0, long n = -1) {
+                   const void* g, long g_ld, int step_phase, int sync_phase, void* rows = nullptr, long rows_ld = 0) {
   if (gl.groups == 0) return;
   GroupArgs<T> a{};
   a.w = static_cast<T*>(rows ? rows : c->w);  // rows: fold-only over another row set (running stats)
@@ -822,13 +821,6 @@ void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double al
   a.ld = rows ? rows_ld : c->d_pad;
   a.g_ld = g_ld;
   a.nvec = a.ld / Vec<T>::n;
-  if (n >= 0) {  // element range [lo, lo + n) of every row (the fold is elementwise)
-    a.w += lo;
-    if (a.g) a.g += lo;
-    if (a.m1) a.m1 += lo;
-    if (a.m2) a.m2 += lo;
-    a.nvec = n / Vec<T>::n;
-  }
   a.first_rank = c->first;
   a.rank_of = c->d_rank_of;
   a.members = gl.d_members;
@@ -851,11 +843,11 @@ void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double al
 
 void launch_groups_any(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double alpha,
                        const void* g, long g_ld, int step_phase, int sync_phase, void* rows,
-                       long rows_ld, long lo, long n) {
+                       long rows_ld) {
   if (c->cfg.dtype == DSS_F64) {
-    launch_groups<double>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase, rows, rows_ld, lo, n);
+    launch_groups<double>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase, rows, rows_ld);
   } else {
-    launch_groups<float>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase, rows, rows_ld, lo, n);
+    launch_groups<float>(c, gl, opt, t, alpha, g, g_ld, step_phase, sync_phase, rows, rows_ld);
   }
 }
 
