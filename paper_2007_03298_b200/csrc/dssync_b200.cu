@@ -209,11 +209,11 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
                                           force_chain(c.get())).max_chain_slots);
       }
       c->chain_slots = slots;
-      // the tiled placement's two-GPU chains prefer longer chunks (4 GPUs,
-      // profiles/r02/chain_chunk_ab_g4.jsonl: C3 744 -> 753, C4 32.0 -> 33.1
-      // iters/s at 16384); packed BSP and contiguous chains keep 8192
-      // (BSP C3 768 -> 690 at 16384)
-      c->chain_chunk = std::min<long>(c->d_pad, c->placed ? DSS_CHAIN_CHUNK_PLACED : DSS_CHAIN_CHUNK);
+      // DS-Sync chains prefer longer chunks than the packed BSP chain
+      // (profiles/r02/chain_chunk_ab_g{2,4}.jsonl, 16384 vs 8192: DS C2 @2
+      // 3204 -> 3250, C3 @4 744 -> 753, C4 @4 32.0 -> 33.1 iters/s; BSP C3
+      // @4 768 -> 690, C2 @2 2657 -> 2346)
+      c->chain_chunk = std::min<long>(c->d_pad, s.kind == DSS_DS_SYNC ? DSS_CHAIN_CHUNK_DS : DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
       // Fused two-shot staging of the owned slices, worst parity and worst

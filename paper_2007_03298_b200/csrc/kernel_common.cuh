@@ -73,8 +73,8 @@ constexpr int kSmallWide = 512;
 #ifndef DSS_CHAIN_CHUNK
 #define DSS_CHAIN_CHUNK 8192
 #endif
-#ifndef DSS_CHAIN_CHUNK_PLACED
-#define DSS_CHAIN_CHUNK_PLACED 16384
+#ifndef DSS_CHAIN_CHUNK_DS
+#define DSS_CHAIN_CHUNK_DS 16384
 #endif
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 8
