@@ -209,11 +209,14 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
                                           force_chain(c.get())).max_chain_slots);
       }
       c->chain_slots = slots;
-      // DS-Sync chains prefer longer chunks than the packed BSP chain
-      // (profiles/r02/chain_chunk_ab_g{2,4}.jsonl, 16384 vs 8192: DS C2 @2
-      // 3204 -> 3250, C3 @4 744 -> 753, C4 @4 32.0 -> 33.1 iters/s; BSP C3
-      // @4 768 -> 690, C2 @2 2657 -> 2346)
-      c->chain_chunk = std::min<long>(c->d_pad, s.kind == DSS_DS_SYNC ? DSS_CHAIN_CHUNK_DS : DSS_CHAIN_CHUNK);
+      // DS-Sync with large rows prefers longer chunks than the packed BSP
+      // chain and than small rows (profiles/r02/chain_chunk_ab_g{2,4}.jsonl,
+      // 16384 vs 8192: DS C2 @2 3204 -> 3250, C2 @4 3480 -> 3560, C3 @4
+      // 744 -> 753, C4 @4 32.0 -> 33.1 iters/s; but BSP C3 @4 768 -> 690,
+      // and the sweep's 64 KB - 64 MB rows lose up to 40%,
+      // profiles/r02/chain_chunk_sweep_ab_g4.jsonl)
+      const bool long_chunks = s.kind == DSS_DS_SYNC && c->d_pad * c->esz >= DSS_CHAIN_CHUNK_DS_MIN_BYTES;
+      c->chain_chunk = std::min<long>(c->d_pad, long_chunks ? DSS_CHAIN_CHUNK_DS : DSS_CHAIN_CHUNK);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
       // Fused two-shot staging of the owned slices, worst parity and worst
