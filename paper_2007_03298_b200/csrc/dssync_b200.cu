@@ -209,7 +209,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
                                           force_chain(c.get())).max_chain_slots);
       }
       c->chain_slots = slots;
-      // DS-Sync with large rows prefers longer chunks than the packed BSP
+      // DS-Sync with rows of 80 MiB or more prefers longer chunks than the packed BSP
       // chain and than small rows (profiles/r02/chain_chunk_ab_g{2,4}.jsonl,
       // 16384 vs 8192: DS C2 @2 3204 -> 3250, C2 @4 3480 -> 3560, C3 @4
       // 744 -> 753, C4 @4 32.0 -> 33.1 iters/s; but BSP C3 @4 768 -> 690,

@@ -77,7 +77,7 @@ constexpr int kSmallWide = 512;
 #define DSS_CHAIN_CHUNK_DS 16384
 #endif
 #ifndef DSS_CHAIN_CHUNK_DS_MIN_BYTES
-#define DSS_CHAIN_CHUNK_DS_MIN_BYTES (96L << 20)
+#define DSS_CHAIN_CHUNK_DS_MIN_BYTES (80L << 20)
 #endif
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 8
