@@ -378,18 +378,18 @@ def step_bytes(cfg, G, rank, d_pad, path=0, esz=4, placement=0):
     P = W // G
     gpu_of = gpu_map(cfg, G, placement)[0]
     mine = {k for k in range(W) if gpu_of[k] == rank}
-    out = {"ds": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0},
-           "bsp": {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0}}
+    z = {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0, "chain_mean_nvlink": 0.0,
+         "chain_hbm": 0.0}
+    out = {"ds": dict(z), "bsp": dict(z)}
     s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, cfg["rect"])
     chunks = d_pad // 64
 
     def chain_out(gpus):
-        # partial row out unless last stage; mean row out if this GPU forwards
-        # in the mean pass (last -> g0 -> ... -> g_{S-2})
+        # rank's outbound rows in the partial-pass kernel (every stage sends
+        # one: the partial, or the mean from the last stage) and in the
+        # mean-pass kernel (a forwarded mean, stages 0..S-3)
         S, j = len(gpus), gpus.index(rank)
-        partial = d * esz if j < S - 1 else 0
-        mean = d * esz if (j == S - 1 or j < S - 2) else 0
-        return partial + mean
+        return d * esz, (d * esz if j < S - 2 else 0)
 
     for p in (0, 1):
         for g in make_partition(s, p).groups:
@@ -402,7 +402,16 @@ def step_bytes(cfg, G, rank, d_pad, path=0, esz=4, placement=0):
             if len(gpus) == 1:
                 continue
             if max(sum(1 for m in g if gpu_of[m] == q) for q in gpus) >= 2:  # ordered chain
-                out["ds"]["chain_nvlink"] += 0.5 * chain_out(gpus)
+                a_bytes, b_bytes = chain_out(gpus)
+                out["ds"]["chain_nvlink"] += 0.5 * a_bytes
+                out["ds"]["chain_mean_nvlink"] += 0.5 * b_bytes
+                # partial-pass HBM bytes: the fused step of the members here
+                # (every array but the params write), the received partial
+                # (stages > 0), the mean into the members here (last stage)
+                S, j = len(gpus), gpus.index(rank)
+                hb = len(here) * d * (bpe - esz) + (d * esz if j > 0 else 0) + \
+                    (len(here) * d * esz if j == S - 1 else 0)
+                out["ds"]["chain_hbm"] += 0.5 * hb
                 continue
             S, j = len(gpus), gpus.index(rank)
             L = (chunks // S + (1 if j < chunks % S else 0)) * 64
@@ -411,7 +420,7 @@ def step_bytes(cfg, G, rank, d_pad, path=0, esz=4, placement=0):
     if G == 1:
         out["bsp"]["group"] = W * d * bpe
     elif P >= 2:
-        out["bsp"]["chain_nvlink"] = chain_out(list(range(G)))
+        out["bsp"]["chain_nvlink"], out["bsp"]["chain_mean_nvlink"] = chain_out(list(range(G)))
         out["bsp"]["group"] = P * d * bpe
     else:
         L = (chunks // G + (1 if rank < chunks % G else 0)) * 64
@@ -515,7 +524,7 @@ class NcclBaseline:
         self.e.apply_step(alpha, check=False)
 
 
-def dominant_roofline(kinds_rows, ms_step, peak, peak_kind, G):
+def dominant_roofline(kinds_rows, ms_step, peak, peak_kind, G, chain_hbm=0.0):
     """Roofline of the kernel with the most time in the step.  HBM kernels
     (group / bsp) against the measured copy peak; cross-GPU kernels (fold =
     push / pull two-shot and one-shot, chain = the ordered chain's partial +
@@ -527,8 +536,17 @@ def dominant_roofline(kinds_rows, ms_step, peak, peak_kind, G):
         elif k == "fold" and v.get("nvlink_bytes_per_step"):
             cand[k] = ("nvlink", v["ms_per_step"], v["launches_per_step"], v["nvlink_bytes_per_step"])
         elif k == "chain" and v.get("nvlink_bytes_per_step"):
-            both = v["ms_per_step"] + kinds_rows.get("chain_mean", {}).get("ms_per_step", 0.0)
-            cand[k] = ("nvlink", both, v["launches_per_step"], v["nvlink_bytes_per_step"])
+            # the partial-pass kernel carries the rank's outbound row of each
+            # chain role and the fused member steps: a fused step + collective
+            # kernel, bounded by the slower of its HBM and NVLink bytes
+            # (B200_PROFILING.md); the mean pass is its own kernel, reported
+            # in its own row
+            link_t = v["nvlink_bytes_per_step"] / (NVLINK_PEAK * 1e9)
+            hbm_t = chain_hbm / (peak * 1e9)
+            if hbm_t > link_t:
+                cand[k] = ("hbm", v["ms_per_step"], v["launches_per_step"], chain_hbm)
+            else:
+                cand[k] = ("nvlink", v["ms_per_step"], v["launches_per_step"], v["nvlink_bytes_per_step"])
     if not cand:
         return None
     k, (bound, ms_, n_, b_) = max(cand.items(), key=lambda kv: kv[1][1])
@@ -688,16 +706,22 @@ def summarize(args, cfg, dtype, G, res, peak, peak_kind):
                            nvlink_bytes_per_step=nb_bytes[key]["fold_nvlink"],
                            nvlink_gbs=nb_bytes[key]["fold_nvlink"] / (ms_ / 1e3) / 1e9 if ms_ else None)
             elif k == "chain_mean":
-                row.update(note="mean pass of the chain (rank 0); its NVLink bytes are counted under chain")
+                b = nb_bytes[key]["chain_mean_nvlink"]
+                row.update(nvlink_bytes_per_step=b, nvlink_gbs=b / (ms_ / 1e3) / 1e9 if ms_ and b else None,
+                           note="mean pass of the chain (rank 0): copies the received mean to the other local "
+                                "members; forwards it on middle stages")
             elif k == "chain":
-                both = ms_ + r["kinds"].get("chain_mean", (0.0, 0))[0]
-                row.update(nvlink_bytes_per_step=nb_bytes[key]["chain_nvlink"],
-                           nvlink_gbs=nb_bytes[key]["chain_nvlink"] / (both / 1e3) / 1e9 if both else None)
+                b = nb_bytes[key]["chain_nvlink"]
+                hb = nb_bytes[key]["chain_hbm"]
+                row.update(nvlink_bytes_per_step=b, nvlink_gbs=b / (ms_ / 1e3) / 1e9 if ms_ else None,
+                           hbm_bytes_per_step=hb or None, hbm_gbs=hb / (ms_ / 1e3) / 1e9 if ms_ and hb else None,
+                           note="partial pass (rank 0): fused member step + ordered fold + one outbound row per "
+                                "chain role (the partial, or the mean from the last stage)")
             rows[k] = row
         return rows
 
     ds_k = kernel_rows(ds, "ds")
-    roof = dominant_roofline(ds_k, ds["ms"], peak, peak_kind, G)
+    roof = dominant_roofline(ds_k, ds["ms"], peak, peak_kind, G, nb_bytes["ds"]["chain_hbm"])
     # the HBM kernel is always reported too (at N > 1 it may not dominate)
     hbm = dominant_roofline({k: v for k, v in ds_k.items() if k in ("group", "bsp")}, ds["ms"], peak, peak_kind, G)
     traffic = None
