@@ -42,7 +42,7 @@ def device_of(rank):
     return rank % torch.cuda.device_count()
 
 
-def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0, placement=0):
+def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0, placement=0, iters=5):
     s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
                      WorldConfig(W, N), 1, rect)
     wd = 0.01 if opt in (1, 3) else 0.0
@@ -62,7 +62,7 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0, placement=0):
     m1, m2 = np.zeros_like(w), np.zeros_like(w)
     steps = np.zeros(W, np.int64)
     alpha = 0.05 if opt < 2 else 0.01
-    for t in range(5):
+    for t in range(iters):
         g = rng.standard_normal((W, d)).astype(np.float32)
         e.upload_all(BUF_GRADS, g[mine])
         if sd:  # fold_running_stats EMA, then the stats ride the step's fold
@@ -82,15 +82,15 @@ def run_case(kind, W, N, rect, opt, d, rank, G, orc, path=0, sd=0, placement=0):
         assert rc[0] == 0
         steps += 1
     # sync-only round too (sync_round semantics over peers)
-    e.sync_round(5, check=False)
+    e.sync_round(iters, check=False)
     if kind == "ds":
-        orc.sync_round(W, N, 5, w, rect=rect)
+        orc.sync_round(W, N, iters, w, rect=rect)
         if sd:
-            orc.sync_round(W, N, 5, rs, rect=rect)
+            orc.sync_round(W, N, iters, rs, rect=rect)
     else:
-        orc.sync_round(W, W, 5, w, kind=0)
+        orc.sync_round(W, W, iters, w, kind=0)
         if sd:
-            orc.sync_round(W, W, 5, rs, kind=0)
+            orc.sync_round(W, W, iters, rs, kind=0)
     e.check()
     got = e.download_all(BUF_PARAMS)
     got_m1 = e.download_all(BUF_MOMENT1) if opt >= 1 else None
@@ -224,6 +224,9 @@ def main():
         for path in (0, 2, 3, 4):
             ok = run_case(*case, rank, G, orc, path, placement=1) and ok
     ok = run_case("ds", 32, 4, True, 2, 1001, rank, G, orc, 0, sd=6, placement=1) and ok
+    # rows past the 80 MiB long-chunk threshold (16384-element chain chunks,
+    # C2-sized rows): a block and a comb iteration plus a sync round
+    ok = run_case("ds", 8, 2, True, 1, 21_000_003, rank, G, orc, 0, iters=2) and ok
     for kind in ("ds",):
         ok = placed_logistic_case(rank, G) and ok
     from paper_2007_03298_b200 import SamplingMode
