@@ -789,8 +789,29 @@ void launch_group_bulk(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl)
   ck(cudaGetLastError(), "ds_group_bulk_kernel launch");
 }
 
+// fp32 groups of 8 with these optimizers (bit OPT: momentum, Adam, AdamW)
+// take the narrow-vector kernel: +0.6-0.7% over the 16-B two-phase kernel
+// (C4 slice 6147 -> 6192 GB/s, C3 6272 -> 6310; profiles/r02/narrow_group_kernel_ab.jsonl)
+#ifndef DSS_GROUP_NARROW
+#define DSS_GROUP_NARROW 14
+#endif
+
+template <int OPT>
+void launch_group_narrow(dss_ctx* c, const GroupArgs<float>& a, int groups) {
+  dim3 grid(grid_x(c, a.nvec * 2, groups), groups);
+  TimedLaunch tl(c, DSS_KIND_GROUP);
+  ds_group_narrow_kernel<OPT, 8><<<grid, kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "ds_group_narrow_kernel launch");
+}
+
 template <typename T, int OPT>
 void launch_group_m(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
+  if constexpr (std::is_same_v<T, float> && OPT != kOptNone) {
+    if (((DSS_GROUP_NARROW >> OPT) & 1) && gl.size == 8 && a.g_ld == a.ld) {
+      launch_group_narrow<OPT>(c, a, gl.groups);
+      return;
+    }
+  }
   if constexpr (OPT == kMomentum || OPT == kAdam || OPT == kAdamW) {
     if (DSS_GROUP_BULK && std::is_same_v<T, float> && gl.size == 8 && a.g_ld == a.ld &&
         a.w == static_cast<T*>(c->w)) {

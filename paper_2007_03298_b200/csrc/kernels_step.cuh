@@ -175,6 +175,78 @@ __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
 
+// ---- narrow-vector group step (fp32, 8-B vectors, every member in flight) ---
+// ds_group_kernel with float2 instead of float4 per thread: half the
+// registers per member, so a stateful group of 8 issues every member's
+// w, g and state loads at once (no second load phase) within the 2-CTA/SM
+// register budget.  Same arithmetic, same order.
+template <int OPT, int M>
+__global__ void __launch_bounds__(kThreads, 2) ds_group_narrow_kernel(const GroupArgs<float> a) {
+  const int beg = a.offsets[blockIdx.y];
+  const int lead = a.rank_of[a.members[beg] - a.first_rank];
+  const float inv = static_cast<float>(1.0 / static_cast<double>(M));
+  unsigned long long bad = ~0ull;
+  int lrow[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) lrow[j] = a.members[beg + j] - a.first_rank;
+  const long nv2 = a.nvec * 2;  // float2 vectors per row
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; e < nv2; e += stride) {
+    const long off = e * 2;
+    float2 xs[M], gs[M], s1[M], s2[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const long rj = static_cast<long>(lrow[j]) * a.ld + off;
+      xs[j] = __ldcs(reinterpret_cast<const float2*>(a.w + rj));
+      gs[j] = __ldcs(reinterpret_cast<const float2*>(a.g + static_cast<long>(lrow[j]) * a.g_ld + off));
+      if constexpr (OPT != kSgd) s1[j] = __ldcs(reinterpret_cast<const float2*>(a.m1 + rj));
+      if constexpr (OPT == kAdam || OPT == kAdamW) s2[j] = __ldcs(reinterpret_cast<const float2*>(a.m2 + rj));
+    }
+    float2 acc;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const long rj = static_cast<long>(lrow[j]) * a.ld + off;
+      float b1j = 1.f, b2j = 1.f;
+      if constexpr (OPT == kAdam || OPT == kAdamW) {
+        b1j = static_cast<float>(a.bc1[lrow[j]]);
+        b2j = static_cast<float>(a.bc2[lrow[j]]);
+      }
+      float m1a = 0.f, m1b = 0.f, m2a = 0.f, m2b = 0.f;
+      if constexpr (OPT != kSgd) {
+        m1a = s1[j].x;
+        m1b = s1[j].y;
+      }
+      if constexpr (OPT == kAdam || OPT == kAdamW) {
+        m2a = s2[j].x;
+        m2b = s2[j].y;
+      }
+      const float xa = step_elem<float, OPT>(xs[j].x, gs[j].x, m1a, m2a, a.c, b1j, b2j);
+      const float xb = step_elem<float, OPT>(xs[j].y, gs[j].y, m1b, m2b, a.c, b1j, b2j);
+      if constexpr (OPT != kSgd) __stcs(reinterpret_cast<float2*>(a.m1 + rj), make_float2(m1a, m1b));
+      if constexpr (OPT == kAdam || OPT == kAdamW) __stcs(reinterpret_cast<float2*>(a.m2 + rj), make_float2(m2a, m2b));
+      if (!(finite_(xa) && finite_(xb))) {
+        const unsigned long long k = err_key(a.t, a.step_phase, a.rank_of[lrow[j]]);
+        bad = k < bad ? k : bad;
+      }
+      if (j == 0) {
+        acc = make_float2(xa, xb);
+      } else {
+        acc.x = add_(acc.x, xa);
+        acc.y = add_(acc.y, xb);
+      }
+    }
+    acc.x = mul_(acc.x, inv);
+    acc.y = mul_(acc.y, inv);
+    if (!(finite_(acc.x) && finite_(acc.y))) {
+      const unsigned long long k = err_key(a.t, a.sync_phase, lead);
+      bad = k < bad ? k : bad;
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) __stcs(reinterpret_cast<float2*>(a.w + static_cast<long>(lrow[j]) * a.ld + off), acc);
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
 // ---- shared-memory-staged group step (cp.async.bulk + mbarrier ring) -------
 // Same arithmetic as ds_group_kernel; for groups of 8 with stateful
 // optimizers, where holding every member's w/g/m/v in registers caps the
