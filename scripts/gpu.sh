@@ -1,5 +1,8 @@
 #!/bin/bash
 # One parametrised GPU-box runner (replaces the round-1 one-off gpu_run*.sh).
+# Companions: ab.sh / e2e_ab.sh (single-GPU library-variant A/B), mgpu_ab.sh
+# (multi-GPU A/B, any bench args e.g. --placement 0/1/2), sweep.sh /
+# sweep_ab.sh (BASELINE config 5), shim_timing.sh, nvlink_probe.sh.
 #   scripts/gpu.sh <task> [args]    run under gpurun, writes to gpurun_out/
 # tasks:
 #   tests            pytest -m gpu (one GPU), then smoke()
