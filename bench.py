@@ -353,12 +353,12 @@ def cpu_run_training_c1():
 
 
 # ---------------------------------------------------------------------------
-def gpu_map(cfg, G, placement):
+def gpu_map(cfg, G, placement, esz=4):
     """gpu_of / row_of of every global rank for the DS engines (dss_placement)."""
     from paper_2007_03298_b200 import StrategyKind, SyncStrategy, Topology, WorldConfig
     from paper_2007_03298_b200 import placement as place
     s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(cfg["W"], cfg["N"]), 1, cfg["rect"])
-    gpu, row, tiling = place(s, G, placement)
+    gpu, row, tiling = place(s, G, placement, cfg["d"], "f64" if esz == 8 else "f32")
     return gpu, row, tiling
 
 
@@ -376,7 +376,7 @@ def step_bytes(cfg, G, rank, d_pad, path=0, esz=4, placement=0):
     W, N, d = cfg["W"], cfg["N"], cfg["d"]
     bpe = BYTES_PER_ELEM[cfg["opt"]] * esz // 4
     P = W // G
-    gpu_of = gpu_map(cfg, G, placement)[0]
+    gpu_of = gpu_map(cfg, G, placement, esz)[0]
     mine = {k for k in range(W) if gpu_of[k] == rank}
     z = {"group": 0.0, "fold_hbm": 0.0, "fold_nvlink": 0.0, "chain_nvlink": 0.0, "chain_mean_nvlink": 0.0,
          "chain_hbm": 0.0}

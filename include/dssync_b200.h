@@ -128,8 +128,8 @@ typedef struct {
                            order and results are unchanged; only which GPU holds which
                            worker.  Ignored (contiguous) for BSP and single-group worlds.
                            2 = auto: the tiling where contiguous packing would leave an
-                           ordered chain >= 3 GPUs deep (C3 / C4 on 4 GPUs), else
-                           contiguous. */
+                           ordered chain >= 3 GPUs deep (C3 / C4 on 4 GPUs) and rows
+                           are past the one-shot size (512 KiB), else contiguous. */
 } dss_config;
 
 typedef struct dss_ctx dss_ctx;
@@ -163,10 +163,12 @@ int dss_check_mixing(const dss_strategy* s, long t);
 int dss_round_outcome(const dss_strategy* s, long t, long payload_dim, dss_outcome* out);
 
 /* Worker placement: gpu_of[k] and row_of[k] (the local row on that GPU) for
- * every global rank k of a context created with this strategy, n_gpus and
- * placement mode (dss_config.placement); *gr / *gc receive the tiling
- * (0, 0 for contiguous packing).  Host only. */
-int dss_placement(const dss_strategy* s, int n_gpus, int placement, int* gpu_of, int* row_of, int* gr, int* gc);
+ * every global rank k of a context created with this strategy, n_gpus,
+ * placement mode (dss_config.placement), dim and dtype (auto mode keeps
+ * rows of the one-shot size contiguous; dim = 0 ignores the row size);
+ * *gr / *gc receive the tiling (0, 0 for contiguous packing).  Host only. */
+int dss_placement(const dss_strategy* s, int n_gpus, int placement, long dim, int dtype, int* gpu_of, int* row_of,
+                  int* gr, int* gc);
 
 /* Multi-GPU plan for (strategy, t, n_gpus, rank): how many groups this GPU
  * folds locally, how many span GPUs, and the [lo, hi) element slice this GPU

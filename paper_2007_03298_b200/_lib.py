@@ -65,8 +65,8 @@ SIGNATURES = {
     "dss_set_stream": (C.c_int, [_P, _P]),
     "dss_local_workers": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "dss_local_ranks": (C.c_int, [_P, _P]),
-    "dss_placement": (C.c_int, [C.POINTER(dss_strategy), C.c_int, C.c_int, _P, _P, C.POINTER(C.c_int),
-                                C.POINTER(C.c_int)]),
+    "dss_placement": (C.c_int, [C.POINTER(dss_strategy), C.c_int, C.c_int, C.c_long, C.c_int, _P, _P,
+                                C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "dss_row_stride": (C.c_long, [_P]),
     "dss_elem_size": (C.c_int, [_P]),
     "dss_device_ptr": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_P)]),

@@ -256,16 +256,18 @@ def check_mixing(cfg, t: int) -> bool:  # schedule.cpp:67-90
     return r == 1
 
 
-def placement(strategy: SyncStrategy, n_gpus: int, mode: int = 1):
+def placement(strategy: SyncStrategy, n_gpus: int, mode: int = 1, dim: int = 0, dtype: str = "f32"):
     """Worker placement of a context (dss_placement): (gpu_of, row_of, (gr, gc))
-    for every global rank; (0, 0) is contiguous packing."""
+    for every global rank; (0, 0) is contiguous packing.  dim / dtype: the
+    row size the auto mode considers (0: ignore)."""
     s = _c_strategy(strategy)
     W = strategy.world.world_size
     gpu = np.zeros(W, dtype=np.int32)
     row = np.zeros(W, dtype=np.int32)
     gr, gc = C.c_int(), C.c_int()
-    _check_global(L.load().dss_placement(C.byref(s), n_gpus, mode, gpu.ctypes.data, row.ctypes.data, C.byref(gr),
-                                         C.byref(gc)))
+    dt = L.DSS_F64 if dtype in ("f64", np.float64) else L.DSS_F32
+    _check_global(L.load().dss_placement(C.byref(s), n_gpus, mode, dim, dt, gpu.ctypes.data, row.ctypes.data,
+                                         C.byref(gr), C.byref(gc)))
     return gpu.tolist(), row.tolist(), (gr.value, gc.value)
 
 

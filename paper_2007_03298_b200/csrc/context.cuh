@@ -414,11 +414,22 @@ StepConsts<T> consts(const dss_ctx* c, double alpha) {
 
 template <typename Args>
 void fill_bias(const dss_ctx* c, Args& a) {
+  // only Adam / AdamW read the bias corrections; workers usually share one
+  // step count, so pow() runs once per distinct count (host launch cost)
+  if (c->cfg.optimizer != DSS_ADAM && c->cfg.optimizer != DSS_ADAMW) return;
   const dss_hparams& h = c->cfg.hp;
+  long last = -1;
+  double b1 = 0.0, b2 = 0.0;
   for (int k = 0; k < c->P; ++k) {
-    const double t = static_cast<double>(c->step_count[static_cast<size_t>(k)] + 1);
-    a.bc1[k] = 1.0 - std::pow(h.beta1, t);  // optim.cpp:76-77
-    a.bc2[k] = 1.0 - std::pow(h.beta2, t);  // optim.cpp:78
+    const long sc = c->step_count[static_cast<size_t>(k)];
+    if (sc != last) {
+      const double t = static_cast<double>(sc + 1);
+      b1 = 1.0 - std::pow(h.beta1, t);  // optim.cpp:76-77
+      b2 = 1.0 - std::pow(h.beta2, t);  // optim.cpp:78
+      last = sc;
+    }
+    a.bc1[k] = b1;
+    a.bc2[k] = b2;
   }
 }
 

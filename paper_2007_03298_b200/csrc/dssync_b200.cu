@@ -132,7 +132,8 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     }
     c->first = cfg->rank * c->P;
     {
-      const Tiling tl = choose_placement(s, cfg->n_gpus, cfg->placement);
+      const Tiling tl = choose_placement(s, cfg->n_gpus, cfg->placement,
+                                         pad_dim(cfg->dim) * (cfg->dtype == DSS_F64 ? 8 : 4), DSS_ONESHOT_MAX_BYTES);
       c->slot_of = placement_slots(s, cfg->n_gpus, tl);
       c->rank_of_slot.assign(c->slot_of.size(), 0);
       for (size_t k = 0; k < c->slot_of.size(); ++k) {
@@ -343,14 +344,15 @@ extern "C" int dss_local_ranks(const dss_ctx* c, int* ranks) {
   return DSS_OK;
 }
 
-extern "C" int dss_placement(const dss_strategy* s, int n_gpus, int placement, int* gpu_of, int* row_of, int* gr,
-                             int* gc) {
+extern "C" int dss_placement(const dss_strategy* s, int n_gpus, int placement, long dim, int dtype, int* gpu_of,
+                             int* row_of, int* gr, int* gc) {
   if (!s || n_gpus < 1 || s->world_size < 1 || s->world_size % n_gpus) {
     return fail(nullptr, DSS_EINVAL, "dss_placement: world_size must be a multiple of n_gpus");
   }
   return guard(nullptr, [&]() -> int {
     if (placement < 0 || placement > 2) throw std::invalid_argument("placement must be 0, 1 or 2");
-    const Tiling tl = choose_placement(*s, n_gpus, placement);
+    const long row_bytes = dim > 0 ? pad_dim(dim) * (dtype == DSS_F64 ? 8 : 4) : 0;
+    const Tiling tl = choose_placement(*s, n_gpus, placement, row_bytes, DSS_ONESHOT_MAX_BYTES);
     const std::vector<int> slot = placement_slots(*s, n_gpus, tl);
     const int P = s->world_size / n_gpus;
     for (size_t k = 0; k < slot.size(); ++k) {
@@ -655,7 +657,8 @@ extern "C" int dss_steps(dss_ctx* c, long t0, long n, const double* alphas, int 
     return DSS_OK;
   }
   for (long i = 0; i < n; ++i) {
-    const int st = dss_step(c, t0 + i, alphas[i], 0, last);
+    // the closed-form round outcome (a host partition) only for the last iteration
+    const int st = dss_step(c, t0 + i, alphas[i], 0, i + 1 == n ? last : nullptr);
     if (st != DSS_OK) return st;
   }
   if (check) return dss_check(c);

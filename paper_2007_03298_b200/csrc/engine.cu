@@ -991,6 +991,10 @@ void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
   }
 }
 
+#ifndef DSS_PUSH_COOP
+#define DSS_PUSH_COOP 1
+#endif
+
 template <typename T, int OPT>
 void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   ++c->chain_epoch;  // flags compare against the shared epoch sequence
@@ -1042,10 +1046,15 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   }
   const long grid = std::max(1L, std::min<long>(static_cast<long>(o) * c->sms, std::max(pl.items, pl.folds)));
   TimedLaunch tl(c, DSS_KIND_FOLD);
-  void* args[] = {&a};
-  ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(grid)),
-                                 dim3(kThreads), args, 0, c->stream),
-     "push_twoshot_kernel cooperative launch");
+  if (DSS_PUSH_COOP) {
+    void* args[] = {&a};
+    ck(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(static_cast<unsigned>(grid)),
+                                   dim3(kThreads), args, 0, c->stream),
+       "push_twoshot_kernel cooperative launch");
+  } else {
+    kern<<<static_cast<int>(grid), kThreads, 0, c->stream>>>(a);
+    ck(cudaGetLastError(), "push_twoshot_kernel launch");
+  }
 }
 
 template <typename T>

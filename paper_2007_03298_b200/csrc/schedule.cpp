@@ -228,9 +228,10 @@ Tiling choose_tiling(const dss_strategy& s, int G) {
   return best;
 }
 
-Tiling choose_placement(const dss_strategy& s, int G, int mode) {
+Tiling choose_placement(const dss_strategy& s, int G, int mode, long row_bytes, long oneshot_bytes) {
   if (mode == 0 || G <= 1) return Tiling{};
   if (mode == 1) return choose_tiling(s, G);
+  if (oneshot_bytes > 0 && row_bytes > 0 && row_bytes <= oneshot_bytes) return Tiling{};
   // auto: is there a deep chain under contiguous packing?
   const int W = s.world_size, P = W / G;
   bool deep_chain = false;

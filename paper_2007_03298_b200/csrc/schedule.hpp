@@ -109,7 +109,11 @@ Tiling choose_tiling(const dss_strategy& s, int n_gpus);
 // (its one-member-per-GPU groups take the push two-shot, which measured
 // faster than the chains a tiling would create: C2 on 4 GPUs 3501 vs 3103
 // iters/s, profiles/r02/placement_ab_g4.jsonl).
-Tiling choose_placement(const dss_strategy& s, int n_gpus, int mode);
+// Rows of at most `oneshot_bytes` (the one-shot regime, 0 = no limit) stay
+// contiguous in auto mode too: there contiguous packing keeps one parity
+// GPU-local while a tiling makes both parities exchange (W=64 on 4 GPUs at
+// 1 KB-256 KB: 0.53-0.73x, profiles/r02/sweeps/).
+Tiling choose_placement(const dss_strategy& s, int n_gpus, int mode, long row_bytes = 0, long oneshot_bytes = 0);
 // slot_of[k] for every global rank k (identity for contiguous packing).
 std::vector<int> placement_slots(const dss_strategy& s, int n_gpus, const Tiling& t);
 // The partition with every member replaced by its slot (member order, i.e.

@@ -29,6 +29,7 @@ torch.cuda.synchronize()
 dist.barrier()
 t0 = time.perf_counter()
 e.steps(200, np.full(K, 0.01))
+t_enq = (time.perf_counter() - t0) / K  # host time to enqueue (dss_steps returns before the GPU is done)
 torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) / K
 e.enable_timing(True)
@@ -42,6 +43,7 @@ for t in range(K):
 host_call = (time.perf_counter() - t1) / K
 if rank == 0:
     print(json.dumps({"W": W, "N": N, "d": d, "G": G, "wall_us_per_iter": wall * 1e6,
+                      "host_enqueue_us_per_iter": t_enq * 1e6,
                       "kernel_us_per_iter_by_kind": {k: round(v[0], 3) for k, v in kinds.items()},
                       "launches_per_iter": {k: v[1] for k, v in kinds.items()}}))
 dist.destroy_process_group()

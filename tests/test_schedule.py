@@ -244,3 +244,16 @@ def test_auto_placement_tiles_only_deep_chains():
     assert placement(c3, 4, 2)[2] == (2, 2) and placement(c4, 4, 2)[2] == (2, 2)
     assert placement(c2, 4, 2)[2] == (0, 0) and placement(c3, 2, 2)[2] == (0, 0)
     assert placement(c4, 8, 2)[2] == (0, 0) and placement(c3, 8, 2)[2] == (0, 0)
+
+
+def test_auto_placement_keeps_one_shot_rows_contiguous():
+    """Rows of the one-shot size (<= 512 KiB) stay contiguous in auto mode:
+    there contiguous packing keeps one parity GPU-local, while a tiling makes
+    both parities exchange."""
+    from paper_2007_03298_b200 import SyncStrategy, StrategyKind, Topology, WorldConfig, placement
+    w64 = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(64, 8))
+    assert placement(w64, 4, 2, dim=256)[2] == (0, 0)
+    assert placement(w64, 4, 2, dim=131072)[2] == (0, 0)      # exactly 512 KiB of fp32
+    assert placement(w64, 4, 2, dim=131072 + 64)[2] == (2, 2)
+    assert placement(w64, 4, 2, dim=65536, dtype="f64")[2] == (0, 0)
+    assert placement(w64, 4, 1, dim=256)[2] == (2, 2)         # forced tiling ignores the size
