@@ -9,7 +9,10 @@
 namespace dssb {
 
 constexpr int kThreads = 256;
-constexpr int kMaxLocal = 128;  // local workers per GPU carried in kernel params
+#ifndef DSS_MAX_LOCAL
+#define DSS_MAX_LOCAL 128
+#endif
+constexpr int kMaxLocal = DSS_MAX_LOCAL;  // local workers per GPU carried in kernel params
 
 // Tuning knobs (compile-time; the defaults are the measured best, see
 // DESIGN.md).  Members whose loads are issued together before the first
