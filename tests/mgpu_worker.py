@@ -227,6 +227,9 @@ def main():
     # rows past the 80 MiB long-chunk threshold (16384-element chain chunks,
     # C2-sized rows): a block and a comb iteration plus a sync round
     ok = run_case("ds", 8, 2, True, 1, 21_000_003, rank, G, orc, 0, iters=2) and ok
+    # the same row size on a tiled placement (two-GPU-deep chains in both parities)
+    if G == 4:
+        ok = run_case("ds", 16, 4, False, 3, 21_000_003, rank, G, orc, 0, placement=1, iters=2) and ok
     for kind in ("ds",):
         ok = placed_logistic_case(rank, G) and ok
     from paper_2007_03298_b200 import SamplingMode
