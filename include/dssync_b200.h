@@ -403,6 +403,19 @@ long dss_launch_count(const dss_ctx* ctx);
  * the variable it checks nothing and returns DSS_OK. */
 int dss_check_guards(dss_ctx* ctx, long* corrupted);
 
+/* Single-device emulation of a G-GPU world (tests): n contexts created on
+ * ONE device as ranks 0..n-1 of an n-GPU world (identical configuration)
+ * are wired to each other's buffers directly and share one stream.
+ * dss_emulate_step then runs one DS-Sync iteration of every rank in two
+ * passes in rank order -- local steps, push phase 1 and the chain's partial
+ * pass, then push phase 2, the pull folds and the chain's mean pass -- so
+ * every cross-rank flag a kernel waits on was released by an earlier launch
+ * on the stream (no concurrently spinning launches).  The kernels, tables
+ * and flag protocol are the multi-GPU ones; results equal a real G-GPU run
+ * bit for bit.  DS-Sync only. */
+int dss_emulate_attach(dss_ctx** ctxs, int n);
+int dss_emulate_step(dss_ctx** ctxs, int n, long t, double alpha, int check);
+
 /* ---- multi-GPU (one process per GPU over NVLink/NVSwitch) ---- */
 /* CUDA IPC handles of this GPU's params, grads, mean-gradient, barrier-flag,
  * chain-row, chain-flag, running-stats, push-staging and push-flag buffers

@@ -116,6 +116,8 @@ SIGNATURES = {
     "dss_ipc_attach": (C.c_int, [_P, _P]),
     "dss_barrier": (C.c_int, [_P]),
     "dss_check_guards": (C.c_int, [_P, C.POINTER(C.c_long)]),
+    "dss_emulate_attach": (C.c_int, [_P, C.c_int]),
+    "dss_emulate_step": (C.c_int, [_P, C.c_int, C.c_long, C.c_double, C.c_int]),
 }
 
 _lib = None

@@ -253,6 +253,13 @@ struct dss_ctx {
   // an out-of-bounds-write detector where compute-sanitizer is unavailable
   long guard = 0;
   std::vector<std::pair<char*, size_t>> guarded;  // (user pointer, user bytes)
+  // single-device emulation of a G-GPU world (dss_emulate_*): every virtual
+  // rank's context lives on one device and shares one stream; a step runs in
+  // two passes over the ranks in order (pass 1: local steps, push phase 1,
+  // chain partial pass; pass 2: push phase 2, pull folds, chain mean pass),
+  // so every flag a kernel waits on was released by an earlier launch
+  bool emulated = false;
+  int emu_pass = 0;  // 0: normal (not emulating); 1 / 2: the pass being issued
 };
 
 namespace dssb {

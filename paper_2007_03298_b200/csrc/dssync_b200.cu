@@ -301,7 +301,11 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
 extern "C" int dss_destroy(dss_ctx* c) {
   if (!c) return DSS_OK;
   if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
-  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->emulated) {
+    cudaDeviceSynchronize();  // the shared stream may belong to another (already destroyed) context
+  } else if (c->stream) {
+    cudaStreamSynchronize(c->stream);
+  }
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocations) cudaFree(p);
   for (auto& pr : c->ev_pending) {
@@ -495,28 +499,33 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
     const int opt = c->cfg.optimizer;
     if (s.kind == DSS_DS_SYNC) {
       const ParityPlan& pp = c->step_plan[t & 1];
-      quiesce(c);
-      // Local groups: fused apply_step + ordered fold + broadcast.
-      for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
+      const bool first = c->emu_pass != 2, second = c->emu_pass != 1;  // emulation passes (both when not emulating)
+      if (first) {
+        quiesce(c);
+        // Local groups: fused apply_step + ordered fold + broadcast.
+        for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
+      }
       if (pp.any_spanning) {
         // Members of spanning groups step in place.  Two-shot groups: after
         // every GPU has stepped, each owner folds its slice over NVLink.
         // Chain groups: the ordered partial/mean passes (flag-synchronised
         // per chunk, no barrier).
-        launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->g, c->d_pad, 0);
+        if (first) launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->g, c->d_pad, 0);
         bool barrier_done = false;
         if (pp.any_push) {
           launch_push_any(c, pp.push, t, alpha);  // fused step + push two-shot
-        } else if (pp.any_twoshot) {
+        } else if (pp.any_twoshot && second) {
           if (multi(c)) barrier(c);
           barrier_done = true;
           launch_fold_any(c, pp.fold, t);
         }
         if (pp.any_chain) launch_chain_any(c, pp.chain, t, alpha);
+        if (!second) return DSS_OK;  // emulation pass 1 ends here
         // one-shot writes no peer params: the next iteration needs no barrier
         c->pending_remote = multi(c) && (pp.any_chain || !(pp.any_push && pp.push.oneshot));
         fold_stats(c, t, barrier_done);
       } else {
+        if (!second) return DSS_OK;
         fold_stats(c, t, false);
       }
     } else if (!multi(c)) {
@@ -960,6 +969,80 @@ extern "C" int dss_ipc_attach(dss_ctx* c, const void* all) {
     ck(cudaStreamSynchronize(c->stream), "attach sync");
     return check_impl(c) == DSS_OK ? DSS_OK : c->last_status;
   });
+}
+
+// ---- single-device emulation of a G-GPU world (tests) ------------------------
+
+extern "C" int dss_emulate_attach(dss_ctx** ctxs, int n) {
+  if (!ctxs || n < 2) return fail(nullptr, DSS_EINVAL, "dss_emulate_attach: need >= 2 contexts");
+  return guard(nullptr, [&]() -> int {
+    for (int r = 0; r < n; ++r) {
+      dss_ctx* c = ctxs[r];
+      if (!c || c->cfg.n_gpus != n || c->cfg.rank != r || c->cfg.device != ctxs[0]->cfg.device || c->attached) {
+        throw std::invalid_argument("dss_emulate_attach: context r must be rank r of an n-GPU world, all on one "
+                                    "device, not yet attached");
+      }
+      long long a[kFingerprintWords], b[kFingerprintWords];
+      fingerprint(c, a);
+      fingerprint(ctxs[0], b);
+      if (std::memcmp(a, b, sizeof(a)) != 0) {
+        throw std::invalid_argument("dss_emulate_attach: rank " + std::to_string(r) +
+                                    " was created with a different configuration");
+      }
+    }
+    ck(cudaSetDevice(ctxs[0]->cfg.device), "cudaSetDevice");
+    for (int r = 0; r < n; ++r) ck(cudaStreamSynchronize(ctxs[r]->stream), "emulate attach sync");
+    for (int r = 0; r < n; ++r) {
+      dss_ctx* c = ctxs[r];
+      c->peer_w.assign(static_cast<size_t>(n), nullptr);
+      c->peer_g = c->peer_mg = c->peer_chain_buf = c->peer_stats = c->peer_push_buf = c->peer_w;
+      c->peer_flag.assign(static_cast<size_t>(n), nullptr);
+      c->peer_chain_flags = c->peer_push_flags = c->peer_flag;
+      for (int q = 0; q < n; ++q) {  // same device, same process: the peers' buffers directly
+        const dss_ctx* p = ctxs[q];
+        c->peer_w[static_cast<size_t>(q)] = p->w;
+        c->peer_g[static_cast<size_t>(q)] = p->g;
+        c->peer_mg[static_cast<size_t>(q)] = p->mg;
+        c->peer_flag[static_cast<size_t>(q)] = p->flags;
+        c->peer_chain_buf[static_cast<size_t>(q)] = p->chain_buf;
+        c->peer_chain_flags[static_cast<size_t>(q)] = p->chain_flags;
+        c->peer_stats[static_cast<size_t>(q)] = p->stats;
+        c->peer_push_buf[static_cast<size_t>(q)] = p->push_buf;
+        c->peer_push_flags[static_cast<size_t>(q)] = p->push_flags;
+      }
+      c->stream = ctxs[0]->stream;  // one stream: launches run in issue order
+      c->emulated = true;
+      c->d_peer_flags = upload_table(c, c->peer_flag);
+      build_plans(c);
+      c->attached = true;
+    }
+    ck(cudaStreamSynchronize(ctxs[0]->stream), "emulate attach sync");
+    return DSS_OK;
+  });
+}
+
+extern "C" int dss_emulate_step(dss_ctx** ctxs, int n, long t, double alpha, int check) {
+  if (!ctxs || n < 2) return fail(nullptr, DSS_EINVAL, "dss_emulate_step: need >= 2 contexts");
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r] || !ctxs[r]->emulated) return fail(ctxs[r], DSS_EINVAL, "dss_emulate_step: not emulate-attached");
+    if (ctxs[r]->cfg.strategy.kind != DSS_DS_SYNC) return fail(ctxs[r], DSS_EINVAL, "dss_emulate_step: DS-Sync only");
+  }
+  // pass 1 in rank order (chain stages only wait on lower GPU indices), then
+  // pass 2 in rank order (push folds, pull folds, the mean pass g0 -> g1 -> ...)
+  for (int pass = 1; pass <= 2; ++pass) {
+    for (int r = 0; r < n; ++r) {
+      ctxs[r]->emu_pass = pass;
+      const int st = dss_step(ctxs[r], t, alpha, 0, nullptr);
+      ctxs[r]->emu_pass = 0;
+      if (st != DSS_OK) return st;
+    }
+  }
+  if (check) {
+    for (int r = 0; r < n; ++r) {
+      if (const int st = dss_check(ctxs[r])) return st;
+    }
+  }
+  return DSS_OK;
 }
 
 extern "C" int dss_check_guards(dss_ctx* c, long* corrupted) {

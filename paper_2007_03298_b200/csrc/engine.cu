@@ -915,7 +915,7 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
   // CTA taking its partial-pass units then its mean-pass units (no lag):
   // bit-exact but slower everywhere -- C2 @2 GPUs 3200 -> 2790, C3 @4 (tiled)
   // 744 -> 572, C4 @4 32.1 -> 21.3 (profiles/r02/chain_fused_ab_g*.jsonl).
-  if (cl.na > 0) {
+  if (cl.na > 0 && c->emu_pass != 2) {
     a.entries = cl.d_a;
     a.n_entries = cl.na;
     const long units = c->chain_nchunks * cl.na;
@@ -924,7 +924,7 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
                                           kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
   }
-  if (cl.nb > 0) {
+  if (cl.nb > 0 && c->emu_pass != 1) {
     a.entries = cl.d_b;
     a.n_entries = cl.nb;
     const long units = c->chain_nchunks * cl.nb;
@@ -949,7 +949,7 @@ void launch_chain_d(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
 
 template <typename T>
 void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
-  ++c->chain_epoch;  // same sequence on every GPU: flags compare against it
+  if (c->emu_pass != 2) ++c->chain_epoch;  // same sequence on every GPU: flags compare against it
   if (cl.opt_mem != kOptNone && cl.opt_dst != kOptNone) throw std::logic_error("chain: one fused step only");
   ChainArgs<T> a{};
   a.src = reinterpret_cast<T* const*>(cl.d_src);
@@ -997,14 +997,15 @@ void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
 
 template <typename T, int OPT>
 void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
-  ++c->chain_epoch;  // flags compare against the shared epoch sequence
+  // emulation pass 2 repeats pass 1's launch numbers (epoch, one-shot seq)
+  if (c->emu_pass != 2) ++c->chain_epoch;  // flags compare against the shared epoch sequence
   PushArgs<T> a{};
   a.items = pl.d_items;
-  a.n_items = pl.items;
+  a.n_items = c->emu_pass == 2 ? 0 : pl.items;  // emulation: phase 1 and phase 2 as two launches
   a.item_dst = pl.d_item_dst;
   a.item_flag = pl.d_item_flag;
   a.folds = pl.d_folds;
-  a.n_folds = pl.folds;
+  a.n_folds = c->emu_pass == 1 ? 0 : pl.folds;
   a.dst = reinterpret_cast<T* const*>(pl.d_dst);
   a.dst_lr = pl.d_dst_lr;
   a.w = static_cast<T*>(c->w);
@@ -1021,7 +1022,8 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   if (pl.oneshot) {
     // rotate the staging buffers; the kernel's acks keep a push from
     // overwriting a buffer its destination still reads (see PushArgs::seq)
-    const long par = static_cast<long>(c->oneshot_seq++ % DSS_ONESHOT_BUFFERS);
+    if (c->emu_pass != 2) ++c->oneshot_seq;
+    const long par = static_cast<long>((c->oneshot_seq - 1) % DSS_ONESHOT_BUFFERS);
     a.stage_shift = (c->oneshot_base_elems + par * c->oneshot_half_elems) * c->esz;
     a.flag_shift = c->oneshot_base_flags + par * c->oneshot_half_flags;
     a.seq = c->oneshot_seq;  // 1, 2, ...: this launch's number
@@ -1044,7 +1046,7 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0), "occupancy");
     o = std::max(o, 1);
   }
-  const long grid = std::max(1L, std::min<long>(static_cast<long>(o) * c->sms, std::max(pl.items, pl.folds)));
+  const long grid = std::max(1L, std::min<long>(static_cast<long>(o) * c->sms, std::max(a.n_items, a.n_folds)));
   TimedLaunch tl(c, DSS_KIND_FOLD);
   if (DSS_PUSH_COOP) {
     void* args[] = {&a};
@@ -1118,7 +1120,7 @@ void launch_bsp(dss_ctx* c, long t, double alpha) {
 }
 
 void barrier(dss_ctx* c) {
-  if (!multi(c)) return;
+  if (!multi(c) || c->emulated) return;  // emulation: the launch order already serialises the ranks
   if (!c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
   ++c->epoch;
   TimedLaunch tl(c, DSS_KIND_BARRIER);
