@@ -47,6 +47,7 @@ def run(W, N, rect, opt, d, G, orc, path=0, placement=0, iters=4):
         assert rc == 0, L.global_error()
         for e in engines:
             e.upload_all(BUF_PARAMS, w[e.local_ranks])
+            e.enable_timing(True)
         m1, m2 = np.zeros_like(w), np.zeros_like(w)
         steps = np.zeros(W, np.int64)
         alpha = 0.05 if opt < 2 else 0.01
@@ -64,6 +65,9 @@ def run(W, N, rect, opt, d, G, orc, path=0, placement=0, iters=4):
             got[e.local_ranks] = e.download_all(BUF_PARAMS)
             if opt >= 1:
                 got_m1[e.local_ranks] = e.download_all(BUF_MOMENT1)
+        kinds = engines[0].kernel_times_by_kind()
+        cross = kinds["fold"][1] + kinds["chain"][1] + kinds["chain_mean"][1]
+        assert cross > 0, ("no cross-GPU kernel ran", kinds)  # the multi-GPU kernels, not a local shortcut
         assert np.array_equal(got, w), (W, N, opt, d, G, path, placement)
         if opt >= 1:
             assert np.array_equal(got_m1, m1)
