@@ -217,7 +217,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // and the sweep's 64 KB - 64 MB rows lose up to 40%,
       // profiles/r02/chain_chunk_sweep_ab_g4.jsonl)
       const bool long_chunks = s.kind == DSS_DS_SYNC && c->d_pad * c->esz >= DSS_CHAIN_CHUNK_DS_MIN_BYTES;
-      c->chain_chunk = std::min<long>(c->d_pad, long_chunks ? DSS_CHAIN_CHUNK_DS : DSS_CHAIN_CHUNK);
+      long chunk = long_chunks ? DSS_CHAIN_CHUNK_DS : DSS_CHAIN_CHUNK;
+      // small rows: shorter chunks, so the chain and one-shot work units
+      // (chunk x group) spread over the SMs instead of serialising a whole
+      // row's member loads on a few CTAs
+      while (chunk > DSS_CHAIN_CHUNK_MIN && c->d_pad < chunk * DSS_CHAIN_MIN_CHUNKS) chunk /= 2;
+      c->chain_chunk = std::min<long>(c->d_pad, chunk);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));
       // Fused two-shot staging of the owned slices, worst parity and worst
@@ -241,11 +246,14 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // chain) only for rows of at most DSS_ONESHOT_MAX_BYTES.
       long rows = 0;
       const bool small_rows = c->d_pad * c->esz <= DSS_ONESHOT_MAX_BYTES;
-      // BSP: gather all W gradient rows (build_bsp_multi_plan).  Its one
-      // fold per chunk serialises W rows on one CTA, so only for small
-      // worlds: at 4 GPUs W=4 / 16 gain 2.4x / 1.9x at 1 KB rows, W=64 loses.
+      // BSP: gather all W gradient rows (build_bsp_multi_plan).  Each fold
+      // unit reads all W rows of a chunk, so only for small worlds or small
+      // totals: at 4 GPUs W=4 / 16 gain 2.4x / 1.9x at 1 KB rows; at 2 GPUs
+      // W=64 gains 15-26% up to 16 KB rows and loses 40% at 256 KB
+      // (profiles/r02/small_rows_ab_g2.jsonl).
       if (s.kind == DSS_BSP && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 && small_rows &&
-          s.world_size <= 16) {
+          (s.world_size <= DSS_BSP_ONESHOT_MAX_W ||
+           static_cast<long>(s.world_size) * c->d_pad * c->esz <= DSS_BSP_ONESHOT_MAX_TOTAL)) {
         c->oneshot[0] = true;
         rows = s.world_size;
       }

@@ -82,6 +82,23 @@ constexpr int kSmallWide = 512;
 #ifndef DSS_CHAIN_CHUNK_DS_MIN_BYTES
 #define DSS_CHAIN_CHUNK_DS_MIN_BYTES (80L << 20)
 #endif
+// rows shorter than DSS_CHAIN_MIN_CHUNKS chunks use shorter chunks, down to
+// DSS_CHAIN_CHUNK_MIN elements (0: off)
+#ifndef DSS_CHAIN_MIN_CHUNKS
+#define DSS_CHAIN_MIN_CHUNKS 64
+#endif
+#ifndef DSS_CHAIN_CHUNK_MIN
+#define DSS_CHAIN_CHUNK_MIN 1024
+#endif
+// BSP over several GPUs gathers all W gradient rows (one-shot) for small
+// rows up to this world size, or while W rows total at most
+// DSS_BSP_ONESHOT_MAX_TOTAL bytes
+#ifndef DSS_BSP_ONESHOT_MAX_W
+#define DSS_BSP_ONESHOT_MAX_W 16
+#endif
+#ifndef DSS_BSP_ONESHOT_MAX_TOTAL
+#define DSS_BSP_ONESHOT_MAX_TOTAL (1L << 20)
+#endif
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 8
 #endif

@@ -546,7 +546,6 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   constexpr int VN = Vec<T>::n;
   __shared__ PushItem it;
   __shared__ PushFold fo;
-  __shared__ int ok_flag;
   __shared__ T* sdst[kMaxFold];
   __shared__ unsigned long long sok;  // bit q: destination q may be written (its flow-control wait succeeded)
   unsigned long long bad = ~0ull;
@@ -617,22 +616,34 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   }
   // phase 2: ordered fold of owned chunks
   for (int u = blockIdx.x; u < a.n_folds; u += gridDim.x) {
-    if (threadIdx.x == 0) {
-      fo = a.folds[u];
-      ok_flag = 1;
-      for (int j = 0; j < fo.S && ok_flag; ++j) {
-        ok_flag = chain_wait(fo.flags + a.flag_shift + j * fo.flag_ld, a.epoch, a.timeout);
-      }
-    }
+    if (threadIdx.x == 0) fo = a.folds[u];
     __syncthreads();
-    if (ok_flag) {
+    // the S row flags are polled in parallel (thread j: row j); a serial
+    // poll costs one system-scope load latency per row
+    int okj = 1;
+    for (int j = threadIdx.x; j < fo.S; j += blockDim.x) {
+      okj &= chain_wait(fo.flags + a.flag_shift + j * fo.flag_ld, a.epoch, a.timeout) ? 1 : 0;
+    }
+    if (__syncthreads_and(okj)) {
       const T inv = static_cast<T>(1.0 / static_cast<double>(fo.S));
       const T* st = reinterpret_cast<const T*>(static_cast<const char*>(fo.stage) + a.stage_shift);
       for (long e = fo.lo / VN + threadIdx.x; e < fo.hi / VN; e += blockDim.x) {
         const long off = e * VN;
         const long so = off - fo.lo;
         Pack<T> acc = ldv_cg(st + so);
-        for (int j = 1; j < fo.S; ++j) {
+        // rows in load batches of 4, added in ascending order
+        int j = 1;
+        for (; j + 4 <= fo.S; j += 4) {
+          Pack<T> x[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) x[b] = ldv_cg(st + (j + b) * fo.stage_ld + so);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+#pragma unroll
+            for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x[b].v[l]);
+          }
+        }
+        for (; j < fo.S; ++j) {
           const Pack<T> x = ldv_cg(st + j * fo.stage_ld + so);
 #pragma unroll
           for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x.v[l]);
@@ -648,25 +659,39 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
           bad = k < bad ? k : bad;
         }
         if constexpr (BSP) {
-          for (int q = 0; q < fo.n_dst; ++q) {  // every local replica steps with the mean gradient
-            const int lr = a.dst_lr[fo.dst_beg + q];
-            const long r = static_cast<long>(lr) * a.ld + off;
-            Pack<T> x = ldv(a.w + r);
-            Pack<T> s1, s2;
-            if constexpr (OPT != kSgd) s1 = ldv(a.m1 + r);
-            if constexpr (OPT == kAdam || OPT == kAdamW) s2 = ldv(a.m2 + r);
-            const T b1 = static_cast<T>(a.bc1[lr]);
-            const T b2 = static_cast<T>(a.bc2[lr]);
-            step_pack<T, OPT>(x, acc, s1, s2, a.c, b1, b2);
-            bool oks = true;
+          // every local replica steps with the mean gradient, replicas in
+          // load batches of 4 (all loads of a batch before its stores)
+          for (int q0 = 0; q0 < fo.n_dst; q0 += 4) {
+            const int nb = fo.n_dst - q0 < 4 ? fo.n_dst - q0 : 4;
+            Pack<T> x[4], s1[4], s2[4];
 #pragma unroll
-            for (int l = 0; l < VN; ++l) oks = oks && finite_(x.v[l]);
-            stv(a.w + r, x);
-            if constexpr (OPT != kSgd) stv(a.m1 + r, s1);
-            if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2);
-            if (!oks) {
-              const unsigned long long k = err_key(a.t, 1, a.rank_of[lr]);
-              bad = k < bad ? k : bad;
+            for (int b = 0; b < 4; ++b) {
+              if (b < nb) {
+                const long r = static_cast<long>(a.dst_lr[fo.dst_beg + q0 + b]) * a.ld + off;
+                x[b] = ldv(a.w + r);
+                if constexpr (OPT != kSgd) s1[b] = ldv(a.m1 + r);
+                if constexpr (OPT == kAdam || OPT == kAdamW) s2[b] = ldv(a.m2 + r);
+              }
+            }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b < nb) {
+                const int lr = a.dst_lr[fo.dst_beg + q0 + b];
+                const long r = static_cast<long>(lr) * a.ld + off;
+                const T b1 = static_cast<T>(a.bc1[lr]);
+                const T b2 = static_cast<T>(a.bc2[lr]);
+                step_pack<T, OPT>(x[b], acc, s1[b], s2[b], a.c, b1, b2);
+                bool oks = true;
+#pragma unroll
+                for (int l = 0; l < VN; ++l) oks = oks && finite_(x[b].v[l]);
+                stv(a.w + r, x[b]);
+                if constexpr (OPT != kSgd) stv(a.m1 + r, s1[b]);
+                if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + r, s2[b]);
+                if (!oks) {
+                  const unsigned long long k = err_key(a.t, 1, a.rank_of[lr]);
+                  bad = k < bad ? k : bad;
+                }
+              }
             }
           }
         } else {

@@ -12,5 +12,5 @@ python - gpurun_out/sweep_ab_g$n.jsonl <<'PY'
 import json, sys
 rows = [json.loads(l) for l in open(sys.argv[1])]
 for r in rows:
-    print(r["variant"][:24], r["N"], r["bytes_per_worker"], round(r["ds_iters_s"], 1))
+    print(r["variant"][:24], r["N"], r["bytes_per_worker"], "ds", round(r["ds_iters_s"], 1), "bsp", round(r["bsp_iters_s"], 1))
 PY

@@ -34,6 +34,8 @@ CASES = [
     ("bsp", 4, 4, False, 3, 2049),
     ("bsp", 16, 16, False, 1, 300_007),  # packed BSP: chain over gradient rows
     ("ds", 64, 8, False, 0, 20_000),     # C4 shape
+    ("bsp", 64, 64, False, 1, 3001),     # W=64 small rows: one-shot gather of all 64 gradient rows
+    ("bsp", 64, 64, False, 3, 20_001),   # W=64 chain with short (small-row) chunks
 ]
 
 
