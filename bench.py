@@ -567,9 +567,10 @@ def dominant_roofline(kinds_rows, ms_step, peak, peak_kind, G, chain_hbm=0.0):
     return r
 
 
-def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False):
-    """DS + BSP iterations of one config on this rank's engine(s).  Returns
-    the per-rank measurements (times already max-over-ranks)."""
+def measure(args, cfg, dtype, G, rank, local, stream, full=True, nccl_only=False):
+    """DS + BSP iterations of one config on this rank's engine(s) (or, with
+    nccl_only, the NCCL baselines of the same rows).  Returns the per-rank
+    measurements (times already max-over-ranks)."""
     import torch
     import torch.distributed as dist
     from paper_2007_03298_b200 import (BUF_GRADS, DsSyncEngine, OptimizerHyperparams, OptimizerKind,
@@ -616,6 +617,23 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False
         return max_over_ranks(a.elapsed_time(b)) / K
 
     res = {}
+    if nccl_only:
+        # The NCCL baselines run in their own pass after all of our
+        # measurements, over fresh engines: a run of our kernels right after
+        # NCCL all-reduces in the same process is intermittently up to 2x
+        # slower (small rows across GPUs: profiles/r02/sweeps/nccl_order_g2.md)
+        for kind, name in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
+            e = make(kind)
+            nb = NcclBaseline(e, cfg, G, rank, args.placement if name == "ds" else 0)
+            fn = (lambda t: nb.ds_step(t, cfg["alpha"])) if name == "ds" else (lambda t: nb.bsp_step(t, cfg["alpha"]))
+            for t in range(3):
+                fn(t)
+            res["nccl_" + name] = timed(fn, 3, max(3, args.steps // 2))
+            del nb
+            e.close()
+            del e
+            torch.cuda.synchronize()
+        return res
     clocks = ClockSampler(local) if full else None
     for kind, name in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
         e = make(kind)
@@ -671,13 +689,6 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, with_nccl=False
             res["e2e_steps"] = K2
             e.check()
             del hg, hw
-        if G > 1 and with_nccl:
-            nb = NcclBaseline(e, cfg, G, rank, args.placement if name == "ds" else 0)
-            fn = (lambda t: nb.ds_step(t, cfg["alpha"])) if name == "ds" else (lambda t: nb.bsp_step(t, cfg["alpha"]))
-            for t in range(3):
-                fn(t)
-            res["nccl_" + name] = timed(fn, 3, max(3, args.steps // 2))
-            del nb
         e.close()
         del e
         torch.cuda.synchronize()
@@ -792,6 +803,8 @@ def our_arm(args, cfg):
         raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if G > 1:
+        from paper_2007_03298_b200.dist import pin_host_cores
+        pin_host_cores(local, int(os.environ.get("LOCAL_WORLD_SIZE", G)))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if cfg["W"] % G:
         raise SystemExit(f"W={cfg['W']} not divisible by {G} GPUs")
@@ -800,7 +813,7 @@ def our_arm(args, cfg):
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
-    res = measure(args, cfg, "f32", G, rank, local, stream, full=True, with_nccl=not args.no_nccl)
+    res = measure(args, cfg, "f32", G, rank, local, stream, full=True)
     logistic_ms = None
     if cfg.get("logistic") and G == 1:
         logistic_ms = logistic_run(args, cfg, local, stream)
@@ -811,6 +824,8 @@ def our_arm(args, cfg):
         if c["W"] % G:
             continue
         extra_res[name] = (c, dtype, measure(args, c, dtype, G, rank, local, stream, full=False))
+    if G > 1 and not args.no_nccl:
+        res.update(measure(args, cfg, "f32", G, rank, local, stream, nccl_only=True))
     if G > 1:
         dist.barrier()
     if rank != 0:

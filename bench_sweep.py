@@ -47,6 +47,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if G > 1:
+        from paper_2007_03298_b200.dist import pin_host_cores
+        pin_host_cores(local, int(os.environ.get("LOCAL_WORLD_SIZE", G)))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -74,6 +76,7 @@ def main():
     while b <= args.max_mb * 1024 * 1024:
         sizes.append(b)
         b *= 4
+    shapes = []
     for N in [int(x) for x in args.groups.split(",")]:
         W = N * N
         if W % G:
@@ -83,54 +86,74 @@ def main():
             d = nbytes // 4
             if P * d * 4 * 2 > args.mem_gb * 1e9:
                 continue
-            K = int(max(5, min(2000, 4e9 / (P * nbytes * 3 + 1))))
-            row = {"N": N, "W": W, "bytes_per_worker": nbytes, "d": d, "n_gpus": G, "steps": K, "opt": args.opt,
-                   "path": args.path, "placement": args.placement}
-            for kind, key in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
-                s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W))
-                e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, d, None, "f32", local, rank, G, path=args.path,
-                                 placement=args.placement if kind == StrategyKind.DS_SYNC else 0)
-                e.set_stream(stream.cuda_stream)
-                if G > 1:
-                    from paper_2007_03298_b200.dist import attach
-                    attach(e)
-                e.quadratic_init(7, 4.0)
-                e.quadratic_gradients(0, 1, 1.0, 0.5)
-                if args.opt == "sync" and kind == StrategyKind.DS_SYNC:
-                    run = lambda K: [e.sync_round(t, check=False) for t in range(K)]  # noqa: E731
-                else:
-                    run = lambda K: e.steps(0, np.full(K, 0.01))  # noqa: E731
-                run(3)
-                ms = timed(run, K)
-                e.check()
-                row[key + "_ms"] = ms
-                row[key + "_iters_s"] = 1000.0 / ms
-                row[key + "_eff_gbs"] = W * d * 4 / (ms / 1e3) / 1e9
-                if key == "bsp" and G > 1 and not args.no_nccl:
-                    # the local gradient rows as one strided view of the engine's
-                    # contiguous [P][row_stride] buffer: no gather copies
-                    ptr, stride = e.device_ptr(BUF_GRADS, e.local_ranks[0]), e.row_stride
+            shapes.append((N, W, P, nbytes, d, int(max(5, min(2000, 4e9 / (P * nbytes * 3 + 1))))))
 
-                    class _A:
-                        __cuda_array_interface__ = {"shape": (P, stride), "typestr": "<f4", "data": (ptr, False),
-                                                    "version": 3}
-                    grads = torch.as_tensor(_A(), device="cuda")[:, :d]
-                    acc = torch.empty(d, dtype=torch.float32, device="cuda")
+    def engine(kind, W, N, d):
+        s = SyncStrategy(kind, Topology.RING, WorldConfig(W, N if kind == StrategyKind.DS_SYNC else W))
+        e = DsSyncEngine(s, OptimizerKind.VANILLA_SGD, d, None, "f32", local, rank, G, path=args.path,
+                         placement=args.placement if kind == StrategyKind.DS_SYNC else 0)
+        e.set_stream(stream.cuda_stream)
+        if G > 1:
+            from paper_2007_03298_b200.dist import attach
+            attach(e)
+        e.quadratic_init(7, 4.0)
+        e.quadratic_gradients(0, 1, 1.0, 0.5)
+        return e
 
-                    def nccl(K):
-                        for _ in range(K):
-                            torch.sum(grads, dim=0, out=acc)
-                            dist.all_reduce(acc)
-                            acc.mul_(1.0 / W)
-                            grads.copy_(acc.expand_as(grads))
-                            e.apply_step(0.01, check=False)
-                    nccl(3)
-                    ms = timed(nccl, K)
-                    row["nccl_bsp_ms"] = ms
-                    row["nccl_bsp_iters_s"] = 1000.0 / ms
-                e.close()
-                del e
-                torch.cuda.synchronize()
+    rows = []
+    for N, W, P, nbytes, d, K in shapes:
+        row = {"N": N, "W": W, "bytes_per_worker": nbytes, "d": d, "n_gpus": G, "steps": K, "opt": args.opt,
+               "path": args.path, "placement": args.placement}
+        for kind, key in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
+            e = engine(kind, W, N, d)
+            if args.opt == "sync" and kind == StrategyKind.DS_SYNC:
+                run = lambda K: [e.sync_round(t, check=False) for t in range(K)]  # noqa: E731
+            else:
+                run = lambda K: e.steps(0, np.full(K, 0.01))  # noqa: E731
+            run(min(50, K))  # warm-up: plans built, caches and the cross-GPU flag protocol in steady state
+            ms = timed(run, K)
+            e.check()
+            row[key + "_ms"] = ms
+            row[key + "_iters_s"] = 1000.0 / ms
+            row[key + "_eff_gbs"] = W * d * 4 / (ms / 1e3) / 1e9
+            e.close()
+            del e
+            torch.cuda.synchronize()
+        rows.append(row)
+        if G == 1 or args.no_nccl:
+            if rank == 0:
+                print(json.dumps(row), flush=True)
+    if G > 1 and not args.no_nccl:
+        # The NCCL baseline in a second pass after all of ours: our kernels
+        # run right after NCCL all-reduces in the same process are
+        # intermittently up to 2x slower (profiles/r02/sweeps/nccl_order_g2.md)
+        for (N, W, P, nbytes, d, K), row in zip(shapes, rows):
+            e = engine(StrategyKind.BSP, W, N, d)
+            # the local gradient rows as one strided view of the engine's
+            # contiguous [P][row_stride] buffer: no gather copies
+            ptr, stride = e.device_ptr(BUF_GRADS, e.local_ranks[0]), e.row_stride
+
+            class _A:
+                __cuda_array_interface__ = {"shape": (P, stride), "typestr": "<f4", "data": (ptr, False),
+                                            "version": 3}
+            grads = torch.as_tensor(_A(), device="cuda")[:, :d]
+            acc = torch.empty(d, dtype=torch.float32, device="cuda")
+
+            def nccl(K):
+                for _ in range(K):
+                    torch.sum(grads, dim=0, out=acc)
+                    dist.all_reduce(acc)
+                    acc.mul_(1.0 / W)
+                    grads.copy_(acc.expand_as(grads))
+                    e.apply_step(0.01, check=False)
+            nccl(3)
+            ms = timed(nccl, K)
+            row["nccl_bsp_ms"] = ms
+            row["nccl_bsp_iters_s"] = 1000.0 / ms
+            del grads, acc
+            e.close()
+            del e
+            torch.cuda.synchronize()
             if rank == 0:
                 print(json.dumps(row), flush=True)
     if G > 1:
