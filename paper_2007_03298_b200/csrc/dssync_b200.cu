@@ -221,7 +221,10 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // small rows: shorter chunks, so the chain and one-shot work units
       // (chunk x group) spread over the SMs instead of serialising a whole
       // row's member loads on a few CTAs
-      while (chunk > DSS_CHAIN_CHUNK_MIN && c->d_pad < chunk * DSS_CHAIN_MIN_CHUNKS) chunk /= 2;
+      const bool bsp = s.kind == DSS_BSP;
+      const long min_chunk = bsp ? DSS_BSP_CHAIN_CHUNK_MIN : DSS_CHAIN_CHUNK_MIN;
+      const long min_chunks = bsp ? DSS_BSP_CHAIN_MIN_CHUNKS : DSS_CHAIN_MIN_CHUNKS;
+      while (chunk > min_chunk && c->d_pad < chunk * min_chunks) chunk /= 2;
       c->chain_chunk = std::min<long>(c->d_pad, chunk);
       c->chain_nchunks = (c->d_pad + c->chain_chunk - 1) / c->chain_chunk;
       c->chain_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(2) * slots * c->d_pad * c->esz));

@@ -90,6 +90,17 @@ constexpr int kSmallWide = 512;
 #ifndef DSS_CHAIN_CHUNK_MIN
 #define DSS_CHAIN_CHUNK_MIN 1024
 #endif
+// BSP folds all of a GPU's rows in every chain unit: more, shorter chunks
+#ifndef DSS_BSP_CHAIN_MIN_CHUNKS
+#define DSS_BSP_CHAIN_MIN_CHUNKS 1184  // 148 SMs x 8 resident chain CTAs
+#endif
+// (Also measured and dropped: stepping the replicas in kernel B, 2 / 4 / 8
+// replicas per entry, instead of on the CTA that folded the chunk -- equal
+// or slower at 4 GPUs, W = 16 / 64, 16 KB - 64 MB rows;
+// profiles/r02/sweeps/bsp_chain_ab_g4.md.)
+#ifndef DSS_BSP_CHAIN_CHUNK_MIN
+#define DSS_BSP_CHAIN_CHUNK_MIN DSS_CHAIN_CHUNK_MIN
+#endif
 // BSP over several GPUs gathers all W gradient rows (one-shot) for small
 // rows up to this world size, or while W rows total at most
 // DSS_BSP_ONESHOT_MAX_TOTAL bytes
