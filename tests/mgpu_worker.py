@@ -186,6 +186,48 @@ def placed_logistic_case(rank, G):
     return ok
 
 
+def busy_case(rank, G):
+    """Cross-GPU push steps issued while another stream keeps every SM busy
+    with matmuls complete (no flag-wait timeout: the cooperative launch
+    keeps the push kernel's CTAs co-resident) and give the same bits as the
+    same steps on an idle GPU."""
+    if torch.cuda.device_count() < G:
+        return True  # oversubscribed ranks share a device: not this case
+    ok = True
+    for kind, W, N, rect, opt, d in (("ds", 8, 2, True, 1, 4097), ("ds", 16, 4, False, 3, 100_003),
+                                     ("bsp", 8, 8, False, 1, 3001)):
+        s = SyncStrategy(StrategyKind.DS_SYNC if kind == "ds" else StrategyKind.BSP, Topology.RING,
+                         WorldConfig(W, N), 1, rect)
+        outs = []
+        for busy in (False, True):
+            e = DsSyncEngine(s, OptimizerKind(opt), d, OptimizerHyperparams(weight_decay=0.01), "f32",
+                             device_of(rank), rank, G)
+            attach(e)
+            e.quadratic_init(7, 4.0)
+            e.quadratic_gradients(0, 1, 1.0, 0.5)
+            torch.cuda.synchronize()
+            dist.barrier()
+            side = torch.cuda.Stream()
+            if busy:
+                with torch.cuda.stream(side):
+                    a = torch.full((8192, 8192), 1e-4, device="cuda")
+                    c = torch.empty_like(a)
+                    for _ in range(12):  # ~0.2 s of full-device matmuls
+                        torch.mm(a, a, out=c)
+            e.steps(0, np.full(24, 0.01))
+            e.check()  # raises on a latched flag-wait timeout
+            torch.cuda.synchronize()
+            outs.append(e.download_all(BUF_PARAMS))
+            e.close()
+        same = bool(np.array_equal(outs[0], outs[1]))
+        flags = [None] * G
+        dist.all_gather_object(flags, same)
+        ok = ok and all(flags)
+        if rank == 0:
+            print(f"case busy-GPU {kind} W={W} N={N} d={d} G={G}: {'OK' if all(flags) else 'MISMATCH'}", flush=True)
+    return ok
+
+
 def fingerprint_case(rank, G):
     """Ranks created with different geometry (here: a different d per rank)
     must refuse to map each other's buffers (dss_ipc_attach fingerprint)."""
@@ -209,6 +251,7 @@ def main():
     dist.init_process_group("gloo")
     orc = Oracle()
     ok = fingerprint_case(rank, G)
+    ok = busy_case(rank, G) and ok
     for case in CASES:
         if case[1] % G:
             continue

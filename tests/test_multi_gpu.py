@@ -33,6 +33,6 @@ def test_two_shot_nvlink_bit_exact(G):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr=127.0.0.1", f"--master-port={29600 + G}", os.path.join(ROOT, "tests", "mgpu_worker.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    print(p.stdout[-4000:])
+    print(p.stdout)  # every case's line (the logs under profiles/ are this output)
     print(p.stderr[-4000:])
     assert p.returncode == 0 and "MGPU PASS" in p.stdout
