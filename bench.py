@@ -634,7 +634,7 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, nccl_only=False
             del e
             torch.cuda.synchronize()
         return res
-    clocks = ClockSampler(local) if full else None
+    clocks = ClockSampler(local)  # every config: its timed region's clocks and throttle reasons
     for kind, name in ((StrategyKind.DS_SYNC, "ds"), (StrategyKind.BSP, "bsp")):
         e = make(kind)
         l0 = e.launch_count
@@ -861,6 +861,7 @@ def our_arm(args, cfg):
         out["configs"] = {}
         for name, (c, dtype, r) in extra_res.items():
             s = summarize(args, c, dtype, G, r, peak, peak_kind)
+            s["clocks"] = r.get("clocks")
             if G == 1 and not args.no_cpu_baseline and dtype == "f32":
                 s["cpu_baseline"] = cpu_baseline(c, seconds=8.0)
             out["configs"][name] = s
