@@ -790,10 +790,14 @@ void launch_group_bulk(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl)
 }
 
 // fp32 groups of 8 with these optimizers (bit OPT: momentum, Adam, AdamW)
-// take the narrow-vector kernel: +0.6-0.7% over the 16-B two-phase kernel
-// (C4 slice 6147 -> 6192 GB/s, C3 6272 -> 6310; profiles/r02/narrow_group_kernel_ab.jsonl)
+// take the narrow-vector kernel.  Momentum only: on an unthrottled box the
+// narrow kernel was +0.6-0.7% at both C3 and the C4 slice
+// (profiles/r02/narrow_group_kernel_ab.jsonl), but the C4 slice's AdamW
+// step runs power-capped (sw_power_cap, SM clocks 1650-1780 MHz), and there
+// its extra load instructions cost 1.9% (5908 vs 6018 GB/s for the 16-B
+// kernel; C3 stays +0.4% narrow: profiles/r02/power_ab_{c3,c4slice}.jsonl)
 #ifndef DSS_GROUP_NARROW
-#define DSS_GROUP_NARROW 14
+#define DSS_GROUP_NARROW 2
 #endif
 
 template <int OPT>
