@@ -18,7 +18,7 @@ mkdir -p gpurun_out
 task=$1; shift
 case "$task" in
   tests)
-    timeout 1500 python -m pytest tests -m gpu -x -q "$@" > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+    timeout 1500 python -m pytest tests -m gpu -x -q -rs "$@" > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
     tail -3 gpurun_out/gpu_tests.log
     timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
     tail -2 gpurun_out/smoke.log ;;
