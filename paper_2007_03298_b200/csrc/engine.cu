@@ -529,7 +529,13 @@ ParityPlan build_bsp_multi_plan(dss_ctx* c) {
     pp.push.bsp = true;
     return pp;
   }
-  const GpuPlan gp = make_plan(part, W, G, c->cfg.rank, c->d_pad, force_chain(c));
+  // Rows up to 4 MiB with at most 4 replicas per GPU: the pull two-shot (one
+  // hop) beats the ordered chain (G stages): W=16 on 4 GPUs +32% at 1 MB,
+  // +23% at 4 MB; the chain wins with more replicas per GPU or longer rows
+  // (profiles/r02/sweeps/bsp_chain_ab_g4.md)
+  const bool pull = DSS_BSP_PULL ||
+                    (c->P <= DSS_BSP_PULL_MAX_P && c->d_pad * c->esz <= DSS_BSP_PULL_MAX_BYTES);
+  const GpuPlan gp = make_plan(part, W, G, c->cfg.rank, c->d_pad, force_chain(c), pull && !force_chain(c));
   pp.any_spanning = true;
   pp.any_twoshot = gp.any_twoshot_globally;
   pp.any_chain = gp.any_chain_globally;

@@ -91,6 +91,19 @@ constexpr int kSmallWide = 512;
 #define DSS_CHAIN_CHUNK_MIN 1024
 #endif
 // BSP folds all of a GPU's rows in every chain unit: more, shorter chunks
+// Packed BSP across GPUs by the pull two-shot (every GPU folds its slice of
+// all W rows, peer loads) instead of the ordered chain: always (A/B knob),
+// or for rows of at most DSS_BSP_PULL_MAX_BYTES with at most
+// DSS_BSP_PULL_MAX_P replicas per GPU
+#ifndef DSS_BSP_PULL
+#define DSS_BSP_PULL 0
+#endif
+#ifndef DSS_BSP_PULL_MAX_P
+#define DSS_BSP_PULL_MAX_P 4
+#endif
+#ifndef DSS_BSP_PULL_MAX_BYTES
+#define DSS_BSP_PULL_MAX_BYTES (4L << 20)
+#endif
 #ifndef DSS_BSP_CHAIN_MIN_CHUNKS
 #define DSS_BSP_CHAIN_MIN_CHUNKS 1184  // 148 SMs x 8 resident chain CTAs
 #endif
