@@ -254,9 +254,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
       // totals: at 4 GPUs W=4 / 16 gain 2.4x / 1.9x at 1 KB rows; at 2 GPUs
       // W=64 gains 15-26% up to 16 KB rows and loses 40% at 256 KB
       // (profiles/r02/small_rows_ab_g2.jsonl).
-      if (s.kind == DSS_BSP && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 && small_rows &&
-          (s.world_size <= DSS_BSP_ONESHOT_MAX_W ||
-           static_cast<long>(s.world_size) * c->d_pad * c->esz <= DSS_BSP_ONESHOT_MAX_TOTAL)) {
+      // Worlds of up to 4 take it up to 4 MiB in total (W=4 at 1 MB rows:
+      // +34% on 2 and 4 GPUs; profiles/r02/sweeps/oneshot_max_ab_g*.jsonl).
+      const long bsp_total = static_cast<long>(s.world_size) * c->d_pad * c->esz;
+      if (s.kind == DSS_BSP && use_push(c.get()) && !force_chain(c.get()) && cfg->path != 4 &&
+          ((small_rows && s.world_size <= DSS_BSP_ONESHOT_MAX_W) || bsp_total <= DSS_BSP_ONESHOT_MAX_TOTAL ||
+           (s.world_size <= 4 && bsp_total <= DSS_BSP_ONESHOT_SMALL_W_TOTAL))) {
         c->oneshot[0] = true;
         rows = s.world_size;
       }

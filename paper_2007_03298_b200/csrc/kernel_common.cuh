@@ -123,6 +123,9 @@ constexpr int kSmallWide = 512;
 #ifndef DSS_BSP_ONESHOT_MAX_TOTAL
 #define DSS_BSP_ONESHOT_MAX_TOTAL (1L << 20)
 #endif
+#ifndef DSS_BSP_ONESHOT_SMALL_W_TOTAL
+#define DSS_BSP_ONESHOT_SMALL_W_TOTAL (4L << 20)  // worlds of up to 4
+#endif
 #ifndef DSS_CHAIN_CTAS_PER_SM
 #define DSS_CHAIN_CTAS_PER_SM 8
 #endif

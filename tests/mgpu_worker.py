@@ -36,6 +36,8 @@ CASES = [
     ("ds", 64, 8, False, 0, 20_000),     # C4 shape
     ("bsp", 64, 64, False, 1, 3001),     # W=64 small rows: one-shot gather of all 64 gradient rows
     ("bsp", 64, 64, False, 3, 20_001),   # W=64 chain with short (small-row) chunks
+    ("bsp", 4, 4, False, 2, 250_001),    # 1 MB rows, W=4: one-shot gather past the small-row limit
+    ("bsp", 16, 16, False, 1, 1_000_003),  # 4 MB rows: pull two-shot at <= 4 replicas per GPU, else chain
 ]
 
 
