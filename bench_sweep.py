@@ -17,6 +17,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 import numpy as np
 
@@ -52,6 +53,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    # ~1 s of device work first: the first shapes are microsecond steps whose
+    # timed region (a few ms) is too short to bring an idle GPU's clocks up
+    a = torch.full((4096, 4096), 1e-3, device="cuda")
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        for _ in range(20):
+            a = torch.mm(a, a).clamp_(-1.0, 1.0)
+        torch.cuda.synchronize()
+    del a
 
     def sync_max(x):
         if G == 1:
