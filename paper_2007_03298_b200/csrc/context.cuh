@@ -197,6 +197,8 @@ struct dss_ctx {
   bool attached = false;
   unsigned long long epoch = 0;
   bool pending_remote = false;
+  unsigned long long xgpu_ops = 0;           // cross-GPU launches so far (barrier, fold, push, chain)
+  unsigned long long bsp_chain_mark = ~0ull; // xgpu_ops right after the last chain-only BSP step
 
   dssb::ParityPlan step_plan[2];   // DS (or BSP at [0])
   dssb::ParityPlan sync_plan[2];   // sync_round (no step)

@@ -568,7 +568,16 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         return DSS_OK;
       }
       c->pending_remote = false;
-      barrier(c);
+      // Back-to-back chain-only BSP steps skip the opening barrier: the chain
+      // reads only this GPU's gradients, writes peers' staging rows only, and
+      // has the same partners every iteration, so a GPU that starts step t+1
+      // has received step t's mean for every chunk -- every GPU has already
+      // consumed every staging row of step t that t+1 overwrites (the mean
+      // of a chunk exists only after all its partials were folded, and a
+      // mean row is refilled only after its reader has started t+1, i.e.
+      // finished t).  Any other cross-GPU launch in between restores it.
+      const bool chain_only = pp.any_chain && !pp.any_twoshot;
+      if (!(chain_only && DSS_BSP_CHAIN_NO_BARRIER && c->xgpu_ops == c->bsp_chain_mark)) barrier(c);
       if (pp.any_twoshot) {
         launch_fold_any(c, pp.fold, t);
         barrier(c);
@@ -576,6 +585,7 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
       if (pp.any_chain) {
         launch_chain_any(c, pp.chain, t, alpha);  // fold -> replica step, fused per chunk
         c->pending_remote = true;
+        if (chain_only) c->bsp_chain_mark = c->xgpu_ops;
       } else {
         launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->mg, 0, 1);
       }

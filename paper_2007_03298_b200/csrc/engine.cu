@@ -908,6 +908,7 @@ void launch_fold(dss_ctx* c, const FoldLaunch& fl, long t) {
 }
 
 void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
+  ++c->xgpu_ops;
   if (c->cfg.dtype == DSS_F64) {
     launch_fold<double>(c, fl, t);
   } else {
@@ -994,6 +995,7 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
 }
 
 void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
+  ++c->xgpu_ops;
   if (c->cfg.dtype == DSS_F64) {
     launch_chain<double>(c, cl, t, alpha);
   } else {
@@ -1081,6 +1083,7 @@ void launch_push(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
 }
 
 void launch_push_any(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
+  ++c->xgpu_ops;
   if (c->cfg.dtype == DSS_F64) {
     launch_push<double>(c, pl, t, alpha);
   } else {
@@ -1133,6 +1136,7 @@ void barrier(dss_ctx* c) {
   if (!multi(c) || c->emulated) return;  // emulation: the launch order already serialises the ranks
   if (!c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
   ++c->epoch;
+  ++c->xgpu_ops;
   TimedLaunch tl(c, DSS_KIND_BARRIER);
   barrier_kernel<<<1, 32 * ((c->cfg.n_gpus + 31) / 32), 0, c->stream>>>(
       c->d_peer_flags, c->flags, c->cfg.rank, c->cfg.n_gpus, c->epoch, c->d_timeout);

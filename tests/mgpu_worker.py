@@ -230,6 +230,43 @@ def busy_case(rank, G):
     return ok
 
 
+def bsp_stream_case(rank, G, orc):
+    """Hundreds of back-to-back BSP steps in one dss_steps call (chain-only
+    plans skip the per-step barrier, pull / one-shot plans keep their own
+    protocol) equal the oracle's loop bit for bit."""
+    ok = True
+    for W, d, opt, iters in ((64, 20_001, 1, 200), (16, 300_007, 1, 100), (8, 250_001, 0, 100)):
+        if W % G:
+            continue
+        s = SyncStrategy(StrategyKind.BSP, Topology.RING, WorldConfig(W, W))
+        hp = OptimizerHyperparams(weight_decay=0.01)
+        rng = np.random.default_rng(77 + W)
+        w = rng.standard_normal((W, d)).astype(np.float32)
+        g = rng.standard_normal((W, d)).astype(np.float32)
+        e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G)
+        attach(e)
+        mine = e.local_ranks
+        e.upload_all(BUF_PARAMS, w[mine])
+        e.upload_all(BUF_GRADS, g[mine])
+        e.steps(0, np.full(iters, 0.01))
+        e.check()
+        got = e.download_all(BUF_PARAMS)
+        parts = [None] * G
+        dist.all_gather_object(parts, (mine, got))
+        e.close()
+        if rank == 0:
+            m1, m2 = np.zeros_like(w), np.zeros_like(w)
+            steps = np.zeros(W, np.int64)
+            for t in range(iters):
+                assert orc.bsp_step(t, opt, hparams(weight_decay=0.01), 0.01, steps, w, g, m1, m2)[0] == 0
+                steps += 1
+            order = np.argsort(np.concatenate([p[0] for p in parts]))
+            same = bool(np.array_equal(np.concatenate([p[1] for p in parts])[order], w))
+            print(f"case bsp stream W={W} d={d} steps={iters} G={G}: {'OK' if same else 'MISMATCH'}", flush=True)
+            ok = ok and same
+    return ok
+
+
 def fingerprint_case(rank, G):
     """Ranks created with different geometry (here: a different d per rank)
     must refuse to map each other's buffers (dss_ipc_attach fingerprint)."""
@@ -254,6 +291,7 @@ def main():
     orc = Oracle()
     ok = fingerprint_case(rank, G)
     ok = busy_case(rank, G) and ok
+    ok = bsp_stream_case(rank, G, orc) and ok
     for case in CASES:
         if case[1] % G:
             continue
