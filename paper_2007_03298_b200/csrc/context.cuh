@@ -197,6 +197,8 @@ struct dss_ctx {
   bool attached = false;
   unsigned long long epoch = 0;
   bool pending_remote = false;
+  bool chain_split = false;         // DS chains: per-parity partial rows and flags (see dss_step)
+  bool pending_chain_only = false;  // the pending remote work is DS step chains only
   unsigned long long xgpu_ops = 0;           // cross-GPU launches so far (barrier, fold, push, chain)
   unsigned long long bsp_chain_mark = ~0ull; // xgpu_ops right after the last chain-only BSP step
 
@@ -462,7 +464,7 @@ void launch_bsp(dss_ctx* c, long t, double alpha);
 // Cross-GPU flag barrier (no-op on one GPU).
 void barrier(dss_ctx* c);
 // Barrier if peers may still be writing into our rows.
-void quiesce(dss_ctx* c);
+void quiesce(dss_ctx* c, bool allow_chain_skip = false);
 void fold_stats(dss_ctx* c, long t, bool barrier_done);
 void bump_steps(dss_ctx* c);
 int check_impl(dss_ctx* c);

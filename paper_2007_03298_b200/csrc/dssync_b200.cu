@@ -292,10 +292,12 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
         pf += cfg->n_gpus;
       }
       c->push_buf = dalloc(c.get(), std::max<size_t>(256, static_cast<size_t>(ps) * c->esz));
+      c->chain_split = s.kind == DSS_DS_SYNC && DSS_CHAIN_INPLACE && DSS_DS_CHAIN_NO_BARRIER;
       c->push_flags = static_cast<unsigned long long*>(
           dalloc(c.get(), std::max<size_t>(64, sizeof(unsigned long long) * static_cast<size_t>(pf))));
       c->chain_flags = static_cast<unsigned long long*>(dalloc(
-          c.get(), std::max<size_t>(64, sizeof(unsigned long long) * 2 * slots * c->chain_nchunks)));
+          c.get(), std::max<size_t>(64, sizeof(unsigned long long) * (c->chain_split ? 4 : 2) * slots *
+                                            c->chain_nchunks)));
     } else {
       c->peer_stats = {c->stats};
       build_plans(c.get());
@@ -515,7 +517,18 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
       const ParityPlan& pp = c->step_plan[t & 1];
       const bool first = c->emu_pass != 2, second = c->emu_pass != 1;  // emulation passes (both when not emulating)
       if (first) {
-        quiesce(c);
+        // Back-to-back DS steps whose cross-GPU work is chains only skip the
+        // opening barrier.  Groups depend only on the parity and each parity
+        // has its own partial rows and flags (chain_split), so a row or flag
+        // refilled at t+1 was last used at t-1 by the same group; its sender
+        // has finished t-1 (a non-last stage waits in kernel B for every
+        // chunk's mean, which exists only after every stage folded that
+        // chunk), so the receiver consumed it.  A member row written in place
+        // at t+1 is written only after its GPU's own t+1 partial, i.e. after
+        // that GPU finished t; and every GPU's kernel B waited for all of its
+        // in-place means of t before its t+1 launches.  Anything else in
+        // between (two-shot, push, sync_round, global mean) keeps the barrier.
+        quiesce(c, true);
         // Local groups: fused apply_step + ordered fold + broadcast.
         for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
       }
@@ -537,6 +550,7 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         if (!second) return DSS_OK;  // emulation pass 1 ends here
         // one-shot writes no peer params: the next iteration needs no barrier
         c->pending_remote = multi(c) && (pp.any_chain || !(pp.any_push && pp.push.oneshot));
+        c->pending_chain_only = c->chain_split && pp.any_chain && !pp.any_push && !pp.any_twoshot;
         fold_stats(c, t, barrier_done);
       } else {
         if (!second) return DSS_OK;
@@ -898,7 +912,8 @@ void fingerprint(const dss_ctx* c, long long* f) {
       c->cfg.strategy.world_size, c->cfg.strategy.group_size, c->cfg.strategy.rectangular,
       c->cfg.n_gpus, c->P, c->d, c->d_pad, c->s, c->chain_slots, c->chain_chunk,
       c->oneshot_base_elems, c->oneshot_half_elems, c->oneshot_rows, c->oneshot_ack_off,
-      c->cfg.path * 1000003LL + c->guard + (static_cast<long long>(c->tile_gr * 64 + c->tile_gc) << 40)};
+      c->cfg.path * 1000003LL + c->guard + (static_cast<long long>(c->tile_gr * 64 + c->tile_gc) << 40) +
+          (static_cast<long long>(c->chain_split) << 60)};
   std::memcpy(f, v, sizeof(v));
 }
 }  // namespace

@@ -93,8 +93,9 @@ void* chain_row(dss_ctx* c, void* base, int region, int slot) {
   return static_cast<char*>(base) +
          (static_cast<size_t>(region) * c->chain_slots + slot) * c->d_pad * c->esz;
 }
-unsigned long long* chain_flag(dss_ctx* c, unsigned long long* base, int region, int slot) {
-  return base + (static_cast<size_t>(region) * c->chain_slots + slot) * c->chain_nchunks;
+// Flags: [parity][region][slot][chunk] (one parity unless chain_split).
+unsigned long long* chain_flag(dss_ctx* c, unsigned long long* base, int region, int slot, int parity = 0) {
+  return base + (static_cast<size_t>(parity * 2 + region) * c->chain_slots + slot) * c->chain_nchunks;
 }
 
 // Chain-fold launch tables for this GPU's roles.  members of role i are
@@ -106,7 +107,12 @@ unsigned long long* chain_flag(dss_ctx* c, unsigned long long* base, int region,
 ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* member_base,
                         const std::vector<std::vector<void*>>& dsts, int err_phase, int opt_mem = kOptNone,
                         int opt_dst = kOptNone, const std::vector<std::vector<int>>& dst_lrs = {},
-                        const Partition* inplace = nullptr) {
+                        const Partition* inplace = nullptr, int parity = 0) {
+  // chain_split (DS, in-place means): parity 1's partials use the region-1
+  // rows (free: the means land in the members' rows) and its own flags
+  const int pf = c->chain_split ? parity : 0;
+  const int prow = pf ? 1 : 0;
+  if (pf && !inplace) throw std::logic_error("chain: parity-split rows need in-place means");
   auto first_member_row = [&](int group, int gpu) -> void* {
     const int* mem = inplace->group(group);
     for (int q = 0; q < inplace->size(group); ++q) {
@@ -140,15 +146,15 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
     for (size_t q = 0; q < dsts[i].size(); ++q) {
       dst_lr.push_back(i < dst_lrs.size() && q < dst_lrs[i].size() ? dst_lrs[i][q] : 0);
     }
-    a.recv = chain_row(c, c->chain_buf, 0, r.slot);
-    a.recv_flags = chain_flag(c, c->chain_flags, 0, r.slot);
+    a.recv = chain_row(c, c->chain_buf, prow, r.slot);
+    a.recv_flags = chain_flag(c, c->chain_flags, 0, r.slot, pf);
     if (!a.last) {
-      a.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.next_gpu)], 0, r.next_slot);
-      a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.next_gpu)], 0, r.next_slot);
+      a.send = chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.next_gpu)], prow, r.next_slot);
+      a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.next_gpu)], 0, r.next_slot, pf);
     } else {
       a.send = inplace ? first_member_row(r.group, r.mean_next_gpu)
                        : chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
-      a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+      a.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot, pf);
     }
     a.err_rank = grank(c, r.first_member);
     a.err_phase = err_phase;
@@ -159,11 +165,11 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
       b.last = 0;
       b.recv = inplace ? dsts[i][0] : chain_row(c, c->chain_buf, 1, r.slot);
       b.dst_skip = inplace ? 1 : 0;
-      b.recv_flags = chain_flag(c, c->chain_flags, 1, r.slot);
+      b.recv_flags = chain_flag(c, c->chain_flags, 1, r.slot, pf);
       if (r.stage < r.S - 2) {
         b.send = inplace ? first_member_row(r.group, r.mean_next_gpu)
                          : chain_row(c, c->peer_chain_buf[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
-        b.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot);
+        b.send_flags = chain_flag(c, c->peer_chain_flags[static_cast<size_t>(r.mean_next_gpu)], 1, r.mean_next_slot, pf);
       } else {
         b.send = nullptr;
         b.send_flags = nullptr;
@@ -457,7 +463,7 @@ ParityPlan build_plan(dss_ctx* c, long t, bool with_step) {
       }
       pp.chain = build_chain(c, gp.chain, c->w, dsts, s.kind == DSS_BSP ? 0 : 1,
                              with_step ? c->cfg.optimizer : kOptNone, kOptNone, lrs,
-                             DSS_CHAIN_INPLACE && multi(c) ? &part : nullptr);
+                             DSS_CHAIN_INPLACE && multi(c) ? &part : nullptr, static_cast<int>(t & 1));
     }
   }
   if (force_fold(c)) pp.any_twoshot = pp.any_spanning;
@@ -1145,9 +1151,12 @@ void barrier(dss_ctx* c) {
 
 // Peers may still be writing group means into our rows (two-shot phase 2 of
 // the previous round): wait for them before touching the rows again.
-void quiesce(dss_ctx* c) {
-  if (c->pending_remote && multi(c)) barrier(c);
+// allow_chain_skip (DS steps only): remote work that is DS step chains only
+// needs no barrier before the next DS step -- see dss_step.
+void quiesce(dss_ctx* c, bool allow_chain_skip) {
+  if (c->pending_remote && multi(c) && !(allow_chain_skip && c->pending_chain_only)) barrier(c);
   c->pending_remote = false;
+  c->pending_chain_only = false;
 }
 
 // Fold the running statistics of iteration t (DS: the parity's groups; BSP:
@@ -1164,6 +1173,7 @@ void fold_stats(dss_ctx* c, long t, bool barrier_done) {
     if (multi(c) && !barrier_done) barrier(c);
     launch_fold_any(c, sp.fold, t);
     c->pending_remote = multi(c);
+    c->pending_chain_only = false;
   }
 }
 

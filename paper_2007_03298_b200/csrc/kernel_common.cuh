@@ -98,6 +98,9 @@ constexpr int kSmallWide = 512;
 #ifndef DSS_BSP_PULL
 #define DSS_BSP_PULL 0
 #endif
+#ifndef DSS_DS_CHAIN_NO_BARRIER
+#define DSS_DS_CHAIN_NO_BARRIER 1
+#endif
 #ifndef DSS_BSP_CHAIN_NO_BARRIER
 #define DSS_BSP_CHAIN_NO_BARRIER 1
 #endif

@@ -267,6 +267,50 @@ def bsp_stream_case(rank, G, orc):
     return ok
 
 
+def ds_stream_case(rank, G, orc):
+    """Tens to hundreds of back-to-back DS steps in one dss_steps call on
+    plans whose cross-GPU work is ordered chains only (the per-step barrier
+    is skipped there; per-parity chain rows and flags) equal the oracle's
+    loop bit for bit, and a sync_round afterwards (barrier restored) too."""
+    ok = True
+    for W, N, rect, opt, d, iters, placement in ((8, 2, True, 1, 250_001, 100, 0),
+                                                 (16, 4, False, 3, 200_003, 60, 1),
+                                                 (32, 4, True, 1, 150_001, 60, 1)):
+        if W % G:
+            continue
+        s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, rect)
+        hp = OptimizerHyperparams(weight_decay=0.01)
+        rng = np.random.default_rng(91 + W)
+        w = rng.standard_normal((W, d)).astype(np.float32)
+        g = rng.standard_normal((W, d)).astype(np.float32)
+        e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G, placement=placement)
+        attach(e)
+        mine = e.local_ranks
+        e.upload_all(BUF_PARAMS, w[mine])
+        e.upload_all(BUF_GRADS, g[mine])
+        alpha = 0.01 if opt >= 2 else 0.05
+        e.steps(0, np.full(iters, alpha))
+        e.sync_round(iters, check=False)
+        e.check()
+        got = e.download_all(BUF_PARAMS)
+        parts = [None] * G
+        dist.all_gather_object(parts, (mine, got))
+        e.close()
+        if rank == 0:
+            m1, m2 = np.zeros_like(w), np.zeros_like(w)
+            steps = np.zeros(W, np.int64)
+            for t in range(iters):
+                assert orc.ds_step(W, N, t, opt, hparams(weight_decay=0.01), alpha, steps, w, g, m1, m2, rect)[0] == 0
+                steps += 1
+            orc.sync_round(W, N, iters, w, rect=rect)
+            order = np.argsort(np.concatenate([p[0] for p in parts]))
+            same = bool(np.array_equal(np.concatenate([p[1] for p in parts])[order], w))
+            print(f"case ds stream W={W} N={N} d={d} steps={iters} placement={placement} G={G}: "
+                  f"{'OK' if same else 'MISMATCH'}", flush=True)
+            ok = ok and same
+    return ok
+
+
 def fingerprint_case(rank, G):
     """Ranks created with different geometry (here: a different d per rank)
     must refuse to map each other's buffers (dss_ipc_attach fingerprint)."""
@@ -292,6 +336,7 @@ def main():
     ok = fingerprint_case(rank, G)
     ok = busy_case(rank, G) and ok
     ok = bsp_stream_case(rank, G, orc) and ok
+    ok = ds_stream_case(rank, G, orc) and ok
     for case in CASES:
         if case[1] % G:
             continue
