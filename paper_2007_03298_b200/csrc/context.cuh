@@ -201,6 +201,13 @@ struct dss_ctx {
   bool pending_chain_only = false;  // the pending remote work is DS step chains only
   unsigned long long xgpu_ops = 0;           // cross-GPU launches so far (barrier, fold, push, chain)
   unsigned long long bsp_chain_mark = ~0ull; // xgpu_ops right after the last chain-only BSP step
+  // split barrier after DS two-shot push steps (DSS_PUSH_SPLIT_BARRIER):
+  // the push kernel arrives (barrier words <- epoch) and the next DS step's
+  // first kernel waits, in place of a barrier launch between the steps
+  unsigned long long split_mark = ~0ull;  // xgpu_ops right after an arriving push
+  unsigned long long wait_epoch = 0;      // pending wait for the next launch (0: none)
+  unsigned* d_arrive_count = nullptr;     // the push kernel's CTA counter
+  bool arrive_next_push = false;          // the next push launch arrives
 
   dssb::ParityPlan step_plan[2];   // DS (or BSP at [0])
   dssb::ParityPlan sync_plan[2];   // sync_round (no step)
@@ -465,6 +472,7 @@ void launch_bsp(dss_ctx* c, long t, double alpha);
 void barrier(dss_ctx* c);
 // Barrier if peers may still be writing into our rows.
 void quiesce(dss_ctx* c, bool allow_chain_skip = false);
+void flush_wait(dss_ctx* c, unsigned long long epoch = 0);
 void fold_stats(dss_ctx* c, long t, bool barrier_done);
 void bump_steps(dss_ctx* c);
 int check_impl(dss_ctx* c);

@@ -182,6 +182,7 @@ extern "C" int dss_create(const dss_config* cfg, dss_ctx** out) {
     c->d_timeout = static_cast<unsigned long long*>(dalloc(c.get(), sizeof(unsigned long long)));
     c->flags = static_cast<unsigned long long*>(
         dalloc(c.get(), sizeof(unsigned long long) * static_cast<size_t>(std::max(cfg->n_gpus, 32))));
+    c->d_arrive_count = static_cast<unsigned*>(dalloc(c.get(), sizeof(unsigned)));
     ck(cudaMallocHost(&c->h_err, sizeof(unsigned long long)), "cudaMallocHost");
 
     {
@@ -500,6 +501,10 @@ extern "C" long dss_get_step_count(const dss_ctx* c, int rank) {
 
 // ------------------------------- hot path ------------------------------------
 
+#ifndef DSS_PUSH_SPLIT_BARRIER
+#define DSS_PUSH_SPLIT_BARRIER 1
+#endif
+
 extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome* out) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
   NvtxRange range(c->cfg.strategy.kind == DSS_DS_SYNC ? "dss_step ds-sync" : "dss_step bsp");
@@ -539,8 +544,16 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         // per chunk, no barrier).
         if (first) launch_groups_any(c, pp.spanning_step, opt, t, alpha, c->g, c->d_pad, 0);
         bool barrier_done = false;
+        // A two-shot push with nothing cross-GPU after it arrives at the split
+        // barrier itself: the next DS step waits in its first kernel instead
+        // of opening with a barrier launch (quiesce).  The plan flags are the
+        // same on every GPU, so every GPU arrives and waits at the same epochs.
+        const bool split = DSS_PUSH_SPLIT_BARRIER && multi(c) && !c->emulated && pp.any_push &&
+                           !pp.push.oneshot && !pp.any_chain && c->s == 0;  // (any_push: no pull fold)
         if (pp.any_push) {
+          c->arrive_next_push = split;
           launch_push_any(c, pp.push, t, alpha);  // fused step + push two-shot
+          if (split) c->split_mark = c->xgpu_ops;
         } else if (pp.any_twoshot && second) {
           if (multi(c)) barrier(c);
           barrier_done = true;

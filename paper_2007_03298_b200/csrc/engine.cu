@@ -785,6 +785,7 @@ void launch_group_t(dss_ctx* c, const GroupArgs<T>& a, int groups) {
 
 template <typename T, int OPT>
 void launch_group_bulk(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl) {
+  if (a.wait_flags) flush_wait(c, a.wait_epoch);
   constexpr int A = (OPT == kAdam || OPT == kAdamW) ? 4 : (OPT == kMomentum ? 3 : 2);
   const size_t smem = static_cast<size_t>(kBulkStages) * 8 * A * kBulkTE * sizeof(T);
   static bool attr_set = false;
@@ -814,6 +815,7 @@ void launch_group_bulk(dss_ctx* c, const GroupArgs<T>& a, const GroupLaunch& gl)
 
 template <int OPT>
 void launch_group_narrow(dss_ctx* c, const GroupArgs<float>& a, int groups) {
+  if (a.wait_flags) flush_wait(c, a.wait_epoch);
   dim3 grid(grid_x(c, a.nvec * 2, groups), groups);
   TimedLaunch tl(c, DSS_KIND_GROUP);
   ds_group_narrow_kernel<OPT, 8><<<grid, kThreads, 0, c->stream>>>(a);
@@ -851,6 +853,13 @@ void launch_groups(dss_ctx* c, const GroupLaunch& gl, int opt, long t, double al
                    const void* g, long g_ld, int step_phase, int sync_phase, void* rows = nullptr, long rows_ld = 0) {
   if (gl.groups == 0) return;
   GroupArgs<T> a{};
+  if (c->wait_epoch) {  // first launch of a step after an arriving push: wait in every CTA
+    a.wait_flags = c->flags;
+    a.wait_n = c->cfg.n_gpus;
+    a.wait_epoch = c->wait_epoch;
+    a.timeout = c->d_timeout;
+    c->wait_epoch = 0;
+  }
   a.w = static_cast<T*>(rows ? rows : c->w);  // rows: fold-only over another row set (running stats)
   a.g = static_cast<const T*>(g);
   a.m1 = static_cast<T*>(c->m1);
@@ -914,6 +923,7 @@ void launch_fold(dss_ctx* c, const FoldLaunch& fl, long t) {
 }
 
 void launch_fold_any(dss_ctx* c, const FoldLaunch& fl, long t) {
+  flush_wait(c);
   ++c->xgpu_ops;
   if (c->cfg.dtype == DSS_F64) {
     launch_fold<double>(c, fl, t);
@@ -1001,6 +1011,7 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
 }
 
 void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
+  flush_wait(c);
   ++c->xgpu_ops;
   if (c->cfg.dtype == DSS_F64) {
     launch_chain<double>(c, cl, t, alpha);
@@ -1037,6 +1048,20 @@ void launch_push_t(dss_ctx* c, const PushLaunch& pl, long t, double alpha) {
   a.epoch = c->chain_epoch;
   a.err = c->d_err;
   a.timeout = c->d_timeout;
+  a.me = c->cfg.rank;
+  a.n_gpus = c->cfg.n_gpus;
+  if (c->wait_epoch) {
+    a.wait_flags = c->flags;
+    a.wait_epoch = c->wait_epoch;
+    c->wait_epoch = 0;
+  }
+  if (c->arrive_next_push) {
+    c->arrive_next_push = false;
+    ++c->epoch;
+    a.arrive_flags = c->d_peer_flags;
+    a.arrive_epoch = c->epoch;
+    a.arrive_count = c->d_arrive_count;
+  }
   if (pl.oneshot) {
     // rotate the staging buffers; the kernel's acks keep a push from
     // overwriting a buffer its destination still reads (see PushArgs::seq)
@@ -1141,6 +1166,7 @@ void launch_bsp(dss_ctx* c, long t, double alpha) {
 void barrier(dss_ctx* c) {
   if (!multi(c) || c->emulated) return;  // emulation: the launch order already serialises the ranks
   if (!c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
+  c->wait_epoch = 0;  // a full barrier subsumes a pending split wait (flags only grow)
   ++c->epoch;
   ++c->xgpu_ops;
   TimedLaunch tl(c, DSS_KIND_BARRIER);
@@ -1153,10 +1179,33 @@ void barrier(dss_ctx* c) {
 // the previous round): wait for them before touching the rows again.
 // allow_chain_skip (DS steps only): remote work that is DS step chains only
 // needs no barrier before the next DS step -- see dss_step.
+// allow_chain_skip also lets a DS step that follows an arriving two-shot push
+// step (and nothing cross-GPU after it) wait in its first kernel instead.
 void quiesce(dss_ctx* c, bool allow_chain_skip) {
-  if (c->pending_remote && multi(c) && !(allow_chain_skip && c->pending_chain_only)) barrier(c);
+  if (c->pending_remote && multi(c) && !(allow_chain_skip && c->pending_chain_only)) {
+    if (allow_chain_skip && c->split_mark == c->xgpu_ops) {
+      c->wait_epoch = c->epoch;
+    } else {
+      barrier(c);
+    }
+  }
+  if (!allow_chain_skip) flush_wait(c);
   c->pending_remote = false;
   c->pending_chain_only = false;
+}
+
+// Launch the waiting half of the split barrier on its own if still pending
+// (epoch: a wait taken from a launch that cannot wait itself).
+void flush_wait(dss_ctx* c, unsigned long long epoch) {
+  if (!epoch) {
+    epoch = c->wait_epoch;
+    c->wait_epoch = 0;
+  }
+  if (!epoch) return;
+  TimedLaunch tl(c, DSS_KIND_BARRIER);
+  split_wait_kernel<<<1, 32 * ((c->cfg.n_gpus + 31) / 32), 0, c->stream>>>(c->flags, c->cfg.n_gpus, epoch,
+                                                                           c->d_timeout);
+  ck(cudaGetLastError(), "split_wait_kernel launch");
 }
 
 // Fold the running statistics of iteration t (DS: the parity's groups; BSP:

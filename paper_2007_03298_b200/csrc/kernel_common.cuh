@@ -280,6 +280,31 @@ __device__ __forceinline__ void latch_error(unsigned long long* err, unsigned lo
   if ((threadIdx.x & 31) == (__ffs(mask) - 1) && k != ~0ull) atomicMin(err, k);
 }
 
+// ---- split cross-GPU barrier: the waiting half -----------------------------
+// A two-shot push kernel ends by storing its epoch into every GPU's barrier
+// flag word (the arriving half, see push_twoshot_kernel); the first kernel of
+// the next step waits here, every CTA before touching any row, instead of a
+// separate barrier launch.  Thread j polls GPU j's word (bounded, ~20 s of
+// globaltimer, then the timeout is latched as in barrier_kernel).
+__device__ __forceinline__ void split_wait(const unsigned long long* flags, int n, unsigned long long epoch,
+                                           unsigned long long* timeout) {
+  if (!flags) return;
+  if (static_cast<int>(threadIdx.x) < n) {
+    unsigned long long start, now, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(start));
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + threadIdx.x) : "memory");
+      if (v >= epoch) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - start > 20000000000ull) {
+        atomicExch(timeout, 1ull);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 
 // ---- synthetic gradients: SplitMix64 + Box-Muller (rng.cpp:8-51) -----------
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

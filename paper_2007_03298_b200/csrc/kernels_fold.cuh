@@ -132,6 +132,13 @@ static __global__ void barrier_kernel(unsigned long long* const* peer_flags, uns
   __threadfence_system();
 }
 
+// The waiting half of the split barrier on its own, for a step whose first
+// launch cannot wait itself.
+static __global__ void split_wait_kernel(const unsigned long long* my_flags, int n, unsigned long long epoch,
+                                         unsigned long long* timeout) {
+  split_wait(my_flags, n, epoch, timeout);
+}
+
 // ---- ordered chain fold across GPUs (comm.cpp:96-110) -------
 // A group spanning GPUs g_0 < ... < g_{S-1}, each holding a contiguous run
 // of its ascending members, is folded as the reference's ring does: the
@@ -529,6 +536,16 @@ template <typename T> struct PushArgs {
   unsigned long long* ack_mine;         // [G] this GPU's ack array
   const int* item_gpu;                  // destination GPU of each item_dst entry
   int me, n_gpus;
+  // split barrier.  wait_*: as GroupArgs (this launch is the first of its
+  // step).  arrive_epoch != 0 (two-shot, no chain or fold after it): the last
+  // CTA to finish stores arrive_epoch into every GPU's barrier word
+  // (arrive_flags[j] + me), after every CTA's phase-2 stores; arrive_count
+  // is a local CTA counter, zero between launches.
+  const unsigned long long* wait_flags;
+  unsigned long long wait_epoch;
+  unsigned long long* const* arrive_flags;
+  unsigned long long arrive_epoch;
+  unsigned* arrive_count;
   StepConsts<T> c;
   double bc1[kMaxLocal];
   double bc2[kMaxLocal];
@@ -549,6 +566,7 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   __shared__ T* sdst[kMaxFold];
   __shared__ unsigned long long sok;  // bit q: destination q may be written (its flow-control wait succeeded)
   unsigned long long bad = ~0ull;
+  split_wait(a.wait_flags, a.n_gpus, a.wait_epoch, a.timeout);
   if (a.seq && blockIdx.x == 0 && threadIdx.x < a.n_gpus) {
     // "I have started launch seq".  The reads this releases (the folds of
     // an earlier launch) finished at a kernel boundary, so a relaxed store
@@ -703,6 +721,21 @@ __global__ void __launch_bounds__(kThreads) push_twoshot_kernel(const PushArgs<T
   }
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
   __threadfence_system();
+  if (a.arrive_epoch) {
+    // arriving half of the split barrier: every CTA's stores (fenced above)
+    // precede its count; the last CTA releases the epoch to every GPU
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(a.arrive_count, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      if (static_cast<int>(threadIdx.x) < a.n_gpus) {
+        __threadfence_system();
+        st_release_sys(a.arrive_flags[threadIdx.x] + a.me, a.arrive_epoch);
+      }
+      if (threadIdx.x == 0) atomicExch(a.arrive_count, 0u);
+    }
+  }
 }
 
 }  // namespace dssb

@@ -28,6 +28,12 @@ template <typename T> struct GroupArgs {
   double bc1[kMaxLocal];  // per local worker bias corrections (optim.cpp:76-78)
   double bc2[kMaxLocal];
   unsigned long long* err;
+  // split barrier (first kernel after a two-shot push step): wait for every
+  // GPU's barrier word to reach wait_epoch before touching rows; null: none
+  const unsigned long long* wait_flags;
+  int wait_n;
+  unsigned long long wait_epoch;
+  unsigned long long* timeout;
 };
 
 // blockIdx.y = group of this launch; threads stride over the row's vectors.
@@ -44,6 +50,7 @@ constexpr int group_min_blocks() {
 template <typename T, int OPT, int M>
 __global__ void __launch_bounds__(kThreads, group_min_blocks<OPT, M>()) ds_group_kernel(const GroupArgs<T> a) {
   constexpr int VN = Vec<T>::n;
+  split_wait(a.wait_flags, a.wait_n, a.wait_epoch, a.timeout);
   const int beg = a.offsets[blockIdx.y];
   const int m = M > 0 ? M : a.offsets[blockIdx.y + 1] - beg;
   const int lead = a.rank_of[a.members[beg] - a.first_rank];  // members[0]: a failed group mean's rank

@@ -268,14 +268,21 @@ def bsp_stream_case(rank, G, orc):
 
 
 def ds_stream_case(rank, G, orc):
-    """Tens to hundreds of back-to-back DS steps in one dss_steps call on
-    plans whose cross-GPU work is ordered chains only (the per-step barrier
-    is skipped there; per-parity chain rows and flags) equal the oracle's
-    loop bit for bit, and a sync_round afterwards (barrier restored) too."""
+    """Tens to hundreds of back-to-back DS steps in one dss_steps call equal
+    the oracle's loop bit for bit, and a sync_round afterwards (barrier
+    restored) too.  Chain-only plans skip the per-step barrier (per-parity
+    chain rows and flags); two-shot push plans replace it with the split
+    barrier (the push kernel arrives, the next step's first kernel waits):
+    push -> local group kernel (C2 shape and W=16 on 4 GPUs, contiguous) and
+    push -> push (W=4 with pairs forced off one-shot, path 4)."""
     ok = True
-    for W, N, rect, opt, d, iters, placement in ((8, 2, True, 1, 250_001, 100, 0),
-                                                 (16, 4, False, 3, 200_003, 60, 1),
-                                                 (32, 4, True, 1, 150_001, 60, 1)):
+    for W, N, rect, opt, d, iters, placement, path in ((8, 2, True, 1, 250_001, 100, 0, 0),
+                                                       (16, 4, False, 3, 200_003, 60, 1, 0),
+                                                       (32, 4, True, 1, 150_001, 60, 1, 0),
+                                                       (8, 2, True, 0, 250_001, 100, 0, 0),
+                                                       (16, 4, False, 3, 200_003, 60, 0, 0),
+                                                       (4, 2, False, 1, 250_001, 100, 0, 4),
+                                                       (4, 2, False, 3, 4097, 200, 0, 4)):
         if W % G:
             continue
         s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, rect)
@@ -283,13 +290,19 @@ def ds_stream_case(rank, G, orc):
         rng = np.random.default_rng(91 + W)
         w = rng.standard_normal((W, d)).astype(np.float32)
         g = rng.standard_normal((W, d)).astype(np.float32)
-        e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G, placement=placement)
+        e = DsSyncEngine(s, OptimizerKind(opt), d, hp, "f32", device_of(rank), rank, G, path=path,
+                         placement=placement)
         attach(e)
         mine = e.local_ranks
         e.upload_all(BUF_PARAMS, w[mine])
         e.upload_all(BUF_GRADS, g[mine])
         alpha = 0.01 if opt >= 2 else 0.05
+        e.enable_timing(True)
         e.steps(0, np.full(iters, alpha))
+        barriers = e.kernel_times_by_kind()["barrier"][1]
+        e.enable_timing(False)
+        # two-shot push plans: no barrier launch between the steps (split barrier)
+        push_plan = placement == 0 and ((W, G) in ((8, 4), (16, 4)) or path == 4)
         e.sync_round(iters, check=False)
         e.check()
         got = e.download_all(BUF_PARAMS)
@@ -305,8 +318,9 @@ def ds_stream_case(rank, G, orc):
             orc.sync_round(W, N, iters, w, rect=rect)
             order = np.argsort(np.concatenate([p[0] for p in parts]))
             same = bool(np.array_equal(np.concatenate([p[1] for p in parts])[order], w))
-            print(f"case ds stream W={W} N={N} d={d} steps={iters} placement={placement} G={G}: "
-                  f"{'OK' if same else 'MISMATCH'}", flush=True)
+            same = same and not (push_plan and barriers)
+            print(f"case ds stream W={W} N={N} opt={opt} d={d} steps={iters} placement={placement} path={path} G={G}: "
+                  f"barriers={barriers} {'OK' if same else 'MISMATCH'}", flush=True)
             ok = ok and same
     return ok
 
