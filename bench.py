@@ -688,6 +688,10 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, nccl_only=False
             res["e2e_ms"] = timed(None, t_e2e + args.warmup, K2, batched=e2e_run)
             res["e2e_steps"] = K2
             e.check()
+            try:
+                res["pcie"] = pcie_ceiling(hg, hw)
+            except RuntimeError as ex:  # out of device memory on a packed config: no ceiling, no failure
+                res["pcie_error"] = str(ex).splitlines()[0]
             del hg, hw
         e.close()
         del e
@@ -695,6 +699,38 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, nccl_only=False
     d_pad = (d + 63) // 64 * 64
     res["bytes"] = step_bytes(cfg, G, rank, d_pad, args.path, esz, args.placement)
     return res
+
+
+def pcie_ceiling(hg, hw, reps=5):
+    """The e2e leg's own ceiling: pinned-host copies of this rank's gradient
+    and param buffers (up to 1 GiB each) by the copy engines, H2D alone, D2H
+    alone and both at once on two streams (what dss_step_host overlaps),
+    GB/s per direction, after the timed region."""
+    import torch
+    n = min(hg.numel(), (1 << 30) // hg.element_size())
+    src, dst = hg.view(-1)[:n], hw.view(-1)[:n]
+    da = torch.empty(n, dtype=hg.dtype, device="cuda")
+    db = torch.empty(n, dtype=hg.dtype, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(h2d, d2h):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    da.copy_(src, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    dst.copy_(db, non_blocking=True)
+        torch.cuda.synchronize()
+        return reps * n * hg.element_size() / (time.perf_counter() - t0) / 1e9
+
+    run(True, True)  # warm-up
+    out = {"h2d_gbs": run(True, False), "d2h_gbs": run(False, True), "bidir_gbs_per_direction": run(True, True),
+           "bytes_per_copy": n * hg.element_size()}
+    del da, db
+    return out
 
 
 def summarize(args, cfg, dtype, G, res, peak, peak_kind):
@@ -771,6 +807,13 @@ def summarize(args, cfg, dtype, G, res, peak, peak_kind):
                       "d2h_bytes_per_step": P * d * esz * G, "steps": res["e2e_steps"],
                       "path": "C-ABI dss_step_host: pinned grads H2D + step + params D2H every step (copies on two "
                               "copy streams, D2H of step t overlapping H2D of step t+1)"}
+        if "pcie" in res:
+            # the e2e roofline: bytes each way per step / step time against
+            # the copy engines' own pinned bidirectional rate on this box
+            pc = dict(res["pcie"])
+            pc["achieved_gbs_per_direction"] = P * d * esz / (res["e2e_ms"] / 1e3) / 1e9
+            pc["frac"] = pc["achieved_gbs_per_direction"] / pc["bidir_gbs_per_direction"]
+            out["e2e"]["pcie"] = pc
     elif "e2e_skipped" in res:
         out["e2e"] = {"value": None, "unit": "iters/s", "skipped": res["e2e_skipped"]}
     if "nccl_ds" in res:
