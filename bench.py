@@ -673,7 +673,11 @@ def measure(args, cfg, dtype, G, rank, local, stream, full=True, nccl_only=False
             big = P * d * esz > (1 << 30)
             K2 = max(3, min(args.steps, args.e2e_steps if big else args.steps))
             if big:
-                K2 = min(K2, 5)
+                # the copy pipeline fills and drains once per timed run (the
+                # first H2D and the last D2H overlap nothing): K steps reach
+                # at most K / (K + 1) of the bidirectional ceiling (5 steps:
+                # 0.84), so large rows get 16 steps (C4 slice: ~4 s)
+                K2 = min(K2, 16)
             tdt = torch.float64 if dtype == "f64" else torch.float32
             hg = torch.empty((P, d), dtype=tdt, pin_memory=True)
             hw = torch.empty((P, d), dtype=tdt, pin_memory=True)
