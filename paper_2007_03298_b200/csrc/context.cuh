@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -22,6 +23,10 @@
 #include "kernels.cuh"
 #include "problems.hpp"
 #include "schedule.hpp"
+
+#ifndef DSS_CHAIN_LAZY_MEAN
+#define DSS_CHAIN_LAZY_MEAN 1
+#endif
 
 namespace dssb {
 
@@ -74,6 +79,7 @@ struct GroupLaunch {
   int groups = 0;
   int* d_members = nullptr;
   int* d_offsets = nullptr;
+  std::vector<int> members;  // host copy (slots, group after group)
 };
 
 struct FoldLaunch {
@@ -95,6 +101,22 @@ struct ChainLaunch {
   int* d_dst_lr = nullptr;         // local row index of each destination
   int opt_mem = -1;                // fused step on the members (DS), kOptNone = fold only
   int opt_dst = -1;                // fused step of the destinations with the mean (BSP)
+  std::vector<ChainEntry> hb;      // host copies of the kernel B entries and destinations
+  std::vector<void*> hdst;
+};
+
+// Deferred chain mean pass (DSS_CHAIN_LAZY_MEAN): a stage-0 GPU of two-GPU
+// chains skips kernel B (copying the mean that arrived in place into its
+// other members' rows) when the next parity's groups are all local; that
+// step's fused kernel waits for the mean chunks and reads every aliased
+// member's params from the row the mean arrived in.
+struct LazyPlan {
+  bool ok = false;
+  int nf = 0;
+  const unsigned long long* flags[4] = {};  // kernel B entries' receive flags (chunk-indexed)
+  int alias[8] = {};                         // local row -> row holding its params
+  int rows[8] = {};                          // next parity's group members (local rows), group after group
+  int nr = 0, m = 0;
 };
 
 struct PushLaunch {
@@ -207,6 +229,12 @@ struct dss_ctx {
   unsigned long long split_mark = ~0ull;  // xgpu_ops right after an arriving push
   unsigned long long wait_epoch = 0;      // pending wait for the next launch (0: none)
   unsigned* d_arrive_count = nullptr;     // the push kernel's CTA counter
+  dssb::LazyPlan lazy_plan[2];            // [chain parity]: its deferred mean pass, consumed at the other parity
+  std::function<void()> lazy_b;           // the deferred kernel B launch (empty: none pending)
+  unsigned long long lazy_epoch = 0;
+  int lazy_parity = -1;                   // parity whose step consumes it
+  bool lazy_consume = false;              // set by dss_step around guard(): do not flush on entry
+  bool defer_b = false;                   // the next chain launch defers its kernel B
   bool arrive_next_push = false;          // the next push launch arrives
 
   dssb::ParityPlan step_plan[2];   // DS (or BSP at [0])
@@ -286,9 +314,17 @@ inline int fail(dss_ctx* c, int status, const std::string& msg, int rank = -1, l
   return status;
 }
 
+void flush_lazy(dss_ctx* c);
+
+// Every C-ABI entry point runs through guard: a deferred chain mean pass is
+// launched first unless the call is the DS step that consumes it.
 template <typename F>
 int guard(dss_ctx* c, F&& f) {
   try {
+    if (c) {
+      if (c->lazy_b && !c->lazy_consume) flush_lazy(c);
+      c->lazy_consume = false;
+    }
     return f();
   } catch (const std::invalid_argument& e) {
     return fail(c, DSS_EINVAL, e.what());
@@ -473,6 +509,8 @@ void barrier(dss_ctx* c);
 // Barrier if peers may still be writing into our rows.
 void quiesce(dss_ctx* c, bool allow_chain_skip = false);
 void flush_wait(dss_ctx* c, unsigned long long epoch = 0);
+dssb::LazyPlan build_lazy(dss_ctx* c, int p);
+void launch_lazy_any(dss_ctx* c, const dssb::LazyPlan& lp, long t, double alpha);
 void fold_stats(dss_ctx* c, long t, bool barrier_done);
 void bump_steps(dss_ctx* c);
 int check_impl(dss_ctx* c);

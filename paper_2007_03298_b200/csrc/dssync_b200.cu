@@ -507,6 +507,7 @@ extern "C" long dss_get_step_count(const dss_ctx* c, int rank) {
 
 extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome* out) {
   if (!c) return fail(nullptr, DSS_EINVAL, "null context");
+  c->lazy_consume = true;  // guard() leaves a deferred mean pass to the step below
   NvtxRange range(c->cfg.strategy.kind == DSS_DS_SYNC ? "dss_step ds-sync" : "dss_step bsp");
   return guard(c, [&]() -> int {
     if (t < 0) throw std::invalid_argument("iteration must be >= 0");
@@ -533,9 +534,19 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
         // that GPU finished t; and every GPU's kernel B waited for all of its
         // in-place means of t before its t+1 launches.  Anything else in
         // between (two-shot, push, sync_round, global mean) keeps the barrier.
+        // A chain step of the other parity may have left its mean pass to
+        // this step (LazyPlan): this step's local groups then run fused with
+        // it; any other order launches the deferred pass first.
+        const bool lazy = c->lazy_b && c->lazy_parity == static_cast<int>(t & 1) && second &&
+                          c->lazy_plan[(t + 1) & 1].ok;
+        if (c->lazy_b && !lazy) flush_lazy(c);
         quiesce(c, true);
-        // Local groups: fused apply_step + ordered fold + broadcast.
-        for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
+        if (lazy) {
+          launch_lazy_any(c, c->lazy_plan[(t + 1) & 1], t, alpha);
+        } else {
+          // Local groups: fused apply_step + ordered fold + broadcast.
+          for (const GroupLaunch& gl : pp.local) launch_groups_any(c, gl, opt, t, alpha, c->g, c->d_pad, 0);
+        }
       }
       if (pp.any_spanning) {
         // Members of spanning groups step in place.  Two-shot groups: after
@@ -559,7 +570,12 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
           barrier_done = true;
           launch_fold_any(c, pp.fold, t);
         }
-        if (pp.any_chain) launch_chain_any(c, pp.chain, t, alpha);
+        if (pp.any_chain) {
+          c->defer_b = c->lazy_plan[t & 1].ok && !c->emulated && c->emu_pass == 0;
+          launch_chain_any(c, pp.chain, t, alpha);
+          c->defer_b = false;
+          if (c->lazy_b) c->lazy_parity = static_cast<int>((t + 1) & 1);
+        }
         if (!second) return DSS_OK;  // emulation pass 1 ends here
         // one-shot writes no peer params: the next iteration needs no barrier
         c->pending_remote = multi(c) && (pp.any_chain || !(pp.any_push && pp.push.oneshot));

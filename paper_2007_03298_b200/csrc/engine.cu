@@ -19,6 +19,7 @@ GroupLaunch make_group_launch(dss_ctx* c, const std::vector<std::vector<int>>& g
     offsets.push_back(static_cast<int>(members.size()));
   }
   gl.groups = static_cast<int>(groups.size());
+  gl.members = members;
   gl.d_members = upload_table(c, members);
   gl.d_offsets = upload_table(c, offsets);
   return gl;
@@ -181,6 +182,8 @@ ChainLaunch build_chain(dss_ctx* c, const std::vector<ChainRole>& roles, void* m
   cl.nb = static_cast<int>(eb.size());
   cl.d_a = upload_table(c, ea);
   cl.d_b = upload_table(c, eb);
+  cl.hb = eb;
+  cl.hdst = dst;
   cl.d_src = upload_table(c, src);
   cl.d_dst = upload_table(c, dst);
   cl.d_src_lr = upload_table(c, src_lr);
@@ -749,6 +752,40 @@ ParityPlan build_stats_plan(dss_ctx* c, const Partition& part) {
   return pp;
 }
 
+// Deferred mean pass of parity p's chains on this GPU (LazyPlan): only when
+// every chain entry here with a mean pass is a stage 0 of a two-GPU chain
+// (the mean arrives in place, nothing to forward) and the other parity's
+// groups are all local, one launch of 2 or 4 rows per group over all P <= 4
+// rows.
+LazyPlan build_lazy(dss_ctx* c, int p) {
+  LazyPlan lp;
+  if (!DSS_CHAIN_LAZY_MEAN || !multi(c) || c->s != 0 || !c->chain_split) return lp;
+  const ParityPlan& pp = c->step_plan[p];
+  const ParityPlan& pq = c->step_plan[1 - p];
+  if (!pp.any_chain || pp.any_push || pp.any_twoshot || !pp.local.empty()) return lp;
+  const ChainLaunch& cl = pp.chain;
+  if (cl.nb == 0 || cl.nb > 4 || cl.opt_dst != kOptNone) return lp;
+  if (pq.any_spanning || pq.local.size() != 1) return lp;
+  const GroupLaunch& gl = pq.local[0];
+  if ((gl.size != 2 && gl.size != 4) || (c->P != 2 && c->P != 4) || gl.groups * gl.size != c->P) return lp;
+  const size_t row_bytes = static_cast<size_t>(c->d_pad) * c->esz;
+  auto row_of = [&](const void* ptr) {
+    return static_cast<int>((static_cast<const char*>(ptr) - static_cast<const char*>(c->w)) / row_bytes);
+  };
+  for (int r = 0; r < c->P; ++r) lp.alias[r] = r;
+  for (const ChainEntry& b : cl.hb) {
+    if (!b.dst_skip || b.send || b.dst_cnt < 1 || b.recv != cl.hdst[static_cast<size_t>(b.dst_beg)]) return lp;
+    const int src = row_of(b.recv);
+    for (int q = 1; q < b.dst_cnt; ++q) lp.alias[row_of(cl.hdst[static_cast<size_t>(b.dst_beg + q)])] = src;
+    lp.flags[lp.nf++] = b.recv_flags;
+  }
+  for (int i = 0; i < c->P; ++i) lp.rows[i] = gl.members[static_cast<size_t>(i)] - c->first;
+  lp.nr = c->P;
+  lp.m = gl.size;
+  lp.ok = true;
+  return lp;
+}
+
 void build_stats_plans(dss_ctx* c) {
   if (c->s == 0) return;
   const dss_strategy& s = c->cfg.strategy;
@@ -759,6 +796,7 @@ void build_plans(dss_ctx* c) {
   const dss_strategy& s = c->cfg.strategy;
   if (s.kind == DSS_DS_SYNC) {
     for (int p = 0; p < 2; ++p) c->step_plan[p] = build_plan(c, p, true);
+    for (int p = 0; p < 2; ++p) c->lazy_plan[p] = build_lazy(c, p);
   } else if (multi(c)) {
     c->step_plan[0] = build_bsp_multi_plan(c);
   }
@@ -951,7 +989,19 @@ void launch_chain_t(dss_ctx* c, const ChainLaunch& cl, ChainArgs<T>& a) {
                                           kThreads, 0, c->stream>>>(a);
     ck(cudaGetLastError(), "chain_partial_kernel launch");
   }
-  if (cl.nb > 0 && c->emu_pass != 1) {
+  if (cl.nb > 0 && c->emu_pass != 1 && c->defer_b) {
+    // deferred: the next step's fused kernel (or flush_lazy) takes it
+    ChainArgs<T> b = a;
+    b.entries = cl.d_b;
+    b.n_entries = cl.nb;
+    const int grid = static_cast<int>(std::min<long>(c->chain_nchunks * cl.nb, c->sms * long{DSS_CHAIN_CTAS_PER_SM}));
+    c->lazy_epoch = a.epoch;
+    c->lazy_b = [c, b, grid]() {
+      TimedLaunch tl(c, DSS_KIND_CHAIN_MEAN);
+      chain_mean_kernel<T, OPTD><<<grid, kThreads, 0, c->stream>>>(b);
+      ck(cudaGetLastError(), "chain_mean_kernel launch (deferred)");
+    };
+  } else if (cl.nb > 0 && c->emu_pass != 1) {
     a.entries = cl.d_b;
     a.n_entries = cl.nb;
     const long units = c->chain_nchunks * cl.nb;
@@ -1166,6 +1216,7 @@ void launch_bsp(dss_ctx* c, long t, double alpha) {
 void barrier(dss_ctx* c) {
   if (!multi(c) || c->emulated) return;  // emulation: the launch order already serialises the ranks
   if (!c->attached) throw PeerError("multi-GPU context used before dss_ipc_attach");
+  flush_lazy(c);
   c->wait_epoch = 0;  // a full barrier subsumes a pending split wait (flags only grow)
   ++c->epoch;
   ++c->xgpu_ops;
@@ -1192,6 +1243,85 @@ void quiesce(dss_ctx* c, bool allow_chain_skip) {
   if (!allow_chain_skip) flush_wait(c);
   c->pending_remote = false;
   c->pending_chain_only = false;
+}
+
+#ifndef DSS_LAZY_CTAS_PER_SM
+#define DSS_LAZY_CTAS_PER_SM 8
+#endif
+
+void flush_lazy(dss_ctx* c) {
+  if (!c->lazy_b) return;
+  std::function<void()> f = std::move(c->lazy_b);
+  c->lazy_b = nullptr;
+  c->lazy_parity = -1;
+  f();
+}
+
+template <typename T, int OPT, int NR, int M>
+void launch_lazy_t(dss_ctx* c, const LazyArgs<T>& a) {
+  const int grid = static_cast<int>(std::min<long>(a.n_chunks, c->sms * long{DSS_LAZY_CTAS_PER_SM}));
+  TimedLaunch tl(c, DSS_KIND_GROUP);
+  lazy_groups_kernel<T, OPT, NR, M><<<grid, kThreads, 0, c->stream>>>(a);
+  ck(cudaGetLastError(), "lazy_groups_kernel launch");
+}
+
+template <typename T, int OPT>
+void launch_lazy_o(dss_ctx* c, const LazyPlan& lp, const LazyArgs<T>& a) {
+  if (lp.nr == 2) {
+    launch_lazy_t<T, OPT, 2, 2>(c, a);
+  } else if (lp.m == 2) {
+    launch_lazy_t<T, OPT, 4, 2>(c, a);
+  } else {
+    launch_lazy_t<T, OPT, 4, 4>(c, a);
+  }
+}
+
+template <typename T>
+void launch_lazy(dss_ctx* c, const LazyPlan& lp, long t, double alpha) {
+  LazyArgs<T> a{};
+  a.w = static_cast<T*>(c->w);
+  a.g = static_cast<const T*>(c->g);
+  a.m1 = static_cast<T*>(c->m1);
+  a.m2 = static_cast<T*>(c->m2);
+  a.ld = c->d_pad;
+  a.chunk = c->chain_chunk;
+  a.len = c->d_pad;
+  a.n_chunks = c->chain_nchunks;
+  for (int i = 0; i < lp.nf; ++i) a.flags[i] = lp.flags[i];
+  a.nf = lp.nf;
+  a.epoch = c->lazy_epoch;
+  a.timeout = c->d_timeout;
+  for (int r = 0; r < lp.nr; ++r) {
+    a.alias[r] = lp.alias[r];
+    a.rows[r] = lp.rows[r];
+    a.rank[r] = c->rank_of_slot[static_cast<size_t>(c->first + r)];
+  }
+  a.t = t;
+  a.step_phase = 0;
+  a.sync_phase = 1;
+  a.err = c->d_err;
+  a.c = consts<T>(c, alpha);
+  fill_bias(c, a);
+  switch (c->cfg.optimizer) {
+    case kSgd: launch_lazy_o<T, kSgd>(c, lp, a); break;
+    case kMomentum: launch_lazy_o<T, kMomentum>(c, lp, a); break;
+    case kAdam: launch_lazy_o<T, kAdam>(c, lp, a); break;
+    case kAdamW: launch_lazy_o<T, kAdamW>(c, lp, a); break;
+    default: throw std::invalid_argument("unknown optimizer kind");
+  }
+}
+
+// The DS step of the consuming parity: the deferred mean pass and the local
+// groups' step in one launch (LazyPlan).
+void launch_lazy_any(dss_ctx* c, const LazyPlan& lp, long t, double alpha) {
+  flush_wait(c);
+  c->lazy_b = nullptr;
+  c->lazy_parity = -1;
+  if (c->cfg.dtype == DSS_F64) {
+    launch_lazy<double>(c, lp, t, alpha);
+  } else {
+    launch_lazy<float>(c, lp, t, alpha);
+  }
 }
 
 // Launch the waiting half of the split barrier on its own if still pending

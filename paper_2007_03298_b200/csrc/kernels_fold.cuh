@@ -474,6 +474,115 @@ __global__ void __launch_bounds__(kThreads) chain_mean_kernel(const ChainArgs<T>
   if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
 }
 
+// ---- deferred chain mean pass fused into the next step's local groups -----
+// After a two-GPU chain step the stage-0 GPU holds each group's mean in one
+// member row (delivered in place by the last stage); instead of copying it to
+// the group's other local members (kernel B), the next step -- whose groups
+// are all local -- reads every member's params through alias[] from the row
+// the mean landed in.  Unit = chain chunk: thread j waits for entry j's mean
+// flag of the chunk, then every thread steps all NR local rows of its
+// element vector (all loads before any store: aliased rows are read by
+// other groups), folds each group of M in ascending order, scales by 1/M
+// and stores the means.  Same arithmetic and order as ds_group_kernel.
+template <typename T> struct LazyArgs {
+  T* w;
+  const T* g;
+  T* m1;
+  T* m2;
+  long ld;
+  long chunk, len, n_chunks;
+  const unsigned long long* flags[4];
+  int nf;
+  unsigned long long epoch;
+  unsigned long long* timeout;
+  int alias[8];
+  int rows[8];
+  int rank[8];  // global rank of local row r
+  long t;
+  int step_phase, sync_phase;
+  unsigned long long* err;
+  StepConsts<T> c;
+  double bc1[kMaxLocal];
+  double bc2[kMaxLocal];
+};
+
+template <typename T, int OPT, int NR, int M>
+__global__ void __launch_bounds__(kThreads) lazy_groups_kernel(const LazyArgs<T> a) {
+  constexpr int VN = Vec<T>::n;
+  __shared__ int ok;
+  unsigned long long bad = ~0ull;
+  const T inv = static_cast<T>(1.0 / static_cast<double>(M));
+  for (long ch = blockIdx.x; ch < a.n_chunks; ch += gridDim.x) {
+    if (threadIdx.x == 0) ok = 1;
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < a.nf && !chain_wait(a.flags[threadIdx.x] + ch, a.epoch, a.timeout)) ok = 0;
+    __syncthreads();
+    const long lo = ch * a.chunk;
+    const long hi = lo + a.chunk < a.len ? lo + a.chunk : a.len;
+    if (ok) {
+      for (long e = lo / VN + threadIdx.x; e < hi / VN; e += blockDim.x) {
+        const long off = e * VN;
+        Pack<T> x[NR], gv[NR], s1[NR], s2[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const long rr = static_cast<long>(a.rows[r]) * a.ld + off;
+          x[r] = ldv(a.w + static_cast<long>(a.alias[a.rows[r]]) * a.ld + off);
+          gv[r] = ldv(a.g + rr);
+          if constexpr (OPT != kSgd) s1[r] = ldv(a.m1 + rr);
+          if constexpr (OPT == kAdam || OPT == kAdamW) s2[r] = ldv(a.m2 + rr);
+        }
+#pragma unroll
+        for (int g0 = 0; g0 < NR; g0 += M) {
+          Pack<T> acc;
+#pragma unroll
+          for (int j = 0; j < M; ++j) {
+            const int r = g0 + j;
+            const int lr = a.rows[r];
+            const long rr = static_cast<long>(lr) * a.ld + off;
+            T b1 = T(1), b2 = T(1);
+            if constexpr (OPT == kAdam || OPT == kAdamW) {
+              b1 = static_cast<T>(a.bc1[lr]);
+              b2 = static_cast<T>(a.bc2[lr]);
+            }
+            step_pack<T, OPT>(x[r], gv[r], s1[r], s2[r], a.c, b1, b2);
+            bool okv = true;
+#pragma unroll
+            for (int l = 0; l < VN; ++l) okv = okv && finite_(x[r].v[l]);
+            if constexpr (OPT != kSgd) stv(a.m1 + rr, s1[r]);
+            if constexpr (OPT == kAdam || OPT == kAdamW) stv(a.m2 + rr, s2[r]);
+            if (!okv) {
+              const unsigned long long k = err_key(a.t, a.step_phase, a.rank[lr]);
+              bad = k < bad ? k : bad;
+            }
+            if (j == 0) {
+              acc = x[r];
+            } else {
+#pragma unroll
+              for (int l = 0; l < VN; ++l) acc.v[l] = add_(acc.v[l], x[r].v[l]);
+            }
+          }
+          if (M != 1) {
+            bool okm = true;
+#pragma unroll
+            for (int l = 0; l < VN; ++l) {
+              acc.v[l] = mul_(acc.v[l], inv);
+              okm = okm && finite_(acc.v[l]);
+            }
+            if (!okm) {
+              const unsigned long long k = err_key(a.t, a.sync_phase, a.rank[a.rows[g0]]);
+              bad = k < bad ? k : bad;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < M; ++j) stv(a.w + static_cast<long>(a.rows[g0 + j]) * a.ld + off, acc);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (__any_sync(__activemask(), bad != ~0ull)) latch_error(a.err, bad);
+}
+
 // ---- fused two-shot (push) over NVLink ------------------------------------
 // For groups with one member per GPU.  One persistent kernel per iteration:
 //   phase 1  each GPU steps its member chunk by chunk and pushes the stepped

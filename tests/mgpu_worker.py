@@ -274,7 +274,10 @@ def ds_stream_case(rank, G, orc):
     chain rows and flags); two-shot push plans replace it with the split
     barrier (the push kernel arrives, the next step's first kernel waits):
     push -> local group kernel (C2 shape and W=16 on 4 GPUs, contiguous) and
-    push -> push (W=4 with pairs forced off one-shot, path 4)."""
+    push -> push (W=4 with pairs forced off one-shot, path 4).  On 2 GPUs
+    the C2 shape's comb chains leave their mean pass to the next block step
+    (deferred, fused with the local groups: LazyPlan), SGD / momentum /
+    AdamW."""
     ok = True
     for W, N, rect, opt, d, iters, placement, path in ((8, 2, True, 1, 250_001, 100, 0, 0),
                                                        (16, 4, False, 3, 200_003, 60, 1, 0),
@@ -282,7 +285,8 @@ def ds_stream_case(rank, G, orc):
                                                        (8, 2, True, 0, 250_001, 100, 0, 0),
                                                        (16, 4, False, 3, 200_003, 60, 0, 0),
                                                        (4, 2, False, 1, 250_001, 100, 0, 4),
-                                                       (4, 2, False, 3, 4097, 200, 0, 4)):
+                                                       (4, 2, False, 3, 4097, 200, 0, 4),
+                                                       (8, 2, True, 3, 250_001, 60, 0, 0)):
         if W % G:
             continue
         s = SyncStrategy(StrategyKind.DS_SYNC, Topology.RING, WorldConfig(W, N), 1, rect)
