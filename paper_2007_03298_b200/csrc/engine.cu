@@ -1245,8 +1245,11 @@ void quiesce(dss_ctx* c, bool allow_chain_skip) {
   c->pending_chain_only = false;
 }
 
+// 2 CTAs per SM: C2 on 2 GPUs 3468-3480 iters/s against 3419-3435 at 4 and
+// 8 (profiles/r02/sweeps/lazy_mean_ctas_ab_g2.jsonl): fewer units in
+// flight follow the arriving mean chunks more closely
 #ifndef DSS_LAZY_CTAS_PER_SM
-#define DSS_LAZY_CTAS_PER_SM 8
+#define DSS_LAZY_CTAS_PER_SM 2
 #endif
 
 void flush_lazy(dss_ctx* c) {
