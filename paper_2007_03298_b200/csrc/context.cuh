@@ -235,6 +235,7 @@ struct dss_ctx {
   int lazy_parity = -1;                   // parity whose step consumes it
   bool lazy_consume = false;              // set by dss_step around guard(): do not flush on entry
   bool defer_b = false;                   // the next chain launch defers its kernel B
+  bool allow_defer = false;               // dss_steps: another step of the same call follows
   bool arrive_next_push = false;          // the next push launch arrives
 
   dssb::ParityPlan step_plan[2];   // DS (or BSP at [0])

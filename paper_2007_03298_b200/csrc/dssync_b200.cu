@@ -571,7 +571,7 @@ extern "C" int dss_step(dss_ctx* c, long t, double alpha, int check, dss_outcome
           launch_fold_any(c, pp.fold, t);
         }
         if (pp.any_chain) {
-          c->defer_b = c->lazy_plan[t & 1].ok && !c->emulated && c->emu_pass == 0;
+          c->defer_b = c->allow_defer && c->lazy_plan[t & 1].ok && !c->emulated && c->emu_pass == 0;
           launch_chain_any(c, pp.chain, t, alpha);
           c->defer_b = false;
           if (c->lazy_b) c->lazy_parity = static_cast<int>((t + 1) & 1);
@@ -734,7 +734,11 @@ extern "C" int dss_steps(dss_ctx* c, long t0, long n, const double* alphas, int 
   }
   for (long i = 0; i < n; ++i) {
     // the closed-form round outcome (a host partition) only for the last iteration
+    // a mean pass may be deferred only to the next step of this same call:
+    // no caller code can read the rows in between, and none stays pending
+    c->allow_defer = i + 1 < n;
     const int st = dss_step(c, t0 + i, alphas[i], 0, i + 1 == n ? last : nullptr);
+    c->allow_defer = false;
     if (st != DSS_OK) return st;
   }
   if (check) return dss_check(c);
