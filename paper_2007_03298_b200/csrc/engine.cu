@@ -1061,6 +1061,10 @@ void launch_chain(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
 }
 
 void launch_chain_any(dss_ctx* c, const ChainLaunch& cl, long t, double alpha) {
+  struct ResetDefer {  // defer_b covers this one launch, even if it throws
+    dss_ctx* c;
+    ~ResetDefer() { c->defer_b = false; }
+  } reset{c};
   flush_wait(c);
   ++c->xgpu_ops;
   if (c->cfg.dtype == DSS_F64) {
