@@ -1250,8 +1250,8 @@ void quiesce(dss_ctx* c, bool allow_chain_skip) {
 }
 
 // 2 CTAs per SM: C2 on 2 GPUs 3468-3480 iters/s against 3419-3435 at 4 and
-// 8 (profiles/r02/sweeps/lazy_mean_ctas_ab_g2.jsonl): fewer units in
-// flight follow the arriving mean chunks more closely
+// 8 (profiles/r02/sweeps/lazy_mean_ctas_ab_g2.jsonl), 3450-3460 against
+// 3419-3431 at 3 and 3267-3272 at 1 (lazy_mean_ctas_ab2_g2.jsonl)
 #ifndef DSS_LAZY_CTAS_PER_SM
 #define DSS_LAZY_CTAS_PER_SM 2
 #endif
